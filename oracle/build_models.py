@@ -1,0 +1,79 @@
+"""Compile the model zoo with the REFERENCE compiler -> models/*.rly.
+
+Oracle tooling (runs in the build container, where /root/reference and
+oracle/_ref/mr_ref exist).  For every model it writes
+
+  models/<name>.src.rly           the unfused source (modelzoo.py)
+  models/<name>_fp32.fused.rly    run_pipeline("fold-scale,fold,dce,fuse")
+  models/<name>_int8.fused.rly    run_pipeline("fold-scale,fold,dce,quantize,fuse")
+  models/<name>.json              calibrated k + seeds + pass lists
+
+The int8 module uses the global scale 2^k that the reference's own
+quant_calibrate (quantize.cpp:138-177) picks on ONE calibration image
+(modelzoo.make_inputs(seed=0)[0]) with the seeded weights; the fixed-k
+compile is checked equal to the stock calibrated run_pipeline on small
+models by tests/test_oracle_ref.py.
+
+The fused modules are the drop-in artifact the backend consumes: the exact
+text the reference's printer (printer.cpp) emits for its fused program.
+
+usage: python oracle/build_models.py [name ...]
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+_ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, _ROOT)
+
+from oracle import ref  # noqa: E402
+from paper_1904_08368_b200 import modelzoo  # noqa: E402
+
+PRE = "fold-scale,fold,dce"
+FP32 = PRE + ",fuse"
+INT8 = PRE + ",quantize,fuse"
+
+CONFIGS = {
+    # name: (builder, kwargs)
+    "resnet18": (modelzoo.resnet18, {}),
+    "resnet18_tiny": (modelzoo.resnet18, dict(image=32, num_classes=10, widths=(32, 32, 64, 64))),
+}
+
+
+def build(name: str, out_dir: str) -> dict:
+    fn, kw = CONFIGS[name]
+    src = fn(**kw)
+    w = modelzoo.make_weights(src, seed=1)
+    x = modelzoo.make_inputs(src, 1, seed=0)
+    t0 = time.time()
+    k = ref.calibrate(src.text, PRE, [x] + ref.weight_list(src, w))
+    t_cal = time.time() - t0
+    fused_fp32 = ref.compile(src.text, FP32, 0)
+    fused_int8 = ref.compile(src.text, INT8, k)
+    open(os.path.join(out_dir, name + ".src.rly"), "w").write(src.text)
+    open(os.path.join(out_dir, name + "_fp32.fused.rly"), "w").write(fused_fp32)
+    open(os.path.join(out_dir, name + "_int8.fused.rly"), "w").write(fused_int8)
+    meta = {
+        "name": name,
+        "builder": fn.__name__,
+        "builder_kwargs": {k2: list(v) if isinstance(v, tuple) else v for k2, v in kw.items()},
+        "weights_seed": 1,
+        "calibration": {"inputs_seed": 0, "images": 1, "k": k, "scale": 2.0 ** k,
+                        "seconds": round(t_cal, 1), "pre_passes": PRE},
+        "passes": {"fp32": FP32, "int8": INT8},
+        "groups": {"fp32": fused_fp32.count("[Primitive=true]"),
+                   "int8": fused_int8.count("[Primitive=true]")},
+    }
+    json.dump(meta, open(os.path.join(out_dir, name + ".json"), "w"), indent=1)
+    return meta
+
+
+if __name__ == "__main__":
+    names = sys.argv[1:] or list(CONFIGS)
+    out = os.path.join(_ROOT, "models")
+    os.makedirs(out, exist_ok=True)
+    for n in names:
+        print(json.dumps(build(n, out)), flush=True)

@@ -1,0 +1,382 @@
+// ref_harness.cpp -- TEST INFRASTRUCTURE (oracle), never linked by the product.
+// Built as the executable oracle/_ref/mr_ref (a subprocess, not a ctypes .so:
+// the reference library crashed when loaded into a numpy-importing process).
+//
+// A thin CLI over the UNMODIFIED reference library (MicroRelay, built from
+// /root/reference/proj/core/src by oracle/Makefile) so pytest drives it as a
+// subprocess (oracle/ref.py):
+//   * parse_module            parser.hpp:17-19
+//   * run_pipeline / passes   passes.cpp:490-501, passes.cpp:452-486
+//   * quant_annotate/_calibrate/_realize   quantize.cpp:92-110, 138-177, 212-245
+//   * interp                  interp.cpp:218-222
+//   * print_module            printer.hpp:17
+//
+// Extension operators: the reference has no
+// pooling or depthwise operator. They are registered through the reference's
+// own public operator API (OpRegistry::register_op on a copy of the builtin
+// registry, as test_registry.cpp:21-31 does), reusing the existing "Conv2D"
+// type relation (registry.cpp:412-469) with a shape-only window argument:
+//   max_pool2d(x, win[C,C,KH,KW], strides, padding)   -> ComplexOutFusable
+//   depthwise_conv2d(x, win[C,C,KH,KW], w[C,1,KH,KW], strides, padding)
+// Their kernels follow kernels.cpp:640-716 conventions: NCHW, padded taps
+// skipped, sequential accumulation (max seeded with the first valid tap,
+// then std::max like reduce_impl kernels.cpp:519-566).
+#include <chrono>
+#include <climits>
+#include <cstdio>
+#include <fstream>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "microrelay/analysis.hpp"
+#include "microrelay/expr.hpp"
+#include "microrelay/infer.hpp"
+#include "microrelay/interp.hpp"
+#include "microrelay/parser.hpp"
+#include "microrelay/passes.hpp"
+#include "microrelay/printer.hpp"
+#include "microrelay/quantize.hpp"
+#include "microrelay/registry.hpp"
+
+using namespace microrelay;
+
+namespace {
+
+const TensorLiteral& tens(const ValueRef& v) {
+  if (!v || v->kind != ValueKind::Tensor) diag_throw(DiagCode::TypeMismatch, "expected tensor");
+  return v->tensor;
+}
+
+// ---- extension kernels (restated in the style of kernels.cpp) -------------
+
+ValueRef k_max_pool2d(const std::vector<ValueRef>& args, const AttrMap& attrs,
+                      const SourceSpan& s) {
+  const TensorLiteral& x = tens(args[0]);
+  const TensorLiteral& win = tens(args[1]);
+  if (!(x.dtype.is_float() && x.dtype.bits == 32))
+    diag_throw(DiagCode::TypeMismatch, "max_pool2d: float32 only", s);
+  auto strides = attr_int_list_opt(attrs, "strides").value_or(std::vector<int64_t>{1, 1});
+  auto padding = attr_int_list_opt(attrs, "padding").value_or(std::vector<int64_t>{0, 0});
+  auto xd = x.shape.to_ints();
+  auto wd = win.shape.to_ints();
+  int64_t N = xd[0], C = xd[1], H = xd[2], W = xd[3], KH = wd[2], KW = wd[3];
+  int64_t sh = strides[0], sw = strides[1], ph = padding[0], pw = padding[1];
+  int64_t OH = (H - KH + 2 * ph) / sh + 1, OW = (W - KW + 2 * pw) / sw + 1;
+  TensorLiteral out = TensorLiteral::zeros(Shape::of({N, C, OH, OW}), x.dtype);
+  const float* xp = x.f32s().data();
+  float* op = out.f32s().data();
+  for (int64_t n = 0; n < N; ++n)
+    for (int64_t c = 0; c < C; ++c)
+      for (int64_t oh = 0; oh < OH; ++oh)
+        for (int64_t ow = 0; ow < OW; ++ow) {
+          float acc = 0.0f;
+          bool seeded = false;
+          for (int64_t kh = 0; kh < KH; ++kh)
+            for (int64_t kw = 0; kw < KW; ++kw) {
+              int64_t h = oh * sh - ph + kh, w = ow * sw - pw + kw;
+              if (h < 0 || h >= H || w < 0 || w >= W) continue;
+              float v = xp[((n * C + c) * H + h) * W + w];
+              if (!seeded) {
+                acc = v;
+                seeded = true;
+              } else {
+                acc = std::max(acc, v);
+              }
+            }
+          op[((n * C + c) * OH + oh) * OW + ow] = acc;
+        }
+  return make_tensor_value(std::move(out));
+}
+
+ValueRef k_depthwise_conv2d(const std::vector<ValueRef>& args, const AttrMap& attrs,
+                            const SourceSpan& s) {
+  const TensorLiteral& x = tens(args[0]);
+  const TensorLiteral& w = tens(args[2]);
+  if (!(x.dtype.is_float() && x.dtype.bits == 32))
+    diag_throw(DiagCode::TypeMismatch, "depthwise_conv2d: float32 only", s);
+  auto strides = attr_int_list_opt(attrs, "strides").value_or(std::vector<int64_t>{1, 1});
+  auto padding = attr_int_list_opt(attrs, "padding").value_or(std::vector<int64_t>{0, 0});
+  auto xd = x.shape.to_ints();
+  auto wd = w.shape.to_ints();
+  int64_t N = xd[0], C = xd[1], H = xd[2], W = xd[3], KH = wd[2], KW = wd[3];
+  if (wd[0] != C || wd[1] != 1)
+    diag_throw(DiagCode::TypeMismatch, "depthwise_conv2d: weight must be [C,1,KH,KW]", s);
+  int64_t sh = strides[0], sw = strides[1], ph = padding[0], pw = padding[1];
+  int64_t OH = (H - KH + 2 * ph) / sh + 1, OW = (W - KW + 2 * pw) / sw + 1;
+  TensorLiteral out = TensorLiteral::zeros(Shape::of({N, C, OH, OW}), x.dtype);
+  const float* xp = x.f32s().data();
+  const float* wp = w.f32s().data();
+  float* op = out.f32s().data();
+  for (int64_t n = 0; n < N; ++n)
+    for (int64_t c = 0; c < C; ++c)
+      for (int64_t oh = 0; oh < OH; ++oh)
+        for (int64_t ow = 0; ow < OW; ++ow) {
+          float facc = 0.0f;
+          for (int64_t kh = 0; kh < KH; ++kh)
+            for (int64_t kw = 0; kw < KW; ++kw) {
+              int64_t h = oh * sh - ph + kh, ww = ow * sw - pw + kw;
+              if (h < 0 || h >= H || ww < 0 || ww >= W) continue;
+              facc += xp[((n * C + c) * H + h) * W + ww] * wp[(c * KH + kh) * KW + kw];
+            }
+          op[((n * C + c) * OH + oh) * OW + ow] = facc;
+        }
+  return make_tensor_value(std::move(out));
+}
+
+std::shared_ptr<const OpRegistry> ext_registry() {
+  static std::shared_ptr<const OpRegistry> reg = [] {
+    auto r = std::make_shared<OpRegistry>(*builtin_registry());
+    std::map<std::string, AttrKind> schema = {{"strides", AttrKind::IntList},
+                                              {"padding", AttrKind::IntList},
+                                              {"layout", AttrKind::String}};
+    r->register_op(OperatorDecl{"max_pool2d", 2, schema, "Conv2D",
+                                FusionPattern::ComplexOutFusable, k_max_pool2d});
+    r->register_op(OperatorDecl{"depthwise_conv2d", 3, schema, "Conv2D",
+                                FusionPattern::ComplexOutFusable, k_depthwise_conv2d});
+    return std::shared_ptr<const OpRegistry>(r);
+  }();
+  return reg;
+}
+
+// ---- fixed-scale quantization ---------------------------------------------
+
+bool is_simq(const ExprRef& e) {
+  return e->kind == ExprKind::Call && e->a->kind == ExprKind::OperatorRef &&
+         e->a->name == "simulated_quantize";
+}
+
+// Sets attr scale on every simulated_quantize call: the same rewrite
+// quant_calibrate applies per trial (with_global_scale, quantize.cpp:123-134).
+ExprRef set_scale(const ExprRef& e, double scale) {
+  if (!e) return e;
+  switch (e->kind) {
+    case ExprKind::LocalVar:
+    case ExprKind::GlobalVar:
+    case ExprKind::Constant:
+    case ExprKind::OperatorRef:
+    case ExprKind::ConstructorRef:
+      return e;
+    default: {
+      auto copy = std::make_shared<Expr>(*e);
+      copy->checked_type = nullptr;
+      if (e->a) copy->a = set_scale(e->a, scale);
+      if (e->b) copy->b = set_scale(e->b, scale);
+      if (e->c) copy->c = set_scale(e->c, scale);
+      copy->elems.clear();
+      for (const auto& x : e->elems) copy->elems.push_back(set_scale(x, scale));
+      copy->clauses.clear();
+      for (const auto& cl : e->clauses) copy->clauses.push_back({cl.pattern, set_scale(cl.body, scale)});
+      if (is_simq(copy)) copy->attrs["scale"] = scale;
+      return copy;
+    }
+  }
+}
+
+double find_scale(const ExprRef& e) {
+  if (!e) return 0;
+  if (is_simq(e)) {
+    auto s = attr_float_opt(e->attrs, "scale");
+    if (s) return *s;
+  }
+  for (const ExprRef& c : {e->a, e->b, e->c}) {
+    double s = find_scale(c);
+    if (s != 0) return s;
+  }
+  for (const auto& x : e->elems) {
+    double s = find_scale(x);
+    if (s != 0) return s;
+  }
+  return 0;
+}
+
+std::vector<std::string> split_passes(const std::string& s) {
+  std::vector<std::string> out;
+  std::string cur;
+  for (char c : s) {
+    if (c == ',') {
+      if (!cur.empty()) out.push_back(cur);
+      cur.clear();
+    } else {
+      cur += c;
+    }
+  }
+  if (!cur.empty()) out.push_back(cur);
+  return out;
+}
+
+ModuleEnv run_passes(const ModuleEnv& m, const std::vector<std::string>& passes) {
+  std::string joined;
+  for (const auto& p : passes) joined += (joined.empty() ? "" : ",") + p;
+  if (joined.empty()) return infer(m);
+  return run_pipeline(m, PassContext::from_pass_list(joined));
+}
+
+// passes before "quantize", "quantize" itself (fixed k), passes after.
+ModuleEnv compile_fixed_k(const ModuleEnv& m0, const std::string& passes, int k) {
+  auto list = split_passes(passes);
+  std::vector<std::string> pre, post;
+  bool quant = false;
+  for (const auto& p : list) {
+    if (p == "quantize") {
+      quant = true;
+    } else {
+      (quant ? post : pre).push_back(p);
+    }
+  }
+  ModuleEnv m = run_passes(m0, pre);
+  if (quant) {
+    // apply_one_pass "quantize" (passes.cpp:471-478) with quant_calibrate
+    // replaced by its result for global scale 2^k.
+    QuantConfig cfg;
+    ModuleEnv annotated = infer(quant_annotate(m, QuantRules::defaults(), cfg));
+    ModuleEnv calibrated = annotated;
+    for (auto& [name, fn] : calibrated.globals) fn = set_scale(fn, std::ldexp(1.0, k));
+    m = infer(quant_realize(infer(calibrated), cfg));
+  }
+  return run_passes(m, post);
+}
+
+// ---- binary tensor files ---------------------------------------------------
+// Format (little endian): int32 count; per tensor: int32 ndim, int64 dims[ndim],
+// float32 data[prod(dims)].
+
+std::vector<TensorLiteral> read_tensors(const std::string& path) {
+  FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) diag_throw(DiagCode::Internal, "cannot open " + path);
+  int32_t n = 0;
+  std::vector<TensorLiteral> out;
+  if (std::fread(&n, 4, 1, f) != 1) diag_throw(DiagCode::Internal, "short read " + path);
+  for (int32_t i = 0; i < n; ++i) {
+    int32_t nd = 0;
+    if (std::fread(&nd, 4, 1, f) != 1) diag_throw(DiagCode::Internal, "short read");
+    std::vector<int64_t> dims(nd);
+    if (nd && std::fread(dims.data(), 8, nd, f) != static_cast<size_t>(nd))
+      diag_throw(DiagCode::Internal, "short read");
+    int64_t cnt = 1;
+    for (auto d : dims) cnt *= d;
+    std::vector<float> v(cnt);
+    if (cnt && std::fread(v.data(), 4, cnt, f) != static_cast<size_t>(cnt))
+      diag_throw(DiagCode::Internal, "short read");
+    out.push_back(TensorLiteral::from_f32(Shape::of(dims), std::move(v)));
+  }
+  std::fclose(f);
+  return out;
+}
+
+void write_tensors(const std::string& path, const std::vector<const TensorLiteral*>& ts) {
+  FILE* f = std::fopen(path.c_str(), "wb");
+  if (!f) diag_throw(DiagCode::Internal, "cannot open " + path);
+  int32_t n = static_cast<int32_t>(ts.size());
+  std::fwrite(&n, 4, 1, f);
+  for (const TensorLiteral* t : ts) {
+    if (!(t->dtype.is_float() && t->dtype.bits == 32))
+      diag_throw(DiagCode::Internal, "result is not float32");
+    auto dims = t->shape.to_ints();
+    int32_t nd = static_cast<int32_t>(dims.size());
+    std::fwrite(&nd, 4, 1, f);
+    std::fwrite(dims.data(), 8, nd, f);
+    std::fwrite(t->f32s().data(), 4, t->f32s().size(), f);
+  }
+  std::fclose(f);
+}
+
+std::string read_file(const std::string& path) {
+  std::ifstream f(path);
+  if (!f) diag_throw(DiagCode::Internal, "cannot open " + path);
+  std::stringstream ss;
+  ss << f.rdbuf();
+  return ss.str();
+}
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+int usage() {
+  std::fprintf(stderr,
+               "usage:\n"
+               "  mr_ref compile  MODEL.rly PASSES K            -> fused module on stdout\n"
+               "  mr_ref calibrated MODEL.rly PASSES ARGS.bin   -> run_pipeline w/ quant_calibrate\n"
+               "  mr_ref calibrate MODEL.rly PRE_PASSES ARGS.bin -> k on stdout\n"
+               "  mr_ref run FUSED.rly WEIGHTS.bin IMAGES.bin OUT.bin\n"
+               "      interp(@main) once per image of IMAGES.bin's first tensor ([B,...] ->\n"
+               "      batch-1 calls), WEIGHTS.bin = the remaining @main args in order;\n"
+               "      per-image seconds on stderr as 'image i t'\n");
+  return 2;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  if (argc < 2) return usage();
+  std::string cmd = argv[1];
+  try {
+    if (cmd == "compile" && argc == 5) {
+      ModuleEnv m = parse_module(read_file(argv[2]), argv[2], ext_registry());
+      std::fputs(print_module(compile_fixed_k(m, argv[3], std::atoi(argv[4]))).c_str(), stdout);
+      return 0;
+    }
+    if ((cmd == "calibrate" || cmd == "calibrated") && argc == 5) {
+      ModuleEnv m = parse_module(read_file(argv[2]), argv[2], ext_registry());
+      std::vector<ValueRef> args;
+      for (auto& t : read_tensors(argv[4])) args.push_back(make_tensor_value(std::move(t)));
+      if (cmd == "calibrated") {
+        // The stock pipeline end to end (passes.cpp:471-478 calls quant_calibrate).
+        PassContext ctx = PassContext::from_pass_list(argv[3]);
+        ctx.calibration_inputs.push_back(args);
+        std::fputs(print_module(run_pipeline(m, ctx)).c_str(), stdout);
+        return 0;
+      }
+      ModuleEnv pre = run_passes(m, split_passes(argv[3]));
+      ModuleEnv cal = quant_calibrate(infer(quant_annotate(pre)), {args}, "main");
+      double s = 0;
+      for (const auto& [name, fn] : cal.globals)
+        if ((s = find_scale(fn)) != 0) break;
+      if (s == 0) diag_throw(DiagCode::Internal, "no simulated_quantize site");
+      std::printf("%d\n", static_cast<int>(std::lround(std::log2(s))));
+      return 0;
+    }
+    if (cmd == "run" && argc == 6) {
+      ModuleEnv m = parse_module(read_file(argv[2]), argv[2], ext_registry());
+      std::vector<TensorLiteral> weights = read_tensors(argv[3]);
+      std::vector<TensorLiteral> images = read_tensors(argv[4]);
+      if (images.size() != 1) diag_throw(DiagCode::Internal, "IMAGES.bin must hold one tensor");
+      const TensorLiteral& batch = images[0];
+      auto dims = batch.shape.to_ints();
+      int64_t B = dims[0], per = batch.num_elements() / std::max<int64_t>(B, 1);
+      std::vector<int64_t> one = dims;
+      one[0] = 1;
+      std::vector<ValueRef> wargs;
+      for (auto& w : weights) wargs.push_back(make_tensor_value(std::move(w)));
+      std::vector<TensorLiteral> results;
+      InterpOptions opts;
+      opts.fuel = INT64_MAX / 2;
+      for (int64_t i = 0; i < B; ++i) {
+        std::vector<float> img(batch.f32s().begin() + i * per, batch.f32s().begin() + (i + 1) * per);
+        std::vector<ValueRef> args{make_tensor_value(TensorLiteral::from_f32(Shape::of(one), std::move(img)))};
+        args.insert(args.end(), wargs.begin(), wargs.end());
+        double t0 = now_s();
+        ValueRef r = interp(m, "main", args, opts);
+        std::fprintf(stderr, "image %lld %.6f\n", static_cast<long long>(i), now_s() - t0);
+        results.push_back(tens(r));
+      }
+      // Concatenate the batch-1 results along axis 0.
+      std::vector<float> all;
+      std::vector<int64_t> rd = results.empty() ? std::vector<int64_t>{0} : results[0].shape.to_ints();
+      for (auto& r : results) all.insert(all.end(), r.f32s().begin(), r.f32s().end());
+      rd[0] = B;
+      TensorLiteral out = TensorLiteral::from_f32(Shape::of(rd), std::move(all));
+      write_tensors(argv[5], {&out});
+      return 0;
+    }
+    return usage();
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "mr_ref: %s\n", e.what());
+    return 1;
+  }
+}

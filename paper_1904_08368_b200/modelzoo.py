@@ -1,0 +1,185 @@
+"""Model sources in the reference's own text format (``.rly``) plus seeded weights.
+
+The reference (MicroRelay) has no model zoo: its only model interchange is the
+text format (``parser.cpp`` / ``printer.cpp``).  This module
+writes the *unfused* CNNs of BASELINE.json's configs as ``def @main(...)``
+programs in that format, with
+
+* conv/dense weights and biases as ``@main`` parameters (so the reference's
+  ``fold`` leaves them alone and the backend hoists their prologues to
+  weight-load time),
+* folded batch-norm as ``multiply(conv, gamma'[C,1,1])`` with gamma' a metadata
+  constant -- ``ScaleFolder::const_of`` only folds constants
+  (``rewrites.cpp:117-126``),
+* pooling as the extension operator ``max_pool2d(x, %win)`` whose window
+  argument is a shape-only ``[C, C, KH, KW]`` parameter typed by the
+  reference's existing ``Conv2D`` relation,
+* a symbolic batch dimension ``?n`` so one fused module serves every batch
+  shard (``test_infer.cpp:90-102``).
+
+Weights come from ``numpy.random.Generator(PCG64(seed))``: He-normal
+N(0, sqrt(2/fan_in)) for conv/dense, N(0, 0.05) for biases, U[0.5, 1.5) for
+gamma' (SURVEY.md 8(d) "Weights and seeds").  The same host buffers go to the
+CPU oracle and to the GPU.
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import Dict, List, Tuple
+
+import numpy as np
+
+
+def fmt_f32(v: float) -> str:
+    """%.9g of a float32, always with a float marker (the parser reads a bare
+    integer token as an int32 scalar, parser.cpp:631)."""
+    s = "%.9g" % float(np.float32(v))
+    if not any(ch in s for ch in ".eEn"):
+        s += ".0"
+    return s
+
+
+@dataclasses.dataclass
+class Param:
+    name: str
+    shape: Tuple  # first dim may be "?n"
+    kind: str  # "input" | "conv_w" | "dense_w" | "bias" | "window"
+
+
+@dataclasses.dataclass
+class ModelSource:
+    name: str
+    text: str
+    params: List[Param]
+    input_shape: Tuple[int, ...]  # per-sample (C, H, W)
+    num_classes: int
+
+    def param_shapes(self, batch: int) -> Dict[str, Tuple[int, ...]]:
+        out = {}
+        for p in self.params:
+            out[p.name] = tuple(batch if d == "?n" else d for d in p.shape)
+        return out
+
+
+class _Builder:
+    def __init__(self, seed: int):
+        self.rng = np.random.Generator(np.random.PCG64(seed))
+        self.params: List[Param] = []
+        self.lines: List[str] = []
+        self.meta: List[str] = []
+        self.counter = 0
+
+    def fresh(self, prefix="v"):
+        self.counter += 1
+        return "%s%d" % (prefix, self.counter)
+
+    def param(self, name, shape, kind):
+        self.params.append(Param(name, tuple(shape), kind))
+        return "%" + name
+
+    def let(self, expr):
+        v = self.fresh()
+        self.lines.append("  let %%%s = %s;" % (v, expr))
+        return "%" + v
+
+    def meta_const(self, values: np.ndarray, shape):
+        vals = ", ".join(fmt_f32(x) for x in np.asarray(values, np.float32).reshape(-1))
+        shp = "(" + ", ".join(str(d) for d in shape) + ")"
+        self.meta.append("  const[%d] = const([%s], %s, float32);" % (len(self.meta), vals, shp))
+        return "meta[Constant][%d]" % (len(self.meta) - 1)
+
+    # layers ---------------------------------------------------------------
+    def conv_bn(self, x, cin, cout, k, stride, pad, tag, relu=True, bn=True):
+        w = self.param("w_" + tag, (cout, cin, k, k), "conv_w")
+        y = self.let("conv2d(%s, %s, strides=(%d, %d), padding=(%d, %d))" % (x, w, stride, stride, pad, pad))
+        if bn:
+            gamma = self.rng.uniform(0.5, 1.5, size=(cout,)).astype(np.float32)
+            y = self.let("multiply(%s, %s)" % (y, self.meta_const(gamma, (cout, 1, 1))))
+        b = self.param("b_" + tag, (cout,), "bias")
+        y = self.let("bias_add(%s, %s)" % (y, b))
+        if relu:
+            y = self.let("relu(%s)" % y)
+        return y
+
+    def max_pool(self, x, c, k, stride, pad, tag):
+        win = self.param("win_" + tag, (c, c, k, k), "window")
+        return self.let("max_pool2d(%s, %s, strides=(%d, %d), padding=(%d, %d))" % (x, win, stride, stride, pad, pad))
+
+    def dense(self, x, cin, cout, tag, relu=False):
+        w = self.param("w_" + tag, (cout, cin), "dense_w")
+        y = self.let("dense(%s, %s)" % (x, w))
+        b = self.param("b_" + tag, (cout,), "bias")
+        y = self.let("bias_add(%s, %s)" % (y, b))
+        if relu:
+            y = self.let("relu(%s)" % y)
+        return y
+
+    def finish(self, name, result, input_shape, num_classes):
+        sig = []
+        for p in self.params:
+            dims = ", ".join(str(d) for d in p.shape)
+            sig.append("%%%s: Tensor[(%s), float32]" % (p.name, dims))
+        body = "\n".join(self.lines)
+        text = "def @main(%s) {\n%s\n  %s\n}\n" % (", ".join(sig), body, result)
+        if self.meta:
+            text += "metadata {\n" + "\n".join(self.meta) + "\n}\n"
+        return ModelSource(name, text, list(self.params), tuple(input_shape), num_classes)
+
+
+def resnet18(image: int = 224, num_classes: int = 1000, seed: int = 1,
+             widths=(64, 128, 256, 512)) -> ModelSource:
+    """ResNet-18 v1 (BasicBlock x [2,2,2,2]) with folded BN, NCHW."""
+    b = _Builder(seed)
+    x = b.param("x", ("?n", 3, image, image), "input")
+    y = b.conv_bn(x, 3, widths[0], 7, 2, 3, "stem")
+    y = b.max_pool(y, widths[0], 3, 2, 1, "pool")
+    hw = (image + 2 * 3 - 7) // 2 + 1
+    hw = (hw + 2 - 3) // 2 + 1
+    cin = widths[0]
+    for li, cout in enumerate(widths):
+        for bi in range(2):
+            stride = 2 if (li > 0 and bi == 0) else 1
+            tag = "l%db%d" % (li + 1, bi)
+            a = b.conv_bn(y, cin, cout, 3, stride, 1, tag + "c1")
+            a = b.conv_bn(a, cout, cout, 3, 1, 1, tag + "c2", relu=False)
+            if stride != 1 or cin != cout:
+                sc = b.conv_bn(y, cin, cout, 1, stride, 0, tag + "ds", relu=False)
+            else:
+                sc = y
+            y = b.let("relu(%s)" % b.let("add(%s, %s)" % (a, sc)))
+            cin = cout
+        if li > 0:
+            hw = (hw + 2 - 3) // 2 + 1
+    g = b.let("sum(%s, axis=(2, 3))" % y)
+    g = b.let("multiply(%s, const %s)" % (g, fmt_f32(1.0 / (hw * hw))))
+    out = b.dense(g, cin, num_classes, "fc")
+    return b.finish("resnet18", out, (3, image, image), num_classes)
+
+
+MODELS = {"resnet18": resnet18}
+
+
+def make_weights(src: ModelSource, seed: int = 1) -> Dict[str, np.ndarray]:
+    """Seeded random-init weights for every non-input parameter (host fp32)."""
+    rng = np.random.Generator(np.random.PCG64(seed + 1000))
+    out = {}
+    for p in src.params:
+        if p.kind == "input":
+            continue
+        shape = tuple(int(d) for d in p.shape)
+        if p.kind in ("conv_w", "dense_w"):
+            fan_in = int(np.prod(shape[1:]))
+            out[p.name] = (rng.standard_normal(shape) * np.sqrt(2.0 / fan_in)).astype(np.float32)
+        elif p.kind == "bias":
+            out[p.name] = (rng.standard_normal(shape) * 0.05).astype(np.float32)
+        elif p.kind == "window":
+            out[p.name] = np.zeros(shape, np.float32)  # shape-only argument
+        else:
+            raise ValueError(p.kind)
+    return out
+
+
+def make_inputs(src: ModelSource, batch: int, seed: int = 0) -> np.ndarray:
+    """Synthetic images x ~ U[0,1), NCHW float32."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return rng.random((batch,) + tuple(src.input_shape), dtype=np.float32)
