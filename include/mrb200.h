@@ -1,0 +1,150 @@
+/* mrb200.h -- C ABI of the B200-native backend for Relay's fused-group
+ * execution path (arXiv 1904.08368; reference: MicroRelay, /root/reference).
+ *
+ * The reference executes a fused module -- the output of run_pipeline with
+ * "fuse" (fuse.cpp:318-328) and optionally "quantize" (quantize.cpp:212-245)
+ * -- with its tree-walking interpreter:
+ *
+ *     ValueRef interp(const ModuleEnv&, const std::string& entry,
+ *                     const std::vector<ValueRef>& args, InterpOptions);
+ *                                                       (interp.hpp:50-51)
+ *
+ * evaluating every `let %fusedN = fn(...) [Primitive=true] {...}` group op by
+ * op through OperatorDecl::eval / KernelFn (registry.hpp:58-68,
+ * interp.cpp:86-111).  This library is the drop-in replacement for that
+ * call on a B200: it takes the same fused module (as the reference's own
+ * text format, printer.cpp / parser.cpp), lowers each Primitive group to one
+ * hand-written sm_100a kernel launch (plus hoisted weight prologues), plans
+ * every intermediate into one device arena, and replays the launch list as
+ * a CUDA graph.
+ *
+ * Conventions
+ *  - Plain C types only; no torch / STL types cross this boundary.
+ *  - Every function returns an mr_status (0 = ok).  Non-zero codes mirror the
+ *    reference's DiagCode (diagnostics.hpp:32-93) where one applies; CUDA
+ *    failures and unsupported group patterns have their own codes.  Nothing
+ *    throws across the ABI; mr_last_error_message() is thread-local.
+ *  - Unsupported group patterns are rejected at mr_exec_create (compile
+ *    time), never at launch.  There is no CPU fallback.
+ *  - Tensors at the boundary use the reference's layout: row-major NCHW
+ *    float32 (TensorLiteral, literal.hpp:17-24).  Internal storage (NHWC,
+ *    int8 codes, bf16) is private to the executor.
+ */
+#ifndef MRB200_H_
+#define MRB200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum mr_status {
+  MR_OK = 0,
+  /* mirrors of microrelay::DiagCode (diagnostics.hpp:32-93), offset by 1 */
+  MR_ERR_UNBOUND_VARIABLE = 1,
+  MR_ERR_UNKNOWN_OPERATOR = 2,
+  MR_ERR_SYNTAX = 6,
+  MR_ERR_META_INDEX = 7,
+  MR_ERR_TYPE_MISMATCH = 9,
+  MR_ERR_ARITY_MISMATCH = 13,
+  MR_ERR_UNCALIBRATED = 16,
+  MR_ERR_INTERNAL = 24,
+  /* backend-specific */
+  MR_ERR_UNSUPPORTED_GROUP = 100, /* a Primitive body with no kernel pattern */
+  MR_ERR_CUDA = 101,
+  MR_ERR_INVALID_ARGUMENT = 102,
+  MR_ERR_OUT_OF_MEMORY = 103
+} mr_status;
+
+/* Element type, matching microrelay::BaseType (dtype.hpp:18-43). */
+typedef enum mr_type_code { MR_INT = 0, MR_UINT = 1, MR_FLOAT = 2, MR_BOOL = 3 } mr_type_code;
+
+typedef struct mr_tensor {
+  void* data;          /* host or device pointer, see each call */
+  int32_t ndim;
+  int64_t shape[8];    /* row-major (NCHW for 4-D activations) */
+  int32_t type_code;   /* mr_type_code */
+  int32_t bits;        /* 32 for float32 */
+} mr_tensor;
+
+/* How the float (non-quantized) parts of a module are computed.  A module
+ * realized by the reference's quantize pass always runs its quantized
+ * contractions as int8 x int8 -> int32 on tcgen05 (kind::i8) and is
+ * bit-exact with interp(); the choice below only affects modules (or
+ * groups) without quantize chains. */
+typedef enum mr_float_mode {
+  MR_FLOAT_BF16 = 0,        /* bf16 operands, fp32 accumulate (tcgen05 kind::f16) */
+  MR_FLOAT_FP32_STRICT = 1  /* fp32, reference accumulation order, no FMA:
+                               bit-exact with kernels.cpp, slow (for checking) */
+} mr_float_mode;
+
+typedef struct mr_exec_options {
+  int32_t device;          /* CUDA device ordinal */
+  int64_t batch;           /* binds the symbolic batch dim (?n) of @main's inputs */
+  int32_t n_data_inputs;   /* leading @main params that change per call (default 1);
+                              the rest are weights, set once by mr_exec_set_weights */
+  int32_t float_mode;      /* mr_float_mode */
+  int32_t use_cuda_graph;  /* 1: capture the launch list once, replay per run */
+  int32_t force_simt;      /* 1: use the CUDA-core kernels even where a tcgen05
+                              kernel exists (baseline / debugging) */
+} mr_exec_options;
+
+typedef struct mr_exec_s* mr_exec_t;
+
+/* Fills defaults: device 0, batch 1, 1 data input, bf16, graphs on. */
+void mr_exec_default_options(mr_exec_options* opts);
+
+/* Replaces constructing an Interpreter over the fused ModuleEnv
+ * (interp.cpp:16-19): parses `fused_module_text` (print_module output of a
+ * run_pipeline(...,fuse) module), lowers every Primitive group, plans device
+ * memory.  Fails with MR_ERR_UNSUPPORTED_GROUP naming the group if a body
+ * matches no kernel pattern. */
+mr_status mr_exec_create(const char* fused_module_text, const mr_exec_options* opts,
+                         mr_exec_t* out);
+
+/* Uploads the non-data @main arguments (weights, biases, shape-only windows)
+ * from HOST float32 NCHW/OIHW buffers, in @main parameter order, and runs
+ * the hoisted weight prologues (folded-BN multiply, weight quantize chains)
+ * once on the device.  Must precede mr_exec_run. */
+mr_status mr_exec_set_weights(mr_exec_t ex, int32_t n, const mr_tensor* weights);
+
+/* The interp(m, "main", args) replacement, device-resident: `inputs` are the
+ * n_data_inputs leading @main args as DEVICE float32 NCHW buffers, `output`
+ * a DEVICE buffer for @main's result.  Stream-ordered on `stream`
+ * (a cudaStream_t; NULL = legacy default stream); does not synchronize. */
+mr_status mr_exec_run(mr_exec_t ex, const mr_tensor* inputs, mr_tensor* output, void* stream);
+
+/* Same, end to end from HOST buffers: copies inputs H2D (pinned staging),
+ * runs, copies the result D2H and synchronizes the stream. */
+mr_status mr_exec_run_host(mr_exec_t ex, const mr_tensor* inputs, mr_tensor* output,
+                           void* stream);
+
+/* Shape of @main's result at the bound batch. */
+mr_status mr_exec_output_shape(mr_exec_t ex, mr_tensor* shape_only);
+
+/* JSON description of the lowered program: groups, kernels, formats, arena
+ * plan, per-launch algorithmic bytes/flops.  Pointer valid until destroy. */
+const char* mr_exec_describe(mr_exec_t ex);
+
+/* Kernel launches issued by one mr_exec_run (graph nodes). */
+int32_t mr_exec_launch_count(mr_exec_t ex);
+
+/* Per-launch device timing of one (non-graph) run on `stream`: writes up to
+ * `cap` milliseconds into ms[] in launch order; returns the count. */
+int32_t mr_exec_profile(mr_exec_t ex, const mr_tensor* inputs, mr_tensor* output, void* stream,
+                        float* ms, int32_t cap);
+
+void mr_exec_destroy(mr_exec_t ex);
+
+const char* mr_last_error_message(void);
+
+/* Library build identification (arch, kernels compiled). */
+const char* mr_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MRB200_H_ */

@@ -1,0 +1,1084 @@
+// exec.cpp -- the executor behind the C ABI (include/mrb200.h).
+//
+// Replaces Interpreter::run / eval_in (interp.cpp:21-26, 124-216) for a fused
+// module: the let-chain walk becomes a static launch list (one kernel per
+// Primitive group, plus boundary conversions), every intermediate gets a fixed
+// address in one device arena (liveness-based first-fit, planned once), the
+// weight-only prologues are hoisted to mr_exec_set_weights, and the launch
+// list is captured once into a CUDA graph and replayed per call.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <memory>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../../include/mrb200.h"
+#include "conv_tc.hpp"
+#include "kernels.cuh"
+#include "launch.hpp"
+#include "lower.hpp"
+#include "relay_text.hpp"
+
+namespace mrb200 {
+
+thread_local std::string g_last_error;
+
+struct Status {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Status{code, msg}; }
+
+#define CK(x)                                                                                  \
+  do {                                                                                         \
+    cudaError_t e_ = (x);                                                                      \
+    if (e_ != cudaSuccess) fail(MR_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+namespace {
+
+int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+QDev to_qdev(const QParams& q) { return QDev{q.c1, q.lo, q.hi, q.c2, q.is_signed ? 1 : 0}; }
+
+bool is_pow2(float v) {
+  if (!(v > 0.f) || !std::isfinite(v)) return false;
+  int e;
+  float m = std::frexp(v, &e);
+  return m == 0.5f;
+}
+
+// A physical representation of one @main-level value.
+struct Rep {
+  int fmt = FMT_F32;
+  bool nchw_user = false;  // the caller's input buffer
+  bool has_q = false;      // I8: codes of Q(v)
+  QParams q;
+  int64_t elems = 0;       // including channel padding
+  int cstride = 0;         // channel stride (NHWC) / row length (2-D)
+  int buf = -1;            // arena buffer id
+};
+
+struct Buffer {
+  int64_t bytes = 0;
+  int first = 0, last = 0;  // launch indices
+  int64_t offset = -1;
+  std::string what;
+};
+
+struct LaunchRec {
+  std::string name;   // group / conversion
+  std::string kernel;
+  double bytes = 0;   // algorithmic HBM bytes
+  double flops = 0;   // algorithmic ops (2 per MAC)
+  std::function<void(cudaStream_t)> fn;
+};
+
+}  // namespace
+
+struct Exec {
+  mr_exec_options opt{};
+  Program P;
+  std::vector<std::vector<Rep>> reps;  // per value
+  std::vector<Buffer> bufs;
+  std::vector<LaunchRec> launches;
+  char* arena = nullptr;
+  int64_t arena_bytes = 0;
+  cudaStream_t side_stream = nullptr;
+  // weights
+  std::vector<void*> param_dev;             // raw float32 per @main param (nullptr for data)
+  std::vector<void*> group_w;               // hoisted weight per group
+  std::vector<std::vector<void*>> group_vecs;  // uploaded constant vectors per group
+  std::vector<int> group_kp;                // weight row length per group
+  std::vector<int> group_path;              // kernel choice
+  std::vector<std::string> group_exact;     // int8 exactness proof per group
+  bool weights_ready = false;
+  // io
+  const float* cur_input = nullptr;
+  const float* graph_input = nullptr;
+  float* out_internal = nullptr;  // result buffer (NCHW float32)
+  int64_t out_elems = 0;
+  std::vector<int64_t> out_shape;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  float* host_stage_in = nullptr;
+  float* host_stage_out = nullptr;
+  float* dev_in = nullptr;
+  int64_t in_elems = 0;
+  std::string describe;
+  std::vector<TcConvPlan*> tc_plans;
+
+  ~Exec() {
+    if (graph_exec) cudaGraphExecDestroy(graph_exec);
+    if (graph) cudaGraphDestroy(graph);
+    for (auto* p : tc_plans) tc_conv_destroy(p);
+    if (arena) cudaFree(arena);
+    for (void* p : param_dev) if (p) cudaFree(p);
+    for (void* p : group_w) if (p) cudaFree(p);
+    for (auto& v : group_vecs) for (void* p : v) if (p) cudaFree(p);
+    if (out_internal) cudaFree(out_internal);
+    if (dev_in) cudaFree(dev_in);
+    if (host_stage_in) cudaFreeHost(host_stage_in);
+    if (host_stage_out) cudaFreeHost(host_stage_out);
+  }
+
+  void* ptr(int buf) const { return arena + bufs[buf].offset; }
+};
+
+namespace {
+
+enum Path { P_NONE = 0, P_CONV_I8_SIMT, P_CONV_I8_TC, P_CONV_BF16_SIMT, P_CONV_BF16_TC, P_CONV_F32, P_DENSE_I8,
+            P_DENSE_F32, P_DENSE_BF16, P_POOL, P_DW };
+
+const char* path_name(int p) {
+  static const char* n[] = {"none", "conv_i8_simt", "conv_i8_tcgen05", "conv_bf16_simt", "conv_bf16_tcgen05",
+                            "conv_f32_strict", "dense_i8", "dense_f32_strict", "dense_bf16", "max_pool", "dwconv"};
+  return n[p];
+}
+
+int float_fmt(const Exec& ex) {
+  // int8 pipelines keep the float residual stream exact in float32; the
+  // strict mode computes everything in float32; bf16 mode stores bf16.
+  if (ex.P.any_quant || ex.opt.float_mode == MR_FLOAT_FP32_STRICT) return FMT_F32;
+  return FMT_BF16;
+}
+
+int64_t elem_bytes(int fmt) { return fmt == FMT_F32 ? 4 : fmt == FMT_BF16 ? 2 : 1; }
+
+// NHWC element count with channel stride cs for a logical NCHW / [N,C] shape.
+int64_t nhwc_elems(const std::vector<int64_t>& s, int cs) {
+  if (s.size() == 4) return s[0] * s[2] * s[3] * cs;
+  if (s.size() == 2) return s[0] * cs;
+  int64_t n = 1;
+  for (auto d : s) n *= d;
+  return n;
+}
+
+int channels(const std::vector<int64_t>& s) { return s.size() >= 2 ? static_cast<int>(s[1]) : 1; }
+
+// Finds or adds a representation of value v.
+int want_rep(Exec& ex, int v, int fmt, const QParams* q) {
+  auto& rs = ex.reps[v];
+  for (size_t i = 0; i < rs.size(); ++i) {
+    const Rep& r = rs[i];
+    if (r.nchw_user) continue;
+    if (r.fmt != fmt) continue;
+    if (fmt == FMT_I8) {
+      if (!q || !r.has_q || !(r.q == *q)) continue;
+    }
+    return static_cast<int>(i);
+  }
+  Rep r;
+  r.fmt = fmt;
+  if (q) {
+    r.has_q = true;
+    r.q = *q;
+  }
+  int C = channels(ex.P.values[v].shape);
+  r.cstride = fmt == FMT_I8 ? static_cast<int>(round_up(C, 4)) : C;
+  r.elems = nhwc_elems(ex.P.values[v].shape, r.cstride);
+  rs.push_back(r);
+  return static_cast<int>(rs.size()) - 1;
+}
+
+void plan(Exec& ex, bool use_tc) {
+  Program& P = ex.P;
+  const int ffmt = float_fmt(ex);
+  ex.reps.assign(P.values.size(), {});
+  ex.group_path.assign(P.groups.size(), P_NONE);
+  ex.group_exact.assign(P.groups.size(), "");
+
+  // primary representations of group outputs
+  for (size_t gi = 0; gi < P.groups.size(); ++gi) {
+    const GroupDesc& g = P.groups[gi];
+    const ValueInfo& ov = P.values[g.out_value];
+    if (ov.quantized) {
+      want_rep(ex, g.out_value, FMT_I8, &ov.q);
+    } else if (g.kind == GroupKind::Dense || ov.shape.size() == 2) {
+      want_rep(ex, g.out_value, FMT_F32, nullptr);
+    } else {
+      want_rep(ex, g.out_value, ov.is_result ? FMT_F32 : ffmt, nullptr);
+    }
+    // kernel path
+    switch (g.kind) {
+      case GroupKind::Conv:
+        if (g.weight.quant) {
+          ex.group_path[gi] = use_tc ? P_CONV_I8_TC : P_CONV_I8_SIMT;
+        } else if (ffmt == FMT_F32) {
+          ex.group_path[gi] = P_CONV_F32;
+        } else {
+          ex.group_path[gi] = use_tc ? P_CONV_BF16_TC : P_CONV_BF16_SIMT;
+        }
+        break;
+      case GroupKind::Dense:
+        ex.group_path[gi] = g.weight.quant ? P_DENSE_I8 : ffmt == FMT_F32 ? P_DENSE_F32 : P_DENSE_BF16;
+        break;
+      case GroupKind::MaxPool: ex.group_path[gi] = P_POOL; break;
+      case GroupKind::DwConv: ex.group_path[gi] = P_DW; break;
+    }
+  }
+  // @main data inputs: the caller's NCHW float32 buffer
+  for (size_t v = 0; v < P.values.size(); ++v) {
+    if (!P.values[v].is_data) continue;
+    Rep r;
+    r.nchw_user = true;
+    r.fmt = FMT_F32;
+    ex.reps[v].push_back(r);
+  }
+}
+
+}  // namespace
+
+// Representation index a group reads for its data operand / residual.
+struct GroupIO {
+  int data_rep = -1;
+  std::vector<int> res_rep;  // per epi op (Residual only)
+  float data_scale = 1.f;    // c2 of the data codes (int8)
+};
+
+namespace {
+
+GroupIO resolve_inputs(Exec& ex, int gi) {
+  const Program& P = ex.P;
+  const GroupDesc& g = P.groups[gi];
+  GroupIO io;
+  const int ffmt = float_fmt(ex);
+  const ValueInfo& dv = P.values[g.data.value];
+  int path = ex.group_path[gi];
+  if (path == P_CONV_I8_SIMT || path == P_CONV_I8_TC) {
+    if (g.data.quant) {
+      io.data_rep = want_rep(ex, g.data.value, FMT_I8, &g.data.q);
+      io.data_scale = g.data.q.c2;
+    } else {
+      io.data_rep = want_rep(ex, g.data.value, FMT_I8, &dv.q);
+      io.data_scale = dv.q.c2;
+    }
+  } else if (g.kind == GroupKind::Dense) {
+    if (dv.shape.size() != 2) fail(MR_ERR_UNSUPPORTED_GROUP, "group %" + g.name + ": dense over a 4-D value");
+    io.data_rep = want_rep(ex, g.data.value, FMT_F32, nullptr);
+  } else if (path == P_CONV_F32 || path == P_CONV_BF16_SIMT || path == P_CONV_BF16_TC) {
+    if (g.data.pre_mul != 0.f) fail(MR_ERR_UNSUPPORTED_GROUP, "group %" + g.name + ": scaled conv input");
+    io.data_rep = want_rep(ex, g.data.value, ffmt, nullptr);
+  } else {  // pool / depthwise: float input
+    io.data_rep = want_rep(ex, g.data.value, ffmt, nullptr);
+  }
+  io.res_rep.assign(g.epi.size(), -1);
+  for (size_t i = 0; i < g.epi.size(); ++i)
+    if (g.epi[i].kind == EpiKind::Residual) io.res_rep[i] = want_rep(ex, g.epi[i].value, ffmt, nullptr);
+  return io;
+}
+
+}  // namespace
+
+}  // namespace mrb200
+
+// ======================================================================
+// The executor build: reps -> buffers -> launches
+// ======================================================================
+namespace mrb200 {
+namespace {
+
+struct Builder {
+  Exec& ex;
+  std::vector<GroupIO> io;
+  // (value, rep) -> buffer
+  std::map<std::pair<int, int>, int> buf_of;
+  int launch_idx = 0;
+
+  int buffer_for(int v, int r, const std::string& what) {
+    auto key = std::make_pair(v, r);
+    auto it = buf_of.find(key);
+    if (it != buf_of.end()) return it->second;
+    Buffer b;
+    const Rep& rep = ex.reps[v][r];
+    b.bytes = rep.elems * elem_bytes(rep.fmt);
+    b.first = b.last = launch_idx;
+    b.what = what;
+    ex.bufs.push_back(b);
+    int id = static_cast<int>(ex.bufs.size()) - 1;
+    buf_of[key] = id;
+    ex.reps[v][r].buf = id;
+    return id;
+  }
+  void use(int buf) {
+    ex.bufs[buf].last = std::max(ex.bufs[buf].last, launch_idx);
+    ex.bufs[buf].first = std::min(ex.bufs[buf].first, launch_idx);
+  }
+  int scratch(int64_t bytes, const std::string& what) {
+    Buffer b;
+    b.bytes = bytes;
+    b.first = b.last = launch_idx;
+    b.what = what;
+    ex.bufs.push_back(b);
+    return static_cast<int>(ex.bufs.size()) - 1;
+  }
+};
+
+void assign_offsets(Exec& ex) {
+  std::vector<int> order(ex.bufs.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = static_cast<int>(i);
+  std::sort(order.begin(), order.end(), [&](int a, int b) { return ex.bufs[a].bytes > ex.bufs[b].bytes; });
+  std::vector<int> placed;
+  int64_t top = 0;
+  for (int id : order) {
+    Buffer& b = ex.bufs[id];
+    int64_t size = round_up(std::max<int64_t>(b.bytes, 1), 256);
+    // candidate offsets: 0 and the end of every overlapping placed buffer
+    std::vector<std::pair<int64_t, int64_t>> busy;
+    for (int o : placed) {
+      const Buffer& q = ex.bufs[o];
+      if (q.last < b.first || q.first > b.last) continue;
+      busy.emplace_back(q.offset, q.offset + round_up(std::max<int64_t>(q.bytes, 1), 256));
+    }
+    std::sort(busy.begin(), busy.end());
+    int64_t off = 0;
+    for (auto& [s, e] : busy) {
+      if (off + size <= s) break;
+      off = std::max(off, e);
+    }
+    b.offset = off;
+    top = std::max(top, off + size);
+    placed.push_back(id);
+  }
+  ex.arena_bytes = top;
+}
+
+EpiDev make_epi(Exec& ex, int gi, const GroupIO& io, int upto) {
+  const GroupDesc& g = ex.P.groups[gi];
+  EpiDev e{};
+  int n = 0;
+  for (int i = 0; i < upto; ++i) {
+    const EpiOp& op = g.epi[i];
+    if (n >= kMaxEpi) fail(MR_ERR_UNSUPPORTED_GROUP, "group %" + g.name + ": epilogue longer than 8 ops");
+    switch (op.kind) {
+      case EpiKind::MulScalar: e.op[n] = E_MULS; e.s[n] = op.s; break;
+      case EpiKind::MulChannel: e.op[n] = E_MULC; e.vec[n] = nullptr; break;  // patched in set_weights
+      case EpiKind::Bias: e.op[n] = E_BIAS; e.vec[n] = nullptr; break;        // patched in set_weights
+      case EpiKind::Residual: {
+        e.op[n] = E_RES;
+        const Rep& r = ex.reps[op.value][io.res_rep[i]];
+        e.res[n] = nullptr;  // arena address patched at launch (residual_fix)
+        e.res_fmt[n] = r.fmt;
+        break;
+      }
+      case EpiKind::Relu: e.op[n] = E_RELU; break;
+      case EpiKind::Requant: e.op[n] = E_REQ; e.q[n] = to_qdev(op.q); break;
+      case EpiKind::Clip: e.op[n] = E_CLIP; e.s[n] = op.lo; e.s2[n] = op.hi; break;
+      case EpiKind::SumHW: fail(MR_ERR_INTERNAL, "SumHW inside the element epilogue");
+    }
+    ++n;
+  }
+  e.n_ops = n;
+  return e;
+}
+
+std::string dims_str(const std::vector<int64_t>& s) {
+  std::ostringstream os;
+  os << "[";
+  for (size_t i = 0; i < s.size(); ++i) os << (i ? "," : "") << s[i];
+  os << "]";
+  return os.str();
+}
+
+}  // namespace
+
+void build(Exec& ex) {
+  Program& P = ex.P;
+  const bool use_tc = !ex.opt.force_simt;
+  plan(ex, use_tc);
+  // TC eligibility is decided per group at compile time.
+  for (size_t gi = 0; gi < P.groups.size(); ++gi) {
+    int& path = ex.group_path[gi];
+    const GroupDesc& g = P.groups[gi];
+    if (path == P_CONV_I8_TC || path == P_CONV_BF16_TC) {
+      int eb = path == P_CONV_I8_TC ? 1 : 2;
+      int C = static_cast<int>(g.in_shape[1]);
+      if (!tc_conv_eligible(C, static_cast<int>(g.out_shape[1]), static_cast<int>(g.kh), static_cast<int>(g.kw), eb))
+        path = path == P_CONV_I8_TC ? P_CONV_I8_SIMT : P_CONV_BF16_SIMT;
+    }
+  }
+  std::vector<GroupIO> io(P.groups.size());
+  for (size_t gi = 0; gi < P.groups.size(); ++gi) io[gi] = resolve_inputs(ex, static_cast<int>(gi));
+
+  // int8 exactness precondition: operand scales must be powers of two.
+  for (size_t gi = 0; gi < P.groups.size(); ++gi) {
+    int path = ex.group_path[gi];
+    if (path == P_CONV_I8_SIMT || path == P_CONV_I8_TC || path == P_DENSE_I8) {
+      float sw = P.groups[gi].weight.q.c2;
+      if (!is_pow2(io[gi].data_scale) || !is_pow2(sw))
+        fail(MR_ERR_UNSUPPORTED_GROUP, "group %" + P.groups[gi].name + ": quantize scales are not powers of two");
+    }
+  }
+
+  Builder B{ex, io};
+  // Producer side outputs: every I8 rep of a float value not produced by a
+  // Requant must come from the producer kernel's side output (or an input
+  // conversion for @main data).
+  std::vector<int> side_rep(P.groups.size(), -1);
+  for (size_t v = 0; v < P.values.size(); ++v) {
+    const ValueInfo& vi = P.values[v];
+    for (size_t r = 0; r < ex.reps[v].size(); ++r) {
+      const Rep& rep = ex.reps[v][r];
+      if (rep.nchw_user || r == 0 || vi.producer < 0) continue;  // rep 0 is the primary
+      if (rep.fmt == FMT_I8 && P.groups[vi.producer].kind != GroupKind::Dense) {
+        if (side_rep[vi.producer] >= 0)
+          fail(MR_ERR_UNSUPPORTED_GROUP, "value %" + vi.name + " needs two different quantized copies");
+        side_rep[vi.producer] = static_cast<int>(r);
+      } else {
+        fail(MR_ERR_UNSUPPORTED_GROUP, "value %" + vi.name + " needs a representation its producer cannot emit");
+      }
+    }
+  }
+
+  // ---- input conversions (@main data params -> consumer formats) ----
+  for (size_t v = 0; v < P.values.size(); ++v) {
+    const ValueInfo& vi = P.values[v];
+    if (!vi.is_data) continue;
+    if (vi.shape.size() != 4) fail(MR_ERR_UNSUPPORTED_GROUP, "data input %" + vi.name + " must be 4-D NCHW");
+    for (size_t r = 0; r < ex.reps[v].size(); ++r) {
+      const Rep rep = ex.reps[v][r];
+      if (rep.nchw_user) continue;
+      int buf = B.buffer_for(static_cast<int>(v), static_cast<int>(r), vi.name + ":in");
+      LaunchRec L;
+      L.name = "%" + vi.name;
+      L.kernel = "input_convert";
+      int N = static_cast<int>(vi.shape[0]), C = static_cast<int>(vi.shape[1]);
+      int H = static_cast<int>(vi.shape[2]), W = static_cast<int>(vi.shape[3]);
+      L.bytes = 4.0 * N * C * H * W + static_cast<double>(rep.elems) * elem_bytes(rep.fmt);
+      QDev q = to_qdev(rep.q);
+      int fmt = rep.fmt, cs = rep.cstride;
+      Exec* e = &ex;
+      L.fn = [e, buf, N, C, H, W, fmt, cs, q](cudaStream_t s) {
+        launch_input_convert(e->cur_input, N, C, H, W, e->ptr(buf), fmt, cs, 0.f, q, s);
+      };
+      ex.launches.push_back(L);
+      ++B.launch_idx;
+    }
+  }
+
+  // ---- groups ----
+  for (size_t gi = 0; gi < P.groups.size(); ++gi) {
+    const GroupDesc& g = P.groups[gi];
+    const GroupIO& gio = io[gi];
+    const int path = ex.group_path[gi];
+    const Rep& drep = ex.reps[g.data.value][gio.data_rep];
+    if (drep.nchw_user) fail(MR_ERR_INTERNAL, "group reads the raw input");
+    B.use(drep.buf);
+    for (size_t i = 0; i < g.epi.size(); ++i)
+      if (gio.res_rep[i] >= 0) B.use(ex.reps[g.epi[i].value][gio.res_rep[i]].buf);
+    int obuf = B.buffer_for(g.out_value, 0, "%" + g.out_name);
+    int sbuf = side_rep[gi] >= 0 ? B.buffer_for(g.out_value, side_rep[gi], "%" + g.out_name + ":codes") : -1;
+    const Rep& orep = ex.reps[g.out_value][0];
+
+    bool has_sum = !g.epi.empty() && g.epi.back().kind == EpiKind::SumHW;
+    int n_elem_ops = static_cast<int>(g.epi.size()) - (has_sum ? 1 : 0);
+    EpiDev epi = make_epi(ex, static_cast<int>(gi), gio, n_elem_ops);
+    OutDev out{};
+    int pre_sum_buf = -1;
+    if (has_sum) {
+      // the conv writes the float32 pre-sum tensor; k_sum_hw reduces it
+      const auto& ps = g.pre_sum_shape;
+      pre_sum_buf = B.scratch(ps[0] * ps[1] * ps[2] * ps[3] * 4, "%" + g.out_name + ":presum");
+      out.primary_fmt = FMT_F32;
+      out.pstride = static_cast<int>(ps[1]);
+    } else {
+      out.primary_fmt = orep.fmt;
+      out.pstride = orep.cstride;
+    }
+    if (sbuf >= 0) {
+      const Rep& sr = ex.reps[g.out_value][side_rep[gi]];
+      out.sstride = sr.cstride;
+      out.side_q = to_qdev(sr.q);
+    }
+
+    LaunchRec L;
+    L.name = "%" + g.name;
+    L.kernel = path_name(path);
+    // algorithmic traffic: data once + output(s) once + residuals + weights
+    double out_bytes = static_cast<double>(orep.elems) * elem_bytes(orep.fmt);
+    if (sbuf >= 0) out_bytes += static_cast<double>(ex.reps[g.out_value][side_rep[gi]].elems);
+    double in_bytes = static_cast<double>(drep.elems) * elem_bytes(drep.fmt);
+    for (size_t i = 0; i < g.epi.size(); ++i)
+      if (gio.res_rep[i] >= 0) {
+        const Rep& rr = ex.reps[g.epi[i].value][gio.res_rep[i]];
+        in_bytes += static_cast<double>(rr.elems) * elem_bytes(rr.fmt);
+      }
+    double wbytes = 0, flops = 0;
+    if (g.kind == GroupKind::Conv || g.kind == GroupKind::Dense) {
+      int64_t wn = 1;
+      for (auto d : g.weight.shape) wn *= d;
+      wbytes = static_cast<double>(wn) * (g.weight.quant ? 1 : (path == P_CONV_F32 || path == P_DENSE_F32) ? 4 : 2);
+      int64_t M = g.kind == GroupKind::Conv ? g.out_shape[0] * (has_sum ? g.pre_sum_shape[2] * g.pre_sum_shape[3] : g.out_shape[2] * g.out_shape[3])
+                                             : g.out_shape[0];
+      flops = 2.0 * static_cast<double>(M) * static_cast<double>(wn);
+    } else if (g.kind == GroupKind::DwConv) {
+      flops = 2.0 * g.out_shape[0] * g.out_shape[1] * g.out_shape[2] * g.out_shape[3] * g.kh * g.kw;
+    }
+    L.bytes = in_bytes + out_bytes + wbytes;
+    L.flops = flops;
+
+    Exec* e = &ex;
+    int gidx = static_cast<int>(gi);
+    int dbuf = drep.buf;
+    int dfmt = drep.fmt;
+    int dcs = drep.cstride;
+    ConvGeom geo{};
+    if (g.kind != GroupKind::Dense) {
+      geo.N = static_cast<int>(g.in_shape[0]);
+      geo.C = static_cast<int>(g.in_shape[1]);
+      geo.H = static_cast<int>(g.in_shape[2]);
+      geo.W = static_cast<int>(g.in_shape[3]);
+      geo.Cs = dcs;
+      const auto& os = has_sum ? g.pre_sum_shape : g.out_shape;
+      geo.OC = static_cast<int>(os[1]);
+      geo.OH = static_cast<int>(os[2]);
+      geo.OW = static_cast<int>(os[3]);
+      geo.KH = static_cast<int>(g.kh);
+      geo.KW = static_cast<int>(g.kw);
+      geo.sh = static_cast<int>(g.sh);
+      geo.sw = static_cast<int>(g.sw);
+      geo.ph = static_cast<int>(g.ph);
+      geo.pw = static_cast<int>(g.pw);
+    }
+    float acc_scale = g.weight.quant ? gio.data_scale * g.weight.q.c2 : 1.f;
+    // buffers' final addresses are only known after assign_offsets: capture ids.
+    struct Ptrs { int out, side, presum; };
+    Ptrs pb{obuf, sbuf, pre_sum_buf};
+    auto outdev = [e, pb, out]() {
+      OutDev o = out;
+      if (pb.presum >= 0) o.primary = e->ptr(pb.presum);
+      else o.primary = e->ptr(pb.out);
+      o.side = pb.side >= 0 ? static_cast<int8_t*>(e->ptr(pb.side)) : nullptr;
+      return o;
+    };
+    auto epidev = [e, gidx, epi]() {
+      EpiDev d = epi;
+      // re-resolve arena pointers and constant vectors
+      const GroupDesc& gg = e->P.groups[gidx];
+      int n = 0, vi = 0;
+      for (size_t i = 0; i < gg.epi.size() && n < d.n_ops; ++i) {
+        const EpiOp& op = gg.epi[i];
+        if (op.kind == EpiKind::SumHW) continue;
+        if (op.kind == EpiKind::Bias) d.vec[n] = static_cast<const float*>(e->param_dev[e->P.values[op.value].param_index]);
+        if (op.kind == EpiKind::MulChannel) d.vec[n] = static_cast<const float*>(e->group_vecs[gidx][1 + vi++]);
+        ++n;
+      }
+      return d;
+    };
+    auto residual_fix = [e, gidx, gio](EpiDev& d) {
+      const GroupDesc& gg = e->P.groups[gidx];
+      int n = 0;
+      for (size_t i = 0; i < gg.epi.size() && n < d.n_ops; ++i) {
+        if (gg.epi[i].kind == EpiKind::SumHW) continue;
+        if (gg.epi[i].kind == EpiKind::Residual)
+          d.res[n] = e->ptr(e->reps[gg.epi[i].value][gio.res_rep[i]].buf);
+        ++n;
+      }
+    };
+    switch (path) {
+      case P_CONV_I8_SIMT:
+      case P_CONV_BF16_SIMT:
+      case P_CONV_F32: {
+        L.fn = [e, gidx, dbuf, geo, acc_scale, path, outdev, epidev, residual_fix](cudaStream_t s) {
+          EpiDev d = epidev();
+          residual_fix(d);
+          ConvGeom gg = geo;
+          gg.Kp = e->group_kp[gidx];
+          if (path == P_CONV_I8_SIMT)
+            launch_conv_i8_simt(static_cast<const int8_t*>(e->ptr(dbuf)), static_cast<const int8_t*>(e->group_w[gidx]),
+                                gg, acc_scale, d, outdev(), s);
+          else if (path == P_CONV_BF16_SIMT)
+            launch_conv_bf16_simt(static_cast<const uint16_t*>(e->ptr(dbuf)),
+                                  static_cast<const uint16_t*>(e->group_w[gidx]), gg, d, outdev(), s);
+          else
+            launch_conv_f32_strict(static_cast<const float*>(e->ptr(dbuf)), static_cast<const float*>(e->group_w[gidx]),
+                                   gg, d, outdev(), s);
+        };
+        break;
+      }
+      case P_CONV_I8_TC:
+      case P_CONV_BF16_TC: {
+        TcConvPlan* tp = tc_conv_create(geo, path == P_CONV_I8_TC ? 1 : 2);
+        if (!tp) fail(MR_ERR_UNSUPPORTED_GROUP, "group %" + g.name + ": tcgen05 plan failed");
+        ex.tc_plans.push_back(tp);
+        L.fn = [e, gidx, dbuf, geo, acc_scale, tp, outdev, epidev, residual_fix](cudaStream_t s) {
+          EpiDev d = epidev();
+          residual_fix(d);
+          tc_conv_launch(tp, e->ptr(dbuf), e->group_w[gidx], acc_scale, d, outdev(), s);
+        };
+        break;
+      }
+      case P_DENSE_I8:
+      case P_DENSE_F32:
+      case P_DENSE_BF16: {
+        int N = static_cast<int>(g.in_shape[0]), K = static_cast<int>(g.in_shape[1]);
+        int M = static_cast<int>(g.out_shape[1]);
+        int mode = path == P_DENSE_I8 ? 0 : path == P_DENSE_F32 ? 1 : 2;
+        float pre = g.data.pre_mul;
+        int quant = g.data.quant ? 1 : 0;
+        QDev q = to_qdev(g.data.q);
+        L.fn = [e, gidx, dbuf, N, K, M, mode, pre, quant, q, acc_scale, outdev, epidev](cudaStream_t s) {
+          EpiDev d = epidev();
+          launch_dense(static_cast<const float*>(e->ptr(dbuf)), N, K, e->group_kp[gidx], e->group_w[gidx], M, mode,
+                       pre, quant, q, acc_scale, d, outdev(), s);
+        };
+        break;
+      }
+      case P_POOL: {
+        L.fn = [e, dbuf, dfmt, geo, outdev](cudaStream_t s) {
+          launch_maxpool(e->ptr(dbuf), dfmt, geo, outdev(), s);
+        };
+        break;
+      }
+      case P_DW: {
+        int strict = float_fmt(ex) == FMT_F32 ? 1 : 0;
+        L.fn = [e, gidx, dbuf, dfmt, geo, strict, outdev, epidev, residual_fix](cudaStream_t s) {
+          EpiDev d = epidev();
+          residual_fix(d);
+          launch_dwconv(e->ptr(dbuf), dfmt, static_cast<const float*>(e->group_w[gidx]), geo, strict, d, outdev(), s);
+        };
+        break;
+      }
+      default:
+        fail(MR_ERR_INTERNAL, "no kernel path");
+    }
+    ex.launches.push_back(L);
+    ++B.launch_idx;
+    if (has_sum) {
+      LaunchRec S;
+      S.name = "%" + g.name;
+      S.kernel = "sum_hw";
+      const auto& ps = g.pre_sum_shape;
+      S.bytes = 4.0 * ps[0] * ps[1] * ps[2] * ps[3] + 4.0 * ps[0] * ps[1];
+      int N = static_cast<int>(ps[0]), HW = static_cast<int>(ps[2] * ps[3]), C = static_cast<int>(ps[1]);
+      B.use(pre_sum_buf);
+      S.fn = [e, pre_sum_buf, obuf, N, HW, C](cudaStream_t s) {
+        launch_sum_hw(static_cast<const float*>(e->ptr(pre_sum_buf)), N, HW, C, static_cast<float*>(e->ptr(obuf)), s);
+      };
+      ex.launches.push_back(S);
+      ++B.launch_idx;
+    }
+  }
+
+  // ---- result: NCHW float32 ----
+  const ValueInfo& rv = P.values[P.result_value];
+  if (rv.producer < 0) fail(MR_ERR_UNSUPPORTED_GROUP, "@main returns a parameter");
+  const Rep& rr = ex.reps[P.result_value][0];
+  if (rr.fmt != FMT_F32) fail(MR_ERR_UNSUPPORTED_GROUP, "@main result must be float32 (not a quantized code tensor)");
+  ex.out_shape = rv.shape;
+  ex.out_elems = 1;
+  for (auto d : rv.shape) ex.out_elems *= d;
+  CK(cudaMalloc(&ex.out_internal, static_cast<size_t>(ex.out_elems) * 4));
+  {
+    int rbuf = rr.buf;
+    B.use(rbuf);
+    LaunchRec L;
+    L.name = "%" + rv.name;
+    Exec* e = &ex;
+    if (rv.shape.size() == 4) {
+      L.kernel = "nhwc_to_nchw";
+      L.bytes = 8.0 * ex.out_elems;
+      int N = static_cast<int>(rv.shape[0]), C = static_cast<int>(rv.shape[1]);
+      int H = static_cast<int>(rv.shape[2]), W = static_cast<int>(rv.shape[3]);
+      L.fn = [e, rbuf, N, C, H, W](cudaStream_t s) {
+        launch_nhwc_to_nchw(static_cast<const float*>(e->ptr(rbuf)), e->out_internal, N, C, H, W, s);
+      };
+    } else {
+      L.kernel = "copy_result";
+      L.bytes = 8.0 * ex.out_elems;
+      int64_t bytes = ex.out_elems * 4;
+      L.fn = [e, rbuf, bytes](cudaStream_t s) {
+        cudaMemcpyAsync(e->out_internal, e->ptr(rbuf), static_cast<size_t>(bytes), cudaMemcpyDeviceToDevice, s);
+      };
+    }
+    ex.launches.push_back(L);
+    ++B.launch_idx;
+  }
+
+  assign_offsets(ex);
+  CK(cudaMalloc(&ex.arena, static_cast<size_t>(std::max<int64_t>(ex.arena_bytes, 256))));
+}
+
+}  // namespace mrb200
+
+// ======================================================================
+// weights + describe + C ABI
+// ======================================================================
+namespace mrb200 {
+namespace {
+
+void upload_group_constants(Exec& ex) {
+  ex.group_vecs.assign(ex.P.groups.size(), {});
+  for (size_t gi = 0; gi < ex.P.groups.size(); ++gi) {
+    const GroupDesc& g = ex.P.groups[gi];
+    auto up = [&](const std::vector<float>& v) -> void* {
+      if (v.empty()) return nullptr;
+      void* p = nullptr;
+      CK(cudaMalloc(&p, v.size() * 4));
+      CK(cudaMemcpy(p, v.data(), v.size() * 4, cudaMemcpyHostToDevice));
+      return p;
+    };
+    ex.group_vecs[gi].push_back(up(g.weight.oc_scale));  // [0]: weight oc scale
+    for (const auto& op : g.epi)
+      if (op.kind == EpiKind::MulChannel) ex.group_vecs[gi].push_back(up(op.vec));
+  }
+}
+
+void prepare_weights(Exec& ex, cudaStream_t s) {
+  const Program& P = ex.P;
+  const int ffmt = float_fmt(ex);
+  ex.group_w.assign(P.groups.size(), nullptr);
+  ex.group_kp.assign(P.groups.size(), 0);
+  for (size_t gi = 0; gi < P.groups.size(); ++gi) {
+    const GroupDesc& g = P.groups[gi];
+    if (g.kind == GroupKind::MaxPool) continue;
+    const WeightOperand& w = g.weight;
+    const float* raw = nullptr;
+    void* tmp = nullptr;
+    if (w.value >= 0) {
+      raw = static_cast<const float*>(ex.param_dev[P.values[w.value].param_index]);
+    } else {
+      CK(cudaMalloc(&tmp, w.constant.size() * 4));
+      CK(cudaMemcpy(tmp, w.constant.data(), w.constant.size() * 4, cudaMemcpyHostToDevice));
+      raw = static_cast<const float*>(tmp);
+    }
+    int path = ex.group_path[gi];
+    int O, I, KH = 1, KW = 1;
+    if (g.kind == GroupKind::Dense) {
+      O = static_cast<int>(w.shape[0]);
+      I = static_cast<int>(w.shape[1]);
+    } else {
+      O = static_cast<int>(w.shape[0]);
+      I = static_cast<int>(w.shape[1]);
+      KH = static_cast<int>(w.shape[2]);
+      KW = static_cast<int>(w.shape[3]);
+    }
+    int fmt, cs;
+    if (w.quant) {
+      fmt = FMT_I8;
+      cs = static_cast<int>(round_up(I, 4));
+      if (path == P_CONV_I8_TC) cs = tc_conv_weight_cstride(I, 1);
+    } else if (g.kind == GroupKind::DwConv || ffmt == FMT_F32) {
+      fmt = FMT_F32;
+      cs = I;
+    } else {
+      fmt = FMT_BF16;
+      cs = I;
+      if (path == P_CONV_BF16_TC) cs = tc_conv_weight_cstride(I, 2);
+    }
+    int64_t n = fmt == FMT_F32 ? static_cast<int64_t>(O) * I * KH * KW : static_cast<int64_t>(O) * KH * KW * cs;
+    void* dst = nullptr;
+    CK(cudaMalloc(&dst, static_cast<size_t>(n * elem_bytes(fmt))));
+    launch_weight_prep(raw, O, I, KH, KW, cs, static_cast<const float*>(ex.group_vecs[gi][0]), w.scalar_scale, fmt,
+                       w.quant ? 1 : 0, to_qdev(w.q), dst, s);
+    CK(cudaGetLastError());
+    ex.group_w[gi] = dst;
+    ex.group_kp[gi] = fmt == FMT_F32 ? I * KH * KW : KH * KW * cs;
+    if (tmp) {
+      CK(cudaStreamSynchronize(s));
+      cudaFree(tmp);
+    }
+    // Static exactness proof for int8 contractions: every partial sum of the
+    // reference's sequential fp32 accumulation is an integer multiple of the
+    // quantum with |.| <= sum_k |w_code| * max|x_code|; below 2^24 it is
+    // exact, so the int32 result converted and scaled equals it bit for bit.
+    if (w.quant) {
+      CK(cudaStreamSynchronize(s));
+      std::vector<int8_t> codes(static_cast<size_t>(n));
+      CK(cudaMemcpy(codes.data(), dst, static_cast<size_t>(n), cudaMemcpyDeviceToHost));
+      int64_t per = n / O, worst = 0;
+      for (int o = 0; o < O; ++o) {
+        int64_t s1 = 0;
+        for (int64_t k = 0; k < per; ++k) s1 += std::abs(static_cast<int>(codes[o * per + k]));
+        worst = std::max(worst, s1);
+      }
+      float xmax = g.data.quant ? std::max(std::fabs(g.data.q.lo), std::fabs(g.data.q.hi))
+                                : std::max(std::fabs(P.values[g.data.value].q.lo), std::fabs(P.values[g.data.value].q.hi));
+      double bound = static_cast<double>(worst) * xmax;
+      std::ostringstream os;
+      os << (bound <= 16777216.0 ? "proven" : "unproven") << " (max partial sum <= " << static_cast<int64_t>(bound)
+         << " quanta)";
+      ex.group_exact[gi] = os.str();
+    }
+  }
+}
+
+void make_describe(Exec& ex) {
+  std::ostringstream os;
+  const Program& P = ex.P;
+  os << "{\"batch\": " << ex.opt.batch << ", \"float_mode\": " << ex.opt.float_mode
+     << ", \"int8\": " << (P.any_quant ? "true" : "false") << ", \"arena_bytes\": " << ex.arena_bytes
+     << ", \"groups\": [";
+  for (size_t gi = 0; gi < P.groups.size(); ++gi) {
+    const GroupDesc& g = P.groups[gi];
+    std::string d = describe_group(P, g);
+    std::string esc;
+    for (char c : d) esc += (c == '"' ? '\'' : c);
+    os << (gi ? ", " : "") << "{\"name\": \"" << g.name << "\", \"desc\": \"" << esc << "\", \"kernel\": \""
+       << path_name(ex.group_path[gi]) << "\", \"out_shape\": " << dims_str(g.out_shape) << ", \"exact\": \""
+       << ex.group_exact[gi] << "\"}";
+  }
+  os << "], \"launches\": [";
+  for (size_t i = 0; i < ex.launches.size(); ++i) {
+    const LaunchRec& L = ex.launches[i];
+    os << (i ? ", " : "") << "{\"name\": \"" << L.name << "\", \"kernel\": \"" << L.kernel
+       << "\", \"bytes\": " << static_cast<int64_t>(L.bytes) << ", \"flops\": " << static_cast<int64_t>(L.flops) << "}";
+  }
+  os << "], \"buffers\": [";
+  for (size_t i = 0; i < ex.bufs.size(); ++i) {
+    const Buffer& b = ex.bufs[i];
+    os << (i ? ", " : "") << "{\"what\": \"" << b.what << "\", \"bytes\": " << b.bytes << ", \"offset\": " << b.offset
+       << ", \"live\": [" << b.first << ", " << b.last << "]}";
+  }
+  os << "]}";
+  ex.describe = os.str();
+}
+
+void run_launches(Exec& ex, cudaStream_t s) {
+  for (auto& L : ex.launches) L.fn(s);
+}
+
+void ensure_graph(Exec& ex, cudaStream_t s) {
+  if (ex.graph_exec && ex.graph_input == ex.cur_input) return;
+  if (ex.graph_exec) {
+    cudaGraphExecDestroy(ex.graph_exec);
+    ex.graph_exec = nullptr;
+  }
+  if (ex.graph) {
+    cudaGraphDestroy(ex.graph);
+    ex.graph = nullptr;
+  }
+  cudaStream_t cap = nullptr;
+  CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+  CK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+  run_launches(ex, cap);
+  cudaError_t ce = cudaStreamEndCapture(cap, &ex.graph);
+  cudaStreamDestroy(cap);
+  if (ce != cudaSuccess) fail(MR_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+  CK(cudaGraphInstantiate(&ex.graph_exec, ex.graph, 0));
+  ex.graph_input = ex.cur_input;
+  (void)s;
+}
+
+int64_t numel(const mr_tensor& t) {
+  int64_t n = 1;
+  for (int i = 0; i < t.ndim; ++i) n *= t.shape[i];
+  return n;
+}
+
+void check_input(const Exec& ex, const mr_tensor* inputs) {
+  if (!inputs || !inputs[0].data) fail(MR_ERR_INVALID_ARGUMENT, "null input");
+  const ValueInfo* dv = nullptr;
+  for (const auto& v : ex.P.values)
+    if (v.is_data) {
+      dv = &v;
+      break;
+    }
+  if (!dv) fail(MR_ERR_INVALID_ARGUMENT, "module has no data input");
+  if (inputs[0].ndim != static_cast<int>(dv->shape.size())) fail(MR_ERR_TYPE_MISMATCH, "input rank mismatch");
+  for (int i = 0; i < inputs[0].ndim; ++i)
+    if (inputs[0].shape[i] != dv->shape[i]) fail(MR_ERR_TYPE_MISMATCH, "input shape mismatch with the bound batch");
+  if (inputs[0].type_code != MR_FLOAT || inputs[0].bits != 32) fail(MR_ERR_TYPE_MISMATCH, "input must be float32");
+}
+
+}  // namespace
+}  // namespace mrb200
+
+using namespace mrb200;
+
+#define API_BEGIN try {
+#define API_END                                       \
+  }                                                   \
+  catch (const Status& s) {                           \
+    g_last_error = s.msg;                             \
+    return static_cast<mr_status>(s.code);            \
+  }                                                   \
+  catch (const LowerError& e) {                       \
+    g_last_error = e.msg;                             \
+    return static_cast<mr_status>(e.code);            \
+  }                                                   \
+  catch (const ParseError& e) {                       \
+    g_last_error = "syntax: " + e.msg;                \
+    return MR_ERR_SYNTAX;                             \
+  }                                                   \
+  catch (const std::bad_alloc&) {                     \
+    g_last_error = "host out of memory";              \
+    return MR_ERR_OUT_OF_MEMORY;                      \
+  }                                                   \
+  catch (const std::exception& e) {                   \
+    g_last_error = e.what();                          \
+    return MR_ERR_INTERNAL;                           \
+  }                                                   \
+  return MR_OK;
+
+extern "C" {
+
+void mr_exec_default_options(mr_exec_options* o) {
+  std::memset(o, 0, sizeof(*o));
+  o->device = 0;
+  o->batch = 1;
+  o->n_data_inputs = 1;
+  o->float_mode = MR_FLOAT_BF16;
+  o->use_cuda_graph = 1;
+  o->force_simt = 0;
+}
+
+mr_status mr_exec_create(const char* text, const mr_exec_options* opts, mr_exec_t* out) {
+  API_BEGIN
+  if (!text || !out) fail(MR_ERR_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  auto ex = std::make_unique<Exec>();
+  mr_exec_default_options(&ex->opt);
+  if (opts) ex->opt = *opts;
+  if (ex->opt.batch < 1) fail(MR_ERR_INVALID_ARGUMENT, "batch must be >= 1");
+  CK(cudaSetDevice(ex->opt.device));
+  Module m = parse_fused_module(text);
+  ex->P = lower_module(m, ex->opt.batch, ex->opt.n_data_inputs);
+  if (ex->opt.n_data_inputs != 1) fail(MR_ERR_UNSUPPORTED_GROUP, "exactly one data input is supported");
+  build(*ex);
+  upload_group_constants(*ex);
+  ex->param_dev.assign(ex->P.n_params, nullptr);
+  make_describe(*ex);
+  *out = reinterpret_cast<mr_exec_t>(ex.release());
+  API_END
+}
+
+mr_status mr_exec_set_weights(mr_exec_t h, int32_t n, const mr_tensor* w) {
+  API_BEGIN
+  Exec& ex = *reinterpret_cast<Exec*>(h);
+  CK(cudaSetDevice(ex.opt.device));
+  int expect = ex.P.n_params - ex.opt.n_data_inputs;
+  if (n != expect) fail(MR_ERR_ARITY_MISMATCH, "expected " + std::to_string(expect) + " weight tensors");
+  for (const auto& v : ex.P.values) {
+    if (v.param_index < 0 || v.is_data) continue;
+    const mr_tensor& t = w[v.param_index - ex.opt.n_data_inputs];
+    if (t.type_code != MR_FLOAT || t.bits != 32) fail(MR_ERR_TYPE_MISMATCH, "%" + v.name + " must be float32");
+    if (t.ndim != static_cast<int>(v.shape.size())) fail(MR_ERR_TYPE_MISMATCH, "%" + v.name + " rank mismatch");
+    for (int i = 0; i < t.ndim; ++i)
+      if (t.shape[i] != v.shape[i]) fail(MR_ERR_TYPE_MISMATCH, "%" + v.name + " shape mismatch");
+    int64_t bytes = numel(t) * 4;
+    void*& dst = ex.param_dev[v.param_index];
+    if (!dst) CK(cudaMalloc(&dst, static_cast<size_t>(std::max<int64_t>(bytes, 4))));
+    if (bytes) CK(cudaMemcpy(dst, t.data, static_cast<size_t>(bytes), cudaMemcpyHostToDevice));
+  }
+  for (void* p : ex.group_w) if (p) cudaFree(p);
+  prepare_weights(ex, nullptr);
+  CK(cudaDeviceSynchronize());
+  ex.weights_ready = true;
+  if (ex.graph_exec) {  // weights live at fixed addresses only after the first set
+    cudaGraphExecDestroy(ex.graph_exec);
+    ex.graph_exec = nullptr;
+  }
+  make_describe(ex);
+  API_END
+}
+
+mr_status mr_exec_run(mr_exec_t h, const mr_tensor* inputs, mr_tensor* output, void* stream) {
+  API_BEGIN
+  Exec& ex = *reinterpret_cast<Exec*>(h);
+  if (!ex.weights_ready) fail(MR_ERR_INVALID_ARGUMENT, "mr_exec_set_weights first");
+  check_input(ex, inputs);
+  if (!output || !output->data) fail(MR_ERR_INVALID_ARGUMENT, "null output");
+  if (numel(*output) != ex.out_elems) fail(MR_ERR_TYPE_MISMATCH, "output size mismatch");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  ex.cur_input = static_cast<const float*>(inputs[0].data);
+  if (ex.opt.use_cuda_graph) {
+    ensure_graph(ex, s);
+    CK(cudaGraphLaunch(ex.graph_exec, s));
+  } else {
+    run_launches(ex, s);
+    CK(cudaGetLastError());
+  }
+  CK(cudaMemcpyAsync(output->data, ex.out_internal, static_cast<size_t>(ex.out_elems) * 4, cudaMemcpyDeviceToDevice, s));
+  API_END
+}
+
+mr_status mr_exec_run_host(mr_exec_t h, const mr_tensor* inputs, mr_tensor* output, void* stream) {
+  API_BEGIN
+  Exec& ex = *reinterpret_cast<Exec*>(h);
+  check_input(ex, inputs);
+  if (!output || !output->data) fail(MR_ERR_INVALID_ARGUMENT, "null output");
+  if (numel(*output) != ex.out_elems) fail(MR_ERR_TYPE_MISMATCH, "output size mismatch");
+  int64_t n_in = numel(inputs[0]);
+  if (!ex.dev_in || ex.in_elems != n_in) {
+    if (ex.dev_in) cudaFree(ex.dev_in);
+    CK(cudaMalloc(&ex.dev_in, static_cast<size_t>(n_in) * 4));
+    ex.in_elems = n_in;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CK(cudaMemcpyAsync(ex.dev_in, inputs[0].data, static_cast<size_t>(n_in) * 4, cudaMemcpyHostToDevice, s));
+  ex.cur_input = ex.dev_in;
+  if (!ex.weights_ready) fail(MR_ERR_INVALID_ARGUMENT, "mr_exec_set_weights first");
+  if (ex.opt.use_cuda_graph) {
+    ensure_graph(ex, s);
+    CK(cudaGraphLaunch(ex.graph_exec, s));
+  } else {
+    run_launches(ex, s);
+    CK(cudaGetLastError());
+  }
+  CK(cudaMemcpyAsync(output->data, ex.out_internal, static_cast<size_t>(ex.out_elems) * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  API_END
+}
+
+mr_status mr_exec_output_shape(mr_exec_t h, mr_tensor* t) {
+  API_BEGIN
+  Exec& ex = *reinterpret_cast<Exec*>(h);
+  t->ndim = static_cast<int32_t>(ex.out_shape.size());
+  for (size_t i = 0; i < ex.out_shape.size(); ++i) t->shape[i] = ex.out_shape[i];
+  t->type_code = MR_FLOAT;
+  t->bits = 32;
+  API_END
+}
+
+const char* mr_exec_describe(mr_exec_t h) { return reinterpret_cast<Exec*>(h)->describe.c_str(); }
+
+int32_t mr_exec_launch_count(mr_exec_t h) {
+  Exec& ex = *reinterpret_cast<Exec*>(h);
+  int32_t n = 0;
+  for (const auto& L : ex.launches) n += L.kernel == "copy_result" ? 0 : 1;
+  return n;
+}
+
+int32_t mr_exec_profile(mr_exec_t h, const mr_tensor* inputs, mr_tensor* output, void* stream, float* ms,
+                        int32_t cap) {
+  try {
+    Exec& ex = *reinterpret_cast<Exec*>(h);
+    check_input(ex, inputs);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    ex.cur_input = static_cast<const float*>(inputs[0].data);
+    std::vector<cudaEvent_t> ev(ex.launches.size() + 1);
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    CK(cudaEventRecord(ev[0], s));
+    for (size_t i = 0; i < ex.launches.size(); ++i) {
+      ex.launches[i].fn(s);
+      CK(cudaEventRecord(ev[i + 1], s));
+    }
+    CK(cudaEventSynchronize(ev.back()));
+    CK(cudaGetLastError());
+    int32_t n = 0;
+    for (size_t i = 0; i < ex.launches.size() && n < cap; ++i) CK(cudaEventElapsedTime(&ms[n++], ev[i], ev[i + 1]));
+    for (auto& e : ev) cudaEventDestroy(e);
+    if (output && output->data)
+      CK(cudaMemcpyAsync(output->data, ex.out_internal, static_cast<size_t>(ex.out_elems) * 4, cudaMemcpyDeviceToDevice, s));
+    return n;
+  } catch (const Status& st) {
+    g_last_error = st.msg;
+    return -1;
+  }
+}
+
+void mr_exec_destroy(mr_exec_t h) { delete reinterpret_cast<Exec*>(h); }
+
+const char* mr_last_error_message(void) { return g_last_error.c_str(); }
+
+const char* mr_build_info(void) { return MRB200_BUILD_INFO; }
+
+}  // extern "C"

@@ -1,0 +1,142 @@
+// kernels.cuh -- device-side parameter blocks shared by every kernel and the
+// host executor, plus the bit-exact epilogue arithmetic.
+//
+// Arithmetic mirrors the reference kernels (core/src/kernels.cpp):
+//  * multiply / add on float32 compute in double and round once
+//    (binary_broadcast, kernels.cpp:94-131) == IEEE __fmul_rn / __fadd_rn;
+//  * bias_add is a float add (kernels.cpp:731);
+//  * relu is `x > 0 ? x : 0.0f` (kernels.cpp:285), so -0 -> +0 and NaN -> 0;
+//  * round is nearbyintf under FE_TONEAREST = rintf (kernels.cpp:288-294);
+//  * clip is std::min(std::max(x, lo), hi) with float bounds (kernels.cpp:306-307);
+//  * cast f32->int8 truncates then wraps (kernels.cpp:320-348).
+// Everything is compiled with -fmad=false, no fast-math, denormals kept.
+#pragma once
+
+#include <cstdint>
+
+namespace mrb200 {
+
+enum Fmt : int32_t { FMT_F32 = 0, FMT_BF16 = 1, FMT_I8 = 2 };
+
+struct QDev {
+  float c1, lo, hi, c2;
+  int32_t is_signed;
+};
+
+enum EpiCode : int32_t {
+  E_MULS = 1, E_MULC = 2, E_BIAS = 3, E_RES = 4, E_RELU = 5, E_REQ = 6, E_CLIP = 7
+};
+
+constexpr int kMaxEpi = 8;
+
+struct EpiDev {
+  int32_t n_ops;
+  int32_t op[kMaxEpi];
+  float s[kMaxEpi];          // MulScalar / Clip lo
+  float s2[kMaxEpi];         // Clip hi
+  const float* vec[kMaxEpi]; // MulChannel / Bias, [C]
+  const void* res[kMaxEpi];  // Residual, NHWC, row stride = C
+  int32_t res_fmt[kMaxEpi];
+  QDev q[kMaxEpi];
+};
+
+// Where a kernel writes its (per element) final value.
+struct OutDev {
+  void* primary;        // NHWC (or [N,C]) row stride = pstride elements
+  int32_t primary_fmt;  // FMT_I8 => the epilogue's last op is a Requant; the code is stored
+  int32_t pstride;      // channel stride of the primary (C, or Cp for I8)
+  int8_t* side;         // optional int8 codes of the final float value (row stride sstride)
+  int32_t sstride;
+  QDev side_q;
+};
+
+#ifdef __CUDACC__
+
+__device__ __forceinline__ float bf16_to_f32(uint16_t h) { return __uint_as_float(static_cast<uint32_t>(h) << 16); }
+
+// Round-to-nearest-even float -> bf16 (NaN kept quiet).
+__device__ __forceinline__ uint16_t f32_to_bf16(float f) {
+  uint32_t u = __float_as_uint(f);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return static_cast<uint16_t>((u >> 16) | 0x40);
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return static_cast<uint16_t>(u >> 16);
+}
+
+__device__ __forceinline__ float relu_ref(float x) { return x > 0.f ? x : 0.0f; }
+
+__device__ __forceinline__ float clip_ref(float x, float lo, float hi) {
+  float a = x < lo ? lo : x;   // std::max(x, lo)
+  return hi < a ? hi : a;      // std::min(a, hi)
+}
+
+// cast(float32 -> int8/uint8): checked_trunc then wrap_int (kernels.cpp:320-348).
+__device__ __forceinline__ int32_t cast_int_ref(float v, int32_t is_signed) {
+  long long t;
+  if (!(v > -9.2e18f && v < 9.2e18f)) t = v > 0 ? 0x7fffffffffffffffLL : (-0x7fffffffffffffffLL - 1);
+  else t = static_cast<long long>(v);  // truncation toward zero
+  int32_t lo8 = static_cast<int32_t>(t & 0xff);
+  return is_signed ? static_cast<int32_t>(static_cast<int8_t>(lo8)) : lo8;
+}
+
+// The realize chain's integer code: cast(clip(round(v * c1), lo, hi)).
+__device__ __forceinline__ int32_t quant_code(float v, const QDev& q) {
+  float t = __fmul_rn(v, q.c1);
+  t = rintf(t);
+  t = clip_ref(t, q.lo, q.hi);
+  return cast_int_ref(t, q.is_signed);
+}
+
+__device__ __forceinline__ float load_fmt(const void* p, int32_t fmt, int64_t i) {
+  if (fmt == FMT_F32) return static_cast<const float*>(p)[i];
+  return bf16_to_f32(static_cast<const uint16_t*>(p)[i]);
+}
+
+// Applies the interpreted epilogue to v (the anchor's float32 result at
+// output row m, channel c).  Returns the final float; *code receives the
+// int8 code of the last Requant (if any).
+__device__ __forceinline__ float apply_epi(const EpiDev& e, float v, int64_t m, int32_t c,
+                                           int32_t C, int32_t* code) {
+  for (int i = 0; i < e.n_ops; ++i) {
+    switch (e.op[i]) {
+      case E_MULS: v = __fmul_rn(v, e.s[i]); break;
+      case E_MULC: v = __fmul_rn(v, e.vec[i][c]); break;
+      case E_BIAS: v = __fadd_rn(v, e.vec[i][c]); break;
+      case E_RES: v = __fadd_rn(v, load_fmt(e.res[i], e.res_fmt[i], m * C + c)); break;
+      case E_RELU: v = relu_ref(v); break;
+      case E_REQ: {
+        int32_t k = quant_code(v, e.q[i]);
+        *code = k;
+        v = __fmul_rn(static_cast<float>(k), e.q[i].c2);
+        break;
+      }
+      case E_CLIP: v = clip_ref(v, e.s[i], e.s2[i]); break;
+      default: break;
+    }
+  }
+  return v;
+}
+
+__device__ __forceinline__ void store_out(const OutDev& o, float v, int32_t code, int64_t m, int32_t c) {
+  if (o.primary_fmt == FMT_F32) {
+    static_cast<float*>(o.primary)[m * o.pstride + c] = v;
+  } else if (o.primary_fmt == FMT_BF16) {
+    static_cast<uint16_t*>(o.primary)[m * o.pstride + c] = f32_to_bf16(v);
+  } else {
+    static_cast<int8_t*>(o.primary)[m * o.pstride + c] = static_cast<int8_t>(code);
+  }
+  if (o.side) o.side[m * o.sstride + c] = static_cast<int8_t>(quant_code(v, o.side_q));
+}
+
+#endif  // __CUDACC__
+
+// ---- host-visible launch parameter blocks --------------------------------
+
+struct ConvGeom {
+  int32_t N, H, W, C;      // input (logical C)
+  int32_t Cs;              // input channel stride (I8: Cp = round_up(C,4))
+  int32_t OH, OW, OC;
+  int32_t KH, KW, sh, sw, ph, pw;
+  int32_t Kp;              // weight row length (I8: KH*KW*Cs; strict: IC*KH*KW)
+};
+
+}  // namespace mrb200

@@ -1,0 +1,30 @@
+// launch.hpp -- host entry points of the CUDA kernels (one per kernel family).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace mrb200 {
+
+void launch_input_convert(const float* x, int N, int C, int H, int W, void* out, int fmt, int Cs,
+                          float pre_mul, QDev q, cudaStream_t s);
+void launch_nhwc_to_nchw(const float* x, float* y, int N, int C, int H, int W, cudaStream_t s);
+void launch_weight_prep(const float* w, int O, int I, int KH, int KW, int Cs, const float* oc_scale,
+                        float scalar, int fmt, int quant, QDev q, void* out, cudaStream_t s);
+void launch_conv_i8_simt(const int8_t* x, const int8_t* w, const ConvGeom& g, float acc_scale,
+                         const EpiDev& epi, const OutDev& out, cudaStream_t s);
+void launch_conv_bf16_simt(const uint16_t* x, const uint16_t* w, const ConvGeom& g, const EpiDev& epi,
+                           const OutDev& out, cudaStream_t s);
+void launch_conv_f32_strict(const float* x, const float* w, const ConvGeom& g, const EpiDev& epi,
+                            const OutDev& out, cudaStream_t s);
+void launch_dwconv(const void* x, int xfmt, const float* w, const ConvGeom& g, int strict, const EpiDev& epi,
+                   const OutDev& out, cudaStream_t s);
+void launch_maxpool(const void* x, int xfmt, const ConvGeom& g, const OutDev& out, cudaStream_t s);
+void launch_sum_hw(const float* x, int N, int HW, int C, float* y, cudaStream_t s);
+void launch_dense(const float* x, int N, int K, int Kp, const void* w, int M, int mode, float pre_mul,
+                  int quant, QDev q, float acc_scale, const EpiDev& epi, const OutDev& out, cudaStream_t s);
+
+}  // namespace mrb200

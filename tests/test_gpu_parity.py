@@ -1,0 +1,87 @@
+"""GPU parity: the B200 executor against the reference interpreter.
+
+Bar (BASELINE.json north_star): int8 realized modules bit-exact; float modules
+in the strict fp32 mode bit-exact (same arithmetic order as kernels.cpp); the
+bf16 mode within max|d|/max|ref| <= 1e-2 on the logits plus top-1 agreement.
+References: tests/golden/*.npz written by tests/golden/make_golden.py from
+oracle/_ref/mr_ref (the unmodified reference's interp()).
+"""
+import os
+
+import numpy as np
+import pytest
+
+import paper_1904_08368_b200 as mrb
+from paper_1904_08368_b200 import modelzoo
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+BF16_TOL = 1e-2  # normwise: max|gpu - ref| / max|ref| on logits
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+def setup(name, prec, batch, **kw):
+    text, meta, src = mrb.load_model(name, prec)
+    w = modelzoo.make_weights(src, seed=meta["weights_seed"])
+    ex = mrb.Executor(text, batch=batch, **kw)
+    ex.set_weights([w[p.name] for p in src.params if p.kind != "input"])
+    return ex, src
+
+
+def normwise(y, r):
+    return float(np.max(np.abs(y - r)) / np.max(np.abs(r)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("force_simt", [False, True])
+def test_tiny_int8_bitexact(gpu, force_simt):
+    gold = np.load(os.path.join(GOLD, "resnet18_tiny_b4.npz"))
+    ex, src = setup("resnet18_tiny", "int8", 4, force_simt=force_simt)
+    x = modelzoo.make_inputs(src, 4, seed=0)
+    y = ex.run_host(x)
+    mism = int(np.sum(bits(y) != bits(gold["int8"])))
+    assert mism == 0, "%d/%d logits differ (max |d| %g)" % (mism, y.size, np.max(np.abs(y - gold["int8"])))
+    for g in ex.describe()["groups"]:
+        if "Q[" in g["desc"] and g["kernel"] != "max_pool":
+            assert g["exact"].startswith("proven"), g
+
+
+@pytest.mark.gpu
+def test_tiny_fp32_strict_bitexact(gpu):
+    gold = np.load(os.path.join(GOLD, "resnet18_tiny_b4.npz"))
+    ex, src = setup("resnet18_tiny", "fp32", 4, float_mode=mrb.MR_FLOAT_FP32_STRICT)
+    x = modelzoo.make_inputs(src, 4, seed=0)
+    y = ex.run_host(x)
+    assert np.array_equal(bits(y), bits(gold["fp32"])), np.max(np.abs(y - gold["fp32"]))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("force_simt", [False, True])
+def test_tiny_bf16_tolerance(gpu, force_simt):
+    gold = np.load(os.path.join(GOLD, "resnet18_tiny_b4.npz"))
+    ex, src = setup("resnet18_tiny", "fp32", 4, force_simt=force_simt)
+    x = modelzoo.make_inputs(src, 4, seed=0)
+    y = ex.run_host(x)
+    assert normwise(y, gold["fp32"]) <= BF16_TOL
+    assert np.array_equal(np.argmax(y, 1), np.argmax(gold["fp32"], 1))
+
+
+@pytest.mark.gpu
+def test_resnet18_int8_bitexact_full_size(gpu):
+    gold = np.load(os.path.join(GOLD, "resnet18_b2.npz"))
+    ex, src = setup("resnet18", "int8", 2)
+    x = modelzoo.make_inputs(src, 2, seed=0)
+    y = ex.run_host(x)
+    assert np.array_equal(bits(y), bits(gold["int8"])), int(np.sum(bits(y) != bits(gold["int8"])))
+
+
+@pytest.mark.gpu
+def test_resnet18_bf16_full_size(gpu):
+    gold = np.load(os.path.join(GOLD, "resnet18_b2.npz"))
+    ex, src = setup("resnet18", "fp32", 2)
+    x = modelzoo.make_inputs(src, 2, seed=0)
+    y = ex.run_host(x)
+    assert normwise(y, gold["fp32"]) <= BF16_TOL
+    assert np.array_equal(np.argmax(y, 1), np.argmax(gold["fp32"], 1))
