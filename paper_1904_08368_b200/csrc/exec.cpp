@@ -263,6 +263,8 @@ GroupIO resolve_inputs(Exec& ex, int gi) {
   } else if (g.kind == GroupKind::Dense) {
     if (dv.shape.size() != 2) fail(MR_ERR_UNSUPPORTED_GROUP, "group %" + g.name + ": dense over a 4-D value");
     io.data_rep = want_rep(ex, g.data.value, FMT_F32, nullptr);
+    if (g.data.quant) io.data_scale = g.data.q.c2;
+    else if (dv.quantized) fail(MR_ERR_UNSUPPORTED_GROUP, "group %" + g.name + ": dense over a coded value");
   } else if (path == P_CONV_F32 || path == P_CONV_BF16_SIMT || path == P_CONV_BF16_TC) {
     if (g.data.pre_mul != 0.f) fail(MR_ERR_UNSUPPORTED_GROUP, "group %" + g.name + ": scaled conv input");
     io.data_rep = want_rep(ex, g.data.value, ffmt, nullptr);
@@ -671,33 +673,28 @@ void build(Exec& ex) {
   const ValueInfo& rv = P.values[P.result_value];
   if (rv.producer < 0) fail(MR_ERR_UNSUPPORTED_GROUP, "@main returns a parameter");
   const Rep& rr = ex.reps[P.result_value][0];
-  if (rr.fmt != FMT_F32) fail(MR_ERR_UNSUPPORTED_GROUP, "@main result must be float32 (not a quantized code tensor)");
   ex.out_shape = rv.shape;
   ex.out_elems = 1;
   for (auto d : rv.shape) ex.out_elems *= d;
   CK(cudaMalloc(&ex.out_internal, static_cast<size_t>(ex.out_elems) * 4));
   {
+    // NCHW float32 at the boundary; a realize-coded result is dequantized
+    // (code * c2, exact) so the value equals the reference's float32 tensor.
     int rbuf = rr.buf;
     B.use(rbuf);
     LaunchRec L;
     L.name = "%" + rv.name;
     Exec* e = &ex;
-    if (rv.shape.size() == 4) {
-      L.kernel = "nhwc_to_nchw";
-      L.bytes = 8.0 * ex.out_elems;
-      int N = static_cast<int>(rv.shape[0]), C = static_cast<int>(rv.shape[1]);
-      int H = static_cast<int>(rv.shape[2]), W = static_cast<int>(rv.shape[3]);
-      L.fn = [e, rbuf, N, C, H, W](cudaStream_t s) {
-        launch_nhwc_to_nchw(static_cast<const float*>(e->ptr(rbuf)), e->out_internal, N, C, H, W, s);
-      };
-    } else {
-      L.kernel = "copy_result";
-      L.bytes = 8.0 * ex.out_elems;
-      int64_t bytes = ex.out_elems * 4;
-      L.fn = [e, rbuf, bytes](cudaStream_t s) {
-        cudaMemcpyAsync(e->out_internal, e->ptr(rbuf), static_cast<size_t>(bytes), cudaMemcpyDeviceToDevice, s);
-      };
-    }
+    L.kernel = "result_to_nchw";
+    L.bytes = static_cast<double>(ex.out_elems) * (4 + elem_bytes(rr.fmt));
+    int N = static_cast<int>(rv.shape[0]), C = static_cast<int>(rv.shape[1]);
+    int H = rv.shape.size() == 4 ? static_cast<int>(rv.shape[2]) : 1;
+    int W = rv.shape.size() == 4 ? static_cast<int>(rv.shape[3]) : 1;
+    int fmt = rr.fmt, cs = rr.cstride;
+    float c2 = rr.has_q ? rr.q.c2 : 1.f;
+    L.fn = [e, rbuf, fmt, cs, c2, N, C, H, W](cudaStream_t s) {
+      launch_nhwc_to_nchw(e->ptr(rbuf), fmt, cs, c2, e->out_internal, N, C, H, W, s);
+    };
     ex.launches.push_back(L);
     ++B.launch_idx;
   }
@@ -1043,7 +1040,7 @@ const char* mr_exec_describe(mr_exec_t h) { return reinterpret_cast<Exec*>(h)->d
 int32_t mr_exec_launch_count(mr_exec_t h) {
   Exec& ex = *reinterpret_cast<Exec*>(h);
   int32_t n = 0;
-  for (const auto& L : ex.launches) n += L.kernel == "copy_result" ? 0 : 1;
+  for (const auto& L : ex.launches) n += L.fn ? 1 : 0;
   return n;
 }
 

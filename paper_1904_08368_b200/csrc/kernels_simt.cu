@@ -43,7 +43,9 @@ __global__ void k_input_convert(const float* __restrict__ x, int N, int C, int H
 
 // ---- NHWC float32 -> NCHW float32 (a 4-D @main result) -------------------------
 
-__global__ void k_nhwc_to_nchw(const float* __restrict__ x, float* __restrict__ y, int N, int C, int H, int W) {
+// fmt FMT_I8: x holds realize codes, the value is code * c2 (exact).
+__global__ void k_nhwc_to_nchw(const void* __restrict__ x, int fmt, int Cs, float c2, float* __restrict__ y, int N,
+                               int C, int H, int W) {
   int64_t total = static_cast<int64_t>(N) * C * H * W;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -53,7 +55,9 @@ __global__ void k_nhwc_to_nchw(const float* __restrict__ x, float* __restrict__ 
     t /= H;
     int c = static_cast<int>(t % C);
     int n = static_cast<int>(t / C);
-    y[i] = x[((static_cast<int64_t>(n) * H + h) * W + w) * C + c];
+    int64_t src = ((static_cast<int64_t>(n) * H + h) * W + w) * Cs + c;
+    if (fmt == FMT_I8) y[i] = __fmul_rn(static_cast<float>(static_cast<const int8_t*>(x)[src]), c2);
+    else y[i] = load_fmt(x, fmt, src);
   }
 }
 
@@ -414,9 +418,10 @@ void launch_input_convert(const float* x, int N, int C, int H, int W, void* out,
   k_input_convert<<<grid_stride_blocks(total), kThreads, 0, s>>>(x, N, C, H, W, out, fmt, Cs, pre_mul, q);
 }
 
-void launch_nhwc_to_nchw(const float* x, float* y, int N, int C, int H, int W, cudaStream_t s) {
+void launch_nhwc_to_nchw(const void* x, int fmt, int Cs, float c2, float* y, int N, int C, int H, int W,
+                         cudaStream_t s) {
   int64_t total = static_cast<int64_t>(N) * C * H * W;
-  k_nhwc_to_nchw<<<grid_stride_blocks(total), kThreads, 0, s>>>(x, y, N, C, H, W);
+  k_nhwc_to_nchw<<<grid_stride_blocks(total), kThreads, 0, s>>>(x, fmt, Cs, c2, y, N, C, H, W);
 }
 
 void launch_weight_prep(const float* w, int O, int I, int KH, int KW, int Cs, const float* oc_scale,

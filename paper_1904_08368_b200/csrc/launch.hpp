@@ -11,7 +11,8 @@ namespace mrb200 {
 
 void launch_input_convert(const float* x, int N, int C, int H, int W, void* out, int fmt, int Cs,
                           float pre_mul, QDev q, cudaStream_t s);
-void launch_nhwc_to_nchw(const float* x, float* y, int N, int C, int H, int W, cudaStream_t s);
+void launch_nhwc_to_nchw(const void* x, int fmt, int Cs, float c2, float* y, int N, int C, int H, int W,
+                         cudaStream_t s);
 void launch_weight_prep(const float* w, int O, int I, int KH, int KW, int Cs, const float* oc_scale,
                         float scalar, int fmt, int quant, QDev q, void* out, cudaStream_t s);
 void launch_conv_i8_simt(const int8_t* x, const int8_t* w, const ConvGeom& g, float acc_scale,
