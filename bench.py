@@ -1,0 +1,355 @@
+"""Benchmark: ResNet-18 fused inference (int8 realized, bf16 float) images/s on B200.
+
+Contract (see the task's bench.py section):
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+One step = one pass of the fused ResNet-18 (22 Primitive groups, reference
+compiler output models/resnet18_int8.fused.rly) over a batch of 256 synthetic
+224x224 images per GPU (BASELINE.json configs[1]); N>1 runs one process per
+GPU (torchrun), each on its own batch shard with no collective on the data path
+(weak scaling).  Timing is on the device (CUDA events around K
+CUDA-graph replays, barrier + synchronize on both sides), max over ranks.
+`e2e` is the same metric through the public API from pinned host buffers
+(H2D input + run + D2H logits every step).  `roofline` is the dominant
+kernel's live CUDA-event duration vs its algorithmic bytes/ops.
+`cpu_baseline` / --impl reference time the reference interpreter
+(oracle/_ref/mr_ref, the unmodified MicroRelay interp()) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ResNet-18 images/sec (int8 & bf16) at 1/2/4/8 B200 vs CPU ref; % roofline"
+UNIT = "images/s"
+BATCH_PER_GPU = 256
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.FIELDS,
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def max_over_ranks(v: float, world: int):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def load(precision):
+    import paper_1904_08368_b200 as mrb
+    from paper_1904_08368_b200 import modelzoo
+    text, meta, src = mrb.load_model("resnet18", precision)
+    w = modelzoo.make_weights(src, seed=meta["weights_seed"])
+    wl = [w[p.name] for p in src.params if p.kind != "input"]
+    return mrb, modelzoo, text, meta, src, wl
+
+
+def time_ours(precision, batch, steps, warmup, rank, world, local):
+    """Device-resident throughput + e2e + per-launch profile for one precision."""
+    import torch
+    mrb, modelzoo, text, meta, src, wl = load(precision)
+    ex = mrb.Executor(text, batch=batch, device=local)
+    ex.set_weights(wl)
+    x_host = modelzoo.make_inputs(src, batch, seed=rank)
+    x_dev = torch.from_numpy(x_host).to(f"cuda:{local}")
+    out = torch.empty(ex.output_shape, dtype=torch.float32, device=f"cuda:{local}")
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+    launches = ex.launch_count()
+    for _ in range(warmup):
+        ex.run_device(x_dev.data_ptr(), x_dev.shape, out.data_ptr(), sh)
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        barrier(world)
+        e0.record(stream)
+        for _ in range(steps):
+            ex.run_device(x_dev.data_ptr(), x_dev.shape, out.data_ptr(), sh)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+    ms = max_over_ranks(e0.elapsed_time(e1), world)
+    ms_step = ms / steps
+    value = batch * world * steps / (ms / 1e3)
+
+    # e2e through the public API from pinned host memory (H2D + run + D2H per step)
+    x_pin = torch.from_numpy(x_host).pin_memory()
+    y_pin = torch.empty(ex.output_shape, dtype=torch.float32).pin_memory()
+    xn, yn = x_pin.numpy(), y_pin.numpy()
+    for _ in range(max(1, warmup)):
+        ex.run_host_into(xn, yn, sh)
+    torch.cuda.synchronize()
+    barrier(world)
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for _ in range(steps):
+        ex.run_host_into(xn, yn, sh)
+    e3.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    ms_e2e = max_over_ranks(e2.elapsed_time(e3), world)
+    e2e = {"value": batch * world * steps / (ms_e2e / 1e3), "unit": UNIT,
+           "h2d_bytes_per_step": int(x_host.nbytes), "d2h_bytes_per_step": int(np.prod(ex.output_shape) * 4),
+           "ms_per_step": ms_e2e / steps}
+
+    # per-launch device times (CUDA events between launches on the same stream)
+    desc = ex.describe()
+    per = np.zeros(len(desc["launches"]))
+    reps = max(3, min(steps, 10))
+    for _ in range(reps):
+        t = ex.profile_device(x_dev.data_ptr(), x_dev.shape, out.data_ptr(), sh)
+        per += np.asarray(t[: len(per)])
+    per /= reps
+    return dict(value=value, ms_step=ms_step, e2e=e2e, clocks=clk.summary(), launches=launches,
+                desc=desc, per_launch_ms=per.tolist(), meta=meta)
+
+
+def roofline(res, precision, pk):
+    """Dominant kernel (largest share of the step) vs its algorithmic bytes/ops."""
+    desc, per = res["desc"], res["per_launch_ms"]
+    # aggregate by kernel family
+    fam = {}
+    for L, ms in zip(desc["launches"], per):
+        f = fam.setdefault(L["kernel"], {"ms": 0.0, "bytes": 0.0, "flops": 0.0, "n": 0})
+        f["ms"] += ms
+        f["bytes"] += L["bytes"]
+        f["flops"] += L["flops"]
+        f["n"] += 1
+    top = max(fam.items(), key=lambda kv: kv[1]["ms"])
+    name, f = top
+    hbm = pk["hbm_gbs"]
+    tc = pk["bf16_tflops"] * (2.0 if precision == "int8" else 1.0)  # int8 = 2x measured bf16 (estimate)
+    t_mem = f["bytes"] / (hbm * 1e9)
+    t_tc = f["flops"] / (tc * 1e12)
+    bound = "hbm" if t_mem >= t_tc else "tensor"
+    secs = f["ms"] / 1e3
+    if bound == "hbm":
+        achieved, peak, unit = f["bytes"] / secs / 1e9, hbm, "GB/s"
+    else:
+        achieved, peak, unit = f["flops"] / secs / 1e12, tc, "TFLOP/s" if precision != "int8" else "TOP/s"
+    total_ms = sum(per)
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        t = json.load(open(tf)).get(precision, {}).get(name)
+        if t is not None:
+            traffic = t
+    # whole-step roofline: sum over launches of max(bytes/BW, flops/peak)
+    t_roof = sum(max(L["bytes"] / (hbm * 1e9), L["flops"] / (tc * 1e12)) for L in desc["launches"])
+    return {"kernel": name, "launches": f["n"], "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+            "frac": achieved / peak, "traffic": traffic, "share_of_step": f["ms"] / total_ms,
+            "peak_source": pk["source"] + ("" if precision != "int8" else "; int8 tensor peak = 2x measured bf16 (estimate)"),
+            "algorithmic": {"bytes": f["bytes"], "ops": f["flops"], "avg_ms": f["ms"] / f["n"]},
+            "step_roofline_ms": t_roof * 1e3, "step_profiled_ms": total_ms,
+            "step_frac": (t_roof * 1e3) / total_ms}
+
+
+def cpu_reference(precision, images, procs, timeout=900):
+    """Reference interp() (oracle/_ref/mr_ref) on `images` images over `procs` processes."""
+    from oracle import ref
+    mrb, modelzoo, text, meta, src, wl = load(precision)
+    x = modelzoo.make_inputs(src, images, seed=0)
+    tmp = tempfile.mkdtemp(prefix="mrref_")
+    fused = os.path.join(tmp, "fused.rly")
+    open(fused, "w").write(text)
+    wf = os.path.join(tmp, "w.bin")
+    ref.write_tensors(wf, wl)
+    shards = np.array_split(np.arange(images), procs)
+    ps = []
+    t0 = time.time()
+    for i, idx in enumerate(shards):
+        if len(idx) == 0:
+            continue
+        xf = os.path.join(tmp, "x%d.bin" % i)
+        ref.write_tensors(xf, [x[idx]])
+        ps.append(subprocess.Popen([ref.EXE, "run", fused, wf, xf, os.path.join(tmp, "o%d.bin" % i)],
+                                   stdout=subprocess.DEVNULL, stderr=subprocess.PIPE, text=True))
+    per_img = []
+    for p in ps:
+        _, err = p.communicate(timeout=timeout)
+        per_img += [float(l.split()[2]) for l in err.splitlines() if l.startswith("image ")]
+        if p.returncode != 0:
+            raise RuntimeError("mr_ref failed: " + err[-500:])
+    wall = time.time() - t0
+    return {"value": images / wall, "unit": UNIT, "cores": len(ps), "kind": "reference",
+            "sample": "%d ResNet-18 %s images (batch-1 interp() calls, 224x224) over %d processes; mean %.1f s/image/core"
+                      % (images, precision, len(ps), float(np.mean(per_img)) if per_img else -1),
+            "seconds": wall}
+
+
+def host_cores():
+    """Host threads for the CPU reference (capped: each interp() worker holds
+    a few hundred MB of materialized intermediates)."""
+    try:
+        n = len(os.sched_getaffinity(0))
+    except Exception:
+        n = os.cpu_count() or 1
+    return max(1, min(n, 64))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=BATCH_PER_GPU, help="images per GPU per step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-bf16", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    warmup = max(args.warmup, 3)
+
+    config = {"workload": "resnet18_int8_b%d" % args.batch, "model": "ResNet-18 (fused, 22 Primitive groups)",
+              "batch_per_gpu": args.batch, "global_batch": args.batch * world, "image": [3, 224, 224],
+              "parallelism": "batch shards, no collectives (dp%d)" % world,
+              "module": "models/resnet18_int8.fused.rly (reference run_pipeline fold-scale,fold,dce,quantize,fuse; k=5)",
+              "l2": "inputs larger than L2: 154 MB fp32 input + ~1.4 GB activations per step, no flush"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        cores = host_cores()
+        steps = min(args.steps, 2)
+        wu = min(args.warmup, 0)
+        vals = []
+        for i in range(wu + steps):
+            r = cpu_reference("int8", cores, cores)
+            if i >= wu:
+                vals.append(r["value"])
+        v = float(np.mean(vals))
+        line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+                "steps": steps, "warmup": wu, "ms_per_step": 1e3 * cores / v, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32 (fake-quant int8)", "data": "synthetic",
+                "config": config,
+                "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
+                                 "sample": r["sample"] + "; each step = one such sample"},
+                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    else:
+        torch.cuda.set_device(local)
+    pk = peaks()
+    res = time_ours("int8", args.batch, args.steps, warmup, rank, world, local)
+    roof = roofline(res, "int8", pk)
+    bf16 = None
+    if not args.no_bf16:
+        rb = time_ours("fp32", args.batch, args.steps, warmup, rank, world, local)
+        bf16 = {"value": rb["value"], "unit": UNIT, "ms_per_step": rb["ms_step"], "e2e": rb["e2e"],
+                "roofline": roofline(rb, "bf16", pk), "gpu_launches": rb["launches"] * args.steps,
+                "module": "models/resnet18_fp32.fused.rly (bf16 operands, fp32 accumulate)"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cores = host_cores()
+            cpu = cpu_reference("int8", cores, cores)
+        except Exception as e:  # reported, not fatal
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": "failed: %s" % e}
+    if rank == 0:
+        line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": warmup, "ms_per_step": res["ms_step"], "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "int8 (int32 accumulate; fp32 epilogue/residual)", "data": "synthetic",
+                "config": config, "e2e": res["e2e"], "gpu_launches": res["launches"] * args.steps,
+                "clocks": res["clocks"], "roofline": roof, "cpu_baseline": cpu, "bf16": bf16,
+                "per_group_ms": {L["name"] + ":" + L["kernel"]: round(ms, 4)
+                                 for L, ms in zip(res["desc"]["launches"], res["per_launch_ms"])}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

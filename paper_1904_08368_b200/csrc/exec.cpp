@@ -61,8 +61,8 @@ struct Rep {
   bool nchw_user = false;  // the caller's input buffer
   bool has_q = false;      // I8: codes of Q(v)
   QParams q;
-  int64_t elems = 0;       // including channel padding
-  int cstride = 0;         // channel stride (NHWC) / row length (2-D)
+  int64_t elems = 0;       // including the zero border and chunk padding
+  Lay lay{};               // P16 (4-D) or row-major (2-D)
   int buf = -1;            // arena buffer id
 };
 
@@ -97,6 +97,7 @@ struct Exec {
   std::vector<void*> group_w;               // hoisted weight per group
   std::vector<std::vector<void*>> group_vecs;  // uploaded constant vectors per group
   std::vector<int> group_kp;                // weight row length per group
+  std::vector<int> group_cs;                // weight channel stride per tap (row layouts)
   std::vector<int> group_path;              // kernel choice
   std::vector<std::string> group_exact;     // int8 exactness proof per group
   bool weights_ready = false;
@@ -152,13 +153,24 @@ int float_fmt(const Exec& ex) {
 
 int64_t elem_bytes(int fmt) { return fmt == FMT_F32 ? 4 : fmt == FMT_BF16 ? 2 : 1; }
 
-// NHWC element count with channel stride cs for a logical NCHW / [N,C] shape.
-int64_t nhwc_elems(const std::vector<int64_t>& s, int cs) {
-  if (s.size() == 4) return s[0] * s[2] * s[3] * cs;
-  if (s.size() == 2) return s[0] * cs;
-  int64_t n = 1;
-  for (auto d : s) n *= d;
-  return n;
+// Layout of a representation: P16 with a kPad border for 4-D values,
+// row-major for 2-D ones.
+Lay make_lay(const std::vector<int64_t>& s, int fmt) {
+  Lay L{};
+  L.C = s.size() >= 2 ? static_cast<int32_t>(s[1]) : 1;
+  if (s.size() == 4) {
+    L.cpc = static_cast<int32_t>(16 / elem_bytes(fmt));
+    L.Pp = s[0] * (s[2] + 2 * kPad) * (s[3] + 2 * kPad);
+  } else {
+    L.cpc = 0;
+    L.Pp = s.empty() ? 1 : s[0];
+  }
+  return L;
+}
+
+int64_t lay_elems(const Lay& L) {
+  if (L.cpc == 0) return L.Pp * L.C;
+  return (L.C + L.cpc - 1) / L.cpc * L.Pp * L.cpc;
 }
 
 int channels(const std::vector<int64_t>& s) { return s.size() >= 2 ? static_cast<int>(s[1]) : 1; }
@@ -181,9 +193,8 @@ int want_rep(Exec& ex, int v, int fmt, const QParams* q) {
     r.has_q = true;
     r.q = *q;
   }
-  int C = channels(ex.P.values[v].shape);
-  r.cstride = fmt == FMT_I8 ? static_cast<int>(round_up(C, 4)) : C;
-  r.elems = nhwc_elems(ex.P.values[v].shape, r.cstride);
+  r.lay = make_lay(ex.P.values[v].shape, fmt);
+  r.elems = lay_elems(r.lay);
   rs.push_back(r);
   return static_cast<int>(rs.size()) - 1;
 }
@@ -455,10 +466,11 @@ void build(Exec& ex) {
       int H = static_cast<int>(vi.shape[2]), W = static_cast<int>(vi.shape[3]);
       L.bytes = 4.0 * N * C * H * W + static_cast<double>(rep.elems) * elem_bytes(rep.fmt);
       QDev q = to_qdev(rep.q);
-      int fmt = rep.fmt, cs = rep.cstride;
+      int fmt = rep.fmt;
+      Lay lay = rep.lay;
       Exec* e = &ex;
-      L.fn = [e, buf, N, C, H, W, fmt, cs, q](cudaStream_t s) {
-        launch_input_convert(e->cur_input, N, C, H, W, e->ptr(buf), fmt, cs, 0.f, q, s);
+      L.fn = [e, buf, N, C, H, W, fmt, lay, q](cudaStream_t s) {
+        launch_input_convert(e->cur_input, N, C, H, W, e->ptr(buf), fmt, lay, 0.f, q, s);
       };
       ex.launches.push_back(L);
       ++B.launch_idx;
@@ -484,19 +496,20 @@ void build(Exec& ex) {
     EpiDev epi = make_epi(ex, static_cast<int>(gi), gio, n_elem_ops);
     OutDev out{};
     int pre_sum_buf = -1;
+    Lay pre_lay{};
     if (has_sum) {
-      // the conv writes the float32 pre-sum tensor; k_sum_hw reduces it
-      const auto& ps = g.pre_sum_shape;
-      pre_sum_buf = B.scratch(ps[0] * ps[1] * ps[2] * ps[3] * 4, "%" + g.out_name + ":presum");
+      // the conv writes the float32 pre-sum tensor (P16); k_sum_hw reduces it
+      pre_lay = make_lay(g.pre_sum_shape, FMT_F32);
+      pre_sum_buf = B.scratch(lay_elems(pre_lay) * 4, "%" + g.out_name + ":presum");
       out.primary_fmt = FMT_F32;
-      out.pstride = static_cast<int>(ps[1]);
+      out.plan = pre_lay;
     } else {
       out.primary_fmt = orep.fmt;
-      out.pstride = orep.cstride;
+      out.plan = orep.lay;
     }
     if (sbuf >= 0) {
       const Rep& sr = ex.reps[g.out_value][side_rep[gi]];
-      out.sstride = sr.cstride;
+      out.slay = sr.lay;
       out.side_q = to_qdev(sr.q);
     }
 
@@ -530,14 +543,13 @@ void build(Exec& ex) {
     int gidx = static_cast<int>(gi);
     int dbuf = drep.buf;
     int dfmt = drep.fmt;
-    int dcs = drep.cstride;
     ConvGeom geo{};
     if (g.kind != GroupKind::Dense) {
       geo.N = static_cast<int>(g.in_shape[0]);
       geo.C = static_cast<int>(g.in_shape[1]);
       geo.H = static_cast<int>(g.in_shape[2]);
       geo.W = static_cast<int>(g.in_shape[3]);
-      geo.Cs = dcs;
+      geo.in = drep.lay;
       const auto& os = has_sum ? g.pre_sum_shape : g.out_shape;
       geo.OC = static_cast<int>(os[1]);
       geo.OH = static_cast<int>(os[2]);
@@ -579,8 +591,11 @@ void build(Exec& ex) {
       int n = 0;
       for (size_t i = 0; i < gg.epi.size() && n < d.n_ops; ++i) {
         if (gg.epi[i].kind == EpiKind::SumHW) continue;
-        if (gg.epi[i].kind == EpiKind::Residual)
-          d.res[n] = e->ptr(e->reps[gg.epi[i].value][gio.res_rep[i]].buf);
+        if (gg.epi[i].kind == EpiKind::Residual) {
+          const Rep& r = e->reps[gg.epi[i].value][gio.res_rep[i]];
+          d.res[n] = e->ptr(r.buf);
+          d.res_lay[n] = r.lay;
+        }
         ++n;
       }
     };
@@ -593,6 +608,7 @@ void build(Exec& ex) {
           residual_fix(d);
           ConvGeom gg = geo;
           gg.Kp = e->group_kp[gidx];
+          gg.Cs = e->group_cs[gidx];
           if (path == P_CONV_I8_SIMT)
             launch_conv_i8_simt(static_cast<const int8_t*>(e->ptr(dbuf)), static_cast<const int8_t*>(e->group_w[gidx]),
                                 gg, acc_scale, d, outdev(), s);
@@ -653,16 +669,36 @@ void build(Exec& ex) {
     }
     ex.launches.push_back(L);
     ++B.launch_idx;
+    // CUDA-core producers write interior pixels only: clear the P16 borders
+    // (the tcgen05 conv writes its own, it computes over the padded grid).
+    bool tc = path == P_CONV_I8_TC || path == P_CONV_BF16_TC;
+    if (!tc && !has_sum && g.out_shape.size() == 4) {
+      for (int b2 : {obuf, sbuf}) {
+        if (b2 < 0) continue;
+        LaunchRec Z;
+        Z.name = "%" + g.name;
+        Z.kernel = "zero_border";
+        Lay zl = b2 == obuf ? orep.lay : ex.reps[g.out_value][side_rep[gi]].lay;
+        int N = static_cast<int>(g.out_shape[0]), H = static_cast<int>(g.out_shape[2]), W = static_cast<int>(g.out_shape[3]);
+        int64_t border = (zl.C + zl.cpc - 1) / zl.cpc * static_cast<int64_t>(N) * (2 * (W + 2) + 2 * H) * 16;
+        Z.bytes = static_cast<double>(border);
+        Z.fn = [e, b2, zl, N, H, W](cudaStream_t s) { launch_zero_border(e->ptr(b2), zl, N, H, W, s); };
+        ex.launches.push_back(Z);
+        ++B.launch_idx;
+      }
+    }
     if (has_sum) {
       LaunchRec S;
       S.name = "%" + g.name;
       S.kernel = "sum_hw";
       const auto& ps = g.pre_sum_shape;
       S.bytes = 4.0 * ps[0] * ps[1] * ps[2] * ps[3] + 4.0 * ps[0] * ps[1];
-      int N = static_cast<int>(ps[0]), HW = static_cast<int>(ps[2] * ps[3]), C = static_cast<int>(ps[1]);
+      int N = static_cast<int>(ps[0]), H = static_cast<int>(ps[2]), W = static_cast<int>(ps[3]);
+      int C = static_cast<int>(ps[1]);
       B.use(pre_sum_buf);
-      S.fn = [e, pre_sum_buf, obuf, N, HW, C](cudaStream_t s) {
-        launch_sum_hw(static_cast<const float*>(e->ptr(pre_sum_buf)), N, HW, C, static_cast<float*>(e->ptr(obuf)), s);
+      S.fn = [e, pre_sum_buf, pre_lay, obuf, N, H, W, C](cudaStream_t s) {
+        launch_sum_hw(static_cast<const float*>(e->ptr(pre_sum_buf)), pre_lay, N, H, W, C,
+                      static_cast<float*>(e->ptr(obuf)), s);
       };
       ex.launches.push_back(S);
       ++B.launch_idx;
@@ -690,10 +726,12 @@ void build(Exec& ex) {
     int N = static_cast<int>(rv.shape[0]), C = static_cast<int>(rv.shape[1]);
     int H = rv.shape.size() == 4 ? static_cast<int>(rv.shape[2]) : 1;
     int W = rv.shape.size() == 4 ? static_cast<int>(rv.shape[3]) : 1;
-    int fmt = rr.fmt, cs = rr.cstride;
+    int fmt = rr.fmt;
+    Lay lay = rr.lay;
+    int is4d = rv.shape.size() == 4 ? 1 : 0;
     float c2 = rr.has_q ? rr.q.c2 : 1.f;
-    L.fn = [e, rbuf, fmt, cs, c2, N, C, H, W](cudaStream_t s) {
-      launch_nhwc_to_nchw(e->ptr(rbuf), fmt, cs, c2, e->out_internal, N, C, H, W, s);
+    L.fn = [e, rbuf, fmt, lay, c2, N, C, H, W, is4d](cudaStream_t s) {
+      launch_to_nchw(e->ptr(rbuf), fmt, lay, c2, e->out_internal, N, C, H, W, is4d, s);
     };
     ex.launches.push_back(L);
     ++B.launch_idx;
@@ -733,6 +771,7 @@ void prepare_weights(Exec& ex, cudaStream_t s) {
   const int ffmt = float_fmt(ex);
   ex.group_w.assign(P.groups.size(), nullptr);
   ex.group_kp.assign(P.groups.size(), 0);
+  ex.group_cs.assign(P.groups.size(), 0);
   for (size_t gi = 0; gi < P.groups.size(); ++gi) {
     const GroupDesc& g = P.groups[gi];
     if (g.kind == GroupKind::MaxPool) continue;
@@ -758,26 +797,34 @@ void prepare_weights(Exec& ex, cudaStream_t s) {
       KW = static_cast<int>(w.shape[3]);
     }
     int fmt, cs;
+    int wl = (path == P_CONV_I8_TC || path == P_CONV_BF16_TC) ? WL_TC : WL_ROWS;
     if (w.quant) {
       fmt = FMT_I8;
       cs = static_cast<int>(round_up(I, 4));
-      if (path == P_CONV_I8_TC) cs = tc_conv_weight_cstride(I, 1);
     } else if (g.kind == GroupKind::DwConv || ffmt == FMT_F32) {
       fmt = FMT_F32;
       cs = I;
     } else {
       fmt = FMT_BF16;
       cs = I;
-      if (path == P_CONV_BF16_TC) cs = tc_conv_weight_cstride(I, 2);
     }
-    int64_t n = fmt == FMT_F32 ? static_cast<int64_t>(O) * I * KH * KW : static_cast<int64_t>(O) * KH * KW * cs;
+    int64_t n;
+    if (fmt == FMT_F32) {
+      n = static_cast<int64_t>(O) * I * KH * KW;
+    } else if (wl == WL_TC) {
+      int cpc = 16 / static_cast<int>(elem_bytes(fmt));
+      n = static_cast<int64_t>(KH) * KW * ((I + cpc - 1) / cpc) * O * cpc;
+    } else {
+      n = static_cast<int64_t>(O) * KH * KW * cs;
+    }
     void* dst = nullptr;
     CK(cudaMalloc(&dst, static_cast<size_t>(n * elem_bytes(fmt))));
-    launch_weight_prep(raw, O, I, KH, KW, cs, static_cast<const float*>(ex.group_vecs[gi][0]), w.scalar_scale, fmt,
-                       w.quant ? 1 : 0, to_qdev(w.q), dst, s);
+    launch_weight_prep(raw, O, I, KH, KW, cs, wl, static_cast<const float*>(ex.group_vecs[gi][0]), w.scalar_scale,
+                       fmt, w.quant ? 1 : 0, to_qdev(w.q), dst, s);
     CK(cudaGetLastError());
     ex.group_w[gi] = dst;
     ex.group_kp[gi] = fmt == FMT_F32 ? I * KH * KW : KH * KW * cs;
+    ex.group_cs[gi] = cs;
     if (tmp) {
       CK(cudaStreamSynchronize(s));
       cudaFree(tmp);
@@ -790,12 +837,13 @@ void prepare_weights(Exec& ex, cudaStream_t s) {
       CK(cudaStreamSynchronize(s));
       std::vector<int8_t> codes(static_cast<size_t>(n));
       CK(cudaMemcpy(codes.data(), dst, static_cast<size_t>(n), cudaMemcpyDeviceToHost));
+      std::vector<int64_t> sums(O, 0);
       int64_t per = n / O, worst = 0;
-      for (int o = 0; o < O; ++o) {
-        int64_t s1 = 0;
-        for (int64_t k = 0; k < per; ++k) s1 += std::abs(static_cast<int>(codes[o * per + k]));
-        worst = std::max(worst, s1);
+      for (int64_t k = 0; k < n; ++k) {
+        int o = wl == WL_TC ? static_cast<int>((k / 16) % O) : static_cast<int>(k / per);
+        sums[o] += std::abs(static_cast<int>(codes[k]));
       }
+      for (int o = 0; o < O; ++o) worst = std::max(worst, sums[o]);
       float xmax = g.data.quant ? std::max(std::fabs(g.data.q.lo), std::fabs(g.data.q.hi))
                                 : std::max(std::fabs(P.values[g.data.value].q.lo), std::fabs(P.values[g.data.value].q.hi));
       double bound = static_cast<double>(worst) * xmax;

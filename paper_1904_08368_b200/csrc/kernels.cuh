@@ -23,6 +23,20 @@ struct QDev {
   int32_t is_signed;
 };
 
+// Physical layout of an activation tensor ("P16"): channels are split into
+// 16-byte chunks (cpc = 16 / element-bytes channels each); each chunk is a
+// plane of N*(H+2p)*(W+2p) pixels over the zero-padded spatial grid:
+//     element (n, c, h, w) at ((c / cpc) * Pp + pix) * cpc + c % cpc,
+//     pix = (n * Hp + h + p) * Wp + (w + p).
+// Borders hold zeros, so a stride-1 3x3 conv reads its 9 taps as 9 row
+// shifts of one contiguous pixel range (conv_tc.cu).  cpc == 0 marks a plain
+// row-major [N, C] tensor (pix = n).
+struct Lay {
+  int32_t cpc;
+  int32_t C;   // logical channels (row length when cpc == 0)
+  int64_t Pp;  // pixels per plane
+};
+
 enum EpiCode : int32_t {
   E_MULS = 1, E_MULC = 2, E_BIAS = 3, E_RES = 4, E_RELU = 5, E_REQ = 6, E_CLIP = 7
 };
@@ -35,18 +49,19 @@ struct EpiDev {
   float s[kMaxEpi];          // MulScalar / Clip lo
   float s2[kMaxEpi];         // Clip hi
   const float* vec[kMaxEpi]; // MulChannel / Bias, [C]
-  const void* res[kMaxEpi];  // Residual, NHWC, row stride = C
+  const void* res[kMaxEpi];  // Residual tensor (same pixel grid as the output)
   int32_t res_fmt[kMaxEpi];
+  Lay res_lay[kMaxEpi];
   QDev q[kMaxEpi];
 };
 
 // Where a kernel writes its (per element) final value.
 struct OutDev {
-  void* primary;        // NHWC (or [N,C]) row stride = pstride elements
+  void* primary;        // P16 (or row-major [N, C])
   int32_t primary_fmt;  // FMT_I8 => the epilogue's last op is a Requant; the code is stored
-  int32_t pstride;      // channel stride of the primary (C, or Cp for I8)
-  int8_t* side;         // optional int8 codes of the final float value (row stride sstride)
-  int32_t sstride;
+  Lay plan;             // primary layout
+  int8_t* side;         // optional int8 codes of the final float value (P16, same grid)
+  Lay slay;
   QDev side_q;
 };
 
@@ -86,22 +101,26 @@ __device__ __forceinline__ int32_t quant_code(float v, const QDev& q) {
   return cast_int_ref(t, q.is_signed);
 }
 
+__host__ __device__ __forceinline__ int64_t lay_off(const Lay& L, int64_t pix, int32_t c) {
+  if (L.cpc == 0) return pix * L.C + c;
+  return (static_cast<int64_t>(c / L.cpc) * L.Pp + pix) * L.cpc + (c % L.cpc);
+}
+
 __device__ __forceinline__ float load_fmt(const void* p, int32_t fmt, int64_t i) {
   if (fmt == FMT_F32) return static_cast<const float*>(p)[i];
   return bf16_to_f32(static_cast<const uint16_t*>(p)[i]);
 }
 
 // Applies the interpreted epilogue to v (the anchor's float32 result at
-// output row m, channel c).  Returns the final float; *code receives the
+// output pixel pix, channel c).  Returns the final float; *code receives the
 // int8 code of the last Requant (if any).
-__device__ __forceinline__ float apply_epi(const EpiDev& e, float v, int64_t m, int32_t c,
-                                           int32_t C, int32_t* code) {
+__device__ __forceinline__ float apply_epi(const EpiDev& e, float v, int64_t pix, int32_t c, int32_t* code) {
   for (int i = 0; i < e.n_ops; ++i) {
     switch (e.op[i]) {
       case E_MULS: v = __fmul_rn(v, e.s[i]); break;
       case E_MULC: v = __fmul_rn(v, e.vec[i][c]); break;
       case E_BIAS: v = __fadd_rn(v, e.vec[i][c]); break;
-      case E_RES: v = __fadd_rn(v, load_fmt(e.res[i], e.res_fmt[i], m * C + c)); break;
+      case E_RES: v = __fadd_rn(v, load_fmt(e.res[i], e.res_fmt[i], lay_off(e.res_lay[i], pix, c))); break;
       case E_RELU: v = relu_ref(v); break;
       case E_REQ: {
         int32_t k = quant_code(v, e.q[i]);
@@ -116,15 +135,16 @@ __device__ __forceinline__ float apply_epi(const EpiDev& e, float v, int64_t m, 
   return v;
 }
 
-__device__ __forceinline__ void store_out(const OutDev& o, float v, int32_t code, int64_t m, int32_t c) {
+__device__ __forceinline__ void store_out(const OutDev& o, float v, int32_t code, int64_t pix, int32_t c) {
+  int64_t i = lay_off(o.plan, pix, c);
   if (o.primary_fmt == FMT_F32) {
-    static_cast<float*>(o.primary)[m * o.pstride + c] = v;
+    static_cast<float*>(o.primary)[i] = v;
   } else if (o.primary_fmt == FMT_BF16) {
-    static_cast<uint16_t*>(o.primary)[m * o.pstride + c] = f32_to_bf16(v);
+    static_cast<uint16_t*>(o.primary)[i] = f32_to_bf16(v);
   } else {
-    static_cast<int8_t*>(o.primary)[m * o.pstride + c] = static_cast<int8_t>(code);
+    static_cast<int8_t*>(o.primary)[i] = static_cast<int8_t>(code);
   }
-  if (o.side) o.side[m * o.sstride + c] = static_cast<int8_t>(quant_code(v, o.side_q));
+  if (o.side) o.side[lay_off(o.slay, pix, c)] = static_cast<int8_t>(quant_code(v, o.side_q));
 }
 
 #endif  // __CUDACC__
@@ -132,11 +152,19 @@ __device__ __forceinline__ void store_out(const OutDev& o, float v, int32_t code
 // ---- host-visible launch parameter blocks --------------------------------
 
 struct ConvGeom {
-  int32_t N, H, W, C;      // input (logical C)
-  int32_t Cs;              // input channel stride (I8: Cp = round_up(C,4))
+  int32_t N, H, W, C;      // input (logical)
+  Lay in;                  // input layout (P16, pad kPad)
   int32_t OH, OW, OC;
   int32_t KH, KW, sh, sw, ph, pw;
-  int32_t Kp;              // weight row length (I8: KH*KW*Cs; strict: IC*KH*KW)
+  int32_t Cs;              // weight channel stride per tap (SIMT layouts)
+  int32_t Kp;              // weight row length (I8/BF16: KH*KW*Cs; strict: IC*KH*KW)
 };
+
+// Every 4-D activation is stored with a one-pixel zero border.
+constexpr int kPad = 1;
+
+__host__ __device__ __forceinline__ int64_t pad_pix(int32_t n, int32_t h, int32_t w, int32_t H, int32_t W) {
+  return (static_cast<int64_t>(n) * (H + 2 * kPad) + h + kPad) * (W + 2 * kPad) + w + kPad;
+}
 
 }  // namespace mrb200

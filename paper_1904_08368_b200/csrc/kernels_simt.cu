@@ -3,6 +3,7 @@
 // variants (int8 dp4a, bf16, and the fp32 reference-order "strict" conv used
 // to check the float lowering bit for bit).  The tensor-core convolutions
 // live in conv_tc.cu; these are the baseline they are measured against.
+// Activations use the padded P16 layout (kernels.cuh).
 #include <cuda_runtime.h>
 
 #include "kernels.cuh"
@@ -14,65 +15,114 @@ namespace {
 
 constexpr int kThreads = 256;
 
-inline unsigned blocks_for(int64_t n, int t = kThreads) { return static_cast<unsigned>((n + t - 1) / t); }
+#define GRID_STRIDE(i, total)                                                         \
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < (total); \
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
 
-// ---- boundary: NCHW float32 -> internal NHWC ---------------------------------
+struct Pix {
+  int32_t n, h, w;  // logical (h, w may be -1 / H for border pixels)
+  bool border;
+};
 
-__global__ void k_input_convert(const float* __restrict__ x, int N, int C, int H, int W, void* out,
-                                int fmt, int Cs, float pre_mul, QDev q) {
-  int64_t total = static_cast<int64_t>(N) * H * W * Cs;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    int c = static_cast<int>(i % Cs);
-    int64_t p = i / Cs;
-    int w = static_cast<int>(p % W);
-    int64_t t = p / W;
-    int h = static_cast<int>(t % H);
-    int n = static_cast<int>(t / H);
-    float v = c < C ? x[((static_cast<int64_t>(n) * C + c) * H + h) * W + w] : 0.f;
-    if (pre_mul != 0.f) v = __fmul_rn(v, pre_mul);
+__device__ __forceinline__ Pix decode_pix(int64_t pix, int32_t H, int32_t W) {
+  const int32_t Hp = H + 2 * kPad, Wp = W + 2 * kPad;
+  Pix p;
+  int32_t wp = static_cast<int32_t>(pix % Wp);
+  int64_t t = pix / Wp;
+  int32_t hp = static_cast<int32_t>(t % Hp);
+  p.n = static_cast<int32_t>(t / Hp);
+  p.h = hp - kPad;
+  p.w = wp - kPad;
+  p.border = p.h < 0 || p.h >= H || p.w < 0 || p.w >= W;
+  return p;
+}
+
+// ---- boundary: NCHW float32 -> P16 -----------------------------------------------
+// Writes every element of the padded buffer (zeros on the border and in the
+// channel padding of the last chunk).
+__global__ void k_input_convert(const float* __restrict__ x, int N, int C, int H, int W, void* out, int fmt,
+                                Lay L, float pre_mul, QDev q) {
+  const int64_t total = static_cast<int64_t>((C + L.cpc - 1) / L.cpc) * L.Pp * L.cpc;
+  GRID_STRIDE(i, total) {
+    int32_t within = static_cast<int32_t>(i % L.cpc);
+    int64_t t = i / L.cpc;
+    int64_t pix = t % L.Pp;
+    int32_t c = static_cast<int32_t>(t / L.Pp) * L.cpc + within;
+    Pix p = decode_pix(pix, H, W);
+    bool live = !p.border && c < C;
+    float v = live ? x[((static_cast<int64_t>(p.n) * C + c) * H + p.h) * W + p.w] : 0.f;
+    if (pre_mul != 0.f && live) v = __fmul_rn(v, pre_mul);
     if (fmt == FMT_F32) {
       static_cast<float*>(out)[i] = v;
     } else if (fmt == FMT_BF16) {
       static_cast<uint16_t*>(out)[i] = f32_to_bf16(v);
     } else {
-      static_cast<int8_t*>(out)[i] = c < C ? static_cast<int8_t>(quant_code(v, q)) : 0;
+      static_cast<int8_t*>(out)[i] = live ? static_cast<int8_t>(quant_code(v, q)) : 0;
     }
   }
 }
 
-// ---- NHWC float32 -> NCHW float32 (a 4-D @main result) -------------------------
-
-// fmt FMT_I8: x holds realize codes, the value is code * c2 (exact).
-__global__ void k_nhwc_to_nchw(const void* __restrict__ x, int fmt, int Cs, float c2, float* __restrict__ y, int N,
-                               int C, int H, int W) {
-  int64_t total = static_cast<int64_t>(N) * C * H * W;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+// ---- P16 / row-major -> NCHW float32 (@main result) -------------------------------
+// fmt FMT_I8: realize codes, the value is code * c2 (exact).
+__global__ void k_to_nchw(const void* __restrict__ x, int fmt, Lay L, float c2, float* __restrict__ y, int N, int C,
+                          int H, int W, int is4d) {
+  const int64_t total = static_cast<int64_t>(N) * C * H * W;
+  GRID_STRIDE(i, total) {
     int w = static_cast<int>(i % W);
     int64_t t = i / W;
     int h = static_cast<int>(t % H);
     t /= H;
     int c = static_cast<int>(t % C);
     int n = static_cast<int>(t / C);
-    int64_t src = ((static_cast<int64_t>(n) * H + h) * W + w) * Cs + c;
+    int64_t pix = is4d ? pad_pix(n, h, w, H, W) : n;
+    int64_t src = lay_off(L, pix, c);
     if (fmt == FMT_I8) y[i] = __fmul_rn(static_cast<float>(static_cast<const int8_t*>(x)[src]), c2);
     else y[i] = load_fmt(x, fmt, src);
   }
 }
 
+// ---- zero the one-pixel border of a P16 buffer (after CUDA-core producers) -------
+__global__ void k_zero_border(void* buf, int64_t Pp, int planes, int N, int H, int W) {
+  const int32_t Hp = H + 2 * kPad, Wp = W + 2 * kPad;
+  const int32_t per = 2 * Wp + 2 * H;  // border pixels per image
+  const int64_t total = static_cast<int64_t>(planes) * N * per;
+  GRID_STRIDE(i, total) {
+    int32_t b = static_cast<int32_t>(i % per);
+    int64_t t = i / per;
+    int32_t n = static_cast<int32_t>(t % N);
+    int32_t plane = static_cast<int32_t>(t / N);
+    int32_t hp, wp;
+    if (b < Wp) {
+      hp = 0;
+      wp = b;
+    } else if (b < 2 * Wp) {
+      hp = Hp - 1;
+      wp = b - Wp;
+    } else {
+      int32_t r = b - 2 * Wp;
+      hp = 1 + r / 2;
+      wp = (r & 1) ? Wp - 1 : 0;
+    }
+    int64_t pix = (static_cast<int64_t>(n) * Hp + hp) * Wp + wp;
+    reinterpret_cast<int4*>(buf)[plane * Pp + pix] = make_int4(0, 0, 0, 0);
+  }
+}
+
 // ---- hoisted weight prologue ----------------------------------------------------
 // OIHW float32 -> kernel layout.  v = w [* oc_scale[o]] [* scalar]; then
-//   I8:   code(v) at [O][KH][KW][Cs]           (K ordered kh, kw, ic; NHWC taps)
-//   BF16: bf16(v) at [O][KH][KW][Cs]
-//   F32:  v       at [O][IC][KH][KW]           (strict: reference loop order)
-__global__ void k_weight_prep(const float* __restrict__ w, int O, int I, int KH, int KW, int Cs,
-                              const float* __restrict__ oc_scale, float scalar, int fmt,
-                              int quant, QDev q, void* out) {
-  int64_t per = static_cast<int64_t>(KH) * KW * Cs;
-  int64_t total = fmt == FMT_F32 ? static_cast<int64_t>(O) * I * KH * KW : static_cast<int64_t>(O) * per;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+//   WL_ROWS (I8 / BF16): [O][KH][KW][Cs]               CUDA-core kernels
+//   WL_TC   (I8 / BF16): [KH*KW][I/cpc][O][cpc]        tcgen05 B operand (16-byte K chunks)
+//   F32 strict:          [O][I][KH][KW]                reference loop order
+__global__ void k_weight_prep(const float* __restrict__ w, int O, int I, int KH, int KW, int Cs, int wl,
+                              const float* __restrict__ oc_scale, float scalar, int fmt, int quant, QDev q,
+                              void* out) {
+  const int cpc = fmt == FMT_I8 ? 16 : 8;
+  const int planes = (I + cpc - 1) / cpc;
+  int64_t total;
+  if (fmt == FMT_F32) total = static_cast<int64_t>(O) * I * KH * KW;
+  else if (wl == WL_TC) total = static_cast<int64_t>(KH) * KW * planes * O * cpc;
+  else total = static_cast<int64_t>(O) * KH * KW * Cs;
+  GRID_STRIDE(i, total) {
     int o, ic, kh, kw;
     if (fmt == FMT_F32) {
       kw = static_cast<int>(i % KW);
@@ -81,6 +131,16 @@ __global__ void k_weight_prep(const float* __restrict__ w, int O, int I, int KH,
       t /= KH;
       ic = static_cast<int>(t % I);
       o = static_cast<int>(t / I);
+    } else if (wl == WL_TC) {
+      int within = static_cast<int>(i % cpc);
+      int64_t t = i / cpc;
+      o = static_cast<int>(t % O);
+      t /= O;
+      int plane = static_cast<int>(t % planes);
+      int tap = static_cast<int>(t / planes);
+      ic = plane * cpc + within;
+      kh = tap / KW;
+      kw = tap % KW;
     } else {
       ic = static_cast<int>(i % Cs);
       int64_t t = i / Cs;
@@ -108,13 +168,28 @@ __global__ void k_weight_prep(const float* __restrict__ w, int O, int I, int KH,
   }
 }
 
+struct OutPix {
+  int64_t m;  // logical output index (n, oh, ow)
+  int32_t n, oh, ow;
+};
+
+__device__ __forceinline__ OutPix decode_out(int64_t m, const ConvGeom& g) {
+  OutPix o;
+  o.m = m;
+  o.ow = static_cast<int32_t>(m % g.OW);
+  int64_t t = m / g.OW;
+  o.oh = static_cast<int32_t>(t % g.OH);
+  o.n = static_cast<int32_t>(t / g.OH);
+  return o;
+}
+
 // ---- convolution, int8 codes, dp4a, int32 accumulate -----------------------------
 // Implicit GEMM: M = N*OH*OW output pixels, N = OC, K = KH*KW*Cs (tap-major,
-// channel-minor, matching NHWC activations and the [O][KH][KW][Cs] weights).
-// 64x64 tile, 256 threads x (4 pixels x 4 channels), K staged 32 bytes at a time.
-// Integer accumulation is exact; the float32 conversion times acc_scale
-// (= c2_x * c2_w, a power of two) equals the reference's fake-quant fp32 conv
-// whenever every sequential partial sum stays below 2^24 quanta.
+// channel-minor).  64x64 tile, 256 threads x (4 pixels x 4 channels), K staged
+// 32 bytes at a time.  Integer accumulation is exact; the float32 conversion
+// times acc_scale (= c2_x * c2_w, a power of two) equals the reference's
+// fake-quant fp32 conv whenever every sequential partial sum stays below 2^24
+// quanta (checked statically at weight load).
 __global__ void __launch_bounds__(256) k_conv_i8_simt(const int8_t* __restrict__ x, const int8_t* __restrict__ w,
                                                       ConvGeom g, float acc_scale, EpiDev epi, OutDev out) {
   __shared__ int32_t As[8][64 + 4];
@@ -126,17 +201,9 @@ __global__ void __launch_bounds__(256) k_conv_i8_simt(const int8_t* __restrict__
   const int tm = tid & 15, tn = tid >> 4;
   const int Kw = g.Kp / 4;
   int acc[4][4] = {};
-  // per-thread A-load pixel coordinates (2 loads per stage, same pixel column)
   const int lp = tid & 63;
-  const int64_t pm = m0 + lp;
-  int pn = 0, poh = 0, pow_ = 0;
-  bool pvalid = pm < M;
-  if (pvalid) {
-    pow_ = static_cast<int>(pm % g.OW);
-    int64_t t = pm / g.OW;
-    poh = static_cast<int>(t % g.OH);
-    pn = static_cast<int>(t / g.OH);
-  }
+  const bool pvalid = m0 + lp < M;
+  const OutPix P = decode_out(pvalid ? m0 + lp : 0, g);
   for (int k0 = 0; k0 < Kw; k0 += 8) {
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
@@ -147,9 +214,9 @@ __global__ void __launch_bounds__(256) k_conv_i8_simt(const int8_t* __restrict__
         int k = word * 4;
         int tap = k / g.Cs, ic = k - tap * g.Cs;
         int kh = tap / g.KW, kwi = tap - kh * g.KW;
-        int h = poh * g.sh - g.ph + kh, ww = pow_ * g.sw - g.pw + kwi;
-        if (h >= 0 && h < g.H && ww >= 0 && ww < g.W)
-          av = *reinterpret_cast<const int32_t*>(x + ((static_cast<int64_t>(pn) * g.H + h) * g.W + ww) * g.Cs + ic);
+        int h = P.oh * g.sh - g.ph + kh, ww = P.ow * g.sw - g.pw + kwi;
+        if (ic < g.C && h >= 0 && h < g.H && ww >= 0 && ww < g.W)
+          av = *reinterpret_cast<const int32_t*>(x + lay_off(g.in, pad_pix(P.n, h, ww, g.H, g.W), ic));
       }
       As[kk][lp] = av;
       int oc = n0 + lp;
@@ -176,13 +243,15 @@ __global__ void __launch_bounds__(256) k_conv_i8_simt(const int8_t* __restrict__
   for (int i = 0; i < 4; ++i) {
     int64_t m = m0 + tm * 4 + i;
     if (m >= M) continue;
+    OutPix o = decode_out(m, g);
+    int64_t pix = pad_pix(o.n, o.oh, o.ow, g.OH, g.OW);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       int c = n0 + tn * 4 + j;
       if (c >= g.OC) continue;
       int32_t code = 0;
-      float v = apply_epi(epi, __fmul_rn(static_cast<float>(acc[i][j]), acc_scale), m, c, g.OC, &code);
-      store_out(out, v, code, m, c);
+      float v = apply_epi(epi, __fmul_rn(static_cast<float>(acc[i][j]), acc_scale), pix, c, &code);
+      store_out(out, v, code, pix, c);
     }
   }
 }
@@ -199,15 +268,8 @@ __global__ void __launch_bounds__(256) k_conv_bf16_simt(const uint16_t* __restri
   const int tm = tid & 15, tn = tid >> 4;
   float acc[4][4] = {};
   const int lp = tid & 63;
-  const int64_t pm = m0 + lp;
-  int pn = 0, poh = 0, pow_ = 0;
-  bool pvalid = pm < M;
-  if (pvalid) {
-    pow_ = static_cast<int>(pm % g.OW);
-    int64_t t = pm / g.OW;
-    poh = static_cast<int>(t % g.OH);
-    pn = static_cast<int>(t / g.OH);
-  }
+  const bool pvalid = m0 + lp < M;
+  const OutPix P = decode_out(pvalid ? m0 + lp : 0, g);
   for (int k0 = 0; k0 < g.Kp; k0 += 16) {
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
@@ -217,9 +279,9 @@ __global__ void __launch_bounds__(256) k_conv_bf16_simt(const uint16_t* __restri
       if (pvalid && k < g.Kp) {
         int tap = k / g.Cs, ic = k - tap * g.Cs;
         int kh = tap / g.KW, kwi = tap - kh * g.KW;
-        int h = poh * g.sh - g.ph + kh, ww = pow_ * g.sw - g.pw + kwi;
-        if (h >= 0 && h < g.H && ww >= 0 && ww < g.W)
-          av = bf16_to_f32(x[((static_cast<int64_t>(pn) * g.H + h) * g.W + ww) * g.Cs + ic]);
+        int h = P.oh * g.sh - g.ph + kh, ww = P.ow * g.sw - g.pw + kwi;
+        if (ic < g.C && h >= 0 && h < g.H && ww >= 0 && ww < g.W)
+          av = bf16_to_f32(x[lay_off(g.in, pad_pix(P.n, h, ww, g.H, g.W), ic)]);
       }
       As[kk][lp] = av;
       int oc = n0 + lp;
@@ -244,13 +306,15 @@ __global__ void __launch_bounds__(256) k_conv_bf16_simt(const uint16_t* __restri
   for (int i = 0; i < 4; ++i) {
     int64_t m = m0 + tm * 4 + i;
     if (m >= M) continue;
+    OutPix o = decode_out(m, g);
+    int64_t pix = pad_pix(o.n, o.oh, o.ow, g.OH, g.OW);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       int c = n0 + tn * 4 + j;
       if (c >= g.OC) continue;
       int32_t code = 0;
-      float v = apply_epi(epi, acc[i][j], m, c, g.OC, &code);
-      store_out(out, v, code, m, c);
+      float v = apply_epi(epi, acc[i][j], pix, c, &code);
+      store_out(out, v, code, pix, c);
     }
   }
 }
@@ -260,79 +324,63 @@ __global__ void __launch_bounds__(256) k_conv_bf16_simt(const uint16_t* __restri
 // (kernels.cpp:681-701), product and sum each rounded (no FMA).
 __global__ void k_conv_f32_strict(const float* __restrict__ x, const float* __restrict__ w, ConvGeom g,
                                   EpiDev epi, OutDev out) {
-  const int64_t M = static_cast<int64_t>(g.N) * g.OH * g.OW;
-  int64_t total = M * g.OC;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  const int64_t total = static_cast<int64_t>(g.N) * g.OH * g.OW * g.OC;
+  GRID_STRIDE(i, total) {
     int oc = static_cast<int>(i % g.OC);
-    int64_t m = i / g.OC;
-    int ow = static_cast<int>(m % g.OW);
-    int64_t t = m / g.OW;
-    int oh = static_cast<int>(t % g.OH);
-    int n = static_cast<int>(t / g.OH);
+    OutPix o = decode_out(i / g.OC, g);
     float facc = 0.0f;
     for (int ic = 0; ic < g.C; ++ic)
       for (int kh = 0; kh < g.KH; ++kh)
         for (int kw = 0; kw < g.KW; ++kw) {
-          int h = oh * g.sh - g.ph + kh, ww = ow * g.sw - g.pw + kw;
+          int h = o.oh * g.sh - g.ph + kh, ww = o.ow * g.sw - g.pw + kw;
           if (h < 0 || h >= g.H || ww < 0 || ww >= g.W) continue;
-          float xv = x[((static_cast<int64_t>(n) * g.H + h) * g.W + ww) * g.Cs + ic];
+          float xv = x[lay_off(g.in, pad_pix(o.n, h, ww, g.H, g.W), ic)];
           float wv = w[((static_cast<int64_t>(oc) * g.C + ic) * g.KH + kh) * g.KW + kw];
           facc = __fadd_rn(facc, __fmul_rn(xv, wv));
         }
+    int64_t pix = pad_pix(o.n, o.oh, o.ow, g.OH, g.OW);
     int32_t code = 0;
-    float v = apply_epi(epi, facc, m, oc, g.OC, &code);
-    store_out(out, v, code, m, oc);
+    float v = apply_epi(epi, facc, pix, oc, &code);
+    store_out(out, v, code, pix, oc);
   }
 }
 
 // ---- depthwise convolution (float; reference order kh -> kw) ---------------------
-__global__ void k_dwconv(const void* __restrict__ x, int xfmt, const float* __restrict__ w, ConvGeom g,
-                         int strict, EpiDev epi, OutDev out) {
-  const int64_t M = static_cast<int64_t>(g.N) * g.OH * g.OW;
-  int64_t total = M * g.C;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+__global__ void k_dwconv(const void* __restrict__ x, int xfmt, const float* __restrict__ w, ConvGeom g, int strict,
+                         EpiDev epi, OutDev out) {
+  const int64_t total = static_cast<int64_t>(g.N) * g.OH * g.OW * g.C;
+  GRID_STRIDE(i, total) {
     int c = static_cast<int>(i % g.C);
-    int64_t m = i / g.C;
-    int ow = static_cast<int>(m % g.OW);
-    int64_t t = m / g.OW;
-    int oh = static_cast<int>(t % g.OH);
-    int n = static_cast<int>(t / g.OH);
+    OutPix o = decode_out(i / g.C, g);
     float facc = 0.0f;
     for (int kh = 0; kh < g.KH; ++kh)
       for (int kw = 0; kw < g.KW; ++kw) {
-        int h = oh * g.sh - g.ph + kh, ww = ow * g.sw - g.pw + kw;
+        int h = o.oh * g.sh - g.ph + kh, ww = o.ow * g.sw - g.pw + kw;
         if (h < 0 || h >= g.H || ww < 0 || ww >= g.W) continue;
-        float xv = load_fmt(x, xfmt, ((static_cast<int64_t>(n) * g.H + h) * g.W + ww) * g.Cs + c);
+        float xv = load_fmt(x, xfmt, lay_off(g.in, pad_pix(o.n, h, ww, g.H, g.W), c));
         float wv = w[(static_cast<int64_t>(c) * g.KH + kh) * g.KW + kw];
         facc = strict ? __fadd_rn(facc, __fmul_rn(xv, wv)) : __fmaf_rn(xv, wv, facc);
       }
+    int64_t pix = pad_pix(o.n, o.oh, o.ow, g.OH, g.OW);
     int32_t code = 0;
-    float v = apply_epi(epi, facc, m, c, g.C, &code);
-    store_out(out, v, code, m, c);
+    float v = apply_epi(epi, facc, pix, c, &code);
+    store_out(out, v, code, pix, c);
   }
 }
 
 // ---- max pooling: max over valid taps, seeded with the first (harness kernel) ----
 __global__ void k_maxpool(const void* __restrict__ x, int xfmt, ConvGeom g, OutDev out) {
-  const int64_t M = static_cast<int64_t>(g.N) * g.OH * g.OW;
-  int64_t total = M * g.C;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  const int64_t total = static_cast<int64_t>(g.N) * g.OH * g.OW * g.C;
+  GRID_STRIDE(i, total) {
     int c = static_cast<int>(i % g.C);
-    int64_t m = i / g.C;
-    int ow = static_cast<int>(m % g.OW);
-    int64_t t = m / g.OW;
-    int oh = static_cast<int>(t % g.OH);
-    int n = static_cast<int>(t / g.OH);
+    OutPix o = decode_out(i / g.C, g);
     float acc = 0.f;
     bool seeded = false;
     for (int kh = 0; kh < g.KH; ++kh)
       for (int kw = 0; kw < g.KW; ++kw) {
-        int h = oh * g.sh - g.ph + kh, ww = ow * g.sw - g.pw + kw;
+        int h = o.oh * g.sh - g.ph + kh, ww = o.ow * g.sw - g.pw + kw;
         if (h < 0 || h >= g.H || ww < 0 || ww >= g.W) continue;
-        float v = load_fmt(x, xfmt, ((static_cast<int64_t>(n) * g.H + h) * g.W + ww) * g.Cs + c);
+        float v = load_fmt(x, xfmt, lay_off(g.in, pad_pix(o.n, h, ww, g.H, g.W), c));
         if (!seeded) {
           acc = v;
           seeded = true;
@@ -340,22 +388,21 @@ __global__ void k_maxpool(const void* __restrict__ x, int xfmt, ConvGeom g, OutD
           acc = acc < v ? v : acc;  // std::max(acc, v)
         }
       }
-    store_out(out, acc, 0, m, c);
+    store_out(out, acc, 0, pad_pix(o.n, o.oh, o.ow, g.OH, g.OW), c);
   }
 }
 
 // ---- sum over HW, sequential in row-major (h, w) order, seeded with the first ----
 // reduce_impl (kernels.cpp:519-566) visits the input row-major, so for a fixed
-// (n, c) the terms arrive in (h, w) order.
-__global__ void k_sum_hw(const float* __restrict__ x, int N, int HW, int C, float* __restrict__ y) {
-  int64_t total = static_cast<int64_t>(N) * C;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+// (n, c) the terms arrive in (h, w) order.  Input P16 float32, output [N, C].
+__global__ void k_sum_hw(const float* __restrict__ x, Lay L, int N, int H, int W, int C, float* __restrict__ y) {
+  const int64_t total = static_cast<int64_t>(N) * C;
+  GRID_STRIDE(i, total) {
     int c = static_cast<int>(i % C);
-    int64_t n = i / C;
-    const float* p = x + n * HW * C + c;
-    float acc = p[0];
-    for (int k = 1; k < HW; ++k) acc = __fadd_rn(acc, p[static_cast<int64_t>(k) * C]);
+    int n = static_cast<int>(i / C);
+    float acc = x[lay_off(L, pad_pix(n, 0, 0, H, W), c)];
+    for (int h = 0; h < H; ++h)
+      for (int w = (h == 0 ? 1 : 0); w < W; ++w) acc = __fadd_rn(acc, x[lay_off(L, pad_pix(n, h, w, H, W), c)]);
     y[i] = acc;
   }
 }
@@ -399,7 +446,7 @@ __global__ void k_dense(const float* __restrict__ x, int N, int K, int Kp, const
     v = acc;
   }
   int32_t code = 0;
-  v = apply_epi(epi, v, n, j, M, &code);
+  v = apply_epi(epi, v, n, j, &code);
   store_out(out, v, code, n, j);
 }
 
@@ -412,22 +459,34 @@ unsigned grid_stride_blocks(int64_t total) {
 
 }  // namespace
 
-void launch_input_convert(const float* x, int N, int C, int H, int W, void* out, int fmt, int Cs,
+void launch_input_convert(const float* x, int N, int C, int H, int W, void* out, int fmt, const Lay& L,
                           float pre_mul, QDev q, cudaStream_t s) {
-  int64_t total = static_cast<int64_t>(N) * H * W * Cs;
-  k_input_convert<<<grid_stride_blocks(total), kThreads, 0, s>>>(x, N, C, H, W, out, fmt, Cs, pre_mul, q);
+  int64_t total = static_cast<int64_t>((C + L.cpc - 1) / L.cpc) * L.Pp * L.cpc;
+  k_input_convert<<<grid_stride_blocks(total), kThreads, 0, s>>>(x, N, C, H, W, out, fmt, L, pre_mul, q);
 }
 
-void launch_nhwc_to_nchw(const void* x, int fmt, int Cs, float c2, float* y, int N, int C, int H, int W,
-                         cudaStream_t s) {
+void launch_to_nchw(const void* x, int fmt, const Lay& L, float c2, float* y, int N, int C, int H, int W, int is4d,
+                    cudaStream_t s) {
   int64_t total = static_cast<int64_t>(N) * C * H * W;
-  k_nhwc_to_nchw<<<grid_stride_blocks(total), kThreads, 0, s>>>(x, fmt, Cs, c2, y, N, C, H, W);
+  k_to_nchw<<<grid_stride_blocks(total), kThreads, 0, s>>>(x, fmt, L, c2, y, N, C, H, W, is4d);
 }
 
-void launch_weight_prep(const float* w, int O, int I, int KH, int KW, int Cs, const float* oc_scale,
+void launch_zero_border(void* buf, const Lay& L, int N, int H, int W, cudaStream_t s) {
+  int planes = (L.C + L.cpc - 1) / L.cpc;
+  int64_t total = static_cast<int64_t>(planes) * N * (2 * (W + 2 * kPad) + 2 * H);
+  k_zero_border<<<grid_stride_blocks(total), kThreads, 0, s>>>(buf, L.Pp, planes, N, H, W);
+}
+
+void launch_weight_prep(const float* w, int O, int I, int KH, int KW, int Cs, int wl, const float* oc_scale,
                         float scalar, int fmt, int quant, QDev q, void* out, cudaStream_t s) {
-  int64_t total = fmt == FMT_F32 ? static_cast<int64_t>(O) * I * KH * KW : static_cast<int64_t>(O) * KH * KW * Cs;
-  k_weight_prep<<<grid_stride_blocks(total), kThreads, 0, s>>>(w, O, I, KH, KW, Cs, oc_scale, scalar, fmt, quant, q, out);
+  int cpc = fmt == FMT_I8 ? 16 : 8;
+  int planes = (I + cpc - 1) / cpc;
+  int64_t total;
+  if (fmt == FMT_F32) total = static_cast<int64_t>(O) * I * KH * KW;
+  else if (wl == WL_TC) total = static_cast<int64_t>(KH) * KW * planes * O * cpc;
+  else total = static_cast<int64_t>(O) * KH * KW * Cs;
+  k_weight_prep<<<grid_stride_blocks(total), kThreads, 0, s>>>(w, O, I, KH, KW, Cs, wl, oc_scale, scalar, fmt, quant,
+                                                              q, out);
 }
 
 void launch_conv_i8_simt(const int8_t* x, const int8_t* w, const ConvGeom& g, float acc_scale,
@@ -461,9 +520,9 @@ void launch_maxpool(const void* x, int xfmt, const ConvGeom& g, const OutDev& ou
   k_maxpool<<<grid_stride_blocks(total), kThreads, 0, s>>>(x, xfmt, g, out);
 }
 
-void launch_sum_hw(const float* x, int N, int HW, int C, float* y, cudaStream_t s) {
+void launch_sum_hw(const float* x, const Lay& L, int N, int H, int W, int C, float* y, cudaStream_t s) {
   int64_t total = static_cast<int64_t>(N) * C;
-  k_sum_hw<<<grid_stride_blocks(total), kThreads, 0, s>>>(x, N, HW, C, y);
+  k_sum_hw<<<grid_stride_blocks(total), kThreads, 0, s>>>(x, L, N, H, W, C, y);
 }
 
 void launch_dense(const float* x, int N, int K, int Kp, const void* w, int M, int mode, float pre_mul,

@@ -9,11 +9,14 @@
 
 namespace mrb200 {
 
-void launch_input_convert(const float* x, int N, int C, int H, int W, void* out, int fmt, int Cs,
+enum WeightLayout : int { WL_ROWS = 0, WL_TC = 1 };
+
+void launch_input_convert(const float* x, int N, int C, int H, int W, void* out, int fmt, const Lay& L,
                           float pre_mul, QDev q, cudaStream_t s);
-void launch_nhwc_to_nchw(const void* x, int fmt, int Cs, float c2, float* y, int N, int C, int H, int W,
-                         cudaStream_t s);
-void launch_weight_prep(const float* w, int O, int I, int KH, int KW, int Cs, const float* oc_scale,
+void launch_to_nchw(const void* x, int fmt, const Lay& L, float c2, float* y, int N, int C, int H, int W, int is4d,
+                    cudaStream_t s);
+void launch_zero_border(void* buf, const Lay& L, int N, int H, int W, cudaStream_t s);
+void launch_weight_prep(const float* w, int O, int I, int KH, int KW, int Cs, int wl, const float* oc_scale,
                         float scalar, int fmt, int quant, QDev q, void* out, cudaStream_t s);
 void launch_conv_i8_simt(const int8_t* x, const int8_t* w, const ConvGeom& g, float acc_scale,
                          const EpiDev& epi, const OutDev& out, cudaStream_t s);
@@ -24,7 +27,7 @@ void launch_conv_f32_strict(const float* x, const float* w, const ConvGeom& g, c
 void launch_dwconv(const void* x, int xfmt, const float* w, const ConvGeom& g, int strict, const EpiDev& epi,
                    const OutDev& out, cudaStream_t s);
 void launch_maxpool(const void* x, int xfmt, const ConvGeom& g, const OutDev& out, cudaStream_t s);
-void launch_sum_hw(const float* x, int N, int HW, int C, float* y, cudaStream_t s);
+void launch_sum_hw(const float* x, const Lay& L, int N, int H, int W, int C, float* y, cudaStream_t s);
 void launch_dense(const float* x, int N, int K, int Kp, const void* w, int M, int mode, float pre_mul,
                   int quant, QDev q, float acc_scale, const EpiDev& epi, const OutDev& out, cudaStream_t s);
 
