@@ -100,6 +100,7 @@ struct Exec {
   std::vector<int> group_cs;                // weight channel stride per tap (row layouts)
   std::vector<int> group_path;              // kernel choice
   std::vector<std::string> group_exact;     // int8 exactness proof per group
+  std::vector<std::string> group_note;      // kernel plan description
   bool weights_ready = false;
   // io
   const float* cur_input = nullptr;
@@ -173,7 +174,6 @@ int64_t lay_elems(const Lay& L) {
   return (L.C + L.cpc - 1) / L.cpc * L.Pp * L.cpc;
 }
 
-int channels(const std::vector<int64_t>& s) { return s.size() >= 2 ? static_cast<int>(s[1]) : 1; }
 
 // Finds or adds a representation of value v.
 int want_rep(Exec& ex, int v, int fmt, const QParams* q) {
@@ -406,15 +406,29 @@ void build(Exec& ex) {
   Program& P = ex.P;
   const bool use_tc = !ex.opt.force_simt;
   plan(ex, use_tc);
-  // TC eligibility is decided per group at compile time.
+  // TC eligibility is decided per group at compile time (geometry only).
   for (size_t gi = 0; gi < P.groups.size(); ++gi) {
     int& path = ex.group_path[gi];
     const GroupDesc& g = P.groups[gi];
     if (path == P_CONV_I8_TC || path == P_CONV_BF16_TC) {
       int eb = path == P_CONV_I8_TC ? 1 : 2;
-      int C = static_cast<int>(g.in_shape[1]);
-      if (!tc_conv_eligible(C, static_cast<int>(g.out_shape[1]), static_cast<int>(g.kh), static_cast<int>(g.kw), eb))
-        path = path == P_CONV_I8_TC ? P_CONV_I8_SIMT : P_CONV_BF16_SIMT;
+      bool has_sum = !g.epi.empty() && g.epi.back().kind == EpiKind::SumHW;
+      const auto& os = has_sum ? g.pre_sum_shape : g.out_shape;
+      ConvGeom t{};
+      t.N = static_cast<int>(g.in_shape[0]);
+      t.C = static_cast<int>(g.in_shape[1]);
+      t.H = static_cast<int>(g.in_shape[2]);
+      t.W = static_cast<int>(g.in_shape[3]);
+      t.OC = static_cast<int>(os[1]);
+      t.OH = static_cast<int>(os[2]);
+      t.OW = static_cast<int>(os[3]);
+      t.KH = static_cast<int>(g.kh);
+      t.KW = static_cast<int>(g.kw);
+      t.sh = static_cast<int>(g.sh);
+      t.sw = static_cast<int>(g.sw);
+      t.ph = static_cast<int>(g.ph);
+      t.pw = static_cast<int>(g.pw);
+      if (!tc_conv_eligible(t, eb)) path = path == P_CONV_I8_TC ? P_CONV_I8_SIMT : P_CONV_BF16_SIMT;
     }
   }
   std::vector<GroupIO> io(P.groups.size());
@@ -626,10 +640,15 @@ void build(Exec& ex) {
         TcConvPlan* tp = tc_conv_create(geo, path == P_CONV_I8_TC ? 1 : 2);
         if (!tp) fail(MR_ERR_UNSUPPORTED_GROUP, "group %" + g.name + ": tcgen05 plan failed");
         ex.tc_plans.push_back(tp);
-        L.fn = [e, gidx, dbuf, geo, acc_scale, tp, outdev, epidev, residual_fix](cudaStream_t s) {
+        char buf[256];
+        ex.group_note.resize(P.groups.size());
+        ex.group_note[gi] = tc_conv_describe(tp, buf, sizeof(buf));
+        std::string gname = g.name;
+        L.fn = [e, gidx, dbuf, acc_scale, tp, outdev, epidev, residual_fix, gname](cudaStream_t s) {
           EpiDev d = epidev();
           residual_fix(d);
-          tc_conv_launch(tp, e->ptr(dbuf), e->group_w[gidx], acc_scale, d, outdev(), s);
+          if (!tc_conv_launch(tp, e->ptr(dbuf), e->group_w[gidx], acc_scale, d, outdev(), s))
+            fail(MR_ERR_CUDA, "group %" + gname + ": TMA descriptor encoding failed");
         };
         break;
       }
@@ -868,7 +887,7 @@ void make_describe(Exec& ex) {
     for (char c : d) esc += (c == '"' ? '\'' : c);
     os << (gi ? ", " : "") << "{\"name\": \"" << g.name << "\", \"desc\": \"" << esc << "\", \"kernel\": \""
        << path_name(ex.group_path[gi]) << "\", \"out_shape\": " << dims_str(g.out_shape) << ", \"exact\": \""
-       << ex.group_exact[gi] << "\"}";
+       << ex.group_exact[gi] << "\", \"plan\": \"" << (gi < ex.group_note.size() ? ex.group_note[gi] : "") << "\"}";
   }
   os << "], \"launches\": [";
   for (size_t i = 0; i < ex.launches.size(); ++i) {
