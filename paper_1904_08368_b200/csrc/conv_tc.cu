@@ -42,10 +42,28 @@ namespace mrb200 {
 namespace {
 
 constexpr int kTileM = 128;
-constexpr int kEpiWarps = 4;
+constexpr int kEpiWarps = 8;
 constexpr int kThreadsTc = (2 + kEpiWarps) * 32;
 constexpr int kMaxTaps = 9;
 constexpr int kSmemBudget = 227 * 1024 - 1024;
+
+enum EpiSig : int { SIG_ANY = 0, SIG_BIAS = 1, SIG_BIAS_RELU = 2, SIG_BIAS_RELU_REQ = 3, SIG_BIAS_RES_RELU = 4 };
+
+// Compile-time epilogue for the op sequences the realize/fuse passes emit.
+inline int epi_signature(const EpiDev& e, const OutDev& o) {
+  auto q_ok = [](const QDev& q) {
+    return q.lo >= -2147483520.f && q.hi <= 2147483520.f && q.lo == q.lo && q.hi == q.hi;
+  };
+  if (o.side && !q_ok(o.side_q)) return SIG_ANY;
+  if (e.n_ops == 1 && e.op[0] == E_BIAS && o.primary_fmt != FMT_I8) return SIG_BIAS;
+  if (e.n_ops == 2 && e.op[0] == E_BIAS && e.op[1] == E_RELU && o.primary_fmt != FMT_I8) return SIG_BIAS_RELU;
+  if (e.n_ops == 3 && e.op[0] == E_BIAS && e.op[1] == E_RELU && e.op[2] == E_REQ && o.primary_fmt == FMT_I8 &&
+      !o.side && q_ok(e.q[2]))
+    return SIG_BIAS_RELU_REQ;
+  if (e.n_ops == 3 && e.op[0] == E_BIAS && e.op[1] == E_RES && e.op[2] == E_RELU && o.primary_fmt != FMT_I8)
+    return SIG_BIAS_RES_RELU;
+  return SIG_ANY;
+}
 
 struct TcArgs {
   int32_t Wp, Hp, H, W;
@@ -159,15 +177,16 @@ __device__ __forceinline__ uint32_t pack4_i8(int a, int b, int c, int d) {
 }
 
 // 16 channels [c0, c0+16) of pixel q through the epilogue, stored as 16-byte chunks.
-template <int EB>
-__device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t (&raw)[16], int64_t q, bool border,
-                                               int c0) {
+// SIG selects a compile-time op sequence for the common fused groups; SIG_ANY
+// interprets EpiDev.  The arithmetic is identical either way (kernels.cuh).
+template <int EB, int SIG>
+__device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* raw, int64_t q, bool border, int c0) {
   const OutDev& o = a.out;
   const int pf = o.primary_fmt;
   if (border) {
     // padded-grid border: the zero border of the P16 output (and side codes)
-    int chunks = pf == FMT_F32 ? 4 : pf == FMT_BF16 ? 2 : 1;
-    int cpc = 16 / (pf == FMT_F32 ? 4 : pf == FMT_BF16 ? 2 : 1);
+    const int chunks = pf == FMT_F32 ? 4 : pf == FMT_BF16 ? 2 : 1;
+    const int cpc = 16 / chunks;
     for (int k = 0; k < chunks; ++k)
       *reinterpret_cast<int4*>(static_cast<char*>(o.primary) + ((static_cast<int64_t>(c0 / cpc + k) * o.plan.Pp + q) * 16)) =
           make_int4(0, 0, 0, 0);
@@ -185,64 +204,94 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t (
     code[i] = 0;
   }
   const EpiDev& e = a.epi;
-  for (int k = 0; k < e.n_ops; ++k) {
-    const int op = e.op[k];
-    if (op == E_MULS) {
+  auto vec16 = [&](const float* base, float (&t)[16]) {
+    const float4* p = reinterpret_cast<const float4*>(base + c0);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = __fmul_rn(v[i], e.s[k]);
-    } else if (op == E_MULC || op == E_BIAS) {
-      const float4* p = reinterpret_cast<const float4*>(e.vec[k] + c0);
-      float t[16];
+    for (int j = 0; j < 4; ++j) {
+      float4 f = __ldg(p + j);
+      t[4 * j] = f.x; t[4 * j + 1] = f.y; t[4 * j + 2] = f.z; t[4 * j + 3] = f.w;
+    }
+  };
+  auto res16 = [&](int k, float (&t)[16]) {
+    const Lay& L = e.res_lay[k];
+    if (e.res_fmt[k] == FMT_F32) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        float4 f = __ldg(p + j);
+        float4 f = *reinterpret_cast<const float4*>(static_cast<const char*>(e.res[k]) +
+                                                    (static_cast<int64_t>(c0 / 4 + j) * L.Pp + q) * 16);
         t[4 * j] = f.x; t[4 * j + 1] = f.y; t[4 * j + 2] = f.z; t[4 * j + 3] = f.w;
       }
-      if (op == E_MULC) {
+    } else {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = __fmul_rn(v[i], t[i]);
-      } else {
+      for (int j = 0; j < 2; ++j) {
+        uint4 u = *reinterpret_cast<const uint4*>(static_cast<const char*>(e.res[k]) +
+                                                  (static_cast<int64_t>(c0 / 8 + j) * L.Pp + q) * 16);
+        uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          t[8 * j + 2 * h] = __uint_as_float(w4[h] << 16);
+          t[8 * j + 2 * h + 1] = __uint_as_float(w4[h] & 0xffff0000u);
+        }
+      }
+    }
+  };
+  if constexpr (SIG == SIG_ANY) {
+    for (int k = 0; k < e.n_ops; ++k) {
+      const int op = e.op[k];
+      if (op == E_MULS) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = __fmul_rn(v[i], e.s[k]);
+      } else if (op == E_MULC || op == E_BIAS) {
+        float t[16];
+        vec16(e.vec[k], t);
+        if (op == E_MULC) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = __fmul_rn(v[i], t[i]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = __fadd_rn(v[i], t[i]);
+        }
+      } else if (op == E_RES) {
+        float t[16];
+        res16(k, t);
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = __fadd_rn(v[i], t[i]);
-      }
-    } else if (op == E_RES) {
-      float t[16];
-      const Lay& L = e.res_lay[k];
-      if (e.res_fmt[k] == FMT_F32) {
+      } else if (op == E_RELU) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          float4 f = *reinterpret_cast<const float4*>(static_cast<const char*>(e.res[k]) +
-                                                      (static_cast<int64_t>(c0 / 4 + j) * L.Pp + q) * 16);
-          t[4 * j] = f.x; t[4 * j + 1] = f.y; t[4 * j + 2] = f.z; t[4 * j + 3] = f.w;
+        for (int i = 0; i < 16; ++i) v[i] = relu_ref(v[i]);
+      } else if (op == E_REQ) {
+        const QDev qd = e.q[k];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          code[i] = quant_code(v[i], qd);
+          v[i] = __fmul_rn(static_cast<float>(code[i]), qd.c2);
         }
-      } else {
+      } else if (op == E_CLIP) {
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          uint4 u = *reinterpret_cast<const uint4*>(static_cast<const char*>(e.res[k]) +
-                                                    (static_cast<int64_t>(c0 / 8 + j) * L.Pp + q) * 16);
-          uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-          for (int h = 0; h < 4; ++h) {
-            t[8 * j + 2 * h] = __uint_as_float(w4[h] << 16);
-            t[8 * j + 2 * h + 1] = __uint_as_float(w4[h] & 0xffff0000u);
-          }
-        }
+        for (int i = 0; i < 16; ++i) v[i] = clip_ref(v[i], e.s[k], e.s2[k]);
       }
+    }
+  } else {
+    // op 0 is always bias_add for the specialised signatures
+    float t[16];
+    vec16(e.vec[0], t);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = __fadd_rn(v[i], t[i]);
-    } else if (op == E_RELU) {
+    for (int i = 0; i < 16; ++i) v[i] = __fadd_rn(v[i], t[i]);
+    if constexpr (SIG == SIG_BIAS_RES_RELU) {
+      float r[16];
+      res16(1, r);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = __fadd_rn(v[i], r[i]);
+    }
+    if constexpr (SIG == SIG_BIAS_RELU || SIG == SIG_BIAS_RELU_REQ || SIG == SIG_BIAS_RES_RELU) {
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = relu_ref(v[i]);
-    } else if (op == E_REQ) {
-      const QDev qd = e.q[k];
+    }
+    if constexpr (SIG == SIG_BIAS_RELU_REQ) {
+      const QDev qd = e.q[2];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        code[i] = quant_code(v[i], qd);
-        v[i] = __fmul_rn(static_cast<float>(code[i]), qd.c2);
-      }
-    } else if (op == E_CLIP) {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = clip_ref(v[i], e.s[k], e.s2[k]);
+      for (int i = 0; i < 16; ++i) code[i] = quant_code_fast(v[i], qd);
+      // v (= code * c2) is only needed for a side output, never emitted here
     }
   }
   char* prim = static_cast<char*>(o.primary);
@@ -268,16 +317,16 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t (
     }
   }
   if (o.side) {
-    int s[16];
+    int sc[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) s[i] = quant_code(v[i], o.side_q);
-    uint4 u = make_uint4(pack4_i8(s[0], s[1], s[2], s[3]), pack4_i8(s[4], s[5], s[6], s[7]),
-                         pack4_i8(s[8], s[9], s[10], s[11]), pack4_i8(s[12], s[13], s[14], s[15]));
+    for (int i = 0; i < 16; ++i) sc[i] = quant_code_fast(v[i], o.side_q);
+    uint4 u = make_uint4(pack4_i8(sc[0], sc[1], sc[2], sc[3]), pack4_i8(sc[4], sc[5], sc[6], sc[7]),
+                         pack4_i8(sc[8], sc[9], sc[10], sc[11]), pack4_i8(sc[12], sc[13], sc[14], sc[15]));
     *reinterpret_cast<uint4*>(reinterpret_cast<char*>(o.side) + (static_cast<int64_t>(c0 / 16) * o.slay.Pp + q) * 16) = u;
   }
 }
 
-template <int EB>
+template <int EB, int SIG>
 __global__ void __launch_bounds__(kThreadsTc, 1)
     k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -395,8 +444,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     }
   } else {
     // ===== epilogue warps =====
-    const int quarter = warp & 3;  // TMEM lanes [32*quarter, +32)
+    // warp w (2..9): TMEM lane quarter w % 4 (hardware lane-access rule),
+    // column half (w - 2) / 4.
+    const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
     const int row = quarter * 32 + lane;
+    const int cols = a.bn / 2;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int mt = m_start; mt < a.m_tiles; mt += m_step) {
@@ -410,11 +463,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         int hp = static_cast<int>((q / a.Wp) % a.Hp);
         border = wp == 0 || wp == a.Wp - 1 || hp == 0 || hp == a.Hp - 1;
       }
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * a.bn);
-      for (int c = 0; c < a.bn; c += 16) {
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+                             static_cast<uint32_t>(acc * a.bn + half * cols);
+      for (int c = 0; c < cols; c += 16) {
         uint32_t raw[16];
         tmem_ld16(taddr + static_cast<uint32_t>(c), raw);  // warp-collective: every lane executes it
-        if (valid) epilogue_chunk<EB>(a, raw, q, border, n_tile * a.bn + c);
+        if (valid) epilogue_chunk<EB, SIG>(a, raw, q, border, n_tile * a.bn + half * cols + c);
       }
       tc_fence_before();
       __syncwarp();
@@ -618,13 +672,27 @@ bool tc_conv_launch(TcConvPlan* p, const void* x, const void* w, float acc_scale
   a.acc_scale = acc_scale;
   a.epi = epi;
   a.out = out;
-  if (p->eb == 1) {
-    cudaFuncSetAttribute(k_conv_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p->smem));
-    k_conv_tc<1><<<p->grid, kThreadsTc, p->smem, s>>>(p->tmA, p->tmB, a);
-  } else {
-    cudaFuncSetAttribute(k_conv_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p->smem));
-    k_conv_tc<2><<<p->grid, kThreadsTc, p->smem, s>>>(p->tmA, p->tmB, a);
+  const int sig = epi_signature(epi, out);
+#define MRB_TC_LAUNCH(EB_, SIG_)                                                                          \
+  do {                                                                                                    \
+    cudaFuncSetAttribute(k_conv_tc<EB_, SIG_>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p->smem)); \
+    k_conv_tc<EB_, SIG_><<<p->grid, kThreadsTc, p->smem, s>>>(p->tmA, p->tmB, a);                       \
+  } while (0)
+#define MRB_TC_SIGS(EB_)                                          \
+  switch (sig) {                                                  \
+    case SIG_BIAS: MRB_TC_LAUNCH(EB_, SIG_BIAS); break;           \
+    case SIG_BIAS_RELU: MRB_TC_LAUNCH(EB_, SIG_BIAS_RELU); break; \
+    case SIG_BIAS_RELU_REQ: MRB_TC_LAUNCH(EB_, SIG_BIAS_RELU_REQ); break; \
+    case SIG_BIAS_RES_RELU: MRB_TC_LAUNCH(EB_, SIG_BIAS_RES_RELU); break; \
+    default: MRB_TC_LAUNCH(EB_, SIG_ANY); break;                  \
   }
+  if (p->eb == 1) {
+    MRB_TC_SIGS(1)
+  } else {
+    MRB_TC_SIGS(2)
+  }
+#undef MRB_TC_SIGS
+#undef MRB_TC_LAUNCH
   return true;
 }
 

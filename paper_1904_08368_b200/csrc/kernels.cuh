@@ -106,6 +106,16 @@ __host__ __device__ __forceinline__ int64_t lay_off(const Lay& L, int64_t pix, i
   return (static_cast<int64_t>(c / L.cpc) * L.Pp + pix) * L.cpc + (c % L.cpc);
 }
 
+// quant_code when the clip bounds lie inside int32 (every realize site:
+// [-128, 127] or [0, 255]): the clipped value is integral, so the truncating
+// cast is exact and the wrap to 8 bits is a plain narrowing.  NaN: clip keeps
+// NaN, cvt.rzi gives 0 == the reference's INT64_MIN & 0xff.
+__device__ __forceinline__ int32_t quant_code_fast(float v, const QDev& q) {
+  float t = clip_ref(rintf(__fmul_rn(v, q.c1)), q.lo, q.hi);
+  int32_t k = __float2int_rz(t);
+  return q.is_signed ? static_cast<int32_t>(static_cast<int8_t>(k)) : (k & 0xff);
+}
+
 __device__ __forceinline__ float load_fmt(const void* p, int32_t fmt, int64_t i) {
   if (fmt == FMT_F32) return static_cast<const float*>(p)[i];
   return bf16_to_f32(static_cast<const uint16_t*>(p)[i]);

@@ -38,26 +38,50 @@ __device__ __forceinline__ Pix decode_pix(int64_t pix, int32_t H, int32_t W) {
 }
 
 // ---- boundary: NCHW float32 -> P16 -----------------------------------------------
-// Writes every element of the padded buffer (zeros on the border and in the
-// channel padding of the last chunk).
+// One thread per 16-byte output chunk (cpc channels of one padded pixel);
+// consecutive threads take consecutive pixels, so the NCHW reads coalesce per
+// channel and the stores are contiguous.  Zeros on the border and in the
+// channel padding of the last chunk.
 __global__ void k_input_convert(const float* __restrict__ x, int N, int C, int H, int W, void* out, int fmt,
                                 Lay L, float pre_mul, QDev q) {
-  const int64_t total = static_cast<int64_t>((C + L.cpc - 1) / L.cpc) * L.Pp * L.cpc;
+  const int planes = (C + L.cpc - 1) / L.cpc;
+  const int64_t total = static_cast<int64_t>(planes) * L.Pp;
   GRID_STRIDE(i, total) {
-    int32_t within = static_cast<int32_t>(i % L.cpc);
-    int64_t t = i / L.cpc;
-    int64_t pix = t % L.Pp;
-    int32_t c = static_cast<int32_t>(t / L.Pp) * L.cpc + within;
+    int64_t pix = i % L.Pp;
+    int32_t c0 = static_cast<int32_t>(i / L.Pp) * L.cpc;
     Pix p = decode_pix(pix, H, W);
-    bool live = !p.border && c < C;
-    float v = live ? x[((static_cast<int64_t>(p.n) * C + c) * H + p.h) * W + p.w] : 0.f;
-    if (pre_mul != 0.f && live) v = __fmul_rn(v, pre_mul);
+    float v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      v[k] = 0.f;
+      if (k < L.cpc && !p.border && c0 + k < C) {
+        v[k] = x[((static_cast<int64_t>(p.n) * C + c0 + k) * H + p.h) * W + p.w];
+        if (pre_mul != 0.f) v[k] = __fmul_rn(v[k], pre_mul);
+      }
+    }
+    char* dst = static_cast<char*>(out) + i * 16;
     if (fmt == FMT_F32) {
-      static_cast<float*>(out)[i] = v;
+      *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
     } else if (fmt == FMT_BF16) {
-      static_cast<uint16_t*>(out)[i] = f32_to_bf16(v);
+      uint32_t w4[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h)
+        w4[h] = static_cast<uint32_t>(f32_to_bf16(v[2 * h])) | (static_cast<uint32_t>(f32_to_bf16(v[2 * h + 1])) << 16);
+      *reinterpret_cast<uint4*>(dst) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
     } else {
-      static_cast<int8_t*>(out)[i] = live ? static_cast<int8_t>(quant_code(v, q)) : 0;
+      uint32_t w4[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        uint32_t u = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          int k = 4 * h + b;
+          int32_t code = (!p.border && c0 + k < C) ? quant_code(v[k], q) : 0;
+          u |= (static_cast<uint32_t>(code) & 0xff) << (8 * b);
+        }
+        w4[h] = u;
+      }
+      *reinterpret_cast<uint4*>(dst) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
     }
   }
 }
@@ -369,26 +393,62 @@ __global__ void k_dwconv(const void* __restrict__ x, int xfmt, const float* __re
 }
 
 // ---- max pooling: max over valid taps, seeded with the first (harness kernel) ----
+// One thread per (output pixel, 16-byte input chunk): 16-byte loads per tap,
+// 16-byte stores, plus the consumers' int8 codes (side) when requested.
 __global__ void k_maxpool(const void* __restrict__ x, int xfmt, ConvGeom g, OutDev out) {
-  const int64_t total = static_cast<int64_t>(g.N) * g.OH * g.OW * g.C;
+  const int cpc = g.in.cpc;
+  const int planes = (g.C + cpc - 1) / cpc;
+  const int64_t M = static_cast<int64_t>(g.N) * g.OH * g.OW;
+  const int64_t total = M * planes;
   GRID_STRIDE(i, total) {
-    int c = static_cast<int>(i % g.C);
-    OutPix o = decode_out(i / g.C, g);
-    float acc = 0.f;
+    int64_t m = i % M;
+    int plane = static_cast<int>(i / M);
+    OutPix o = decode_out(m, g);
+    float acc[8];
     bool seeded = false;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k] = 0.f;
     for (int kh = 0; kh < g.KH; ++kh)
       for (int kw = 0; kw < g.KW; ++kw) {
         int h = o.oh * g.sh - g.ph + kh, ww = o.ow * g.sw - g.pw + kw;
         if (h < 0 || h >= g.H || ww < 0 || ww >= g.W) continue;
-        float v = load_fmt(x, xfmt, lay_off(g.in, pad_pix(o.n, h, ww, g.H, g.W), c));
-        if (!seeded) {
-          acc = v;
-          seeded = true;
+        const char* src = static_cast<const char*>(x) + (plane * g.in.Pp + pad_pix(o.n, h, ww, g.H, g.W)) * 16;
+        float v[8];
+        if (xfmt == FMT_F32) {
+          float4 f = *reinterpret_cast<const float4*>(src);
+          v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
         } else {
-          acc = acc < v ? v : acc;  // std::max(acc, v)
+          uint4 u = *reinterpret_cast<const uint4*>(src);
+          uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            v[2 * b] = __uint_as_float(w4[b] << 16);
+            v[2 * b + 1] = __uint_as_float(w4[b] & 0xffff0000u);
+          }
         }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          if (k >= cpc) break;
+          acc[k] = !seeded ? v[k] : (acc[k] < v[k] ? v[k] : acc[k]);  // std::max(acc, v)
+        }
+        seeded = true;
       }
-    store_out(out, acc, 0, pad_pix(o.n, o.oh, o.ow, g.OH, g.OW), c);
+    int64_t pix = pad_pix(o.n, o.oh, o.ow, g.OH, g.OW);
+    char* dst = static_cast<char*>(out.primary) + (plane * out.plan.Pp + pix) * 16;
+    if (out.primary_fmt == FMT_F32) {
+      *reinterpret_cast<float4*>(dst) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    } else {
+      uint32_t w4[4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        w4[b] = static_cast<uint32_t>(f32_to_bf16(acc[2 * b])) | (static_cast<uint32_t>(f32_to_bf16(acc[2 * b + 1])) << 16);
+      *reinterpret_cast<uint4*>(dst) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+    }
+    if (out.side) {
+      int c0 = plane * cpc;
+      for (int k = 0; k < cpc; ++k)
+        if (c0 + k < g.C) out.side[lay_off(out.slay, pix, c0 + k)] = static_cast<int8_t>(quant_code(acc[k], out.side_q));
+    }
   }
 }
 
@@ -461,7 +521,7 @@ unsigned grid_stride_blocks(int64_t total) {
 
 void launch_input_convert(const float* x, int N, int C, int H, int W, void* out, int fmt, const Lay& L,
                           float pre_mul, QDev q, cudaStream_t s) {
-  int64_t total = static_cast<int64_t>((C + L.cpc - 1) / L.cpc) * L.Pp * L.cpc;
+  int64_t total = static_cast<int64_t>((C + L.cpc - 1) / L.cpc) * L.Pp;
   k_input_convert<<<grid_stride_blocks(total), kThreads, 0, s>>>(x, N, C, H, W, out, fmt, L, pre_mul, q);
 }
 
@@ -516,7 +576,7 @@ void launch_dwconv(const void* x, int xfmt, const float* w, const ConvGeom& g, i
 }
 
 void launch_maxpool(const void* x, int xfmt, const ConvGeom& g, const OutDev& out, cudaStream_t s) {
-  int64_t total = static_cast<int64_t>(g.N) * g.OH * g.OW * g.C;
+  int64_t total = static_cast<int64_t>(g.N) * g.OH * g.OW * ((g.C + g.in.cpc - 1) / g.in.cpc);
   k_maxpool<<<grid_stride_blocks(total), kThreads, 0, s>>>(x, xfmt, g, out);
 }
 
