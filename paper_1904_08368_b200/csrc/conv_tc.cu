@@ -32,8 +32,10 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <vector>
 
 #include "conv_tc.hpp"
 
@@ -44,7 +46,6 @@ namespace {
 constexpr int kTileM = 128;
 constexpr int kEpiWarps = 8;
 constexpr int kThreadsTc = (2 + kEpiWarps) * 32;
-constexpr int kMaxTaps = 9;
 constexpr int kSmemBudget = 227 * 1024 - 1024;
 
 enum EpiSig : int { SIG_ANY = 0, SIG_BIAS = 1, SIG_BIAS_RELU = 2, SIG_BIAS_RELU_REQ = 3, SIG_BIAS_RES_RELU = 4 };
@@ -54,7 +55,7 @@ inline int epi_signature(const EpiDev& e, const OutDev& o) {
   auto q_ok = [](const QDev& q) {
     return q.lo >= -2147483520.f && q.hi <= 2147483520.f && q.lo == q.lo && q.hi == q.hi;
   };
-  if (o.side && !q_ok(o.side_q)) return SIG_ANY;
+  if (o.side && o.side_fmt == FMT_I8 && !q_ok(o.side_q)) return SIG_ANY;
   if (e.n_ops == 1 && e.op[0] == E_BIAS && o.primary_fmt != FMT_I8) return SIG_BIAS;
   if (e.n_ops == 2 && e.op[0] == E_BIAS && e.op[1] == E_RELU && o.primary_fmt != FMT_I8) return SIG_BIAS_RELU;
   if (e.n_ops == 3 && e.op[0] == E_BIAS && e.op[1] == E_RELU && e.op[2] == E_REQ && o.primary_fmt == FMT_I8 &&
@@ -65,16 +66,30 @@ inline int epi_signature(const EpiDev& e, const OutDev& o) {
   return SIG_ANY;
 }
 
+constexpr int kMaxSteps = 40;
+
+// One tcgen05.mma of a tile's K loop: byte offsets (relative to the A stage
+// base + row shift, and to the B stage / resident base) and the leading byte
+// offsets (distance between the two 16-byte K halves of the instruction).
+struct MmaStep {
+  uint32_t a_off, a_lbo, b_off, b_lbo;
+};
+
+enum OutMode : int32_t { OUT_SAME = 0, OUT_REMAP = 1 };
+
 struct TcArgs {
-  int32_t Wp, Hp, H, W;
-  int64_t Pp;           // pixels per plane (input grid == output grid)
-  int32_t m_tiles, n_tiles, Cc, pps, k_stages, halo;
-  int32_t taps;
-  int32_t delta[kMaxTaps];  // tap row offset inside the halo
-  int32_t bn;
+  // M grid: the pixel grid of the A source (padded grid, phase grid, s2d grid)
+  int32_t N, Hg, Wg;
+  int64_t Pg;  // N*Hg*Wg
+  int32_t m_tiles, n_tiles, bn, Cc, pps, k_stages, sub0, subs, hg;
+  int32_t dmin;  // smallest tap row offset (tile row 0 + dmin = first halo row)
+  int32_t n_steps;
+  MmaStep steps[kMaxSteps];
+  uint32_t b_ks_stride;  // resident B: bytes between consecutive K stages
   int32_t resident_b;
   int32_t a_stage_bytes, b_stage_bytes, b_res_bytes, n_stages;
   uint32_t idesc;
+  int32_t out_mode, OH, OW;  // OUT_REMAP: valid outputs are grid (y < OH, x < OW)
   float acc_scale;
   EpiDev epi;
   OutDev out;
@@ -176,23 +191,33 @@ __device__ __forceinline__ uint32_t pack4_i8(int a, int b, int c, int d) {
          ((static_cast<uint32_t>(c) & 0xff) << 16) | ((static_cast<uint32_t>(d) & 0xff) << 24);
 }
 
-// 16 channels [c0, c0+16) of pixel q through the epilogue, stored as 16-byte chunks.
-// SIG selects a compile-time op sequence for the common fused groups; SIG_ANY
-// interprets EpiDev.  The arithmetic is identical either way (kernels.cuh).
+// Where one output row (pixel) of the tile lands.
+struct RowDst {
+  int64_t pix;        // NORMAL padded-grid index of the output pixel (primary, residual)
+  int64_t side_base;  // side chunk index of plane 0
+  int64_t side_pstride;
+  bool border;        // OUT_SAME: padded-grid border -> zeros
+};
+
+__device__ __forceinline__ void store16(void* base, int64_t chunk, uint4 v) {
+  *reinterpret_cast<uint4*>(static_cast<char*>(base) + chunk * 16) = v;
+}
+
+// 16 channels [c0, c0+16) of one output pixel through the epilogue, stored as
+// 16-byte chunks.  SIG selects a compile-time op sequence for the common
+// fused groups; SIG_ANY interprets EpiDev.  The arithmetic is identical either
+// way (kernels.cuh).
 template <int EB, int SIG>
-__device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* raw, int64_t q, bool border, int c0) {
+__device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* raw, const RowDst& d, int c0) {
   const OutDev& o = a.out;
   const int pf = o.primary_fmt;
-  if (border) {
-    // padded-grid border: the zero border of the P16 output (and side codes)
-    const int chunks = pf == FMT_F32 ? 4 : pf == FMT_BF16 ? 2 : 1;
-    const int cpc = 16 / chunks;
-    for (int k = 0; k < chunks; ++k)
-      *reinterpret_cast<int4*>(static_cast<char*>(o.primary) + ((static_cast<int64_t>(c0 / cpc + k) * o.plan.Pp + q) * 16)) =
-          make_int4(0, 0, 0, 0);
+  const int pcpc = pf == FMT_F32 ? 4 : pf == FMT_BF16 ? 8 : 16;
+  const int scpc = o.side_fmt == FMT_BF16 ? 8 : 16;
+  if (d.border) {
+    for (int k = 0; k < 16 / pcpc; ++k) store16(o.primary, (c0 / pcpc + k) * o.plan.Pp + d.pix, make_uint4(0, 0, 0, 0));
     if (o.side)
-      *reinterpret_cast<int4*>(reinterpret_cast<char*>(o.side) + ((static_cast<int64_t>(c0 / 16) * o.slay.Pp + q) * 16)) =
-          make_int4(0, 0, 0, 0);
+      for (int k = 0; k < 16 / scpc; ++k)
+        store16(o.side, d.side_base + (c0 / scpc + k) * d.side_pstride, make_uint4(0, 0, 0, 0));
     return;
   }
   float v[16];
@@ -218,14 +243,14 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         float4 f = *reinterpret_cast<const float4*>(static_cast<const char*>(e.res[k]) +
-                                                    (static_cast<int64_t>(c0 / 4 + j) * L.Pp + q) * 16);
+                                                    (static_cast<int64_t>(c0 / 4 + j) * L.Pp + d.pix) * 16);
         t[4 * j] = f.x; t[4 * j + 1] = f.y; t[4 * j + 2] = f.z; t[4 * j + 3] = f.w;
       }
     } else {
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         uint4 u = *reinterpret_cast<const uint4*>(static_cast<const char*>(e.res[k]) +
-                                                  (static_cast<int64_t>(c0 / 8 + j) * L.Pp + q) * 16);
+                                                  (static_cast<int64_t>(c0 / 8 + j) * L.Pp + d.pix) * 16);
         uint32_t w4[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
@@ -294,16 +319,16 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
       // v (= code * c2) is only needed for a side output, never emitted here
     }
   }
-  char* prim = static_cast<char*>(o.primary);
   if (pf == FMT_I8) {
-    uint4 u = make_uint4(pack4_i8(code[0], code[1], code[2], code[3]), pack4_i8(code[4], code[5], code[6], code[7]),
-                         pack4_i8(code[8], code[9], code[10], code[11]), pack4_i8(code[12], code[13], code[14], code[15]));
-    *reinterpret_cast<uint4*>(prim + (static_cast<int64_t>(c0 / 16) * o.plan.Pp + q) * 16) = u;
+    store16(o.primary, (c0 / 16) * o.plan.Pp + d.pix,
+            make_uint4(pack4_i8(code[0], code[1], code[2], code[3]), pack4_i8(code[4], code[5], code[6], code[7]),
+                       pack4_i8(code[8], code[9], code[10], code[11]), pack4_i8(code[12], code[13], code[14], code[15])));
   } else if (pf == FMT_F32) {
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-      *reinterpret_cast<float4*>(prim + (static_cast<int64_t>(c0 / 4 + j) * o.plan.Pp + q) * 16) =
-          make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      store16(o.primary, (c0 / 4 + j) * o.plan.Pp + d.pix,
+              make_uint4(__float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]), __float_as_uint(v[4 * j + 2]),
+                         __float_as_uint(v[4 * j + 3])));
   } else {
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
@@ -312,19 +337,32 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
       for (int h = 0; h < 4; ++h)
         w4[h] = static_cast<uint32_t>(f32_to_bf16(v[8 * j + 2 * h])) |
                 (static_cast<uint32_t>(f32_to_bf16(v[8 * j + 2 * h + 1])) << 16);
-      *reinterpret_cast<uint4*>(prim + (static_cast<int64_t>(c0 / 8 + j) * o.plan.Pp + q) * 16) =
-          make_uint4(w4[0], w4[1], w4[2], w4[3]);
+      store16(o.primary, (c0 / 8 + j) * o.plan.Pp + d.pix, make_uint4(w4[0], w4[1], w4[2], w4[3]));
     }
   }
   if (o.side) {
-    int sc[16];
+    if (o.side_fmt == FMT_I8) {
+      int sc[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) sc[i] = quant_code_fast(v[i], o.side_q);
-    uint4 u = make_uint4(pack4_i8(sc[0], sc[1], sc[2], sc[3]), pack4_i8(sc[4], sc[5], sc[6], sc[7]),
-                         pack4_i8(sc[8], sc[9], sc[10], sc[11]), pack4_i8(sc[12], sc[13], sc[14], sc[15]));
-    *reinterpret_cast<uint4*>(reinterpret_cast<char*>(o.side) + (static_cast<int64_t>(c0 / 16) * o.slay.Pp + q) * 16) = u;
+      for (int i = 0; i < 16; ++i) sc[i] = quant_code_fast(v[i], o.side_q);
+      store16(o.side, d.side_base + (c0 / 16) * d.side_pstride,
+              make_uint4(pack4_i8(sc[0], sc[1], sc[2], sc[3]), pack4_i8(sc[4], sc[5], sc[6], sc[7]),
+                         pack4_i8(sc[8], sc[9], sc[10], sc[11]), pack4_i8(sc[12], sc[13], sc[14], sc[15])));
+    } else {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        uint32_t w4[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h)
+          w4[h] = static_cast<uint32_t>(f32_to_bf16(v[8 * j + 2 * h])) |
+                  (static_cast<uint32_t>(f32_to_bf16(v[8 * j + 2 * h + 1])) << 16);
+        store16(o.side, d.side_base + (c0 / 8 + j) * d.side_pstride, make_uint4(w4[0], w4[1], w4[2], w4[3]));
+      }
+    }
   }
 }
+
+__device__ __forceinline__ int floor_div8(int v) { return v >= 0 ? v / 8 : -((7 - v) / 8); }
 
 template <int EB, int SIG>
 __global__ void __launch_bounds__(kThreadsTc, 1)
@@ -378,20 +416,19 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       // ===== TMA producer =====
       if (a.resident_b) {
         mbar_expect_tx(bfull, a.b_res_bytes);
-        tma_load_4d(smB, &tmB, bfull, 0, n_tile * a.bn, 0, 0);
+        tma_load_4d(smB, &tmB, bfull, 0, n_tile * a.bn / 8, 0, 0);
       }
       int stage = 0;
       uint32_t phase = 0;
       for (int mt = m_start; mt < a.m_tiles; mt += m_step) {
-        const int64_t q0 = static_cast<int64_t>(mt) * kTileM;
-        const int row0 = static_cast<int>(q0 - (a.taps > 1 ? a.Wp + 1 : 0));
+        const int row0 = mt * kTileM + a.dmin;
+        const int g0 = floor_div8(row0);
         for (int ks = 0; ks < a.k_stages; ++ks) {
           mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* dA = smA + stage * a.a_stage_bytes;
           mbar_expect_tx(&full[stage], a.a_stage_bytes + (a.resident_b ? 0 : a.b_stage_bytes));
-          tma_load_3d(dA, &tmA, &full[stage], 0, row0, ks * a.pps);
+          tma_load_4d(smA + stage * a.a_stage_bytes, &tmA, &full[stage], 0, g0, a.sub0, ks * a.pps);
           if (!a.resident_b)
-            tma_load_4d(smB + stage * a.b_stage_bytes, &tmB, &full[stage], 0, n_tile * a.bn, ks * a.pps, 0);
+            tma_load_4d(smB + stage * a.b_stage_bytes, &tmB, &full[stage], 0, n_tile * a.bn / 8, ks * a.pps, 0);
           if (++stage == a.n_stages) {
             stage = 0;
             phase ^= 1;
@@ -403,31 +440,27 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     if (lane == 0) {
       // ===== MMA issuer (one thread) =====
       if (a.resident_b) mbar_wait(bfull, 0);
-      const uint32_t a_plane = static_cast<uint32_t>(a.halo) * 16;  // LBO of A
-      const uint32_t b_plane = static_cast<uint32_t>(a.bn) * 16;    // LBO of B
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      const uint32_t smB_u = smem_u32(smB);
+      const uint32_t smA_u = smem_u32(smA);
       for (int mt = m_start; mt < a.m_tiles; mt += m_step) {
+        const int row0 = mt * kTileM + a.dmin;
+        const uint32_t shift16 = static_cast<uint32_t>(row0 - 8 * floor_div8(row0)) * 16;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * a.bn);
         for (int ks = 0; ks < a.k_stages; ++ks) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t sA = smem_u32(smA + stage * a.a_stage_bytes);
-          const uint32_t sB = a.resident_b ? smem_u32(smB) : smem_u32(smB + stage * a.b_stage_bytes);
-          for (int t = 0; t < a.taps; ++t) {
-            for (int kp = 0; kp < a.pps; kp += 2) {
-              const uint32_t aaddr = sA + static_cast<uint32_t>(kp) * a_plane + static_cast<uint32_t>(a.delta[t]) * 16;
-              uint32_t bplane;
-              if (a.resident_b) bplane = static_cast<uint32_t>(t * a.Cc + ks * a.pps + kp);
-              else bplane = static_cast<uint32_t>(t * a.pps + kp);
-              const uint32_t baddr = sB + bplane * b_plane;
-              const uint32_t accum = (ks | t | kp) != 0 ? 1u : 0u;
-              umma<EB>(tmem_d, umma_desc(aaddr, a_plane, 128), umma_desc(baddr, b_plane, 128), a.idesc, accum);
-            }
+          const uint32_t sA = smA_u + stage * a.a_stage_bytes + shift16;
+          const uint32_t sB = a.resident_b ? smB_u + ks * a.b_ks_stride : smB_u + stage * a.b_stage_bytes;
+          for (int st = 0; st < a.n_steps; ++st) {
+            const MmaStep m = a.steps[st];
+            umma<EB>(tmem_d, umma_desc(sA + m.a_off, m.a_lbo, 128), umma_desc(sB + m.b_off, m.b_lbo, 128), a.idesc,
+                     (ks | st) != 0 ? 1u : 0u);
           }
           umma_commit(&empty[stage]);  // frees the smem stage when these MMAs retire
           if (++stage == a.n_stages) {
@@ -450,25 +483,49 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     const int half = (warp - 2) >> 2;
     const int row = quarter * 32 + lane;
     const int cols = a.bn / 2;
+    const Lay& sl = a.out.slay;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int mt = m_start; mt < a.m_tiles; mt += m_step) {
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int64_t q = static_cast<int64_t>(mt) * kTileM + row;
-      bool valid = q < a.Pp;
-      bool border = true;
+      RowDst d;
+      bool valid = q < a.Pg;
+      d.border = false;
+      d.pix = 0;
       if (valid) {
-        int wp = static_cast<int>(q % a.Wp);
-        int hp = static_cast<int>((q / a.Wp) % a.Hp);
-        border = wp == 0 || wp == a.Wp - 1 || hp == 0 || hp == a.Hp - 1;
+        const int x = static_cast<int>(q % a.Wg);
+        const int64_t t = q / a.Wg;
+        const int y = static_cast<int>(t % a.Hg);
+        const int n = static_cast<int>(t / a.Hg);
+        if (a.out_mode == OUT_SAME) {
+          d.pix = q;
+          d.border = x == 0 || x == a.Wg - 1 || y == 0 || y == a.Hg - 1;
+        } else {
+          valid = y < a.OH && x < a.OW;
+          d.pix = (static_cast<int64_t>(n) * (a.OH + 2 * kPad) + y + kPad) * (a.OW + 2 * kPad) + x + kPad;
+        }
+        if (a.out.side) {
+          if (sl.kind == LAY_PHASE) {
+            const int wp = static_cast<int>(d.pix % sl.Wp);
+            const int64_t tt = d.pix / sl.Wp;
+            const int hp = static_cast<int>(tt % sl.Hp);
+            const int64_t nn = tt / sl.Hp;
+            d.side_base = static_cast<int64_t>((hp & 1) * 2 + (wp & 1)) * sl.Pp + (nn * sl.Hq + hp / 2) * sl.Wq + wp / 2;
+            d.side_pstride = 4 * sl.Pp;
+          } else {
+            d.side_base = d.pix;
+            d.side_pstride = sl.Pp;
+          }
+        }
       }
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
                              static_cast<uint32_t>(acc * a.bn + half * cols);
       for (int c = 0; c < cols; c += 16) {
         uint32_t raw[16];
         tmem_ld16(taddr + static_cast<uint32_t>(c), raw);  // warp-collective: every lane executes it
-        if (valid) epilogue_chunk<EB, SIG>(a, raw, q, border, n_tile * a.bn + half * cols + c);
+        if (valid) epilogue_chunk<EB, SIG>(a, raw, d, n_tile * a.bn + half * cols + c);
       }
       tc_fence_before();
       __syncwarp();
@@ -504,94 +561,185 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }  // namespace
 
 struct TcConvPlan {
-  ConvGeom g;
-  int eb;
+  TcConvSpec spec;
   TcArgs args;
-  int grid;
-  size_t smem;
+  int grid = 0;
+  size_t smem = 0;
   const void* map_x = nullptr;
   const void* map_w = nullptr;
   CUtensorMap tmA, tmB;
 };
 
+// Taps of a conv kind: (sub-grid, row offset in the sub-grid's pixel space).
+struct Tap {
+  int sub, delta;
+};
+
 static bool choose(TcConvPlan& p) {
-  const ConvGeom& g = p.g;
-  const int eb = p.eb;
-  const int cpc = 16 / eb;
+  const TcConvSpec& sp = p.spec;
   TcArgs& a = p.args;
   std::memset(&a, 0, sizeof(a));
-  if (g.sh != 1 || g.sw != 1) return false;
-  bool k3 = g.KH == 3 && g.KW == 3 && g.ph == 1 && g.pw == 1;
-  bool k1 = g.KH == 1 && g.KW == 1 && g.ph == 0 && g.pw == 0;
-  if (!k3 && !k1) return false;
-  if (g.OH != g.H || g.OW != g.W) return false;
-  if (g.C % (2 * cpc) != 0) return false;  // whole 32-byte MMA K steps, no stale chunk lanes
-  if (g.OC % 16 != 0) return false;
-  a.Wp = g.W + 2 * kPad;
-  a.Hp = g.H + 2 * kPad;
-  a.H = g.H;
-  a.W = g.W;
-  a.Pp = static_cast<int64_t>(g.N) * a.Hp * a.Wp;
-  a.taps = k3 ? 9 : 1;
-  int halo = k3 ? kTileM + 2 * a.Wp + 2 : kTileM;
-  halo = (halo + 7) / 8 * 8;
-  if (halo > 256) return false;  // one TMA box per plane
-  a.halo = halo;
-  for (int kh = 0, t = 0; kh < g.KH; ++kh)
-    for (int kw = 0; kw < g.KW; ++kw, ++t) a.delta[t] = k3 ? kh * a.Wp + kw : 0;
-  a.Cc = g.C / cpc;
-  a.m_tiles = static_cast<int>((a.Pp + kTileM - 1) / kTileM);
-  // tile N: largest of 256/128/64/32/16 dividing OC
+  const int eb = sp.elem_bytes;
+  const int cpc = 16 / eb;
+  if (sp.OC % 16 != 0) return false;
+  std::vector<Tap> taps;
+  int cc = 0;       // A chunk planes
+  bool pair_taps = false;  // int8 stem: K halves = two adjacent taps (LBO 16 B)
+  a.N = sp.N;
+  switch (sp.kind) {
+    case TC_S1: {
+      // stride-1 3x3/pad-1 or 1x1/pad-0 over the NORMAL padded grid; output
+      // grid == input grid
+      bool k3 = sp.KH == 3 && sp.KW == 3, k1 = sp.KH == 1 && sp.KW == 1;
+      if (!k3 && !k1) return false;
+      if (sp.C % (2 * cpc)) return false;
+      a.Hg = sp.H + 2 * kPad;
+      a.Wg = sp.W + 2 * kPad;
+      a.out_mode = OUT_SAME;
+      cc = sp.C / cpc;
+      a.subs = 1;
+      for (int kh = 0; kh < sp.KH; ++kh)
+        for (int kw = 0; kw < sp.KW; ++kw) taps.push_back({0, k3 ? (kh - 1) * a.Wg + (kw - 1) : 0});
+      break;
+    }
+    case TC_S2_PHASE: {
+      // stride-2 3x3/pad-1 (4 phases) or 1x1/pad-0 (phase (1,1)) over the
+      // PHASE layout: tap (kh, kw) reads sub-grid (kh&1, kw&1) at (kh/2, kw/2)
+      bool k3 = sp.KH == 3 && sp.KW == 3, k1 = sp.KH == 1 && sp.KW == 1;
+      if (!k3 && !k1) return false;
+      if (sp.C % (2 * cpc)) return false;
+      if ((sp.H & 1) || (sp.W & 1)) return false;
+      a.Hg = (sp.H + 2 * kPad + 1) / 2;
+      a.Wg = (sp.W + 2 * kPad + 1) / 2;
+      a.out_mode = OUT_REMAP;
+      a.OH = sp.OH;
+      a.OW = sp.OW;
+      cc = sp.C / cpc;
+      a.subs = 4;
+      if (k3) {
+        for (int kh = 0; kh < 3; ++kh)
+          for (int kw = 0; kw < 3; ++kw) taps.push_back({(kh & 1) * 2 + (kw & 1), (kh / 2) * a.Wg + kw / 2});
+      } else {
+        a.sub0 = 3;  // only phase (1, 1) is read: load just that sub-grid
+        a.subs = 1;
+        taps.push_back({0, 0});
+      }
+      break;
+    }
+    case TC_STEM_S2D: {
+      // KxK stride-2 over the space-to-depth input: TA x TA stride-1 taps of
+      // 4*C s2d channels; output (oh, ow) at s2d grid (oh, ow)
+      const int TA = (sp.KH + 1) / 2;
+      if (sp.KH != sp.KW || 4 * sp.C > 16) return false;
+      a.Hg = sp.Hs;
+      a.Wg = sp.Ws;
+      a.out_mode = OUT_REMAP;
+      a.OH = sp.OH;
+      a.OW = sp.OW;
+      cc = (4 * sp.C + cpc - 1) / cpc;  // 1 (int8) or 2 (bf16)
+      a.subs = 1;
+      for (int ta = 0; ta < TA; ++ta)
+        for (int tb = 0; tb < TA; ++tb) taps.push_back({0, ta * a.Wg + tb});
+      pair_taps = cc == 1;
+      if (pair_taps && (TA & 1)) return false;
+      break;
+    }
+    default:
+      return false;
+  }
+  a.Pg = static_cast<int64_t>(a.N) * a.Hg * a.Wg;
+  a.m_tiles = static_cast<int>((a.Pg + kTileM - 1) / kTileM);
+  int dmin = 1 << 30, dmax = -(1 << 30);
+  for (const Tap& t : taps) {
+    dmin = std::min(dmin, t.delta);
+    dmax = std::max(dmax, t.delta + (pair_taps ? 1 : 0));
+  }
+  a.dmin = dmin;
+  a.hg = (7 + kTileM + dmax - dmin + 7) / 8;  // 8-pixel rows per sub-grid and plane
+  if (a.hg > 256) return false;
+  const int ntaps = static_cast<int>(taps.size());
+  // weights (TMA B): [ntaps][cc][OC][16 B]
+  const int barrier_bytes = 256;
+  auto a_stage = [&](int pps) { return pps * a.subs * a.hg * 128; };
+  auto steps_for = [&](int pps) { return pair_taps ? ntaps / 2 : ntaps * pps / 2; };
   int bn = 0;
   for (int c : {256, 128, 64, 32, 16})
-    if (g.OC % c == 0) {
+    if (sp.OC % c == 0) {
       bn = c;
       break;
     }
   if (!bn) return false;
+  bool found = false;
   // resident weights if they fit beside >= 3 A stages, else stream them
-  const int barrier_bytes = 256;
-  auto a_stage = [&](int pps) { return pps * halo * 16; };
-  int best = -1;
-  for (int cand_bn = bn; cand_bn >= 16; cand_bn /= 2) {
-    if (g.OC % cand_bn) continue;
-    int b_res = a.taps * a.Cc * cand_bn * 16;
-    for (int pps : {8, 4, 2}) {
-      if (a.Cc % pps) continue;
+  for (int cand = bn; cand >= 16 && !found; cand /= 2) {
+    if (sp.OC % cand) continue;
+    int b_res = ntaps * cc * cand * 16;
+    for (int pps : {8, 4, 2, 1}) {
+      if (cc % pps || (pps & 1 && !pair_taps) || steps_for(pps) > kMaxSteps) continue;
       int ns = (kSmemBudget - barrier_bytes - b_res) / a_stage(pps);
       if (ns >= 3) {
-        a.bn = cand_bn;
+        a.bn = cand;
         a.resident_b = 1;
         a.b_res_bytes = b_res;
         a.pps = pps;
         a.n_stages = ns > 8 ? 8 : ns;
-        best = 1;
+        found = true;
         break;
       }
     }
-    if (best > 0) break;
-    if (cand_bn <= 64) break;  // below 64 columns prefer streaming B at a wide tile
+    if (cand <= 64) break;  // below 64 columns prefer streaming B at a wide tile
   }
-  if (best < 0) {
+  if (!found) {
     a.bn = bn > 256 ? 256 : bn;
     a.resident_b = 0;
     for (int pps : {4, 2}) {
-      if (a.Cc % pps) continue;
-      int bst = a.taps * pps * a.bn * 16;
+      if (cc % pps || pair_taps || steps_for(pps) > kMaxSteps) continue;
+      int bst = ntaps * pps * a.bn * 16;
       int ns = (kSmemBudget - barrier_bytes) / (a_stage(pps) + bst);
       if (ns >= 2) {
         a.pps = pps;
         a.b_stage_bytes = bst;
         a.n_stages = ns > 6 ? 6 : ns;
-        best = 2;
+        found = true;
         break;
       }
     }
-    if (best < 0) return false;
+    if (!found) return false;
   }
+  a.Cc = cc;
   a.a_stage_bytes = a_stage(a.pps);
-  a.k_stages = a.Cc / a.pps;
-  a.n_tiles = g.OC / a.bn;
+  a.k_stages = cc / a.pps;
+  a.n_tiles = sp.OC / a.bn;
+  // MMA step table (byte offsets; A relative to stage base + row shift)
+  const uint32_t a_sub = static_cast<uint32_t>(a.hg) * 128;
+  const uint32_t a_plane = a_sub * static_cast<uint32_t>(a.subs);
+  const uint32_t b_plane = static_cast<uint32_t>(a.bn) * 16;
+  const int bplanes = a.resident_b ? cc : a.pps;  // planes per tap in the smem B buffer
+  a.b_ks_stride = a.resident_b ? static_cast<uint32_t>(a.pps) * b_plane : 0;
+  a.n_steps = 0;
+  if (pair_taps) {
+    for (int t = 0; t < ntaps; t += 2) {
+      MmaStep m;
+      m.a_off = static_cast<uint32_t>(taps[t].delta - dmin) * 16;
+      m.a_lbo = 16;
+      m.b_off = static_cast<uint32_t>(t * bplanes) * b_plane;
+      m.b_lbo = static_cast<uint32_t>(bplanes) * b_plane;
+      a.steps[a.n_steps++] = m;
+    }
+  } else {
+    for (int t = 0; t < ntaps; ++t)
+      for (int kp = 0; kp < a.pps; kp += 2) {
+        MmaStep m;
+        m.a_off = static_cast<uint32_t>(kp) * a_plane + static_cast<uint32_t>(taps[t].sub) * a_sub +
+                  static_cast<uint32_t>(taps[t].delta - dmin) * 16;
+        m.a_lbo = a_plane;
+        m.b_off = static_cast<uint32_t>(t * bplanes + kp) * b_plane;
+        m.b_lbo = b_plane;
+        a.steps[a.n_steps++] = m;
+      }
+  }
+  p.spec.taps = ntaps;
+  p.spec.wplanes = cc;
   // instruction descriptor: D fmt [4,6), A fmt [7,10), B fmt [10,13), K-major A/B,
   // N>>3 [17,23), M>>4 [24,29)
   uint32_t idesc = 0;
@@ -612,17 +760,17 @@ static bool choose(TcConvPlan& p) {
   return true;
 }
 
-bool tc_conv_eligible(const ConvGeom& g, int elem_bytes) {
+bool tc_conv_plan_ok(TcConvSpec& spec) {
   TcConvPlan p;
-  p.g = g;
-  p.eb = elem_bytes;
-  return choose(p);
+  p.spec = spec;
+  if (!choose(p)) return false;
+  spec = p.spec;
+  return true;
 }
 
-TcConvPlan* tc_conv_create(const ConvGeom& g, int elem_bytes) {
+TcConvPlan* tc_conv_create(const TcConvSpec& spec) {
   auto* p = new TcConvPlan();
-  p->g = g;
-  p->eb = elem_bytes;
+  p->spec = spec;
   if (!choose(*p) || !encode_fn()) {
     delete p;
     return nullptr;
@@ -630,28 +778,31 @@ TcConvPlan* tc_conv_create(const ConvGeom& g, int elem_bytes) {
   return p;
 }
 
-static bool encode_maps(TcConvPlan& p, const void* x, const void* w) {
+static bool encode_maps(TcConvPlan& p, const void* x, const Lay& xl, const void* w) {
   TcArgs& a = p.args;
   auto enc = encode_fn();
-  // A: [planes][pixels][16 B] -> dims {16, Pp, Cc}, box {16, halo, pps}
+  // A: chunk planes of `subs` sub-grids of Pp pixels (multiple of 8) x 16 B,
+  // moved as 128-byte (8-pixel) rows: dims {128 B, Pp/8, subs, Cc}
   {
-    cuuint64_t dims[3] = {16, static_cast<cuuint64_t>(a.Pp), static_cast<cuuint64_t>(a.Cc)};
-    cuuint64_t strides[2] = {16, static_cast<cuuint64_t>(a.Pp) * 16};
-    cuuint32_t box[3] = {16, static_cast<cuuint32_t>(a.halo), static_cast<cuuint32_t>(a.pps)};
-    cuuint32_t es[3] = {1, 1, 1};
-    if (enc(&p.tmA, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(x), dims, strides, box, es,
+    const cuuint64_t tsubs = xl.kind == LAY_PHASE ? 4 : 1;
+    cuuint64_t dims[4] = {128, static_cast<cuuint64_t>(xl.Pp / 8), tsubs, static_cast<cuuint64_t>(a.Cc)};
+    cuuint64_t strides[3] = {128, static_cast<cuuint64_t>(xl.Pp) * 16, static_cast<cuuint64_t>(xl.Pp) * 16 * tsubs};
+    cuuint32_t box[4] = {128, static_cast<cuuint32_t>(a.hg), static_cast<cuuint32_t>(a.subs),
+                         static_cast<cuuint32_t>(a.pps)};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    if (enc(&p.tmA, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(x), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return false;
   }
-  // B: [taps][planes][OC][16 B] -> dims {16, OC, Cc, taps}
+  // B: [taps][planes][OC][16 B] -> dims {128 B (8 rows), OC/8, planes, taps}
   {
-    cuuint64_t dims[4] = {16, static_cast<cuuint64_t>(p.g.OC), static_cast<cuuint64_t>(a.Cc),
-                          static_cast<cuuint64_t>(a.taps)};
-    cuuint64_t strides[3] = {16, static_cast<cuuint64_t>(p.g.OC) * 16,
-                             static_cast<cuuint64_t>(p.g.OC) * 16 * static_cast<cuuint64_t>(a.Cc)};
-    cuuint32_t box[4] = {16, static_cast<cuuint32_t>(a.bn),
-                         static_cast<cuuint32_t>(a.resident_b ? a.Cc : a.pps), static_cast<cuuint32_t>(a.taps)};
+    const int OC = p.spec.OC;
+    cuuint64_t dims[4] = {128, static_cast<cuuint64_t>(OC / 8), static_cast<cuuint64_t>(a.Cc),
+                          static_cast<cuuint64_t>(p.spec.taps)};
+    cuuint64_t strides[3] = {128, static_cast<cuuint64_t>(OC) * 16, static_cast<cuuint64_t>(OC) * 16 * a.Cc};
+    cuuint32_t box[4] = {128, static_cast<cuuint32_t>(a.bn / 8),
+                         static_cast<cuuint32_t>(a.resident_b ? a.Cc : a.pps), static_cast<cuuint32_t>(p.spec.taps)};
     cuuint32_t es[4] = {1, 1, 1, 1};
     if (enc(&p.tmB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(w), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -663,10 +814,10 @@ static bool encode_maps(TcConvPlan& p, const void* x, const void* w) {
   return true;
 }
 
-bool tc_conv_launch(TcConvPlan* p, const void* x, const void* w, float acc_scale, const EpiDev& epi,
+bool tc_conv_launch(TcConvPlan* p, const void* x, const Lay& xl, const void* w, float acc_scale, const EpiDev& epi,
                     const OutDev& out, cudaStream_t s) {
   if (p->map_x != x || p->map_w != w) {
-    if (!encode_maps(*p, x, w)) return false;
+    if (!encode_maps(*p, x, xl, w)) return false;
   }
   TcArgs a = p->args;
   a.acc_scale = acc_scale;
@@ -686,7 +837,7 @@ bool tc_conv_launch(TcConvPlan* p, const void* x, const void* w, float acc_scale
     case SIG_BIAS_RES_RELU: MRB_TC_LAUNCH(EB_, SIG_BIAS_RES_RELU); break; \
     default: MRB_TC_LAUNCH(EB_, SIG_ANY); break;                  \
   }
-  if (p->eb == 1) {
+  if (p->spec.elem_bytes == 1) {
     MRB_TC_SIGS(1)
   } else {
     MRB_TC_SIGS(2)
@@ -700,9 +851,10 @@ void tc_conv_destroy(TcConvPlan* p) { delete p; }
 
 const char* tc_conv_describe(const TcConvPlan* p, char* buf, int n) {
   const TcArgs& a = p->args;
-  std::snprintf(buf, n, "tcgen05 %s M128xN%d taps=%d halo=%d pps=%d stages=%d B=%s grid=%d smem=%zu",
-                p->eb == 1 ? "i8" : "bf16", a.bn, a.taps, a.halo, a.pps, a.n_stages, a.resident_b ? "resident" : "streamed",
-                p->grid, p->smem);
+  static const char* kinds[] = {"s1", "s2-phase", "stem-s2d"};
+  std::snprintf(buf, n, "tcgen05 %s %s M128xN%d taps=%d steps=%d grid=%dx%d hg=%d pps=%d stages=%d B=%s ctas=%d smem=%zu",
+                p->spec.elem_bytes == 1 ? "i8" : "bf16", kinds[p->spec.kind], a.bn, p->spec.taps, a.n_steps, a.Hg,
+                a.Wg, a.hg, a.pps, a.n_stages, a.resident_b ? "resident" : "streamed", p->grid, p->smem);
   return buf;
 }
 

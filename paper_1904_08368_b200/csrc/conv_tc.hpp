@@ -7,14 +7,28 @@
 
 namespace mrb200 {
 
+// Which halo formulation a conv group uses (decided at compile time).
+enum TcKind : int {
+  TC_S1 = 0,        // stride-1 3x3/pad-1 or 1x1 over a LAY_NORMAL input
+  TC_S2_PHASE = 1,  // stride-2 3x3/pad-1 or 1x1 over a LAY_PHASE input
+  TC_STEM_S2D = 2,  // KxK stride-2 stem over the LAY_S2D network input
+};
+
+struct TcConvSpec {
+  int kind;
+  int elem_bytes;  // 1: int8 (kind::i8), 2: bf16 (kind::f16)
+  int N, C, H, W, OC, OH, OW, KH, KW;
+  int Hs, Ws;      // TC_STEM_S2D input grid
+  // filled by planning
+  int taps = 0, wplanes = 0;  // weight layout [taps][wplanes][OC][16 B]
+};
+
 struct TcConvPlan;
 
-// Compile-time eligibility of a conv group (stride-1 3x3/pad-1 or 1x1, channel
-// counts in whole 32-byte MMA K steps, halo within one TMA box).
-bool tc_conv_eligible(const ConvGeom& g, int elem_bytes);
-TcConvPlan* tc_conv_create(const ConvGeom& g, int elem_bytes);
-// x: P16 activations (pad kPad), w: [taps][C/cpc][OC][cpc] weights (WL_TC).
-bool tc_conv_launch(TcConvPlan* p, const void* x, const void* w, float acc_scale, const EpiDev& epi,
+// Compile-time eligibility (fills taps / wplanes).
+bool tc_conv_plan_ok(TcConvSpec& spec);
+TcConvPlan* tc_conv_create(const TcConvSpec& spec);
+bool tc_conv_launch(TcConvPlan* p, const void* x, const Lay& xl, const void* w, float acc_scale, const EpiDev& epi,
                     const OutDev& out, cudaStream_t s);
 void tc_conv_destroy(TcConvPlan* p);
 const char* tc_conv_describe(const TcConvPlan* p, char* buf, int n);

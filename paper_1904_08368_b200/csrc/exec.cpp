@@ -101,6 +101,7 @@ struct Exec {
   std::vector<int> group_path;              // kernel choice
   std::vector<std::string> group_exact;     // int8 exactness proof per group
   std::vector<std::string> group_note;      // kernel plan description
+  std::vector<TcConvSpec> group_tc;         // tcgen05 formulation per conv group
   bool weights_ready = false;
   // io
   const float* cur_input = nullptr;
@@ -154,14 +155,30 @@ int float_fmt(const Exec& ex) {
 
 int64_t elem_bytes(int fmt) { return fmt == FMT_F32 ? 4 : fmt == FMT_BF16 ? 2 : 1; }
 
-// Layout of a representation: P16 with a kPad border for 4-D values,
-// row-major for 2-D ones.
-Lay make_lay(const std::vector<int64_t>& s, int fmt) {
+// Layout of a representation: P16 (NORMAL / PHASE / S2D) with a kPad
+// border for 4-D values, row-major for 2-D ones.  Plane strides are padded to
+// 8 pixels (128-byte TMA rows).  S2D takes the stem's input padding.
+Lay make_lay(const std::vector<int64_t>& s, int fmt, int kind, int s2d_pad = 0) {
   Lay L{};
   L.C = s.size() >= 2 ? static_cast<int32_t>(s[1]) : 1;
+  L.kind = LAY_NORMAL;
   if (s.size() == 4) {
     L.cpc = static_cast<int32_t>(16 / elem_bytes(fmt));
-    L.Pp = s[0] * (s[2] + 2 * kPad) * (s[3] + 2 * kPad);
+    L.kind = kind;
+    L.Hp = static_cast<int32_t>(s[2] + 2 * kPad);
+    L.Wp = static_cast<int32_t>(s[3] + 2 * kPad);
+    if (kind == LAY_NORMAL) {
+      L.Pp = round_up(s[0] * L.Hp * L.Wp, 8);
+    } else if (kind == LAY_PHASE) {
+      L.Hq = (L.Hp + 1) / 2;
+      L.Wq = (L.Wp + 1) / 2;
+      L.Pp = round_up(s[0] * L.Hq * L.Wq, 8);
+    } else {  // LAY_S2D: 4*C s2d channels on a ceil((H+2p)/2) grid
+      L.C = static_cast<int32_t>(4 * s[1]);
+      L.Hq = static_cast<int32_t>((s[2] + 2 * s2d_pad + 1) / 2);
+      L.Wq = static_cast<int32_t>((s[3] + 2 * s2d_pad + 1) / 2);
+      L.Pp = round_up(s[0] * L.Hq * L.Wq, 8);
+    }
   } else {
     L.cpc = 0;
     L.Pp = s.empty() ? 1 : s[0];
@@ -171,17 +188,19 @@ Lay make_lay(const std::vector<int64_t>& s, int fmt) {
 
 int64_t lay_elems(const Lay& L) {
   if (L.cpc == 0) return L.Pp * L.C;
-  return (L.C + L.cpc - 1) / L.cpc * L.Pp * L.cpc;
+  int64_t planes = (L.C + L.cpc - 1) / L.cpc;
+  return planes * (L.kind == LAY_PHASE ? 4 : 1) * L.Pp * L.cpc;
 }
 
 
 // Finds or adds a representation of value v.
-int want_rep(Exec& ex, int v, int fmt, const QParams* q) {
+int want_rep(Exec& ex, int v, int fmt, const QParams* q, int kind = LAY_NORMAL, int s2d_pad = 0) {
   auto& rs = ex.reps[v];
+  if (ex.P.values[v].shape.size() != 4) kind = LAY_NORMAL;
   for (size_t i = 0; i < rs.size(); ++i) {
     const Rep& r = rs[i];
     if (r.nchw_user) continue;
-    if (r.fmt != fmt) continue;
+    if (r.fmt != fmt || r.lay.kind != kind) continue;
     if (fmt == FMT_I8) {
       if (!q || !r.has_q || !(r.q == *q)) continue;
     }
@@ -193,7 +212,7 @@ int want_rep(Exec& ex, int v, int fmt, const QParams* q) {
     r.has_q = true;
     r.q = *q;
   }
-  r.lay = make_lay(ex.P.values[v].shape, fmt);
+  r.lay = make_lay(ex.P.values[v].shape, fmt, kind, s2d_pad);
   r.elems = lay_elems(r.lay);
   rs.push_back(r);
   return static_cast<int>(rs.size()) - 1;
@@ -263,12 +282,19 @@ GroupIO resolve_inputs(Exec& ex, int gi) {
   const int ffmt = float_fmt(ex);
   const ValueInfo& dv = P.values[g.data.value];
   int path = ex.group_path[gi];
+  // data layout kind the tcgen05 formulation needs (CUDA-core kernels read NORMAL)
+  int kind = LAY_NORMAL, s2d_pad = 0;
+  if (path == P_CONV_I8_TC || path == P_CONV_BF16_TC) {
+    const TcConvSpec& sp = ex.group_tc[gi];
+    kind = sp.kind == TC_S2_PHASE ? LAY_PHASE : sp.kind == TC_STEM_S2D ? LAY_S2D : LAY_NORMAL;
+    s2d_pad = static_cast<int>(g.ph);
+  }
   if (path == P_CONV_I8_SIMT || path == P_CONV_I8_TC) {
     if (g.data.quant) {
-      io.data_rep = want_rep(ex, g.data.value, FMT_I8, &g.data.q);
+      io.data_rep = want_rep(ex, g.data.value, FMT_I8, &g.data.q, kind, s2d_pad);
       io.data_scale = g.data.q.c2;
     } else {
-      io.data_rep = want_rep(ex, g.data.value, FMT_I8, &dv.q);
+      io.data_rep = want_rep(ex, g.data.value, FMT_I8, &dv.q, kind, s2d_pad);
       io.data_scale = dv.q.c2;
     }
   } else if (g.kind == GroupKind::Dense) {
@@ -278,7 +304,7 @@ GroupIO resolve_inputs(Exec& ex, int gi) {
     else if (dv.quantized) fail(MR_ERR_UNSUPPORTED_GROUP, "group %" + g.name + ": dense over a coded value");
   } else if (path == P_CONV_F32 || path == P_CONV_BF16_SIMT || path == P_CONV_BF16_TC) {
     if (g.data.pre_mul != 0.f) fail(MR_ERR_UNSUPPORTED_GROUP, "group %" + g.name + ": scaled conv input");
-    io.data_rep = want_rep(ex, g.data.value, ffmt, nullptr);
+    io.data_rep = want_rep(ex, g.data.value, ffmt, nullptr, kind, s2d_pad);
   } else {  // pool / depthwise: float input
     io.data_rep = want_rep(ex, g.data.value, ffmt, nullptr);
   }
@@ -297,6 +323,8 @@ GroupIO resolve_inputs(Exec& ex, int gi) {
 // ======================================================================
 namespace mrb200 {
 namespace {
+
+bool g_has_sum(const GroupDesc& g) { return !g.epi.empty() && g.epi.back().kind == EpiKind::SumHW; }
 
 struct Builder {
   Exec& ex;
@@ -406,30 +434,45 @@ void build(Exec& ex) {
   Program& P = ex.P;
   const bool use_tc = !ex.opt.force_simt;
   plan(ex, use_tc);
-  // TC eligibility is decided per group at compile time (geometry only).
+  // tcgen05 formulation per conv group, decided at compile time from the
+  // geometry: stride-1 halo (3x3/1x1), stride-2 over phase-split inputs, or
+  // the space-to-depth stem; anything else runs on the CUDA-core kernel.
+  ex.group_tc.assign(P.groups.size(), TcConvSpec{});
   for (size_t gi = 0; gi < P.groups.size(); ++gi) {
     int& path = ex.group_path[gi];
     const GroupDesc& g = P.groups[gi];
-    if (path == P_CONV_I8_TC || path == P_CONV_BF16_TC) {
-      int eb = path == P_CONV_I8_TC ? 1 : 2;
-      bool has_sum = !g.epi.empty() && g.epi.back().kind == EpiKind::SumHW;
-      const auto& os = has_sum ? g.pre_sum_shape : g.out_shape;
-      ConvGeom t{};
-      t.N = static_cast<int>(g.in_shape[0]);
-      t.C = static_cast<int>(g.in_shape[1]);
-      t.H = static_cast<int>(g.in_shape[2]);
-      t.W = static_cast<int>(g.in_shape[3]);
-      t.OC = static_cast<int>(os[1]);
-      t.OH = static_cast<int>(os[2]);
-      t.OW = static_cast<int>(os[3]);
-      t.KH = static_cast<int>(g.kh);
-      t.KW = static_cast<int>(g.kw);
-      t.sh = static_cast<int>(g.sh);
-      t.sw = static_cast<int>(g.sw);
-      t.ph = static_cast<int>(g.ph);
-      t.pw = static_cast<int>(g.pw);
-      if (!tc_conv_eligible(t, eb)) path = path == P_CONV_I8_TC ? P_CONV_I8_SIMT : P_CONV_BF16_SIMT;
+    if (path != P_CONV_I8_TC && path != P_CONV_BF16_TC) continue;
+    bool has_sum = !g.epi.empty() && g.epi.back().kind == EpiKind::SumHW;
+    const auto& os = has_sum ? g.pre_sum_shape : g.out_shape;
+    TcConvSpec sp{};
+    sp.elem_bytes = path == P_CONV_I8_TC ? 1 : 2;
+    sp.N = static_cast<int>(g.in_shape[0]);
+    sp.C = static_cast<int>(g.in_shape[1]);
+    sp.H = static_cast<int>(g.in_shape[2]);
+    sp.W = static_cast<int>(g.in_shape[3]);
+    sp.OC = static_cast<int>(os[1]);
+    sp.OH = static_cast<int>(os[2]);
+    sp.OW = static_cast<int>(os[3]);
+    sp.KH = static_cast<int>(g.kh);
+    sp.KW = static_cast<int>(g.kw);
+    bool same3 = g.kh == 3 && g.kw == 3 && g.ph == 1 && g.pw == 1;
+    bool one = g.kh == 1 && g.kw == 1 && g.ph == 0 && g.pw == 0;
+    bool ok = false;
+    if (g.sh == 1 && g.sw == 1 && (same3 || one)) {
+      sp.kind = TC_S1;
+      ok = tc_conv_plan_ok(sp);
+    } else if (g.sh == 2 && g.sw == 2 && (same3 || one)) {
+      sp.kind = TC_S2_PHASE;
+      ok = tc_conv_plan_ok(sp);
+    } else if (g.sh == 2 && g.sw == 2 && g.kh == g.kw && (g.kh & 1) && g.ph == g.kh / 2 && g.pw == g.kw / 2 &&
+               P.values[g.data.value].is_data) {
+      sp.kind = TC_STEM_S2D;
+      sp.Hs = static_cast<int>((sp.H + 2 * g.ph + 1) / 2);
+      sp.Ws = static_cast<int>((sp.W + 2 * g.pw + 1) / 2);
+      ok = tc_conv_plan_ok(sp);
     }
+    if (ok) ex.group_tc[gi] = sp;
+    else path = path == P_CONV_I8_TC ? P_CONV_I8_SIMT : P_CONV_BF16_SIMT;
   }
   std::vector<GroupIO> io(P.groups.size());
   for (size_t gi = 0; gi < P.groups.size(); ++gi) io[gi] = resolve_inputs(ex, static_cast<int>(gi));
@@ -454,9 +497,10 @@ void build(Exec& ex) {
     for (size_t r = 0; r < ex.reps[v].size(); ++r) {
       const Rep& rep = ex.reps[v][r];
       if (rep.nchw_user || r == 0 || vi.producer < 0) continue;  // rep 0 is the primary
-      if (rep.fmt == FMT_I8 && P.groups[vi.producer].kind != GroupKind::Dense) {
+      if ((rep.fmt == FMT_I8 || rep.fmt == FMT_BF16) && P.groups[vi.producer].kind != GroupKind::Dense &&
+          !g_has_sum(P.groups[vi.producer])) {
         if (side_rep[vi.producer] >= 0)
-          fail(MR_ERR_UNSUPPORTED_GROUP, "value %" + vi.name + " needs two different quantized copies");
+          fail(MR_ERR_UNSUPPORTED_GROUP, "value %" + vi.name + " needs more than two representations");
         side_rep[vi.producer] = static_cast<int>(r);
       } else {
         fail(MR_ERR_UNSUPPORTED_GROUP, "value %" + vi.name + " needs a representation its producer cannot emit");
@@ -482,9 +526,13 @@ void build(Exec& ex) {
       QDev q = to_qdev(rep.q);
       int fmt = rep.fmt;
       Lay lay = rep.lay;
+      int s2d_pad = 0;
+      if (lay.kind == LAY_S2D)
+        for (int c : vi.consumers)
+          if (P.groups[c].data.value == static_cast<int>(v)) s2d_pad = static_cast<int>(P.groups[c].ph);
       Exec* e = &ex;
-      L.fn = [e, buf, N, C, H, W, fmt, lay, q](cudaStream_t s) {
-        launch_input_convert(e->cur_input, N, C, H, W, e->ptr(buf), fmt, lay, 0.f, q, s);
+      L.fn = [e, buf, N, C, H, W, fmt, lay, s2d_pad, q](cudaStream_t s) {
+        launch_input_convert(e->cur_input, N, C, H, W, e->ptr(buf), fmt, lay, s2d_pad, 0.f, q, s);
       };
       ex.launches.push_back(L);
       ++B.launch_idx;
@@ -513,7 +561,7 @@ void build(Exec& ex) {
     Lay pre_lay{};
     if (has_sum) {
       // the conv writes the float32 pre-sum tensor (P16); k_sum_hw reduces it
-      pre_lay = make_lay(g.pre_sum_shape, FMT_F32);
+      pre_lay = make_lay(g.pre_sum_shape, FMT_F32, LAY_NORMAL);
       pre_sum_buf = B.scratch(lay_elems(pre_lay) * 4, "%" + g.out_name + ":presum");
       out.primary_fmt = FMT_F32;
       out.plan = pre_lay;
@@ -524,6 +572,7 @@ void build(Exec& ex) {
     if (sbuf >= 0) {
       const Rep& sr = ex.reps[g.out_value][side_rep[gi]];
       out.slay = sr.lay;
+      out.side_fmt = sr.fmt;
       out.side_q = to_qdev(sr.q);
     }
 
@@ -532,7 +581,10 @@ void build(Exec& ex) {
     L.kernel = path_name(path);
     // algorithmic traffic: data once + output(s) once + residuals + weights
     double out_bytes = static_cast<double>(orep.elems) * elem_bytes(orep.fmt);
-    if (sbuf >= 0) out_bytes += static_cast<double>(ex.reps[g.out_value][side_rep[gi]].elems);
+    if (sbuf >= 0) {
+      const Rep& sr = ex.reps[g.out_value][side_rep[gi]];
+      out_bytes += static_cast<double>(sr.elems) * elem_bytes(sr.fmt);
+    }
     double in_bytes = static_cast<double>(drep.elems) * elem_bytes(drep.fmt);
     for (size_t i = 0; i < g.epi.size(); ++i)
       if (gio.res_rep[i] >= 0) {
@@ -583,7 +635,7 @@ void build(Exec& ex) {
       OutDev o = out;
       if (pb.presum >= 0) o.primary = e->ptr(pb.presum);
       else o.primary = e->ptr(pb.out);
-      o.side = pb.side >= 0 ? static_cast<int8_t*>(e->ptr(pb.side)) : nullptr;
+      o.side = pb.side >= 0 ? e->ptr(pb.side) : nullptr;
       return o;
     };
     auto epidev = [e, gidx, epi]() {
@@ -637,17 +689,18 @@ void build(Exec& ex) {
       }
       case P_CONV_I8_TC:
       case P_CONV_BF16_TC: {
-        TcConvPlan* tp = tc_conv_create(geo, path == P_CONV_I8_TC ? 1 : 2);
+        TcConvPlan* tp = tc_conv_create(ex.group_tc[gi]);
         if (!tp) fail(MR_ERR_UNSUPPORTED_GROUP, "group %" + g.name + ": tcgen05 plan failed");
         ex.tc_plans.push_back(tp);
         char buf[256];
         ex.group_note.resize(P.groups.size());
         ex.group_note[gi] = tc_conv_describe(tp, buf, sizeof(buf));
         std::string gname = g.name;
-        L.fn = [e, gidx, dbuf, acc_scale, tp, outdev, epidev, residual_fix, gname](cudaStream_t s) {
+        Lay dlay = drep.lay;
+        L.fn = [e, gidx, dbuf, dlay, acc_scale, tp, outdev, epidev, residual_fix, gname](cudaStream_t s) {
           EpiDev d = epidev();
           residual_fix(d);
-          if (!tc_conv_launch(tp, e->ptr(dbuf), e->group_w[gidx], acc_scale, d, outdev(), s))
+          if (!tc_conv_launch(tp, e->ptr(dbuf), dlay, e->group_w[gidx], acc_scale, d, outdev(), s))
             fail(MR_ERR_CUDA, "group %" + gname + ": TMA descriptor encoding failed");
         };
         break;
@@ -690,8 +743,8 @@ void build(Exec& ex) {
     ++B.launch_idx;
     // CUDA-core producers write interior pixels only: clear the P16 borders
     // (the tcgen05 conv writes its own, it computes over the padded grid).
-    bool tc = path == P_CONV_I8_TC || path == P_CONV_BF16_TC;
-    if (!tc && !has_sum && g.out_shape.size() == 4) {
+    bool tc_same = (path == P_CONV_I8_TC || path == P_CONV_BF16_TC) && ex.group_tc[gi].kind == TC_S1;
+    if (!tc_same && !has_sum && g.out_shape.size() == 4) {
       for (int b2 : {obuf, sbuf}) {
         if (b2 < 0) continue;
         LaunchRec Z;
@@ -701,7 +754,7 @@ void build(Exec& ex) {
         int N = static_cast<int>(g.out_shape[0]), H = static_cast<int>(g.out_shape[2]), W = static_cast<int>(g.out_shape[3]);
         int64_t border = (zl.C + zl.cpc - 1) / zl.cpc * static_cast<int64_t>(N) * (2 * (W + 2) + 2 * H) * 16;
         Z.bytes = static_cast<double>(border);
-        Z.fn = [e, b2, zl, N, H, W](cudaStream_t s) { launch_zero_border(e->ptr(b2), zl, N, H, W, s); };
+        Z.fn = [e, b2, zl, N](cudaStream_t s) { launch_zero_border(e->ptr(b2), zl, N, s); };
         ex.launches.push_back(Z);
         ++B.launch_idx;
       }
@@ -816,7 +869,8 @@ void prepare_weights(Exec& ex, cudaStream_t s) {
       KW = static_cast<int>(w.shape[3]);
     }
     int fmt, cs;
-    int wl = (path == P_CONV_I8_TC || path == P_CONV_BF16_TC) ? WL_TC : WL_ROWS;
+    int wl = WL_ROWS;
+    if (path == P_CONV_I8_TC || path == P_CONV_BF16_TC) wl = ex.group_tc[gi].kind == TC_STEM_S2D ? WL_S2D : WL_TC;
     if (w.quant) {
       fmt = FMT_I8;
       cs = static_cast<int>(round_up(I, 4));
@@ -830,9 +884,10 @@ void prepare_weights(Exec& ex, cudaStream_t s) {
     int64_t n;
     if (fmt == FMT_F32) {
       n = static_cast<int64_t>(O) * I * KH * KW;
-    } else if (wl == WL_TC) {
+    } else if (wl == WL_TC || wl == WL_S2D) {
+      const TcConvSpec& sp = ex.group_tc[gi];
       int cpc = 16 / static_cast<int>(elem_bytes(fmt));
-      n = static_cast<int64_t>(KH) * KW * ((I + cpc - 1) / cpc) * O * cpc;
+      n = static_cast<int64_t>(sp.taps) * sp.wplanes * O * cpc;
     } else {
       n = static_cast<int64_t>(O) * KH * KW * cs;
     }
@@ -859,7 +914,7 @@ void prepare_weights(Exec& ex, cudaStream_t s) {
       std::vector<int64_t> sums(O, 0);
       int64_t per = n / O, worst = 0;
       for (int64_t k = 0; k < n; ++k) {
-        int o = wl == WL_TC ? static_cast<int>((k / 16) % O) : static_cast<int>(k / per);
+        int o = wl != WL_ROWS ? static_cast<int>((k / 16) % O) : static_cast<int>(k / per);
         sums[o] += std::abs(static_cast<int>(codes[k]));
       }
       for (int o = 0; o < O; ++o) worst = std::max(worst, sums[o]);

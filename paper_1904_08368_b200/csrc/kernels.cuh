@@ -25,16 +25,29 @@ struct QDev {
 
 // Physical layout of an activation tensor ("P16"): channels are split into
 // 16-byte chunks (cpc = 16 / element-bytes channels each); each chunk is a
-// plane of N*(H+2p)*(W+2p) pixels over the zero-padded spatial grid:
-//     element (n, c, h, w) at ((c / cpc) * Pp + pix) * cpc + c % cpc,
-//     pix = (n * Hp + h + p) * Wp + (w + p).
-// Borders hold zeros, so a stride-1 3x3 conv reads its 9 taps as 9 row
-// shifts of one contiguous pixel range (conv_tc.cu).  cpc == 0 marks a plain
-// row-major [N, C] tensor (pix = n).
+// plane over the zero-padded pixel grid (pad kPad):
+//   LAY_NORMAL  element (n, c, h, w) at ((c / cpc) * Pp + pix) * cpc + c % cpc,
+//               pix = (n * Hp + h + kPad) * Wp + (w + kPad)
+//   LAY_PHASE   the padded grid split into its 4 stride-2 phases, so a
+//               stride-2 conv reads each phase with stride 1: padded pixel
+//               (hp, wp) -> sub-grid (hp & 1) * 2 + (wp & 1), position
+//               (n * Hq + hp / 2) * Wq + wp / 2; sub-grids of Pp pixels
+//   LAY_S2D     the network input in space-to-depth form for a 7x7/s2 stem
+//               (written by input_convert, read by the stem tcgen05 conv only)
+// Plane / sub-grid strides are padded to a multiple of 8 pixels so the
+// tcgen05 conv can move 128-byte (8-pixel) TMA rows.  Borders hold zeros, so
+// a stride-1 3x3 conv reads its 9 taps as 9 row shifts of one contiguous
+// pixel range (conv_tc.cu).  cpc == 0 marks a plain row-major [N, C] tensor
+// (pix = n).
+enum LayKind : int32_t { LAY_NORMAL = 0, LAY_PHASE = 1, LAY_S2D = 2 };
+
 struct Lay {
   int32_t cpc;
-  int32_t C;   // logical channels (row length when cpc == 0)
-  int64_t Pp;  // pixels per plane
+  int32_t C;     // logical channels (row length when cpc == 0)
+  int64_t Pp;    // pixel stride of a plane (NORMAL) / sub-grid (PHASE, S2D)
+  int32_t kind;  // LayKind
+  int32_t Hp, Wp;  // padded grid
+  int32_t Hq, Wq;  // PHASE / S2D sub-grid
 };
 
 enum EpiCode : int32_t {
@@ -60,7 +73,8 @@ struct OutDev {
   void* primary;        // P16 (or row-major [N, C])
   int32_t primary_fmt;  // FMT_I8 => the epilogue's last op is a Requant; the code is stored
   Lay plan;             // primary layout
-  int8_t* side;         // optional int8 codes of the final float value (P16, same grid)
+  void* side;           // optional second copy of the final float value for other consumers:
+  int32_t side_fmt;     //   FMT_I8 (realize codes with side_q) or FMT_BF16, any P16 kind
   Lay slay;
   QDev side_q;
 };
@@ -101,9 +115,24 @@ __device__ __forceinline__ int32_t quant_code(float v, const QDev& q) {
   return cast_int_ref(t, q.is_signed);
 }
 
+// Chunk index (16-byte units) of the chunk holding channel c of the padded
+// pixel pix (NORMAL-grid linear index) in layout L.
+__host__ __device__ __forceinline__ int64_t lay_chunk(const Lay& L, int64_t pix, int32_t c) {
+  const int64_t plane = c / L.cpc;
+  if (L.kind == LAY_PHASE) {
+    int32_t wp = static_cast<int32_t>(pix % L.Wp);
+    int64_t t = pix / L.Wp;
+    int32_t hp = static_cast<int32_t>(t % L.Hp);
+    int64_t n = t / L.Hp;
+    int32_t sub = (hp & 1) * 2 + (wp & 1);
+    return (plane * 4 + sub) * L.Pp + (n * L.Hq + hp / 2) * L.Wq + wp / 2;
+  }
+  return plane * L.Pp + pix;
+}
+
 __host__ __device__ __forceinline__ int64_t lay_off(const Lay& L, int64_t pix, int32_t c) {
   if (L.cpc == 0) return pix * L.C + c;
-  return (static_cast<int64_t>(c / L.cpc) * L.Pp + pix) * L.cpc + (c % L.cpc);
+  return lay_chunk(L, pix, c) * L.cpc + (c % L.cpc);
 }
 
 // quant_code when the clip bounds lie inside int32 (every realize site:
@@ -154,7 +183,10 @@ __device__ __forceinline__ void store_out(const OutDev& o, float v, int32_t code
   } else {
     static_cast<int8_t*>(o.primary)[i] = static_cast<int8_t>(code);
   }
-  if (o.side) o.side[lay_off(o.slay, pix, c)] = static_cast<int8_t>(quant_code(v, o.side_q));
+  if (o.side) {
+    if (o.side_fmt == FMT_I8) static_cast<int8_t*>(o.side)[lay_off(o.slay, pix, c)] = static_cast<int8_t>(quant_code(v, o.side_q));
+    else static_cast<uint16_t*>(o.side)[lay_off(o.slay, pix, c)] = f32_to_bf16(v);
+  }
 }
 
 #endif  // __CUDACC__

@@ -43,23 +43,46 @@ __device__ __forceinline__ Pix decode_pix(int64_t pix, int32_t H, int32_t W) {
 // channel and the stores are contiguous.  Zeros on the border and in the
 // channel padding of the last chunk.
 __global__ void k_input_convert(const float* __restrict__ x, int N, int C, int H, int W, void* out, int fmt,
-                                Lay L, float pre_mul, QDev q) {
-  const int planes = (C + L.cpc - 1) / L.cpc;
-  const int64_t total = static_cast<int64_t>(planes) * L.Pp;
+                                Lay L, int s2d_pad, float pre_mul, QDev q) {
+  const int planes = L.kind == LAY_S2D ? (4 * C + L.cpc - 1) / L.cpc : (C + L.cpc - 1) / L.cpc;
+  const int64_t grid_pix = L.kind == LAY_S2D ? static_cast<int64_t>(N) * L.Hq * L.Wq
+                                             : static_cast<int64_t>(N) * (H + 2 * kPad) * (W + 2 * kPad);
+  const int64_t total = static_cast<int64_t>(planes) * grid_pix;
   GRID_STRIDE(i, total) {
-    int64_t pix = i % L.Pp;
-    int32_t c0 = static_cast<int32_t>(i / L.Pp) * L.cpc;
-    Pix p = decode_pix(pix, H, W);
+    int64_t pix = i % grid_pix;
+    int32_t pl = static_cast<int32_t>(i / grid_pix);
     float v[16];
+    bool live[16];
+    int64_t dst_chunk;
+    if (L.kind == LAY_S2D) {
+      // s2d pixel (n, si, sj), channel sc = (py*2 + px)*C + c  <-  x[n][c][2si+py-pad][2sj+px-pad]
+      int32_t sj = static_cast<int32_t>(pix % L.Wq);
+      int64_t t = pix / L.Wq;
+      int32_t si = static_cast<int32_t>(t % L.Hq);
+      int32_t n = static_cast<int32_t>(t / L.Hq);
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      v[k] = 0.f;
-      if (k < L.cpc && !p.border && c0 + k < C) {
-        v[k] = x[((static_cast<int64_t>(p.n) * C + c0 + k) * H + p.h) * W + p.w];
-        if (pre_mul != 0.f) v[k] = __fmul_rn(v[k], pre_mul);
+      for (int k = 0; k < 16; ++k) {
+        int sc = pl * L.cpc + k;
+        int ph = sc / C, c = sc - ph * C;
+        int y = 2 * si + (ph >> 1) - s2d_pad, xx = 2 * sj + (ph & 1) - s2d_pad;
+        live[k] = k < L.cpc && sc < 4 * C && y >= 0 && y < H && xx >= 0 && xx < W;
+        v[k] = live[k] ? x[((static_cast<int64_t>(n) * C + c) * H + y) * W + xx] : 0.f;
       }
+      dst_chunk = pl * L.Pp + pix;
+    } else {
+      Pix p = decode_pix(pix, H, W);
+      int32_t c0 = pl * L.cpc;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        live[k] = k < L.cpc && !p.border && c0 + k < C;
+        v[k] = live[k] ? x[((static_cast<int64_t>(p.n) * C + c0 + k) * H + p.h) * W + p.w] : 0.f;
+      }
+      dst_chunk = lay_chunk(L, pix, c0);
     }
-    char* dst = static_cast<char*>(out) + i * 16;
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (pre_mul != 0.f && live[k]) v[k] = __fmul_rn(v[k], pre_mul);
+    char* dst = static_cast<char*>(out) + dst_chunk * 16;
     if (fmt == FMT_F32) {
       *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
     } else if (fmt == FMT_BF16) {
@@ -76,7 +99,7 @@ __global__ void k_input_convert(const float* __restrict__ x, int N, int C, int H
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           int k = 4 * h + b;
-          int32_t code = (!p.border && c0 + k < C) ? quant_code(v[k], q) : 0;
+          int32_t code = live[k] ? quant_code(v[k], q) : 0;
           u |= (static_cast<uint32_t>(code) & 0xff) << (8 * b);
         }
         w4[h] = u;
@@ -105,10 +128,12 @@ __global__ void k_to_nchw(const void* __restrict__ x, int fmt, Lay L, float c2, 
   }
 }
 
-// ---- zero the one-pixel border of a P16 buffer (after CUDA-core producers) -------
-__global__ void k_zero_border(void* buf, int64_t Pp, int planes, int N, int H, int W) {
-  const int32_t Hp = H + 2 * kPad, Wp = W + 2 * kPad;
+// ---- zero the one-pixel border of a P16 buffer (after producers that write
+// interior pixels only) -- NORMAL or PHASE layout -----------------------------------
+__global__ void k_zero_border(void* buf, Lay L, int N) {
+  const int32_t Hp = L.Hp, Wp = L.Wp, H = Hp - 2 * kPad;
   const int32_t per = 2 * Wp + 2 * H;  // border pixels per image
+  const int planes = (L.C + L.cpc - 1) / L.cpc;
   const int64_t total = static_cast<int64_t>(planes) * N * per;
   GRID_STRIDE(i, total) {
     int32_t b = static_cast<int32_t>(i % per);
@@ -128,7 +153,7 @@ __global__ void k_zero_border(void* buf, int64_t Pp, int planes, int N, int H, i
       wp = (r & 1) ? Wp - 1 : 0;
     }
     int64_t pix = (static_cast<int64_t>(n) * Hp + hp) * Wp + wp;
-    reinterpret_cast<int4*>(buf)[plane * Pp + pix] = make_int4(0, 0, 0, 0);
+    reinterpret_cast<int4*>(buf)[lay_chunk(L, pix, plane * L.cpc)] = make_int4(0, 0, 0, 0);
   }
 }
 
@@ -137,14 +162,18 @@ __global__ void k_zero_border(void* buf, int64_t Pp, int planes, int N, int H, i
 //   WL_ROWS (I8 / BF16): [O][KH][KW][Cs]               CUDA-core kernels
 //   WL_TC   (I8 / BF16): [KH*KW][I/cpc][O][cpc]        tcgen05 B operand (16-byte K chunks)
 //   F32 strict:          [O][I][KH][KW]                reference loop order
+//   WL_S2D  (I8 / BF16): [TA*TA][4I/cpc][O][cpc]      stride-2 stem over the space-to-depth
+//                        input: tap (a, b), s2d channel (py*2+px)*I + c  <-  w[o][c][2a+py][2b+px]
 __global__ void k_weight_prep(const float* __restrict__ w, int O, int I, int KH, int KW, int Cs, int wl,
                               const float* __restrict__ oc_scale, float scalar, int fmt, int quant, QDev q,
                               void* out) {
   const int cpc = fmt == FMT_I8 ? 16 : 8;
-  const int planes = (I + cpc - 1) / cpc;
+  const int TA = (KH + 1) / 2;
+  const int planes = wl == WL_S2D ? (4 * I + cpc - 1) / cpc : (I + cpc - 1) / cpc;
   int64_t total;
   if (fmt == FMT_F32) total = static_cast<int64_t>(O) * I * KH * KW;
   else if (wl == WL_TC) total = static_cast<int64_t>(KH) * KW * planes * O * cpc;
+  else if (wl == WL_S2D) total = static_cast<int64_t>(TA) * TA * planes * O * cpc;
   else total = static_cast<int64_t>(O) * KH * KW * Cs;
   GRID_STRIDE(i, total) {
     int o, ic, kh, kw;
@@ -165,6 +194,19 @@ __global__ void k_weight_prep(const float* __restrict__ w, int O, int I, int KH,
       ic = plane * cpc + within;
       kh = tap / KW;
       kw = tap % KW;
+    } else if (wl == WL_S2D) {
+      int within = static_cast<int>(i % cpc);
+      int64_t t = i / cpc;
+      o = static_cast<int>(t % O);
+      t /= O;
+      int plane = static_cast<int>(t % planes);
+      int tap = static_cast<int>(t / planes);
+      int sc = plane * cpc + within;
+      int ph = sc / I;
+      ic = sc - ph * I;
+      kh = 2 * (tap / TA) + (ph >> 1);
+      kw = 2 * (tap % TA) + (ph & 1);
+      if (sc >= 4 * I || kh >= KH || kw >= KW) ic = I;  // structural zero
     } else {
       ic = static_cast<int>(i % Cs);
       int64_t t = i / Cs;
@@ -446,8 +488,12 @@ __global__ void k_maxpool(const void* __restrict__ x, int xfmt, ConvGeom g, OutD
     }
     if (out.side) {
       int c0 = plane * cpc;
-      for (int k = 0; k < cpc; ++k)
-        if (c0 + k < g.C) out.side[lay_off(out.slay, pix, c0 + k)] = static_cast<int8_t>(quant_code(acc[k], out.side_q));
+      for (int k = 0; k < cpc; ++k) {
+        if (c0 + k >= g.C) break;
+        int64_t so = lay_off(out.slay, pix, c0 + k);
+        if (out.side_fmt == FMT_I8) static_cast<int8_t*>(out.side)[so] = static_cast<int8_t>(quant_code(acc[k], out.side_q));
+        else static_cast<uint16_t*>(out.side)[so] = f32_to_bf16(acc[k]);
+      }
     }
   }
 }
@@ -520,9 +566,12 @@ unsigned grid_stride_blocks(int64_t total) {
 }  // namespace
 
 void launch_input_convert(const float* x, int N, int C, int H, int W, void* out, int fmt, const Lay& L,
-                          float pre_mul, QDev q, cudaStream_t s) {
-  int64_t total = static_cast<int64_t>((C + L.cpc - 1) / L.cpc) * L.Pp;
-  k_input_convert<<<grid_stride_blocks(total), kThreads, 0, s>>>(x, N, C, H, W, out, fmt, L, pre_mul, q);
+                          int s2d_pad, float pre_mul, QDev q, cudaStream_t s) {
+  int planes = L.kind == LAY_S2D ? (4 * C + L.cpc - 1) / L.cpc : (C + L.cpc - 1) / L.cpc;
+  int64_t grid_pix = L.kind == LAY_S2D ? static_cast<int64_t>(N) * L.Hq * L.Wq
+                                       : static_cast<int64_t>(N) * (H + 2 * kPad) * (W + 2 * kPad);
+  k_input_convert<<<grid_stride_blocks(planes * grid_pix), kThreads, 0, s>>>(x, N, C, H, W, out, fmt, L, s2d_pad,
+                                                                            pre_mul, q);
 }
 
 void launch_to_nchw(const void* x, int fmt, const Lay& L, float c2, float* y, int N, int C, int H, int W, int is4d,
@@ -531,19 +580,21 @@ void launch_to_nchw(const void* x, int fmt, const Lay& L, float c2, float* y, in
   k_to_nchw<<<grid_stride_blocks(total), kThreads, 0, s>>>(x, fmt, L, c2, y, N, C, H, W, is4d);
 }
 
-void launch_zero_border(void* buf, const Lay& L, int N, int H, int W, cudaStream_t s) {
+void launch_zero_border(void* buf, const Lay& L, int N, cudaStream_t s) {
   int planes = (L.C + L.cpc - 1) / L.cpc;
-  int64_t total = static_cast<int64_t>(planes) * N * (2 * (W + 2 * kPad) + 2 * H);
-  k_zero_border<<<grid_stride_blocks(total), kThreads, 0, s>>>(buf, L.Pp, planes, N, H, W);
+  int64_t total = static_cast<int64_t>(planes) * N * (2 * L.Wp + 2 * (L.Hp - 2 * kPad));
+  k_zero_border<<<grid_stride_blocks(total), kThreads, 0, s>>>(buf, L, N);
 }
 
 void launch_weight_prep(const float* w, int O, int I, int KH, int KW, int Cs, int wl, const float* oc_scale,
                         float scalar, int fmt, int quant, QDev q, void* out, cudaStream_t s) {
   int cpc = fmt == FMT_I8 ? 16 : 8;
-  int planes = (I + cpc - 1) / cpc;
+  int TA = (KH + 1) / 2;
+  int planes = wl == WL_S2D ? (4 * I + cpc - 1) / cpc : (I + cpc - 1) / cpc;
   int64_t total;
   if (fmt == FMT_F32) total = static_cast<int64_t>(O) * I * KH * KW;
   else if (wl == WL_TC) total = static_cast<int64_t>(KH) * KW * planes * O * cpc;
+  else if (wl == WL_S2D) total = static_cast<int64_t>(TA) * TA * planes * O * cpc;
   else total = static_cast<int64_t>(O) * KH * KW * Cs;
   k_weight_prep<<<grid_stride_blocks(total), kThreads, 0, s>>>(w, O, I, KH, KW, Cs, wl, oc_scale, scalar, fmt, quant,
                                                               q, out);
