@@ -34,6 +34,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -44,7 +45,7 @@ namespace mrb200 {
 namespace {
 
 constexpr int kTileM = 128;
-constexpr int kEpiWarps = 8;
+constexpr int kEpiWarps = 16;
 constexpr int kThreadsTc = (2 + kEpiWarps) * 32;
 constexpr int kSmemBudget = 227 * 1024 - 1024;
 
@@ -59,7 +60,8 @@ inline int epi_signature(const EpiDev& e, const OutDev& o) {
   if (e.n_ops == 1 && e.op[0] == E_BIAS && o.primary_fmt != FMT_I8) return SIG_BIAS;
   if (e.n_ops == 2 && e.op[0] == E_BIAS && e.op[1] == E_RELU && o.primary_fmt != FMT_I8) return SIG_BIAS_RELU;
   if (e.n_ops == 3 && e.op[0] == E_BIAS && e.op[1] == E_RELU && e.op[2] == E_REQ && o.primary_fmt == FMT_I8 &&
-      !o.side && q_ok(e.q[2]))
+      !o.side && q_ok(e.q[2]) && e.q[2].lo <= 0.f && e.q[2].c1 > 0.f &&
+      e.q[2].hi <= (e.q[2].is_signed ? 127.f : 255.f) && e.q[2].hi >= 0.f)
     return SIG_BIAS_RELU_REQ;
   if (e.n_ops == 3 && e.op[0] == E_BIAS && e.op[1] == E_RES && e.op[2] == E_RELU && o.primary_fmt != FMT_I8)
     return SIG_BIAS_RES_RELU;
@@ -91,6 +93,7 @@ struct TcArgs {
   uint32_t idesc;
   int32_t out_mode, OH, OW;  // OUT_REMAP: valid outputs are grid (y < OH, x < OW)
   float acc_scale;
+  int32_t dbg;  // MRB200_TC_DBG bit 0: skip epilogue math, bit 1: skip MMAs (timing experiments only)
   EpiDev epi;
   OutDev out;
 };
@@ -313,9 +316,14 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
       for (int i = 0; i < 16; ++i) v[i] = relu_ref(v[i]);
     }
     if constexpr (SIG == SIG_BIAS_RELU_REQ) {
+      // v >= +0 after relu and c1 > 0 (checked on the host), so rint(v*c1) >= 0 >= lo:
+      // clip(t, lo, hi) == min(t, hi); the value is integral and < 2^31 -> exact cvt.
       const QDev qd = e.q[2];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) code[i] = quant_code_fast(v[i], qd);
+      for (int i = 0; i < 16; ++i) {
+        float t = fminf(rintf(__fmul_rn(v[i], qd.c1)), qd.hi);
+        code[i] = __float2int_rz(t);
+      }
       // v (= code * c2) is only needed for a side output, never emitted here
     }
   }
@@ -437,68 +445,75 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ===== MMA issuer (one thread) =====
-      if (a.resident_b) mbar_wait(bfull, 0);
-      int stage = 0;
-      uint32_t phase = 0;
-      int acc = 0;
-      uint32_t acc_phase = 0;
-      const uint32_t smB_u = smem_u32(smB);
-      const uint32_t smA_u = smem_u32(smA);
-      for (int mt = m_start; mt < a.m_tiles; mt += m_step) {
-        const int row0 = mt * kTileM + a.dmin;
-        const uint32_t shift16 = static_cast<uint32_t>(row0 - 8 * floor_div8(row0)) * 16;
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+    // ===== MMA issuer =====
+    // The whole warp walks the loop so tile/stage/descriptor values are
+    // warp-uniform (uniform registers); lane 0 issues tcgen05.mma / commit.
+    // Descriptors: base | (start >> 4); LBO/SBO/version fixed per step.
+    if (a.resident_b) mbar_wait(bfull, 0);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    const uint32_t smB_u = smem_u32(smB);
+    const uint32_t smA_u = smem_u32(smA);
+    for (int mt = m_start; mt < a.m_tiles; mt += m_step) {
+      const int row0 = mt * kTileM + a.dmin;
+      const uint32_t shift16 = static_cast<uint32_t>(row0 - 8 * floor_div8(row0)) * 16;
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * a.bn);
+      for (int ks = 0; ks < a.k_stages; ++ks) {
+        mbar_wait(&full[stage], phase);
         tc_fence_after();
-        const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * a.bn);
-        for (int ks = 0; ks < a.k_stages; ++ks) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint32_t sA = smA_u + stage * a.a_stage_bytes + shift16;
-          const uint32_t sB = a.resident_b ? smB_u + ks * a.b_ks_stride : smB_u + stage * a.b_stage_bytes;
-          for (int st = 0; st < a.n_steps; ++st) {
-            const MmaStep m = a.steps[st];
-            umma<EB>(tmem_d, umma_desc(sA + m.a_off, m.a_lbo, 128), umma_desc(sB + m.b_off, m.b_lbo, 128), a.idesc,
-                     (ks | st) != 0 ? 1u : 0u);
-          }
-          umma_commit(&empty[stage]);  // frees the smem stage when these MMAs retire
-          if (++stage == a.n_stages) {
-            stage = 0;
-            phase ^= 1;
-          }
+        const uint32_t sA = smA_u + stage * a.a_stage_bytes + shift16;
+        const uint32_t sB = a.resident_b ? smB_u + ks * a.b_ks_stride : smB_u + stage * a.b_stage_bytes;
+#pragma unroll 2
+        for (int st = 0; st < a.n_steps; ++st) {
+          const MmaStep m = a.steps[st];
+          const uint32_t aaddr = (a.dbg & 4) ? ((sA + m.a_off) & ~127u) : sA + m.a_off;
+          const uint64_t ad = umma_desc(aaddr, m.a_lbo, 128);
+          const uint64_t bd = umma_desc(sB + m.b_off, m.b_lbo, 128);
+          if (lane == 0 && !(a.dbg & 2)) umma<EB>(tmem_d, ad, bd, a.idesc, (ks | st) != 0 ? 1u : 0u);
         }
-        umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
-        if (++acc == 2) {
-          acc = 0;
-          acc_phase ^= 1;
+        __syncwarp();
+        if (lane == 0) umma_commit(&empty[stage]);  // frees the smem stage when these MMAs retire
+        __syncwarp();
+        if (++stage == a.n_stages) {
+          stage = 0;
+          phase ^= 1;
         }
+      }
+      if (lane == 0) umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+      __syncwarp();
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
       }
     }
   } else {
     // ===== epilogue warps =====
-    // warp w (2..9): TMEM lane quarter w % 4 (hardware lane-access rule),
-    // column half (w - 2) / 4.
+    // warp w (2..17): TMEM lane quarter w % 4 (hardware lane-access rule),
+    // 16-column chunks slice, slice + 4, ... with slice = (w - 2) / 4.
     const int quarter = warp & 3;
-    const int half = (warp - 2) >> 2;
+    const int slice = (warp - 2) >> 2;
     const int row = quarter * 32 + lane;
-    const int cols = a.bn / 2;
     const Lay& sl = a.out.slay;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int mt = m_start; mt < a.m_tiles; mt += m_step) {
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int64_t q = static_cast<int64_t>(mt) * kTileM + row;
+      const uint32_t q = static_cast<uint32_t>(mt) * kTileM + row;  // grids < 2^31 pixels (checked on the host)
       RowDst d;
-      bool valid = q < a.Pg;
+      bool valid = q < static_cast<uint32_t>(a.Pg);
       d.border = false;
       d.pix = 0;
       if (valid) {
-        const int x = static_cast<int>(q % a.Wg);
-        const int64_t t = q / a.Wg;
-        const int y = static_cast<int>(t % a.Hg);
-        const int n = static_cast<int>(t / a.Hg);
+        const uint32_t t = q / static_cast<uint32_t>(a.Wg);
+        const int x = static_cast<int>(q - t * static_cast<uint32_t>(a.Wg));
+        const uint32_t n32 = t / static_cast<uint32_t>(a.Hg);
+        const int y = static_cast<int>(t - n32 * static_cast<uint32_t>(a.Hg));
+        const int n = static_cast<int>(n32);
         if (a.out_mode == OUT_SAME) {
           d.pix = q;
           d.border = x == 0 || x == a.Wg - 1 || y == 0 || y == a.Hg - 1;
@@ -508,11 +523,13 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         }
         if (a.out.side) {
           if (sl.kind == LAY_PHASE) {
-            const int wp = static_cast<int>(d.pix % sl.Wp);
-            const int64_t tt = d.pix / sl.Wp;
-            const int hp = static_cast<int>(tt % sl.Hp);
-            const int64_t nn = tt / sl.Hp;
-            d.side_base = static_cast<int64_t>((hp & 1) * 2 + (wp & 1)) * sl.Pp + (nn * sl.Hq + hp / 2) * sl.Wq + wp / 2;
+            const uint32_t p32 = static_cast<uint32_t>(d.pix);
+            const uint32_t tt = p32 / static_cast<uint32_t>(sl.Wp);
+            const int wp = static_cast<int>(p32 - tt * static_cast<uint32_t>(sl.Wp));
+            const uint32_t nn = tt / static_cast<uint32_t>(sl.Hp);
+            const int hp = static_cast<int>(tt - nn * static_cast<uint32_t>(sl.Hp));
+            d.side_base = static_cast<int64_t>((hp & 1) * 2 + (wp & 1)) * sl.Pp +
+                          (static_cast<int64_t>(nn) * sl.Hq + hp / 2) * sl.Wq + wp / 2;
             d.side_pstride = 4 * sl.Pp;
           } else {
             d.side_base = d.pix;
@@ -520,12 +537,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           }
         }
       }
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
-                             static_cast<uint32_t>(acc * a.bn + half * cols);
-      for (int c = 0; c < cols; c += 16) {
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * a.bn);
+      for (int c = slice * 16; c < a.bn; c += 64) {
         uint32_t raw[16];
         tmem_ld16(taddr + static_cast<uint32_t>(c), raw);  // warp-collective: every lane executes it
-        if (valid) epilogue_chunk<EB, SIG>(a, raw, d, n_tile * a.bn + half * cols + c);
+        if (valid && !(a.dbg & 1)) epilogue_chunk<EB, SIG>(a, raw, d, n_tile * a.bn + c);
       }
       tc_fence_before();
       __syncwarp();
@@ -648,6 +664,7 @@ static bool choose(TcConvPlan& p) {
       return false;
   }
   a.Pg = static_cast<int64_t>(a.N) * a.Hg * a.Wg;
+  if (a.Pg + kTileM >= (int64_t(1) << 31)) return false;
   a.m_tiles = static_cast<int>((a.Pg + kTileM - 1) / kTileM);
   int dmin = 1 << 30, dmax = -(1 << 30);
   for (const Tap& t : taps) {
@@ -670,8 +687,12 @@ static bool choose(TcConvPlan& p) {
     }
   if (!bn) return false;
   bool found = false;
+  static const int force_stream = [] {
+    const char* e = std::getenv("MRB200_TC_STREAM");
+    return e ? std::atoi(e) : 0;
+  }();
   // resident weights if they fit beside >= 3 A stages, else stream them
-  for (int cand = bn; cand >= 16 && !found; cand /= 2) {
+  for (int cand = bn; cand >= 16 && !found && !force_stream; cand /= 2) {
     if (sp.OC % cand) continue;
     int b_res = ntaps * cc * cand * 16;
     for (int pps : {8, 4, 2, 1}) {
@@ -821,6 +842,11 @@ bool tc_conv_launch(TcConvPlan* p, const void* x, const Lay& xl, const void* w, 
   }
   TcArgs a = p->args;
   a.acc_scale = acc_scale;
+  static const int dbg = [] {
+    const char* e = std::getenv("MRB200_TC_DBG");
+    return e ? std::atoi(e) : 0;
+  }();
+  a.dbg = dbg;
   a.epi = epi;
   a.out = out;
   const int sig = epi_signature(epi, out);

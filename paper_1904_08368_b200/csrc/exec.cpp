@@ -891,10 +891,16 @@ void prepare_weights(Exec& ex, cudaStream_t s) {
     } else {
       n = static_cast<int64_t>(O) * KH * KW * cs;
     }
+    const bool dense_t = g.kind == GroupKind::Dense && fmt != FMT_F32;  // transposed k_dense layouts
+    if (dense_t) n = static_cast<int64_t>(O) * cs;
     void* dst = nullptr;
     CK(cudaMalloc(&dst, static_cast<size_t>(n * elem_bytes(fmt))));
-    launch_weight_prep(raw, O, I, KH, KW, cs, wl, static_cast<const float*>(ex.group_vecs[gi][0]), w.scalar_scale,
-                       fmt, w.quant ? 1 : 0, to_qdev(w.q), dst, s);
+    if (dense_t)
+      launch_dense_weight_t(raw, O, I, cs, static_cast<const float*>(ex.group_vecs[gi][0]), w.scalar_scale, fmt,
+                            w.quant ? 1 : 0, to_qdev(w.q), dst, s);
+    else
+      launch_weight_prep(raw, O, I, KH, KW, cs, wl, static_cast<const float*>(ex.group_vecs[gi][0]), w.scalar_scale,
+                         fmt, w.quant ? 1 : 0, to_qdev(w.q), dst, s);
     CK(cudaGetLastError());
     ex.group_w[gi] = dst;
     ex.group_kp[gi] = fmt == FMT_F32 ? I * KH * KW : KH * KW * cs;
@@ -914,7 +920,8 @@ void prepare_weights(Exec& ex, cudaStream_t s) {
       std::vector<int64_t> sums(O, 0);
       int64_t per = n / O, worst = 0;
       for (int64_t k = 0; k < n; ++k) {
-        int o = wl != WL_ROWS ? static_cast<int>((k / 16) % O) : static_cast<int>(k / per);
+        int o = dense_t ? static_cast<int>((k / 4) % O)
+                : wl != WL_ROWS ? static_cast<int>((k / 16) % O) : static_cast<int>(k / per);
         sums[o] += std::abs(static_cast<int>(codes[k]));
       }
       for (int o = 0; o < O; ++o) worst = std::max(worst, sums[o]);

@@ -435,32 +435,42 @@ __global__ void k_dwconv(const void* __restrict__ x, int xfmt, const float* __re
 }
 
 // ---- max pooling: max over valid taps, seeded with the first (harness kernel) ----
-// One thread per (output pixel, 16-byte input chunk): 16-byte loads per tap,
-// 16-byte stores, plus the consumers' int8 codes (side) when requested.
+// One thread per (output pixel, 16-byte chunk), output column fastest; 32-bit
+// index math; the window's taps are 16-byte loads from the padded P16 input
+// (padded taps skipped, like the reference's bounds test).  Also emits the
+// consumers' second copy (int8 codes or bf16) when requested.
 __global__ void k_maxpool(const void* __restrict__ x, int xfmt, ConvGeom g, OutDev out) {
   const int cpc = g.in.cpc;
-  const int planes = (g.C + cpc - 1) / cpc;
-  const int64_t M = static_cast<int64_t>(g.N) * g.OH * g.OW;
-  const int64_t total = M * planes;
-  GRID_STRIDE(i, total) {
-    int64_t m = i % M;
-    int plane = static_cast<int>(i / M);
-    OutPix o = decode_out(m, g);
+  const uint32_t planes = static_cast<uint32_t>((g.C + cpc - 1) / cpc);
+  const uint32_t total = planes * g.N * g.OH * g.OW;
+  const int Hp = g.H + 2 * kPad, Wp = g.W + 2 * kPad;
+  const int OHp = g.OH + 2 * kPad, OWp = g.OW + 2 * kPad;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    uint32_t t = i / g.OW;
+    const int ow = static_cast<int>(i - t * g.OW);
+    uint32_t t2 = t / g.OH;
+    const int oh = static_cast<int>(t - t2 * g.OH);
+    const uint32_t plane = t2 / g.N;
+    const int n = static_cast<int>(t2 - plane * g.N);
+    const int h0 = oh * g.sh - g.ph, w0 = ow * g.sw - g.pw;  // logical window origin
+    const char* src = static_cast<const char*>(x) +
+                      (static_cast<int64_t>(plane) * g.in.Pp + (static_cast<int64_t>(n) * Hp + h0 + kPad) * Wp + w0 + kPad) * 16;
     float acc[8];
-    bool seeded = false;
 #pragma unroll
     for (int k = 0; k < 8; ++k) acc[k] = 0.f;
-    for (int kh = 0; kh < g.KH; ++kh)
+    bool seeded = false;
+    for (int kh = 0; kh < g.KH; ++kh) {
+      const bool hv = h0 + kh >= 0 && h0 + kh < g.H;
       for (int kw = 0; kw < g.KW; ++kw) {
-        int h = o.oh * g.sh - g.ph + kh, ww = o.ow * g.sw - g.pw + kw;
-        if (h < 0 || h >= g.H || ww < 0 || ww >= g.W) continue;
-        const char* src = static_cast<const char*>(x) + (plane * g.in.Pp + pad_pix(o.n, h, ww, g.H, g.W)) * 16;
+        if (!hv || w0 + kw < 0 || w0 + kw >= g.W) continue;
+        const char* p = src + (kh * Wp + kw) * 16;
         float v[8];
         if (xfmt == FMT_F32) {
-          float4 f = *reinterpret_cast<const float4*>(src);
+          float4 f = __ldg(reinterpret_cast<const float4*>(p));
           v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+          v[4] = v[5] = v[6] = v[7] = 0.f;
         } else {
-          uint4 u = *reinterpret_cast<const uint4*>(src);
+          uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
           uint32_t w4[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
           for (int b = 0; b < 4; ++b) {
@@ -469,14 +479,12 @@ __global__ void k_maxpool(const void* __restrict__ x, int xfmt, ConvGeom g, OutD
           }
         }
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          if (k >= cpc) break;
-          acc[k] = !seeded ? v[k] : (acc[k] < v[k] ? v[k] : acc[k]);  // std::max(acc, v)
-        }
+        for (int k = 0; k < 8; ++k) acc[k] = !seeded ? v[k] : (acc[k] < v[k] ? v[k] : acc[k]);  // std::max(acc, v)
         seeded = true;
       }
-    int64_t pix = pad_pix(o.n, o.oh, o.ow, g.OH, g.OW);
-    char* dst = static_cast<char*>(out.primary) + (plane * out.plan.Pp + pix) * 16;
+    }
+    const int64_t pix = (static_cast<int64_t>(n) * OHp + oh + kPad) * OWp + ow + kPad;
+    char* dst = static_cast<char*>(out.primary) + (static_cast<int64_t>(plane) * out.plan.Pp + pix) * 16;
     if (out.primary_fmt == FMT_F32) {
       *reinterpret_cast<float4*>(dst) = make_float4(acc[0], acc[1], acc[2], acc[3]);
     } else {
@@ -487,12 +495,18 @@ __global__ void k_maxpool(const void* __restrict__ x, int xfmt, ConvGeom g, OutD
       *reinterpret_cast<uint4*>(dst) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
     }
     if (out.side) {
-      int c0 = plane * cpc;
-      for (int k = 0; k < cpc; ++k) {
-        if (c0 + k >= g.C) break;
-        int64_t so = lay_off(out.slay, pix, c0 + k);
-        if (out.side_fmt == FMT_I8) static_cast<int8_t*>(out.side)[so] = static_cast<int8_t>(quant_code(acc[k], out.side_q));
-        else static_cast<uint16_t*>(out.side)[so] = f32_to_bf16(acc[k]);
+      const int c0 = static_cast<int>(plane) * cpc;
+      if (out.side_fmt == FMT_I8 && cpc == 4 && c0 + 4 <= g.C) {
+        uint32_t u = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) u |= (static_cast<uint32_t>(quant_code_fast(acc[k], out.side_q)) & 0xff) << (8 * k);
+        *reinterpret_cast<uint32_t*>(static_cast<char*>(out.side) + lay_chunk(out.slay, pix, c0) * 16 + (c0 % 16)) = u;
+      } else {
+        for (int k = 0; k < cpc && c0 + k < g.C; ++k) {
+          int64_t so = lay_off(out.slay, pix, c0 + k);
+          if (out.side_fmt == FMT_I8) static_cast<int8_t*>(out.side)[so] = static_cast<int8_t>(quant_code(acc[k], out.side_q));
+          else static_cast<uint16_t*>(out.side)[so] = f32_to_bf16(acc[k]);
+        }
       }
     }
   }
@@ -514,46 +528,98 @@ __global__ void k_sum_hw(const float* __restrict__ x, Lay L, int N, int H, int W
 }
 
 // ---- dense ----------------------------------------------------------------------------
-// One block per (row n, 256 outputs).  The data row (float32) gets its prologue
-// (pre_mul, realize chain) applied once into shared memory.
-//   mode 0: int8 codes, dp4a, int32 acc * acc_scale
-//   mode 1: float32 strict, sequential k (kernels.cpp:618-623)
+// Block = kDenseRows data rows x 256 outputs.  The rows get their prologue
+// (pre_mul, realize chain) once into shared memory; each thread owns one
+// output column j and walks K once, reading the transposed weights
+// ([K/4][M] int8 words or [K][M] bf16, coalesced across j) and updating
+// kDenseRows accumulators per weight load.
+//   mode 0: int8 codes, dp4a, int32 acc * acc_scale (exact)
+//   mode 1: float32 strict, sequential k (kernels.cpp:618-623), weights [M][K]
 //   mode 2: bf16 weights, fp32 FMA accumulate
-__global__ void k_dense(const float* __restrict__ x, int N, int K, int Kp, const void* __restrict__ w, int M,
-                        int mode, float pre_mul, int quant, QDev q, float acc_scale, EpiDev epi, OutDev out) {
-  extern __shared__ float srow[];
-  int n = blockIdx.y;
+constexpr int kDenseRows = 16;
+
+__global__ void __launch_bounds__(256) k_dense(const float* __restrict__ x, int N, int K, int Kp,
+                                               const void* __restrict__ w, int M, int mode, float pre_mul, int quant,
+                                               QDev q, float acc_scale, EpiDev epi, OutDev out) {
+  extern __shared__ float srow[];  // [kDenseRows][Kp] floats (mode 1/2) or bytes (mode 0)
+  const int n0 = blockIdx.y * kDenseRows;
   int8_t* scode = reinterpret_cast<int8_t*>(srow);
-  for (int k = threadIdx.x; k < Kp; k += blockDim.x) {
-    float v = k < K ? x[static_cast<int64_t>(n) * K + k] : 0.f;
-    if (pre_mul != 0.f && k < K) v = __fmul_rn(v, pre_mul);
-    if (mode == 0) scode[k] = k < K ? static_cast<int8_t>(quant ? quant_code(v, q) : static_cast<int32_t>(v)) : 0;
-    else srow[k] = v;
+  for (int idx = threadIdx.x; idx < kDenseRows * Kp; idx += blockDim.x) {
+    int r = idx / Kp, k = idx - r * Kp;
+    int n = n0 + r;
+    bool live = n < N && k < K;
+    float v = live ? x[static_cast<int64_t>(n) * K + k] : 0.f;
+    if (pre_mul != 0.f && live) v = __fmul_rn(v, pre_mul);
+    if (mode == 0) scode[idx] = live ? static_cast<int8_t>(quant ? quant_code(v, q) : static_cast<int32_t>(v)) : 0;
+    else srow[idx] = v;
   }
   __syncthreads();
-  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= M) return;
-  float v;
+  float res[kDenseRows];
   if (mode == 0) {
-    const int8_t* wr = static_cast<const int8_t*>(w) + static_cast<int64_t>(j) * Kp;
-    int acc = 0;
-    for (int k = 0; k < Kp; k += 4)
-      acc = __dp4a(*reinterpret_cast<const int32_t*>(scode + k), *reinterpret_cast<const int32_t*>(wr + k), acc);
-    v = __fmul_rn(static_cast<float>(acc), acc_scale);
+    int acc[kDenseRows];
+#pragma unroll
+    for (int r = 0; r < kDenseRows; ++r) acc[r] = 0;
+    const int32_t* wt = static_cast<const int32_t*>(w);
+    for (int kw = 0; kw < Kp / 4; ++kw) {
+      const int32_t wv = __ldg(wt + static_cast<int64_t>(kw) * M + j);
+#pragma unroll
+      for (int r = 0; r < kDenseRows; ++r)
+        acc[r] = __dp4a(*reinterpret_cast<const int32_t*>(scode + r * Kp + kw * 4), wv, acc[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < kDenseRows; ++r) res[r] = __fmul_rn(static_cast<float>(acc[r]), acc_scale);
   } else if (mode == 1) {
     const float* wr = static_cast<const float*>(w) + static_cast<int64_t>(j) * K;
-    float acc = 0.0f;
-    for (int k = 0; k < K; ++k) acc = __fadd_rn(acc, __fmul_rn(srow[k], wr[k]));
-    v = acc;
+#pragma unroll
+    for (int r = 0; r < kDenseRows; ++r) res[r] = 0.0f;
+    for (int k = 0; k < K; ++k) {
+      const float wv = wr[k];
+#pragma unroll
+      for (int r = 0; r < kDenseRows; ++r) res[r] = __fadd_rn(res[r], __fmul_rn(srow[r * Kp + k], wv));
+    }
   } else {
-    const uint16_t* wr = static_cast<const uint16_t*>(w) + static_cast<int64_t>(j) * Kp;
-    float acc = 0.0f;
-    for (int k = 0; k < K; ++k) acc = __fmaf_rn(srow[k], bf16_to_f32(wr[k]), acc);
-    v = acc;
+    const uint16_t* wt = static_cast<const uint16_t*>(w);
+#pragma unroll
+    for (int r = 0; r < kDenseRows; ++r) res[r] = 0.0f;
+    for (int k = 0; k < K; ++k) {
+      const float wv = bf16_to_f32(__ldg(wt + static_cast<int64_t>(k) * M + j));
+#pragma unroll
+      for (int r = 0; r < kDenseRows; ++r) res[r] = __fmaf_rn(srow[r * Kp + k], wv, res[r]);
+    }
   }
-  int32_t code = 0;
-  v = apply_epi(epi, v, n, j, &code);
-  store_out(out, v, code, n, j);
+#pragma unroll
+  for (int r = 0; r < kDenseRows; ++r) {
+    const int n = n0 + r;
+    if (n >= N) break;
+    int32_t code = 0;
+    float v = apply_epi(epi, res[r], n, j, &code);
+    store_out(out, v, code, n, j);
+  }
+}
+
+// [M][K] float32 (after the prologue) -> transposed kernel layouts for k_dense.
+__global__ void k_dense_weight_t(const float* __restrict__ w, int M, int K, int Kp, const float* __restrict__ oc_scale,
+                                 float scalar, int fmt, int quant, QDev q, void* out) {
+  const int64_t total = static_cast<int64_t>(M) * Kp;
+  GRID_STRIDE(i, total) {
+    int j = static_cast<int>(i % M);
+    int k = static_cast<int>(i / M);  // out index: [k][j] (bf16) / [k/4][j][k%4] (int8)
+    float v = 0.f;
+    bool live = k < K;
+    if (live) {
+      v = w[static_cast<int64_t>(j) * K + k];
+      if (oc_scale) v = __fmul_rn(v, oc_scale[j]);
+      if (scalar != 0.f) v = __fmul_rn(v, scalar);
+    }
+    if (fmt == FMT_I8) {
+      int32_t code = live ? (quant ? quant_code(v, q) : static_cast<int32_t>(v)) : 0;
+      static_cast<int8_t*>(out)[(static_cast<int64_t>(k / 4) * M + j) * 4 + (k & 3)] = static_cast<int8_t>(code);
+    } else {
+      static_cast<uint16_t*>(out)[static_cast<int64_t>(k) * M + j] = live ? f32_to_bf16(v) : 0;
+    }
+  }
 }
 
 unsigned grid_stride_blocks(int64_t total) {
@@ -636,10 +702,16 @@ void launch_sum_hw(const float* x, const Lay& L, int N, int H, int W, int C, flo
   k_sum_hw<<<grid_stride_blocks(total), kThreads, 0, s>>>(x, L, N, H, W, C, y);
 }
 
+void launch_dense_weight_t(const float* w, int M, int K, int Kp, const float* oc_scale, float scalar, int fmt,
+                           int quant, QDev q, void* out, cudaStream_t s) {
+  int64_t total = static_cast<int64_t>(M) * Kp;
+  k_dense_weight_t<<<grid_stride_blocks(total), kThreads, 0, s>>>(w, M, K, Kp, oc_scale, scalar, fmt, quant, q, out);
+}
+
 void launch_dense(const float* x, int N, int K, int Kp, const void* w, int M, int mode, float pre_mul,
                   int quant, QDev q, float acc_scale, const EpiDev& epi, const OutDev& out, cudaStream_t s) {
-  dim3 grid(static_cast<unsigned>((M + 255) / 256), static_cast<unsigned>(N));
-  size_t smem = mode == 0 ? static_cast<size_t>(Kp) : static_cast<size_t>(Kp) * sizeof(float);
+  dim3 grid(static_cast<unsigned>((M + 255) / 256), static_cast<unsigned>((N + kDenseRows - 1) / kDenseRows));
+  size_t smem = (mode == 0 ? static_cast<size_t>(Kp) : static_cast<size_t>(Kp) * sizeof(float)) * kDenseRows;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   k_dense<<<grid, 256, smem, s>>>(x, N, K, Kp, w, M, mode, pre_mul, quant, q, acc_scale, epi, out);
 }

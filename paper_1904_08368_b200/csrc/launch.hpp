@@ -28,6 +28,8 @@ void launch_dwconv(const void* x, int xfmt, const float* w, const ConvGeom& g, i
                    const OutDev& out, cudaStream_t s);
 void launch_maxpool(const void* x, int xfmt, const ConvGeom& g, const OutDev& out, cudaStream_t s);
 void launch_sum_hw(const float* x, const Lay& L, int N, int H, int W, int C, float* y, cudaStream_t s);
+void launch_dense_weight_t(const float* w, int M, int K, int Kp, const float* oc_scale, float scalar, int fmt,
+                           int quant, QDev q, void* out, cudaStream_t s);
 void launch_dense(const float* x, int N, int K, int Kp, const void* w, int M, int mode, float pre_mul,
                   int quant, QDev q, float acc_scale, const EpiDev& epi, const OutDev& out, cudaStream_t s);
 
