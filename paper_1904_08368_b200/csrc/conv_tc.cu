@@ -8,25 +8,28 @@
 // relu, requantize, clip) is applied in registers after tcgen05.ld before
 // 16-byte vector stores -- no intermediate tensor touches HBM.
 //
-// Halo implicit GEMM.  Activations are stored P16 (kernels.cuh): per 16-byte
-// channel chunk, one plane over the zero-padded pixel grid.  The GEMM's M
-// dimension enumerates that padded grid directly (M = N*(H+2)*(W+2)), so for
-// a stride-1 "same" conv every tap (kh, kw) of output pixel q reads input
-// pixel q + (kh-1)*Wp + (kw-1).  A 128-row output tile therefore needs ONE
-// contiguous input range of 128 + 2*Wp + 2 pixels per chunk plane, fetched by
-// a single TMA load; the 9 taps are 9 UMMA shared-memory descriptors whose
-// start addresses differ by whole 16-byte rows (K-major, no-swizzle canonical
-// layout: core matrices of 8 rows x 16 bytes, SBO = 128 B between 8-row
-// groups, LBO = plane stride between the two 16-byte K halves).  L2->SM
-// traffic for A is ~(128 + 2Wp + 2)/128 of the output tile instead of the 9x
-// of an im2col gather.  Border rows of the padded grid are computed and
+// Halo implicit GEMM.  Activations are stored "PK" (kernels.cuh): per chunk of
+// kb channel bytes (128 or 64), one plane over the zero-padded pixel grid, one
+// kb-byte row per pixel.  The GEMM's M dimension enumerates that padded grid
+// directly (M = N*(H+2)*(W+2)), so for a stride-1 "same" conv every tap
+// (kh, kw) of output pixel q reads input pixel q + (kh-1)*Wp + (kw-1).  A
+// 128-row output tile therefore needs ONE contiguous input range of
+// 128 + 2*Wp + 2 pixel rows per chunk plane, fetched by a single TMA load with
+// the 128B/64B swizzle; the 9 taps are 9 UMMA K-major shared-memory
+// descriptors whose start addresses differ by whole kb-byte rows (the swizzle
+// is a function of the shared-memory address, so any row start is valid).
+// L2->SM traffic for A is ~(128 + 2Wp + 2)/128 of the output tile instead of
+// the 9x of an im2col gather.  Border rows of the padded grid are computed and
 // written as zeros, which is exactly the zero border the next conv needs.
+// Stride-2 convs read a phase-split input (4 stride-1 sub-grids); the 7x7
+// stem reads a 16-byte space-to-depth input through the no-swizzle canonical
+// layout (8-pixel core-matrix rows).
 //
 // Kernel structure (persistent, warp-specialised, one CTA per SM):
 //   warp 0      TMA producer: weights once (resident) or per stage, A halo
 //               stages through an mbarrier ring
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2-5   epilogue: tcgen05.ld -> epilogue -> st.global.v4
+//   warp 1      TMEM allocator + tcgen05.mma issuer (one lane issues)
+//   warps 2-17  epilogue: tcgen05.ld -> epilogue -> st.global.v4
 //   TMEM        2 accumulator buffers (tile i epilogue overlaps tile i+1 MMA)
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -68,13 +71,14 @@ inline int epi_signature(const EpiDev& e, const OutDev& o) {
   return SIG_ANY;
 }
 
-constexpr int kMaxSteps = 40;
+constexpr int kMaxSteps = 64;
 
 // One tcgen05.mma of a tile's K loop: byte offsets (relative to the A stage
 // base + row shift, and to the B stage / resident base) and the leading byte
 // offsets (distance between the two 16-byte K halves of the instruction).
 struct MmaStep {
   uint32_t a_off, a_lbo, b_off, b_lbo;
+  uint32_t a_lo, b_lo;  // descriptor low words relative to the stage base: off>>4 | (lbo>>4) << 16
 };
 
 enum OutMode : int32_t { OUT_SAME = 0, OUT_REMAP = 1 };
@@ -84,7 +88,11 @@ struct TcArgs {
   int32_t N, Hg, Wg;
   int64_t Pg;  // N*Hg*Wg
   int32_t m_tiles, n_tiles, bn, Cc, pps, k_stages, sub0, subs, hg;
+  int32_t sub;         // 128-row M tiles per super-tile (share B descriptors and the pipeline handshakes)
+  int32_t nbox, hbox;  // A TMA boxes per (plane, sub-grid) block and their height in TMA rows
   int32_t dmin;  // smallest tap row offset (tile row 0 + dmin = first halo row)
+  int32_t kb;    // operand chunk bytes: 128 / 64 (swizzled rows) or 16 (no-swizzle, 8-pixel TMA rows)
+  uint32_t desc_hi;  // SBO / version / layout-type bits [32,64) of every smem descriptor
   int32_t n_steps;
   MmaStep steps[kMaxSteps];
   uint32_t b_ks_stride;  // resident B: bytes between consecutive K stages
@@ -92,8 +100,14 @@ struct TcArgs {
   int32_t a_stage_bytes, b_stage_bytes, b_res_bytes, n_stages;
   uint32_t idesc;
   int32_t out_mode, OH, OW;  // OUT_REMAP: valid outputs are grid (y < OH, x < OW)
+  // fused max_pool2d (pool != 0): one super-tile = the `band` conv output rows
+  // of one pooled row; the conv epilogue stages them in shared memory and the
+  // pooled row is written instead of the conv output
+  int32_t pool, pkh, pkw, psh, psw, pph, ppw, poh, pow, band, stage_stride, relu_last;
   float acc_scale;
-  int32_t dbg;  // MRB200_TC_DBG bit 0: skip epilogue math, bit 1: skip MMAs (timing experiments only)
+  int32_t dbg;  // MRB200_TC_DBG (timing experiments only): 1 skip epilogue math, 2 hoisted descriptors, 4 no MMAs,
+                //   16 CTA-0 timestamps of the fused-pool epilogue
+  unsigned long long* stamps;
   EpiDev epi;
   OutDev out;
 };
@@ -145,16 +159,17 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
-// K-major, no-swizzle UMMA shared-memory descriptor (sm_100 version 1):
-// start>>4 [0,14), LBO>>4 [16,30), SBO>>4 [32,46), version [46,48) = 1,
-// base offset 0, layout type SWIZZLE_NONE (0) [61,64).
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
-  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
-  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
-  d |= static_cast<uint64_t>(1) << 46;
-  return d;
+// K-major UMMA shared-memory descriptor (sm_100 version 1): start>>4 [0,14),
+// LBO>>4 [16,30), SBO>>4 [32,46), version [46,48) = 1, base offset 0,
+// layout type [61,64) (0 none, 2 128B swizzle, 4 64B swizzle).  The high word
+// is per-kernel constant (TcArgs::desc_hi).
+__host__ __device__ __forceinline__ uint32_t umma_desc_hi(uint32_t sbo, uint32_t layout) {
+  return ((sbo >> 4) & 0x3FFF) | (1u << 14) | (layout << 29);
+}
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t hi) {
+  const uint32_t lo = ((saddr >> 4) & 0x3FFF) | (((lbo >> 4) & 0x3FFF) << 16);
+  return (static_cast<uint64_t>(hi) << 32) | lo;
 }
 
 template <int EB>
@@ -170,6 +185,31 @@ __device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t adesc, uint64_t b
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
   }
+}
+
+// Warp-collective forms: every lane executes them with warp-uniform operands
+// (kept in uniform registers), elect.sync picks the one issuing lane (always
+// the same lane, so the commit tracks the MMAs it issued).
+template <int EB>
+__device__ __forceinline__ void umma_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  if constexpr (EB == 1) {
+    asm volatile(
+        "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+  } else {
+    asm volatile(
+        "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+  }
+}
+
+__device__ __forceinline__ void umma_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(smem_u32(bar))
+      : "memory");
 }
 
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
@@ -202,25 +242,59 @@ struct RowDst {
   bool border;        // OUT_SAME: padded-grid border -> zeros
 };
 
-__device__ __forceinline__ void store16(void* base, int64_t chunk, uint4 v) {
-  *reinterpret_cast<uint4*>(static_cast<char*>(base) + chunk * 16) = v;
+// Byte offset of the 16-byte granule holding channel c (chunk-plane stride
+// `pstride` and base `cbase` in chunk units, so PHASE sub-grids fit too).
+__device__ __forceinline__ int64_t gran_byte(const Lay& L, int64_t cbase, int64_t pstride, int c) {
+  return ((c / L.cpc) * pstride + cbase) * L.kb + static_cast<int64_t>(c % L.cpc) * (L.kb / L.cpc);
+}
+
+__device__ __forceinline__ void st16(void* base, int64_t byte, uint4 v) {
+  *reinterpret_cast<uint4*>(static_cast<char*>(base) + byte) = v;
 }
 
 // 16 channels [c0, c0+16) of one output pixel through the epilogue, stored as
-// 16-byte chunks.  SIG selects a compile-time op sequence for the common
+// 16-byte granules.  SIG selects a compile-time op sequence for the common
 // fused groups; SIG_ANY interprets EpiDev.  The arithmetic is identical either
 // way (kernels.cuh).
+// Float result of the element epilogue for 16 channels (no stores): used by
+// the fused pool, whose conv epilogue is bias_add [-> relu] (checked on the host).
+template <int EB>
+__device__ __forceinline__ void epilogue_values(const TcArgs& a, const uint32_t* raw, int c0, float (&v)[16]) {
+  const EpiDev& e = a.epi;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    if constexpr (EB == 1) v[i] = __fmul_rn(static_cast<float>(static_cast<int32_t>(raw[i])), a.acc_scale);
+    else v[i] = __uint_as_float(raw[i]);
+  }
+  for (int k = 0; k < e.n_ops; ++k) {
+    if (e.op[k] == E_BIAS) {
+      const float4* p = reinterpret_cast<const float4*>(e.vec[k] + c0);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float4 f = __ldg(p + j);
+        v[4 * j] = __fadd_rn(v[4 * j], f.x);
+        v[4 * j + 1] = __fadd_rn(v[4 * j + 1], f.y);
+        v[4 * j + 2] = __fadd_rn(v[4 * j + 2], f.z);
+        v[4 * j + 3] = __fadd_rn(v[4 * j + 3], f.w);
+      }
+    } else if (e.op[k] == E_RELU) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = relu_ref(v[i]);
+    }
+  }
+}
+
 template <int EB, int SIG>
 __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* raw, const RowDst& d, int c0) {
   const OutDev& o = a.out;
   const int pf = o.primary_fmt;
-  const int pcpc = pf == FMT_F32 ? 4 : pf == FMT_BF16 ? 8 : 16;
-  const int scpc = o.side_fmt == FMT_BF16 ? 8 : 16;
+  const int peb = pf == FMT_F32 ? 4 : pf == FMT_BF16 ? 2 : 1;  // 16-byte granules per 16 channels
+  const int seb = o.side_fmt == FMT_BF16 ? 2 : 1;
   if (d.border) {
-    for (int k = 0; k < 16 / pcpc; ++k) store16(o.primary, (c0 / pcpc + k) * o.plan.Pp + d.pix, make_uint4(0, 0, 0, 0));
+    for (int g = 0; g < peb; ++g) st16(o.primary, gran_byte(o.plan, d.pix, o.plan.Pp, c0 + g * 16 / peb), make_uint4(0, 0, 0, 0));
     if (o.side)
-      for (int k = 0; k < 16 / scpc; ++k)
-        store16(o.side, d.side_base + (c0 / scpc + k) * d.side_pstride, make_uint4(0, 0, 0, 0));
+      for (int g = 0; g < seb; ++g)
+        st16(o.side, gran_byte(o.slay, d.side_base, d.side_pstride, c0 + g * 16 / seb), make_uint4(0, 0, 0, 0));
     return;
   }
   float v[16];
@@ -245,15 +319,13 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
     if (e.res_fmt[k] == FMT_F32) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        float4 f = *reinterpret_cast<const float4*>(static_cast<const char*>(e.res[k]) +
-                                                    (static_cast<int64_t>(c0 / 4 + j) * L.Pp + d.pix) * 16);
+        float4 f = *reinterpret_cast<const float4*>(static_cast<const char*>(e.res[k]) + gran_byte(L, d.pix, L.Pp, c0 + 4 * j));
         t[4 * j] = f.x; t[4 * j + 1] = f.y; t[4 * j + 2] = f.z; t[4 * j + 3] = f.w;
       }
     } else {
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
-        uint4 u = *reinterpret_cast<const uint4*>(static_cast<const char*>(e.res[k]) +
-                                                  (static_cast<int64_t>(c0 / 8 + j) * L.Pp + d.pix) * 16);
+        uint4 u = *reinterpret_cast<const uint4*>(static_cast<const char*>(e.res[k]) + gran_byte(L, d.pix, L.Pp, c0 + 8 * j));
         uint32_t w4[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
@@ -328,15 +400,15 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
     }
   }
   if (pf == FMT_I8) {
-    store16(o.primary, (c0 / 16) * o.plan.Pp + d.pix,
-            make_uint4(pack4_i8(code[0], code[1], code[2], code[3]), pack4_i8(code[4], code[5], code[6], code[7]),
-                       pack4_i8(code[8], code[9], code[10], code[11]), pack4_i8(code[12], code[13], code[14], code[15])));
+    st16(o.primary, gran_byte(o.plan, d.pix, o.plan.Pp, c0),
+         make_uint4(pack4_i8(code[0], code[1], code[2], code[3]), pack4_i8(code[4], code[5], code[6], code[7]),
+                    pack4_i8(code[8], code[9], code[10], code[11]), pack4_i8(code[12], code[13], code[14], code[15])));
   } else if (pf == FMT_F32) {
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-      store16(o.primary, (c0 / 4 + j) * o.plan.Pp + d.pix,
-              make_uint4(__float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]), __float_as_uint(v[4 * j + 2]),
-                         __float_as_uint(v[4 * j + 3])));
+      st16(o.primary, gran_byte(o.plan, d.pix, o.plan.Pp, c0 + 4 * j),
+           make_uint4(__float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]), __float_as_uint(v[4 * j + 2]),
+                      __float_as_uint(v[4 * j + 3])));
   } else {
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
@@ -345,7 +417,7 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
       for (int h = 0; h < 4; ++h)
         w4[h] = static_cast<uint32_t>(f32_to_bf16(v[8 * j + 2 * h])) |
                 (static_cast<uint32_t>(f32_to_bf16(v[8 * j + 2 * h + 1])) << 16);
-      store16(o.primary, (c0 / 8 + j) * o.plan.Pp + d.pix, make_uint4(w4[0], w4[1], w4[2], w4[3]));
+      st16(o.primary, gran_byte(o.plan, d.pix, o.plan.Pp, c0 + 8 * j), make_uint4(w4[0], w4[1], w4[2], w4[3]));
     }
   }
   if (o.side) {
@@ -353,9 +425,9 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
       int sc[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) sc[i] = quant_code_fast(v[i], o.side_q);
-      store16(o.side, d.side_base + (c0 / 16) * d.side_pstride,
-              make_uint4(pack4_i8(sc[0], sc[1], sc[2], sc[3]), pack4_i8(sc[4], sc[5], sc[6], sc[7]),
-                         pack4_i8(sc[8], sc[9], sc[10], sc[11]), pack4_i8(sc[12], sc[13], sc[14], sc[15])));
+      st16(o.side, gran_byte(o.slay, d.side_base, d.side_pstride, c0),
+           make_uint4(pack4_i8(sc[0], sc[1], sc[2], sc[3]), pack4_i8(sc[4], sc[5], sc[6], sc[7]),
+                      pack4_i8(sc[8], sc[9], sc[10], sc[11]), pack4_i8(sc[12], sc[13], sc[14], sc[15])));
     } else {
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
@@ -364,13 +436,22 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
         for (int h = 0; h < 4; ++h)
           w4[h] = static_cast<uint32_t>(f32_to_bf16(v[8 * j + 2 * h])) |
                   (static_cast<uint32_t>(f32_to_bf16(v[8 * j + 2 * h + 1])) << 16);
-        store16(o.side, d.side_base + (c0 / 8 + j) * d.side_pstride, make_uint4(w4[0], w4[1], w4[2], w4[3]));
+        st16(o.side, gran_byte(o.slay, d.side_base, d.side_pstride, c0 + 8 * j), make_uint4(w4[0], w4[1], w4[2], w4[3]));
       }
     }
   }
 }
 
 __device__ __forceinline__ int floor_div8(int v) { return v >= 0 ? v / 8 : -((7 - v) / 8); }
+
+// First grid row of super-tile mt, offset by the smallest tap shift: linear
+// super-tiles, or (pool) the `band` rows starting at psh * p - pph of image n.
+__device__ __forceinline__ int tile_start(const TcArgs& a, int mt, int msub) {
+  if (!a.pool) return mt * msub;
+  const int n = mt / a.poh, p = mt - n * a.poh;
+  return (n * a.Hg + p * a.psh - a.pph) * a.Wg;
+}
+__device__ __forceinline__ int tile_row0(const TcArgs& a, int mt, int msub) { return tile_start(a, mt, msub) + a.dmin; }
 
 template <int EB, int SIG>
 __global__ void __launch_bounds__(kThreadsTc, 1)
@@ -387,13 +468,16 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   uint64_t* tempty = tfull + 2;
   uint64_t* bfull = tempty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
+  uint8_t* smem_pool = reinterpret_cast<uint8_t*>(bars) + 256;  // fused-pool staging (a.band * Wg rows)
+
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   const int n_tile = blockIdx.x % a.n_tiles;
   const int m_start = blockIdx.x / a.n_tiles;
   const int m_step = gridDim.x / a.n_tiles;
-  const uint32_t tmem_cols = a.bn * 2 <= 32 ? 32 : a.bn * 2 <= 64 ? 64 : a.bn * 2 <= 128 ? 128 : a.bn * 2 <= 256 ? 256 : 512;
+  const int tcols = 2 * a.sub * a.bn;
+  const uint32_t tmem_cols = tcols <= 32 ? 32 : tcols <= 64 ? 64 : tcols <= 128 ? 128 : tcols <= 256 ? 256 : 512;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < a.n_stages; ++i) {
@@ -419,24 +503,34 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  const int msub = a.sub * kTileM;  // rows of a super-tile
   if (warp == 0) {
     if (lane == 0) {
       // ===== TMA producer =====
       if (a.resident_b) {
         mbar_expect_tx(bfull, a.b_res_bytes);
-        tma_load_4d(smB, &tmB, bfull, 0, n_tile * a.bn / 8, 0, 0);
+        tma_load_4d(smB, &tmB, bfull, 0, n_tile * a.bn / (a.kb == 16 ? 8 : 1), 0, 0);
       }
+      const int row_bytes = a.kb == 16 ? 128 : a.kb;
       int stage = 0;
       uint32_t phase = 0;
       for (int mt = m_start; mt < a.m_tiles; mt += m_step) {
-        const int row0 = mt * kTileM + a.dmin;
-        const int g0 = floor_div8(row0);
+        const int row0 = tile_row0(a, mt, msub);
+        // no-swizzle (kb 16) maps move 8-pixel 128-byte rows; swizzled maps one pixel row
+        const int r0 = a.kb == 16 ? floor_div8(row0) : row0;
         for (int ks = 0; ks < a.k_stages; ++ks) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], a.a_stage_bytes + (a.resident_b ? 0 : a.b_stage_bytes));
-          tma_load_4d(smA + stage * a.a_stage_bytes, &tmA, &full[stage], 0, g0, a.sub0, ks * a.pps);
+          // A stage layout [pps][subs][hg rows][row]: one box per (plane, sub-grid, row block)
+          uint8_t* dA = smA + stage * a.a_stage_bytes;
+          for (int pl = 0; pl < a.pps; ++pl)
+            for (int sg = 0; sg < a.subs; ++sg)
+              for (int bx = 0; bx < a.nbox; ++bx)
+                tma_load_4d(dA + ((pl * a.subs + sg) * a.hg + bx * a.hbox) * row_bytes, &tmA, &full[stage], 0,
+                            r0 + bx * a.hbox, a.sub0 + sg, ks * a.pps + pl);
           if (!a.resident_b)
-            tma_load_4d(smB + stage * a.b_stage_bytes, &tmB, &full[stage], 0, n_tile * a.bn / 8, ks * a.pps, 0);
+            tma_load_4d(smB + stage * a.b_stage_bytes, &tmB, &full[stage], 0, n_tile * a.bn / (a.kb == 16 ? 8 : 1),
+                        ks * a.pps, 0);
           if (++stage == a.n_stages) {
             stage = 0;
             phase ^= 1;
@@ -446,9 +540,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     }
   } else if (warp == 1) {
     // ===== MMA issuer =====
-    // The whole warp walks the loop so tile/stage/descriptor values are
-    // warp-uniform (uniform registers); lane 0 issues tcgen05.mma / commit.
-    // Descriptors: base | (start >> 4); LBO/SBO/version fixed per step.
+    // The whole warp walks the loop (warp-uniform values); elect.sync inside
+    // the tcgen05.mma / commit asm picks the issuing lane.  A super-tile is
+    // `sub` 128-row M tiles that share every B descriptor: one stage wait,
+    // one accumulator wait and two commits per super-tile.
     if (a.resident_b) mbar_wait(bfull, 0);
     int stage = 0;
     uint32_t phase = 0;
@@ -456,35 +551,43 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     uint32_t acc_phase = 0;
     const uint32_t smB_u = smem_u32(smB);
     const uint32_t smA_u = smem_u32(smA);
+    const uint64_t hi = static_cast<uint64_t>(a.desc_hi) << 32;
+    const uint32_t sub_step16 = static_cast<uint32_t>(kTileM * a.kb) >> 4;  // 128 rows, in descriptor units
     for (int mt = m_start; mt < a.m_tiles; mt += m_step) {
-      const int row0 = mt * kTileM + a.dmin;
-      const uint32_t shift16 = static_cast<uint32_t>(row0 - 8 * floor_div8(row0)) * 16;
+      const int row0 = tile_row0(a, mt, msub);
+      const uint32_t shift16 = a.kb == 16 ? static_cast<uint32_t>(row0 - 8 * floor_div8(row0)) * 16 : 0u;
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
-      const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * a.bn);
+      const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * a.sub * a.bn);
       for (int ks = 0; ks < a.k_stages; ++ks) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         const uint32_t sA = smA_u + stage * a.a_stage_bytes + shift16;
         const uint32_t sB = a.resident_b ? smB_u + ks * a.b_ks_stride : smB_u + stage * a.b_stage_bytes;
-#pragma unroll 2
+        const uint32_t a16 = sA >> 4, b16 = sB >> 4;
+        if (a.dbg & 2) {
+          // timing experiment: same MMA count, one hoisted descriptor pair (wrong results)
+          const uint64_t bd = hi | (a.steps[0].b_lo + b16);
+          const uint64_t ad = hi | (a.steps[0].a_lo + a16);
+          const int n = a.n_steps * a.sub;
+#pragma unroll 1
+          for (int i = 0; i < n; ++i) umma_elect<EB>(tmem_d, ad, bd, a.idesc, (ks | i) != 0 ? 1u : 0u);
+        } else if (!(a.dbg & 4))
         for (int st = 0; st < a.n_steps; ++st) {
-          const MmaStep m = a.steps[st];
-          const uint32_t aaddr = (a.dbg & 4) ? ((sA + m.a_off) & ~127u) : sA + m.a_off;
-          const uint64_t ad = umma_desc(aaddr, m.a_lbo, 128);
-          const uint64_t bd = umma_desc(sB + m.b_off, m.b_lbo, 128);
-          if (lane == 0 && !(a.dbg & 2)) umma<EB>(tmem_d, ad, bd, a.idesc, (ks | st) != 0 ? 1u : 0u);
+          const uint64_t bd = hi | (a.steps[st].b_lo + b16);
+          const uint32_t alo = a.steps[st].a_lo + a16;
+          const uint32_t accum = (ks | st) != 0 ? 1u : 0u;
+#pragma unroll 4
+          for (int sb = 0; sb < a.sub; ++sb)
+            umma_elect<EB>(tmem_d + static_cast<uint32_t>(sb * a.bn), hi | (alo + sb * sub_step16), bd, a.idesc, accum);
         }
-        __syncwarp();
-        if (lane == 0) umma_commit(&empty[stage]);  // frees the smem stage when these MMAs retire
-        __syncwarp();
+        umma_commit_elect(&empty[stage]);  // frees the smem stage when these MMAs retire
         if (++stage == a.n_stages) {
           stage = 0;
           phase ^= 1;
         }
       }
-      if (lane == 0) umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
-      __syncwarp();
+      umma_commit_elect(&tfull[acc]);  // accumulator ready for the epilogue
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -492,55 +595,175 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     }
   } else {
     // ===== epilogue warps =====
-    // warp w (2..17): TMEM lane quarter w % 4 (hardware lane-access rule),
-    // 16-column chunks slice, slice + 4, ... with slice = (w - 2) / 4.
+    // warp w (2..17): TMEM lane quarter w % 4 (hardware lane-access rule);
+    // the super-tile's (sub-tile, 16-column chunk) items are dealt round-robin
+    // to the 4 warps of each quarter.
     const int quarter = warp & 3;
     const int slice = (warp - 2) >> 2;
     const int row = quarter * 32 + lane;
     const Lay& sl = a.out.slay;
+    const int chunks = a.bn / 16;
     int acc = 0;
     uint32_t acc_phase = 0;
+    float* stg = reinterpret_cast<float*>(smem_pool);
     for (int mt = m_start; mt < a.m_tiles; mt += m_step) {
+      if ((a.dbg & 16) && a.pool && blockIdx.x == 0 && threadIdx.x == 64 && (mt - m_start) / m_step < 16)
+        a.stamps[((mt - m_start) / m_step) * 8 + 5] = clock64();
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const uint32_t q = static_cast<uint32_t>(mt) * kTileM + row;  // grids < 2^31 pixels (checked on the host)
-      RowDst d;
-      bool valid = q < static_cast<uint32_t>(a.Pg);
-      d.border = false;
-      d.pix = 0;
-      if (valid) {
-        const uint32_t t = q / static_cast<uint32_t>(a.Wg);
-        const int x = static_cast<int>(q - t * static_cast<uint32_t>(a.Wg));
-        const uint32_t n32 = t / static_cast<uint32_t>(a.Hg);
-        const int y = static_cast<int>(t - n32 * static_cast<uint32_t>(a.Hg));
-        const int n = static_cast<int>(n32);
-        if (a.out_mode == OUT_SAME) {
-          d.pix = q;
-          d.border = x == 0 || x == a.Wg - 1 || y == 0 || y == a.Hg - 1;
-        } else {
-          valid = y < a.OH && x < a.OW;
-          d.pix = (static_cast<int64_t>(n) * (a.OH + 2 * kPad) + y + kPad) * (a.OW + 2 * kPad) + x + kPad;
-        }
-        if (a.out.side) {
-          if (sl.kind == LAY_PHASE) {
-            const uint32_t p32 = static_cast<uint32_t>(d.pix);
-            const uint32_t tt = p32 / static_cast<uint32_t>(sl.Wp);
-            const int wp = static_cast<int>(p32 - tt * static_cast<uint32_t>(sl.Wp));
-            const uint32_t nn = tt / static_cast<uint32_t>(sl.Hp);
-            const int hp = static_cast<int>(tt - nn * static_cast<uint32_t>(sl.Hp));
-            d.side_base = static_cast<int64_t>((hp & 1) * 2 + (wp & 1)) * sl.Pp +
-                          (static_cast<int64_t>(nn) * sl.Hq + hp / 2) * sl.Wq + wp / 2;
-            d.side_pstride = 4 * sl.Pp;
-          } else {
-            d.side_base = d.pix;
-            d.side_pstride = sl.Pp;
+      if (a.pool) {
+        // ---- fused max_pool2d: stage the band's conv outputs, then pool ----
+        const bool stamp = (a.dbg & 16) && blockIdx.x == 0 && threadIdx.x == 64 && (mt - m_start) / m_step < 16;
+        const int si = (mt - m_start) / m_step;
+        if (stamp) a.stamps[si * 8 + 0] = clock64();
+        const int n = mt / a.poh, p = mt - n * a.poh;
+        const int y0 = p * a.psh - a.pph;  // first conv output row of the band
+        for (int item = slice; item < a.sub * chunks; item += 4) {
+          const int sb = item / chunks;
+          const int c = (item - sb * chunks) * 16;
+          const int r = sb * kTileM + row;  // row inside the band
+          const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+                                 static_cast<uint32_t>((acc * a.sub + sb) * a.bn + c);
+          uint32_t raw[16];
+          tmem_ld16(taddr, raw);
+          if (r < a.band * a.Wg && !(a.dbg & 1)) {
+            float v[16];
+            epilogue_values<EB>(a, raw, c, v);
+            // staging is granule-plane-major: [c / 4][band pixel] float4 -> conflict-free
+            float4* dst = reinterpret_cast<float4*>(stg) + (c / 4) * a.stage_stride + r;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dst[j * a.stage_stride] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           }
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);  // TMEM drained into shared memory
+        if (stamp) a.stamps[si * 8 + 1] = clock64();
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+        if (stamp) a.stamps[si * 8 + 2] = clock64();
+        // pooled row p: out (pw, 4 channels) = max over the valid window taps.
+        // relu_last: every staged value is >= +0 and not NaN (relu is the
+        // conv epilogue's last op), so the reference's ordered max seeded with
+        // the first valid tap equals fmaxf over the window with padded taps as
+        // +0; otherwise the ordered, seeded form is evaluated.
+        const OutDev& o = a.out;
+        const int granules = a.bn / 4;
+        for (int it = threadIdx.x - 64; it < ((a.dbg & 1) ? 0 : a.pow * granules); it += kEpiWarps * 32) {
+          const int g4 = it / a.pow, pw = it - g4 * a.pow;  // pixel-fastest: coalesced stores
+          const int c0 = g4 * 4;
+          const int x0 = pw * a.psw - a.ppw;
+          float mx[4] = {0.f, 0.f, 0.f, 0.f};
+          if (a.relu_last) {
+            for (int kh = 0; kh < a.pkh; ++kh) {
+              const bool yv = y0 + kh >= 0 && y0 + kh < a.OH;
+              const float4* rowp = reinterpret_cast<const float4*>(stg) + g4 * a.stage_stride + kh * a.Wg;
+#pragma unroll 3
+              for (int kw = 0; kw < a.pkw; ++kw) {
+                const int x = x0 + kw;
+                const bool ok = yv && x >= 0 && x < a.OW;
+                float4 f = rowp[ok ? x : 0];
+                if (!ok) f = make_float4(0.f, 0.f, 0.f, 0.f);
+                mx[0] = fmaxf(mx[0], f.x);
+                mx[1] = fmaxf(mx[1], f.y);
+                mx[2] = fmaxf(mx[2], f.z);
+                mx[3] = fmaxf(mx[3], f.w);
+              }
+            }
+          } else {
+            bool seeded = false;
+            for (int kh = 0; kh < a.pkh; ++kh) {
+              const int y = y0 + kh;
+              if (y < 0 || y >= a.OH) continue;
+              for (int kw = 0; kw < a.pkw; ++kw) {
+                const int x = x0 + kw;
+                if (x < 0 || x >= a.OW) continue;
+                const float4 f = reinterpret_cast<const float4*>(stg)[g4 * a.stage_stride + kh * a.Wg + x];
+                const float vv[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) mx[k] = !seeded ? vv[k] : (mx[k] < vv[k] ? vv[k] : mx[k]);
+                seeded = true;
+              }
+            }
+          }
+          const int64_t pix = (static_cast<int64_t>(n) * (a.poh + 2 * kPad) + p + kPad) * (a.pow + 2 * kPad) + pw + kPad;
+          const int c = n_tile * a.bn + c0;
+          if (o.primary_fmt == FMT_F32) {
+            st16(o.primary, gran_byte(o.plan, pix, o.plan.Pp, c),
+                 make_uint4(__float_as_uint(mx[0]), __float_as_uint(mx[1]), __float_as_uint(mx[2]), __float_as_uint(mx[3])));
+          } else {  // bf16 pipeline: 4 channels = 8 bytes
+            *reinterpret_cast<uint2*>(static_cast<char*>(o.primary) + gran_byte(o.plan, pix, o.plan.Pp, c)) =
+                make_uint2(static_cast<uint32_t>(f32_to_bf16(mx[0])) | (static_cast<uint32_t>(f32_to_bf16(mx[1])) << 16),
+                           static_cast<uint32_t>(f32_to_bf16(mx[2])) | (static_cast<uint32_t>(f32_to_bf16(mx[3])) << 16));
+          }
+          if (o.side) {
+            char* sbase = static_cast<char*>(o.side) + lay_byte(o.slay, pix, c);
+            if (o.side_fmt == FMT_I8) {
+              uint32_t u = 0;
+#pragma unroll
+              for (int k = 0; k < 4; ++k) u |= (static_cast<uint32_t>(quant_code_fast(mx[k], o.side_q)) & 0xff) << (8 * k);
+              *reinterpret_cast<uint32_t*>(sbase) = u;
+            } else {
+              *reinterpret_cast<uint2*>(sbase) =
+                  make_uint2(static_cast<uint32_t>(f32_to_bf16(mx[0])) | (static_cast<uint32_t>(f32_to_bf16(mx[1])) << 16),
+                             static_cast<uint32_t>(f32_to_bf16(mx[2])) | (static_cast<uint32_t>(f32_to_bf16(mx[3])) << 16));
+            }
+          }
+        }
+        if (stamp) a.stamps[si * 8 + 3] = clock64();
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");  // staging free for the next band
+        if (stamp) a.stamps[si * 8 + 4] = clock64();
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+        continue;
       }
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * a.bn);
-      for (int c = slice * 16; c < a.bn; c += 64) {
+      int cur_sb = -1;
+      RowDst d;
+      bool valid = false;
+      for (int item = slice; item < a.sub * chunks; item += 4) {
+        const int sb = item / chunks;
+        const int c = (item - sb * chunks) * 16;
+        if (sb != cur_sb) {
+          cur_sb = sb;
+          const uint32_t q = static_cast<uint32_t>(mt * a.sub + sb) * kTileM + row;  // grids < 2^31 pixels
+          valid = q < static_cast<uint32_t>(a.Pg);
+          d.border = false;
+          d.pix = 0;
+          if (valid) {
+            const uint32_t t = q / static_cast<uint32_t>(a.Wg);
+            const int x = static_cast<int>(q - t * static_cast<uint32_t>(a.Wg));
+            const uint32_t n32 = t / static_cast<uint32_t>(a.Hg);
+            const int y = static_cast<int>(t - n32 * static_cast<uint32_t>(a.Hg));
+            const int n = static_cast<int>(n32);
+            if (a.out_mode == OUT_SAME) {
+              d.pix = q;
+              d.border = x == 0 || x == a.Wg - 1 || y == 0 || y == a.Hg - 1;
+            } else {
+              valid = y < a.OH && x < a.OW;
+              d.pix = (static_cast<int64_t>(n) * (a.OH + 2 * kPad) + y + kPad) * (a.OW + 2 * kPad) + x + kPad;
+            }
+            if (a.out.side) {
+              if (sl.kind == LAY_PHASE) {
+                const uint32_t p32 = static_cast<uint32_t>(d.pix);
+                const uint32_t tt = p32 / static_cast<uint32_t>(sl.Wp);
+                const int wp = static_cast<int>(p32 - tt * static_cast<uint32_t>(sl.Wp));
+                const uint32_t nn = tt / static_cast<uint32_t>(sl.Hp);
+                const int hp = static_cast<int>(tt - nn * static_cast<uint32_t>(sl.Hp));
+                d.side_base = static_cast<int64_t>((hp & 1) * 2 + (wp & 1)) * sl.Pp +
+                              (static_cast<int64_t>(nn) * sl.Hq + hp / 2) * sl.Wq + wp / 2;
+                d.side_pstride = 4 * sl.Pp;
+              } else {
+                d.side_base = d.pix;
+                d.side_pstride = sl.Pp;
+              }
+            }
+          }
+        }
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+                               static_cast<uint32_t>((acc * a.sub + sb) * a.bn + c);
         uint32_t raw[16];
-        tmem_ld16(taddr + static_cast<uint32_t>(c), raw);  // warp-collective: every lane executes it
+        tmem_ld16(taddr, raw);  // warp-collective: every lane executes it
         if (valid && !(a.dbg & 1)) epilogue_chunk<EB, SIG>(a, raw, d, n_tile * a.bn + c);
       }
       tc_fence_before();
@@ -591,28 +814,34 @@ struct Tap {
   int sub, delta;
 };
 
-static bool choose(TcConvPlan& p) {
-  const TcConvSpec& sp = p.spec;
+static bool choose_kb(TcConvPlan& p, int kb_pick) {
+  TcConvSpec& sp = p.spec;
   TcArgs& a = p.args;
   std::memset(&a, 0, sizeof(a));
   const int eb = sp.elem_bytes;
-  const int cpc = 16 / eb;
   if (sp.OC % 16 != 0) return false;
   std::vector<Tap> taps;
-  int cc = 0;       // A chunk planes
+  int kb = 16;             // operand chunk bytes
+  int cc = 0;              // A chunk planes
   bool pair_taps = false;  // int8 stem: K halves = two adjacent taps (LBO 16 B)
   a.N = sp.N;
+  a.sub0 = 0;
+  auto swz_kb = [&](int C) {  // the candidate chunk width, if the channels fill whole chunks
+    const int bytes = C * eb;
+    return (bytes % kb_pick == 0) ? kb_pick : 0;
+  };
   switch (sp.kind) {
     case TC_S1: {
       // stride-1 3x3/pad-1 or 1x1/pad-0 over the NORMAL padded grid; output
       // grid == input grid
       bool k3 = sp.KH == 3 && sp.KW == 3, k1 = sp.KH == 1 && sp.KW == 1;
       if (!k3 && !k1) return false;
-      if (sp.C % (2 * cpc)) return false;
+      kb = swz_kb(sp.C);
+      if (!kb) return false;
       a.Hg = sp.H + 2 * kPad;
       a.Wg = sp.W + 2 * kPad;
       a.out_mode = OUT_SAME;
-      cc = sp.C / cpc;
+      cc = sp.C * eb / kb;
       a.subs = 1;
       for (int kh = 0; kh < sp.KH; ++kh)
         for (int kw = 0; kw < sp.KW; ++kw) taps.push_back({0, k3 ? (kh - 1) * a.Wg + (kw - 1) : 0});
@@ -623,14 +852,15 @@ static bool choose(TcConvPlan& p) {
       // PHASE layout: tap (kh, kw) reads sub-grid (kh&1, kw&1) at (kh/2, kw/2)
       bool k3 = sp.KH == 3 && sp.KW == 3, k1 = sp.KH == 1 && sp.KW == 1;
       if (!k3 && !k1) return false;
-      if (sp.C % (2 * cpc)) return false;
+      kb = swz_kb(sp.C);
+      if (!kb) return false;
       if ((sp.H & 1) || (sp.W & 1)) return false;
       a.Hg = (sp.H + 2 * kPad + 1) / 2;
       a.Wg = (sp.W + 2 * kPad + 1) / 2;
       a.out_mode = OUT_REMAP;
       a.OH = sp.OH;
       a.OW = sp.OW;
-      cc = sp.C / cpc;
+      cc = sp.C * eb / kb;
       a.subs = 4;
       if (k3) {
         for (int kh = 0; kh < 3; ++kh)
@@ -643,16 +873,18 @@ static bool choose(TcConvPlan& p) {
       break;
     }
     case TC_STEM_S2D: {
-      // KxK stride-2 over the space-to-depth input: TA x TA stride-1 taps of
-      // 4*C s2d channels; output (oh, ow) at s2d grid (oh, ow)
+      // KxK stride-2 over the 16-byte space-to-depth input: TA x TA stride-1
+      // taps of 4*C s2d channels; output (oh, ow) at s2d grid (oh, ow).  No
+      // swizzle: 8-pixel core-matrix rows.
       const int TA = (sp.KH + 1) / 2;
       if (sp.KH != sp.KW || 4 * sp.C > 16) return false;
+      kb = 16;
       a.Hg = sp.Hs;
       a.Wg = sp.Ws;
       a.out_mode = OUT_REMAP;
       a.OH = sp.OH;
       a.OW = sp.OW;
-      cc = (4 * sp.C + cpc - 1) / cpc;  // 1 (int8) or 2 (bf16)
+      cc = (4 * sp.C * eb + 15) / 16;  // 1 (int8) or 2 (bf16)
       a.subs = 1;
       for (int ta = 0; ta < TA; ++ta)
         for (int tb = 0; tb < TA; ++tb) taps.push_back({0, ta * a.Wg + tb});
@@ -663,22 +895,23 @@ static bool choose(TcConvPlan& p) {
     default:
       return false;
   }
+  a.kb = kb;
   a.Pg = static_cast<int64_t>(a.N) * a.Hg * a.Wg;
   if (a.Pg + kTileM >= (int64_t(1) << 31)) return false;
-  a.m_tiles = static_cast<int>((a.Pg + kTileM - 1) / kTileM);
   int dmin = 1 << 30, dmax = -(1 << 30);
   for (const Tap& t : taps) {
     dmin = std::min(dmin, t.delta);
     dmax = std::max(dmax, t.delta + (pair_taps ? 1 : 0));
   }
   a.dmin = dmin;
-  a.hg = (7 + kTileM + dmax - dmin + 7) / 8;  // 8-pixel rows per sub-grid and plane
-  if (a.hg > 256) return false;
   const int ntaps = static_cast<int>(taps.size());
-  // weights (TMA B): [ntaps][cc][OC][16 B]
-  const int barrier_bytes = 256;
-  auto a_stage = [&](int pps) { return pps * a.subs * a.hg * 128; };
-  auto steps_for = [&](int pps) { return pair_taps ? ntaps / 2 : ntaps * pps / 2; };
+  int barrier_bytes = 256;
+  const int ksteps = kb / 32 > 0 ? kb / 32 : 1;  // 32-byte MMA K steps per chunk row
+  const int row_bytes = kb == 16 ? 128 : kb;     // TMA row: 8 pixels (kb 16) or one pixel
+  auto steps_for = [&](int pps) {
+    if (pair_taps) return ntaps / 2;
+    return kb == 16 ? ntaps * pps / 2 : ntaps * pps * ksteps;
+  };
   int bn = 0;
   for (int c : {256, 128, 64, 32, 16})
     if (sp.OC % c == 0) {
@@ -686,81 +919,161 @@ static bool choose(TcConvPlan& p) {
       break;
     }
   if (!bn) return false;
-  bool found = false;
   static const int force_stream = [] {
     const char* e = std::getenv("MRB200_TC_STREAM");
     return e ? std::atoi(e) : 0;
   }();
-  // resident weights if they fit beside >= 3 A stages, else stream them
-  for (int cand = bn; cand >= 16 && !found && !force_stream; cand /= 2) {
-    if (sp.OC % cand) continue;
-    int b_res = ntaps * cc * cand * 16;
-    for (int pps : {8, 4, 2, 1}) {
-      if (cc % pps || (pps & 1 && !pair_taps) || steps_for(pps) > kMaxSteps) continue;
-      int ns = (kSmemBudget - barrier_bytes - b_res) / a_stage(pps);
-      if (ns >= 3) {
-        a.bn = cand;
-        a.resident_b = 1;
-        a.b_res_bytes = b_res;
-        a.pps = pps;
-        a.n_stages = ns > 8 ? 8 : ns;
-        found = true;
-        break;
+  // A rows per (sub-grid, plane) block for a super-tile of `sub` M tiles,
+  // split into <= 256-row TMA boxes (rows aligned for the swizzle atom)
+  auto geom = [&](int sub, int* hg, int* nbox, int* hbox) {
+    int need = kTileM * sub + dmax - dmin;
+    if (kb == 16) need = (7 + need + 7) / 8;
+    const int align = kb == 16 ? 1 : 1024 / kb;
+    *nbox = (need + 255) / 256;
+    *hbox = ((need + *nbox - 1) / *nbox + align - 1) / align * align;
+    *hg = *nbox * *hbox;
+    return *hbox <= 256;
+  };
+  // Preference: the widest N tile (MMA time grows with N and hides the
+  // per-instruction issue cost), then as many 128-row sub-tiles as TMEM
+  // (2 x sub x N <= 512 columns) and shared memory allow, resident weights
+  // before streamed ones.
+  bool found = false;
+  auto try_cfg = [&](int cand, int sub, bool resident) {
+    if (sp.OC % cand || 2 * sub * cand > 512) return false;
+    int hg, nbox, hbox;
+    if (!geom(sub, &hg, &nbox, &hbox)) return false;
+    const int rows_bytes = hg * row_bytes;
+    auto a_stage = [&](int pps) { return pps * a.subs * rows_bytes; };
+    if (resident) {
+      const int b_res = ntaps * cc * cand * kb;
+      for (int pps : {8, 4, 2, 1}) {
+        if (cc % pps || (kb == 16 && (pps & 1) && !pair_taps) || steps_for(pps) > kMaxSteps) continue;
+        int ns = (kSmemBudget - barrier_bytes - b_res) / a_stage(pps);
+        if (ns >= 3) {
+          a.resident_b = 1;
+          a.b_res_bytes = b_res;
+          a.pps = pps;
+          a.n_stages = ns > 8 ? 8 : ns;
+          a.bn = cand;
+          a.sub = sub;
+          a.hg = hg;
+          a.nbox = nbox;
+          a.hbox = hbox;
+          a.a_stage_bytes = a_stage(pps);
+          return true;
+        }
       }
+      return false;
     }
-    if (cand <= 64) break;  // below 64 columns prefer streaming B at a wide tile
-  }
-  if (!found) {
-    a.bn = bn > 256 ? 256 : bn;
-    a.resident_b = 0;
-    for (int pps : {4, 2}) {
-      if (cc % pps || pair_taps || steps_for(pps) > kMaxSteps) continue;
-      int bst = ntaps * pps * a.bn * 16;
+    for (int pps : {4, 2, 1}) {
+      if (cc % pps || pair_taps || (kb == 16 && (pps & 1)) || steps_for(pps) > kMaxSteps) continue;
+      const int bst = ntaps * pps * cand * kb;
       int ns = (kSmemBudget - barrier_bytes) / (a_stage(pps) + bst);
       if (ns >= 2) {
+        a.resident_b = 0;
         a.pps = pps;
         a.b_stage_bytes = bst;
         a.n_stages = ns > 6 ? 6 : ns;
-        found = true;
-        break;
+        a.bn = cand;
+        a.sub = sub;
+        a.hg = hg;
+        a.nbox = nbox;
+        a.hbox = hbox;
+        a.a_stage_bytes = a_stage(pps);
+        return true;
       }
     }
-    if (!found) return false;
+    return false;
+  };
+  if (sp.pool) {
+    // fused max_pool2d: one super-tile = the pkh conv rows of one pooled row,
+    // whole channel range in one N tile, staging in shared memory
+    if (a.out_mode != OUT_REMAP || sp.OC > 256) return false;
+    a.pool = 1;
+    a.pkh = sp.pkh;
+    a.pkw = sp.pkw;
+    a.psh = sp.psh;
+    a.psw = sp.psw;
+    a.pph = sp.pph;
+    a.ppw = sp.ppw;
+    a.poh = sp.poh;
+    a.pow = sp.pow;
+    a.band = sp.pkh;
+    const int sub = (a.band * a.Wg + kTileM - 1) / kTileM;
+    a.stage_stride = (sub * kTileM + 1) | 1;  // float4 elements per granule plane (odd: spread banks)
+    const int staging = (sp.OC / 4) * a.stage_stride * 16;
+    // the staging buffer shares the budget with the pipeline
+    barrier_bytes += staging;
+    found = try_cfg(sp.OC, sub, true);
+    if (!found || a.n_stages < 2) return false;
+  } else {
+    for (int cand = bn > 256 ? 256 : bn; cand >= 16 && !found; cand /= 2) {
+      for (int sub : {4, 2, 1}) {
+        if (!force_stream && try_cfg(cand, sub, true)) { found = true; break; }
+        if (try_cfg(cand, sub, false)) { found = true; break; }
+      }
+    }
   }
+  if (!found) return false;
+  a.m_tiles = a.pool ? sp.N * sp.poh : static_cast<int>((a.Pg + kTileM * a.sub - 1) / (kTileM * a.sub));
+  const int rows_bytes = a.hg * row_bytes;
   a.Cc = cc;
-  a.a_stage_bytes = a_stage(a.pps);
   a.k_stages = cc / a.pps;
   a.n_tiles = sp.OC / a.bn;
-  // MMA step table (byte offsets; A relative to stage base + row shift)
-  const uint32_t a_sub = static_cast<uint32_t>(a.hg) * 128;
+  // MMA step table (byte offsets; A relative to stage base [+ row shift for kb 16])
+  const uint32_t a_sub = static_cast<uint32_t>(rows_bytes);
   const uint32_t a_plane = a_sub * static_cast<uint32_t>(a.subs);
-  const uint32_t b_plane = static_cast<uint32_t>(a.bn) * 16;
-  const int bplanes = a.resident_b ? cc : a.pps;  // planes per tap in the smem B buffer
+  const uint32_t b_plane = static_cast<uint32_t>(a.bn) * static_cast<uint32_t>(kb);
+  const int bplanes = a.resident_b ? cc : a.pps;  // chunk planes per tap in the smem B buffer
   a.b_ks_stride = a.resident_b ? static_cast<uint32_t>(a.pps) * b_plane : 0;
   a.n_steps = 0;
-  if (pair_taps) {
-    for (int t = 0; t < ntaps; t += 2) {
-      MmaStep m;
-      m.a_off = static_cast<uint32_t>(taps[t].delta - dmin) * 16;
-      m.a_lbo = 16;
-      m.b_off = static_cast<uint32_t>(t * bplanes) * b_plane;
-      m.b_lbo = static_cast<uint32_t>(bplanes) * b_plane;
-      a.steps[a.n_steps++] = m;
-    }
-  } else {
-    for (int t = 0; t < ntaps; ++t)
-      for (int kp = 0; kp < a.pps; kp += 2) {
+  if (kb == 16) {
+    a.desc_hi = umma_desc_hi(128, 0);  // no swizzle: SBO = 8 rows x 16 B
+    if (pair_taps) {
+      for (int t = 0; t < ntaps; t += 2) {
         MmaStep m;
-        m.a_off = static_cast<uint32_t>(kp) * a_plane + static_cast<uint32_t>(taps[t].sub) * a_sub +
-                  static_cast<uint32_t>(taps[t].delta - dmin) * 16;
-        m.a_lbo = a_plane;
-        m.b_off = static_cast<uint32_t>(t * bplanes + kp) * b_plane;
-        m.b_lbo = b_plane;
+        m.a_off = static_cast<uint32_t>(taps[t].delta - dmin) * 16;
+        m.a_lbo = 16;
+        m.b_off = static_cast<uint32_t>(t * bplanes) * b_plane;
+        m.b_lbo = static_cast<uint32_t>(bplanes) * b_plane;
         a.steps[a.n_steps++] = m;
       }
+    } else {
+      for (int t = 0; t < ntaps; ++t)
+        for (int kp = 0; kp < a.pps; kp += 2) {
+          MmaStep m;
+          m.a_off = static_cast<uint32_t>(kp) * a_plane + static_cast<uint32_t>(taps[t].sub) * a_sub +
+                    static_cast<uint32_t>(taps[t].delta - dmin) * 16;
+          m.a_lbo = a_plane;
+          m.b_off = static_cast<uint32_t>(t * bplanes + kp) * b_plane;
+          m.b_lbo = b_plane;
+          a.steps[a.n_steps++] = m;
+        }
+    }
+  } else {
+    // swizzled K-major: SBO = 8 rows x kb; the 32-byte K step is a start-address advance
+    a.desc_hi = umma_desc_hi(8 * kb, kb == 128 ? 2 : 4);
+    for (int t = 0; t < ntaps; ++t)
+      for (int kp = 0; kp < a.pps; ++kp)
+        for (int kk = 0; kk < ksteps; ++kk) {
+          MmaStep m;
+          m.a_off = static_cast<uint32_t>(kp) * a_plane + static_cast<uint32_t>(taps[t].sub) * a_sub +
+                    static_cast<uint32_t>(taps[t].delta - dmin) * kb + kk * 32;
+          m.a_lbo = 16;
+          m.b_off = static_cast<uint32_t>(t * bplanes + kp) * b_plane + kk * 32;
+          m.b_lbo = 16;
+          a.steps[a.n_steps++] = m;
+        }
   }
-  p.spec.taps = ntaps;
-  p.spec.wplanes = cc;
+  for (int i = 0; i < a.n_steps; ++i) {
+    MmaStep& m = a.steps[i];
+    m.a_lo = ((m.a_off >> 4) & 0x3FFF) | (((m.a_lbo >> 4) & 0x3FFF) << 16);
+    m.b_lo = ((m.b_off >> 4) & 0x3FFF) | (((m.b_lbo >> 4) & 0x3FFF) << 16);
+  }
+  sp.taps = ntaps;
+  sp.wplanes = cc;
+  sp.kb = kb;
   // instruction descriptor: D fmt [4,6), A fmt [7,10), B fmt [10,13), K-major A/B,
   // N>>3 [17,23), M>>4 [24,29)
   uint32_t idesc = 0;
@@ -777,8 +1090,35 @@ static bool choose(TcConvPlan& p) {
   if (per_n > a.m_tiles) per_n = a.m_tiles;
   p.grid = per_n * a.n_tiles;
   int body = a.resident_b ? a.b_res_bytes : a.b_stage_bytes * a.n_stages;
-  p.smem = 1024 + body + a.a_stage_bytes * a.n_stages + barrier_bytes;
+  p.smem = 1024 + body + a.a_stage_bytes * a.n_stages + barrier_bytes + kMaxSteps * 8;
   return true;
+}
+
+// Plans the kernel for a conv group: chunk width (128B, then 64B rows; the
+// stem uses 16-byte rows), N tile, resident vs streamed weights, pipeline
+// depth.  spec.kb on input forces the chunk width (another consumer of the
+// same representation already fixed it).
+static bool choose(TcConvPlan& p) {
+  const TcConvSpec keep = p.spec;
+  if (p.spec.kind == TC_STEM_S2D) return choose_kb(p, 16);
+  const int forced = p.spec.kb;
+  for (int kb : {128, 64}) {
+    if (forced && kb != forced) continue;
+    p.spec = keep;
+    if (choose_kb(p, kb)) {
+      // prefer 128-byte rows unless they force an N tile below 128 that 64-byte rows avoid
+      if (kb == 128 && !forced && p.args.bn < 128 && p.spec.OC >= 128) {
+        TcConvPlan alt;
+        alt.spec = keep;
+        if (choose_kb(alt, 64) && alt.args.bn > p.args.bn) {
+          p = alt;
+        }
+      }
+      return true;
+    }
+  }
+  p.spec = keep;
+  return false;
 }
 
 bool tc_conv_plan_ok(TcConvSpec& spec) {
@@ -802,31 +1142,36 @@ TcConvPlan* tc_conv_create(const TcConvSpec& spec) {
 static bool encode_maps(TcConvPlan& p, const void* x, const Lay& xl, const void* w) {
   TcArgs& a = p.args;
   auto enc = encode_fn();
-  // A: chunk planes of `subs` sub-grids of Pp pixels (multiple of 8) x 16 B,
-  // moved as 128-byte (8-pixel) rows: dims {128 B, Pp/8, subs, Cc}
+  const int kb = a.kb;
+  const CUtensorMapSwizzle swz =
+      kb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : kb == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE;
+  // kb 128/64: one pixel row per TMA row (dims {kb, Pp, subs, Cc});
+  // kb 16:     8-pixel 128-byte rows (dims {128, Pp/8, subs, Cc}, Pp % 8 == 0)
+  const cuuint64_t row_bytes = kb == 16 ? 128 : kb;
+  const cuuint64_t rows = kb == 16 ? static_cast<cuuint64_t>(xl.Pp / 8) : static_cast<cuuint64_t>(xl.Pp);
   {
     const cuuint64_t tsubs = xl.kind == LAY_PHASE ? 4 : 1;
-    cuuint64_t dims[4] = {128, static_cast<cuuint64_t>(xl.Pp / 8), tsubs, static_cast<cuuint64_t>(a.Cc)};
-    cuuint64_t strides[3] = {128, static_cast<cuuint64_t>(xl.Pp) * 16, static_cast<cuuint64_t>(xl.Pp) * 16 * tsubs};
-    cuuint32_t box[4] = {128, static_cast<cuuint32_t>(a.hg), static_cast<cuuint32_t>(a.subs),
-                         static_cast<cuuint32_t>(a.pps)};
+    cuuint64_t dims[4] = {row_bytes, rows, tsubs, static_cast<cuuint64_t>(a.Cc)};
+    cuuint64_t strides[3] = {row_bytes, static_cast<cuuint64_t>(xl.Pp) * kb, static_cast<cuuint64_t>(xl.Pp) * kb * tsubs};
+    cuuint32_t box[4] = {static_cast<cuuint32_t>(row_bytes), static_cast<cuuint32_t>(a.hbox), 1, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     if (enc(&p.tmA, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(x), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return false;
   }
-  // B: [taps][planes][OC][16 B] -> dims {128 B (8 rows), OC/8, planes, taps}
+  // B: [taps][chunk planes][OC][kb] -> dims {row, OC rows, planes, taps}
   {
     const int OC = p.spec.OC;
-    cuuint64_t dims[4] = {128, static_cast<cuuint64_t>(OC / 8), static_cast<cuuint64_t>(a.Cc),
-                          static_cast<cuuint64_t>(p.spec.taps)};
-    cuuint64_t strides[3] = {128, static_cast<cuuint64_t>(OC) * 16, static_cast<cuuint64_t>(OC) * 16 * a.Cc};
-    cuuint32_t box[4] = {128, static_cast<cuuint32_t>(a.bn / 8),
+    const cuuint64_t brow = kb == 16 ? 128 : kb;
+    const cuuint64_t brows = kb == 16 ? OC / 8 : OC;
+    cuuint64_t dims[4] = {brow, brows, static_cast<cuuint64_t>(a.Cc), static_cast<cuuint64_t>(p.spec.taps)};
+    cuuint64_t strides[3] = {brow, static_cast<cuuint64_t>(OC) * kb, static_cast<cuuint64_t>(OC) * kb * a.Cc};
+    cuuint32_t box[4] = {static_cast<cuuint32_t>(brow), static_cast<cuuint32_t>(kb == 16 ? a.bn / 8 : a.bn),
                          static_cast<cuuint32_t>(a.resident_b ? a.Cc : a.pps), static_cast<cuuint32_t>(p.spec.taps)};
     cuuint32_t es[4] = {1, 1, 1, 1};
     if (enc(&p.tmB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(w), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return false;
   }
@@ -842,11 +1187,15 @@ bool tc_conv_launch(TcConvPlan* p, const void* x, const Lay& xl, const void* w, 
   }
   TcArgs a = p->args;
   a.acc_scale = acc_scale;
+  a.relu_last = epi.n_ops > 0 && epi.op[epi.n_ops - 1] == E_RELU;
   static const int dbg = [] {
     const char* e = std::getenv("MRB200_TC_DBG");
     return e ? std::atoi(e) : 0;
   }();
   a.dbg = dbg;
+  static unsigned long long* stamps = nullptr;
+  if ((dbg & 16) && !stamps) cudaMalloc(&stamps, 8 * 16 * 8);
+  a.stamps = stamps;
   a.epi = epi;
   a.out = out;
   const int sig = epi_signature(epi, out);
@@ -870,6 +1219,20 @@ bool tc_conv_launch(TcConvPlan* p, const void* x, const Lay& xl, const void* w, 
   }
 #undef MRB_TC_SIGS
 #undef MRB_TC_LAUNCH
+  if ((dbg & 16) && a.pool) {
+    cudaStreamCaptureStatus cs;
+    cudaStreamIsCapturing(s, &cs);
+    if (cs == cudaStreamCaptureStatusNone) {
+      unsigned long long h[16 * 8];
+      cudaStreamSynchronize(s);
+      cudaMemcpy(h, stamps, sizeof(h), cudaMemcpyDeviceToHost);
+      for (int t = 1; t < 12; ++t)
+        std::fprintf(stderr, "POOLSTAMP tile %2d wait_tfull %6lld stage %6lld bar1 %6lld pool %6lld bar2 %6lld\n", t,
+                     (long long)(h[t * 8 + 0] - h[t * 8 + 5]), (long long)(h[t * 8 + 1] - h[t * 8 + 0]),
+                     (long long)(h[t * 8 + 2] - h[t * 8 + 1]), (long long)(h[t * 8 + 3] - h[t * 8 + 2]),
+                     (long long)(h[t * 8 + 4] - h[t * 8 + 3]));
+    }
+  }
   return true;
 }
 
@@ -878,9 +1241,10 @@ void tc_conv_destroy(TcConvPlan* p) { delete p; }
 const char* tc_conv_describe(const TcConvPlan* p, char* buf, int n) {
   const TcArgs& a = p->args;
   static const char* kinds[] = {"s1", "s2-phase", "stem-s2d"};
-  std::snprintf(buf, n, "tcgen05 %s %s M128xN%d taps=%d steps=%d grid=%dx%d hg=%d pps=%d stages=%d B=%s ctas=%d smem=%zu",
-                p->spec.elem_bytes == 1 ? "i8" : "bf16", kinds[p->spec.kind], a.bn, p->spec.taps, a.n_steps, a.Hg,
-                a.Wg, a.hg, a.pps, a.n_stages, a.resident_b ? "resident" : "streamed", p->grid, p->smem);
+  std::snprintf(buf, n,
+                "tcgen05 %s %s %dx(M128)xN%d kb=%d taps=%d steps=%d grid=%dx%d rows=%dx%d pps=%d stages=%d B=%s ctas=%d smem=%zu",
+                p->spec.elem_bytes == 1 ? "i8" : "bf16", kinds[p->spec.kind], a.sub, a.bn, a.kb, p->spec.taps, a.n_steps,
+                a.Hg, a.Wg, a.nbox, a.hbox, a.pps, a.n_stages, a.resident_b ? "resident" : "streamed", p->grid, p->smem);
   return buf;
 }
 

@@ -19,8 +19,12 @@ struct TcConvSpec {
   int elem_bytes;  // 1: int8 (kind::i8), 2: bf16 (kind::f16)
   int N, C, H, W, OC, OH, OW, KH, KW;
   int Hs, Ws;      // TC_STEM_S2D input grid
+  // Fused max_pool2d consumer (cross-group fusion of conv -> max_pool2d, the
+  // conv output never leaves the SM): window, stride, padding, pooled dims.
+  int pool = 0, pkh = 0, pkw = 0, psh = 1, psw = 1, pph = 0, ppw = 0, poh = 0, pow = 0;
   // filled by planning
-  int taps = 0, wplanes = 0;  // weight layout [taps][wplanes][OC][16 B]
+  int taps = 0, wplanes = 0;  // weight layout [taps][wplanes][OC][kb bytes]
+  int kb = 0;                 // operand chunk bytes (the data representation's chunk width)
 };
 
 struct TcConvPlan;

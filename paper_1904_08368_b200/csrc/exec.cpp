@@ -102,6 +102,9 @@ struct Exec {
   std::vector<std::string> group_exact;     // int8 exactness proof per group
   std::vector<std::string> group_note;      // kernel plan description
   std::vector<TcConvSpec> group_tc;         // tcgen05 formulation per conv group
+  std::map<int, int> want_kb;               // value -> chunk width its tcgen05 consumers read
+  std::vector<int> fused_pool;              // conv group -> its max_pool2d consumer executed in-kernel, or -1
+  std::vector<char> fused_away;             // group executed inside another group's launch
   bool weights_ready = false;
   // io
   const float* cur_input = nullptr;
@@ -158,12 +161,13 @@ int64_t elem_bytes(int fmt) { return fmt == FMT_F32 ? 4 : fmt == FMT_BF16 ? 2 : 
 // Layout of a representation: P16 (NORMAL / PHASE / S2D) with a kPad
 // border for 4-D values, row-major for 2-D ones.  Plane strides are padded to
 // 8 pixels (128-byte TMA rows).  S2D takes the stem's input padding.
-Lay make_lay(const std::vector<int64_t>& s, int fmt, int kind, int s2d_pad = 0) {
+Lay make_lay(const std::vector<int64_t>& s, int fmt, int kind, int s2d_pad = 0, int kb = 16) {
   Lay L{};
   L.C = s.size() >= 2 ? static_cast<int32_t>(s[1]) : 1;
   L.kind = LAY_NORMAL;
+  L.kb = kb;
   if (s.size() == 4) {
-    L.cpc = static_cast<int32_t>(16 / elem_bytes(fmt));
+    L.cpc = static_cast<int32_t>(kb / elem_bytes(fmt));
     L.kind = kind;
     L.Hp = static_cast<int32_t>(s[2] + 2 * kPad);
     L.Wp = static_cast<int32_t>(s[3] + 2 * kPad);
@@ -193,14 +197,17 @@ int64_t lay_elems(const Lay& L) {
 }
 
 
-// Finds or adds a representation of value v.
-int want_rep(Exec& ex, int v, int fmt, const QParams* q, int kind = LAY_NORMAL, int s2d_pad = 0) {
+// Finds or adds a representation of value v.  kb 0 = any chunk width (the
+// value's preferred one when creating).
+int want_rep(Exec& ex, int v, int fmt, const QParams* q, int kind = LAY_NORMAL, int s2d_pad = 0, int kb = 0) {
   auto& rs = ex.reps[v];
   if (ex.P.values[v].shape.size() != 4) kind = LAY_NORMAL;
+  if (fmt == FMT_F32 || kind == LAY_S2D) kb = 16;
   for (size_t i = 0; i < rs.size(); ++i) {
     const Rep& r = rs[i];
     if (r.nchw_user) continue;
     if (r.fmt != fmt || r.lay.kind != kind) continue;
+    if (kb && r.lay.kb != kb) continue;
     if (fmt == FMT_I8) {
       if (!q || !r.has_q || !(r.q == *q)) continue;
     }
@@ -212,10 +219,97 @@ int want_rep(Exec& ex, int v, int fmt, const QParams* q, int kind = LAY_NORMAL, 
     r.has_q = true;
     r.q = *q;
   }
-  r.lay = make_lay(ex.P.values[v].shape, fmt, kind, s2d_pad);
+  if (!kb) {
+    auto it = ex.want_kb.find(v);
+    kb = it != ex.want_kb.end() ? it->second : 16;
+  }
+  r.lay = make_lay(ex.P.values[v].shape, fmt, kind, s2d_pad, kb);
   r.elems = lay_elems(r.lay);
   rs.push_back(r);
   return static_cast<int>(rs.size()) - 1;
+}
+
+// tcgen05 formulation per conv group, decided at compile time from the
+// geometry: stride-1 halo (3x3/1x1), stride-2 over phase-split inputs, or
+// the space-to-depth stem; anything else runs on the CUDA-core kernel.
+void decide_tc(Exec& ex) {
+  Program& P = ex.P;
+  std::map<int, int> phase_kb;
+  ex.fused_pool.assign(P.groups.size(), -1);
+  ex.fused_away.assign(P.groups.size(), 0);
+  ex.group_tc.assign(P.groups.size(), TcConvSpec{});
+  for (size_t gi = 0; gi < P.groups.size(); ++gi) {
+    int& path = ex.group_path[gi];
+    const GroupDesc& g = P.groups[gi];
+    if (path != P_CONV_I8_TC && path != P_CONV_BF16_TC) continue;
+    bool has_sum = !g.epi.empty() && g.epi.back().kind == EpiKind::SumHW;
+    const auto& os = has_sum ? g.pre_sum_shape : g.out_shape;
+    TcConvSpec sp{};
+    sp.elem_bytes = path == P_CONV_I8_TC ? 1 : 2;
+    sp.N = static_cast<int>(g.in_shape[0]);
+    sp.C = static_cast<int>(g.in_shape[1]);
+    sp.H = static_cast<int>(g.in_shape[2]);
+    sp.W = static_cast<int>(g.in_shape[3]);
+    sp.OC = static_cast<int>(os[1]);
+    sp.OH = static_cast<int>(os[2]);
+    sp.OW = static_cast<int>(os[3]);
+    sp.KH = static_cast<int>(g.kh);
+    sp.KW = static_cast<int>(g.kw);
+    bool same3 = g.kh == 3 && g.kw == 3 && g.ph == 1 && g.pw == 1;
+    bool one = g.kh == 1 && g.kw == 1 && g.ph == 0 && g.pw == 0;
+    bool ok = false;
+    if (g.sh == 1 && g.sw == 1 && (same3 || one)) {
+      sp.kind = TC_S1;
+      ok = tc_conv_plan_ok(sp);
+    } else if (g.sh == 2 && g.sw == 2 && (same3 || one)) {
+      sp.kind = TC_S2_PHASE;
+      auto pk = phase_kb.find(g.data.value);  // one phase-split copy per value
+      if (pk != phase_kb.end()) sp.kb = pk->second;
+      ok = tc_conv_plan_ok(sp);
+    } else if (g.sh == 2 && g.sw == 2 && g.kh == g.kw && (g.kh & 1) && g.ph == g.kh / 2 && g.pw == g.kw / 2 &&
+               P.values[g.data.value].is_data) {
+      sp.kind = TC_STEM_S2D;
+      sp.Hs = static_cast<int>((sp.H + 2 * g.ph + 1) / 2);
+      sp.Ws = static_cast<int>((sp.W + 2 * g.pw + 1) / 2);
+      ok = tc_conv_plan_ok(sp);
+    }
+    if (ok && sp.kind == TC_STEM_S2D) {
+      // cross-group fusion: conv -> max_pool2d when the
+      // pool is the conv output's only consumer; same arithmetic, the conv
+      // tensor never reaches HBM
+      const ValueInfo& ov = P.values[g.out_value];
+      bool epi_ok = true;
+      for (const auto& op : g.epi) epi_ok = epi_ok && (op.kind == EpiKind::Bias || op.kind == EpiKind::Relu);
+      if (ov.consumers.size() == 1 && !ov.is_result && epi_ok && !ov.quantized) {
+        const int pj = ov.consumers[0];
+        const GroupDesc& pg = P.groups[pj];
+        if (pg.kind == GroupKind::MaxPool && pg.data.value == g.out_value && ex.group_path[pj] == P_POOL) {
+          TcConvSpec fs = sp;
+          fs.pool = 1;
+          fs.pkh = static_cast<int>(pg.kh);
+          fs.pkw = static_cast<int>(pg.kw);
+          fs.psh = static_cast<int>(pg.sh);
+          fs.psw = static_cast<int>(pg.sw);
+          fs.pph = static_cast<int>(pg.ph);
+          fs.ppw = static_cast<int>(pg.pw);
+          fs.poh = static_cast<int>(pg.out_shape[2]);
+          fs.pow = static_cast<int>(pg.out_shape[3]);
+          if (tc_conv_plan_ok(fs)) {
+            sp = fs;
+            ex.fused_pool[gi] = pj;
+            ex.fused_away[pj] = 1;
+          }
+        }
+      }
+    }
+    if (ok) {
+      ex.group_tc[gi] = sp;
+      if (sp.kind == TC_S1) ex.want_kb[g.data.value] = sp.kb;
+      if (sp.kind == TC_S2_PHASE) phase_kb[g.data.value] = sp.kb;
+    } else {
+      path = path == P_CONV_I8_TC ? P_CONV_I8_SIMT : P_CONV_BF16_SIMT;
+    }
+  }
 }
 
 void plan(Exec& ex, bool use_tc) {
@@ -225,18 +319,9 @@ void plan(Exec& ex, bool use_tc) {
   ex.group_path.assign(P.groups.size(), P_NONE);
   ex.group_exact.assign(P.groups.size(), "");
 
-  // primary representations of group outputs
+  // kernel path per group
   for (size_t gi = 0; gi < P.groups.size(); ++gi) {
     const GroupDesc& g = P.groups[gi];
-    const ValueInfo& ov = P.values[g.out_value];
-    if (ov.quantized) {
-      want_rep(ex, g.out_value, FMT_I8, &ov.q);
-    } else if (g.kind == GroupKind::Dense || ov.shape.size() == 2) {
-      want_rep(ex, g.out_value, FMT_F32, nullptr);
-    } else {
-      want_rep(ex, g.out_value, ov.is_result ? FMT_F32 : ffmt, nullptr);
-    }
-    // kernel path
     switch (g.kind) {
       case GroupKind::Conv:
         if (g.weight.quant) {
@@ -252,6 +337,19 @@ void plan(Exec& ex, bool use_tc) {
         break;
       case GroupKind::MaxPool: ex.group_path[gi] = P_POOL; break;
       case GroupKind::DwConv: ex.group_path[gi] = P_DW; break;
+    }
+  }
+  decide_tc(ex);
+  // primary representations of group outputs (chunk width from want_kb)
+  for (size_t gi = 0; gi < P.groups.size(); ++gi) {
+    const GroupDesc& g = P.groups[gi];
+    const ValueInfo& ov = P.values[g.out_value];
+    if (ov.quantized) {
+      want_rep(ex, g.out_value, FMT_I8, &ov.q);
+    } else if (g.kind == GroupKind::Dense || ov.shape.size() == 2) {
+      want_rep(ex, g.out_value, FMT_F32, nullptr);
+    } else {
+      want_rep(ex, g.out_value, ov.is_result ? FMT_F32 : ffmt, nullptr);
     }
   }
   // @main data inputs: the caller's NCHW float32 buffer
@@ -283,18 +381,19 @@ GroupIO resolve_inputs(Exec& ex, int gi) {
   const ValueInfo& dv = P.values[g.data.value];
   int path = ex.group_path[gi];
   // data layout kind the tcgen05 formulation needs (CUDA-core kernels read NORMAL)
-  int kind = LAY_NORMAL, s2d_pad = 0;
+  int kind = LAY_NORMAL, s2d_pad = 0, kb = 0;
   if (path == P_CONV_I8_TC || path == P_CONV_BF16_TC) {
     const TcConvSpec& sp = ex.group_tc[gi];
     kind = sp.kind == TC_S2_PHASE ? LAY_PHASE : sp.kind == TC_STEM_S2D ? LAY_S2D : LAY_NORMAL;
     s2d_pad = static_cast<int>(g.ph);
+    kb = sp.kb;
   }
   if (path == P_CONV_I8_SIMT || path == P_CONV_I8_TC) {
     if (g.data.quant) {
-      io.data_rep = want_rep(ex, g.data.value, FMT_I8, &g.data.q, kind, s2d_pad);
+      io.data_rep = want_rep(ex, g.data.value, FMT_I8, &g.data.q, kind, s2d_pad, kb);
       io.data_scale = g.data.q.c2;
     } else {
-      io.data_rep = want_rep(ex, g.data.value, FMT_I8, &dv.q, kind, s2d_pad);
+      io.data_rep = want_rep(ex, g.data.value, FMT_I8, &dv.q, kind, s2d_pad, kb);
       io.data_scale = dv.q.c2;
     }
   } else if (g.kind == GroupKind::Dense) {
@@ -304,7 +403,7 @@ GroupIO resolve_inputs(Exec& ex, int gi) {
     else if (dv.quantized) fail(MR_ERR_UNSUPPORTED_GROUP, "group %" + g.name + ": dense over a coded value");
   } else if (path == P_CONV_F32 || path == P_CONV_BF16_SIMT || path == P_CONV_BF16_TC) {
     if (g.data.pre_mul != 0.f) fail(MR_ERR_UNSUPPORTED_GROUP, "group %" + g.name + ": scaled conv input");
-    io.data_rep = want_rep(ex, g.data.value, ffmt, nullptr, kind, s2d_pad);
+    io.data_rep = want_rep(ex, g.data.value, ffmt, nullptr, kind, s2d_pad, kb);
   } else {  // pool / depthwise: float input
     io.data_rep = want_rep(ex, g.data.value, ffmt, nullptr);
   }
@@ -434,46 +533,6 @@ void build(Exec& ex) {
   Program& P = ex.P;
   const bool use_tc = !ex.opt.force_simt;
   plan(ex, use_tc);
-  // tcgen05 formulation per conv group, decided at compile time from the
-  // geometry: stride-1 halo (3x3/1x1), stride-2 over phase-split inputs, or
-  // the space-to-depth stem; anything else runs on the CUDA-core kernel.
-  ex.group_tc.assign(P.groups.size(), TcConvSpec{});
-  for (size_t gi = 0; gi < P.groups.size(); ++gi) {
-    int& path = ex.group_path[gi];
-    const GroupDesc& g = P.groups[gi];
-    if (path != P_CONV_I8_TC && path != P_CONV_BF16_TC) continue;
-    bool has_sum = !g.epi.empty() && g.epi.back().kind == EpiKind::SumHW;
-    const auto& os = has_sum ? g.pre_sum_shape : g.out_shape;
-    TcConvSpec sp{};
-    sp.elem_bytes = path == P_CONV_I8_TC ? 1 : 2;
-    sp.N = static_cast<int>(g.in_shape[0]);
-    sp.C = static_cast<int>(g.in_shape[1]);
-    sp.H = static_cast<int>(g.in_shape[2]);
-    sp.W = static_cast<int>(g.in_shape[3]);
-    sp.OC = static_cast<int>(os[1]);
-    sp.OH = static_cast<int>(os[2]);
-    sp.OW = static_cast<int>(os[3]);
-    sp.KH = static_cast<int>(g.kh);
-    sp.KW = static_cast<int>(g.kw);
-    bool same3 = g.kh == 3 && g.kw == 3 && g.ph == 1 && g.pw == 1;
-    bool one = g.kh == 1 && g.kw == 1 && g.ph == 0 && g.pw == 0;
-    bool ok = false;
-    if (g.sh == 1 && g.sw == 1 && (same3 || one)) {
-      sp.kind = TC_S1;
-      ok = tc_conv_plan_ok(sp);
-    } else if (g.sh == 2 && g.sw == 2 && (same3 || one)) {
-      sp.kind = TC_S2_PHASE;
-      ok = tc_conv_plan_ok(sp);
-    } else if (g.sh == 2 && g.sw == 2 && g.kh == g.kw && (g.kh & 1) && g.ph == g.kh / 2 && g.pw == g.kw / 2 &&
-               P.values[g.data.value].is_data) {
-      sp.kind = TC_STEM_S2D;
-      sp.Hs = static_cast<int>((sp.H + 2 * g.ph + 1) / 2);
-      sp.Ws = static_cast<int>((sp.W + 2 * g.pw + 1) / 2);
-      ok = tc_conv_plan_ok(sp);
-    }
-    if (ok) ex.group_tc[gi] = sp;
-    else path = path == P_CONV_I8_TC ? P_CONV_I8_SIMT : P_CONV_BF16_SIMT;
-  }
   std::vector<GroupIO> io(P.groups.size());
   for (size_t gi = 0; gi < P.groups.size(); ++gi) io[gi] = resolve_inputs(ex, static_cast<int>(gi));
 
@@ -541,17 +600,22 @@ void build(Exec& ex) {
 
   // ---- groups ----
   for (size_t gi = 0; gi < P.groups.size(); ++gi) {
+    if (ex.fused_away[gi]) continue;  // runs inside its producer's launch
     const GroupDesc& g = P.groups[gi];
     const GroupIO& gio = io[gi];
     const int path = ex.group_path[gi];
+    const int fp = ex.fused_pool[gi];                 // fused max_pool2d consumer
+    const int ov = fp >= 0 ? P.groups[fp].out_value : g.out_value;  // value this launch writes
+    const int sgi = fp >= 0 ? fp : static_cast<int>(gi);            // group owning the side output
     const Rep& drep = ex.reps[g.data.value][gio.data_rep];
     if (drep.nchw_user) fail(MR_ERR_INTERNAL, "group reads the raw input");
     B.use(drep.buf);
     for (size_t i = 0; i < g.epi.size(); ++i)
       if (gio.res_rep[i] >= 0) B.use(ex.reps[g.epi[i].value][gio.res_rep[i]].buf);
-    int obuf = B.buffer_for(g.out_value, 0, "%" + g.out_name);
-    int sbuf = side_rep[gi] >= 0 ? B.buffer_for(g.out_value, side_rep[gi], "%" + g.out_name + ":codes") : -1;
-    const Rep& orep = ex.reps[g.out_value][0];
+    const std::string oname = fp >= 0 ? P.groups[fp].out_name : g.out_name;
+    int obuf = B.buffer_for(ov, 0, "%" + oname);
+    int sbuf = side_rep[sgi] >= 0 ? B.buffer_for(ov, side_rep[sgi], "%" + oname + ":codes") : -1;
+    const Rep& orep = ex.reps[ov][0];
 
     bool has_sum = !g.epi.empty() && g.epi.back().kind == EpiKind::SumHW;
     int n_elem_ops = static_cast<int>(g.epi.size()) - (has_sum ? 1 : 0);
@@ -570,19 +634,19 @@ void build(Exec& ex) {
       out.plan = orep.lay;
     }
     if (sbuf >= 0) {
-      const Rep& sr = ex.reps[g.out_value][side_rep[gi]];
+      const Rep& sr = ex.reps[ov][side_rep[sgi]];
       out.slay = sr.lay;
       out.side_fmt = sr.fmt;
       out.side_q = to_qdev(sr.q);
     }
 
     LaunchRec L;
-    L.name = "%" + g.name;
-    L.kernel = path_name(path);
+    L.name = "%" + g.name + (fp >= 0 ? "+%" + P.groups[fp].name : "");
+    L.kernel = std::string(path_name(path)) + (fp >= 0 ? "+max_pool" : "");
     // algorithmic traffic: data once + output(s) once + residuals + weights
     double out_bytes = static_cast<double>(orep.elems) * elem_bytes(orep.fmt);
     if (sbuf >= 0) {
-      const Rep& sr = ex.reps[g.out_value][side_rep[gi]];
+      const Rep& sr = ex.reps[ov][side_rep[sgi]];
       out_bytes += static_cast<double>(sr.elems) * elem_bytes(sr.fmt);
     }
     double in_bytes = static_cast<double>(drep.elems) * elem_bytes(drep.fmt);
@@ -744,14 +808,15 @@ void build(Exec& ex) {
     // CUDA-core producers write interior pixels only: clear the P16 borders
     // (the tcgen05 conv writes its own, it computes over the padded grid).
     bool tc_same = (path == P_CONV_I8_TC || path == P_CONV_BF16_TC) && ex.group_tc[gi].kind == TC_S1;
-    if (!tc_same && !has_sum && g.out_shape.size() == 4) {
+    const auto& zshape = fp >= 0 ? P.groups[fp].out_shape : g.out_shape;
+    if (!tc_same && !has_sum && zshape.size() == 4) {
       for (int b2 : {obuf, sbuf}) {
         if (b2 < 0) continue;
         LaunchRec Z;
         Z.name = "%" + g.name;
         Z.kernel = "zero_border";
-        Lay zl = b2 == obuf ? orep.lay : ex.reps[g.out_value][side_rep[gi]].lay;
-        int N = static_cast<int>(g.out_shape[0]), H = static_cast<int>(g.out_shape[2]), W = static_cast<int>(g.out_shape[3]);
+        Lay zl = b2 == obuf ? orep.lay : ex.reps[ov][side_rep[sgi]].lay;
+        int N = static_cast<int>(zshape[0]), H = static_cast<int>(zshape[2]), W = static_cast<int>(zshape[3]);
         int64_t border = (zl.C + zl.cpc - 1) / zl.cpc * static_cast<int64_t>(N) * (2 * (W + 2) + 2 * H) * 16;
         Z.bytes = static_cast<double>(border);
         Z.fn = [e, b2, zl, N](cudaStream_t s) { launch_zero_border(e->ptr(b2), zl, N, s); };
@@ -886,8 +951,9 @@ void prepare_weights(Exec& ex, cudaStream_t s) {
       n = static_cast<int64_t>(O) * I * KH * KW;
     } else if (wl == WL_TC || wl == WL_S2D) {
       const TcConvSpec& sp = ex.group_tc[gi];
-      int cpc = 16 / static_cast<int>(elem_bytes(fmt));
+      int cpc = sp.kb / static_cast<int>(elem_bytes(fmt));
       n = static_cast<int64_t>(sp.taps) * sp.wplanes * O * cpc;
+      cs = sp.kb;  // k_weight_prep: chunk bytes for the tcgen05 layouts
     } else {
       n = static_cast<int64_t>(O) * KH * KW * cs;
     }
@@ -921,7 +987,7 @@ void prepare_weights(Exec& ex, cudaStream_t s) {
       int64_t per = n / O, worst = 0;
       for (int64_t k = 0; k < n; ++k) {
         int o = dense_t ? static_cast<int>((k / 4) % O)
-                : wl != WL_ROWS ? static_cast<int>((k / 16) % O) : static_cast<int>(k / per);
+                : wl != WL_ROWS ? static_cast<int>((k / ex.group_tc[gi].kb) % O) : static_cast<int>(k / per);
         sums[o] += std::abs(static_cast<int>(codes[k]));
       }
       for (int o = 0; o < O; ++o) worst = std::max(worst, sums[o]);

@@ -23,9 +23,9 @@ struct QDev {
   int32_t is_signed;
 };
 
-// Physical layout of an activation tensor ("P16"): channels are split into
-// 16-byte chunks (cpc = 16 / element-bytes channels each); each chunk is a
-// plane over the zero-padded pixel grid (pad kPad):
+// Physical layout of an activation tensor ("PK"): channels are split into
+// chunks of kb bytes (kb = 16, 64 or 128; cpc = kb / element-bytes channels
+// each); each chunk is a plane over the zero-padded pixel grid (pad kPad):
 //   LAY_NORMAL  element (n, c, h, w) at ((c / cpc) * Pp + pix) * cpc + c % cpc,
 //               pix = (n * Hp + h + kPad) * Wp + (w + kPad)
 //   LAY_PHASE   the padded grid split into its 4 stride-2 phases, so a
@@ -34,11 +34,13 @@ struct QDev {
 //               (n * Hq + hp / 2) * Wq + wp / 2; sub-grids of Pp pixels
 //   LAY_S2D     the network input in space-to-depth form for a 7x7/s2 stem
 //               (written by input_convert, read by the stem tcgen05 conv only)
-// Plane / sub-grid strides are padded to a multiple of 8 pixels so the
-// tcgen05 conv can move 128-byte (8-pixel) TMA rows.  Borders hold zeros, so
-// a stride-1 3x3 conv reads its 9 taps as 9 row shifts of one contiguous
-// pixel range (conv_tc.cu).  cpc == 0 marks a plain row-major [N, C] tensor
-// (pix = n).
+// A pixel's kb-byte chunk is one row of a tcgen05 operand tile: kb = 128 / 64
+// rows are TMA-loaded with the matching 128B / 64B swizzle, and a stride-1
+// 3x3 conv reads its 9 taps as 9 row shifts of one contiguous pixel range
+// (conv_tc.cu).  kb = 16 ("P16") is used where no tensor-core conv reads the
+// tensor (float32 residual stream: warp-coalesced epilogue loads) and for the
+// 16-byte stem input.  Plane strides are padded to a multiple of 8 pixels.
+// Borders hold zeros.  cpc == 0 marks a plain row-major [N, C] tensor (pix = n).
 enum LayKind : int32_t { LAY_NORMAL = 0, LAY_PHASE = 1, LAY_S2D = 2 };
 
 struct Lay {
@@ -46,6 +48,7 @@ struct Lay {
   int32_t C;     // logical channels (row length when cpc == 0)
   int64_t Pp;    // pixel stride of a plane (NORMAL) / sub-grid (PHASE, S2D)
   int32_t kind;  // LayKind
+  int32_t kb;    // chunk bytes
   int32_t Hp, Wp;  // padded grid
   int32_t Hq, Wq;  // PHASE / S2D sub-grid
 };
@@ -133,6 +136,11 @@ __host__ __device__ __forceinline__ int64_t lay_chunk(const Lay& L, int64_t pix,
 __host__ __device__ __forceinline__ int64_t lay_off(const Lay& L, int64_t pix, int32_t c) {
   if (L.cpc == 0) return pix * L.C + c;
   return lay_chunk(L, pix, c) * L.cpc + (c % L.cpc);
+}
+
+// Byte offset of channel c (c % (16 / eb) == 0 for a 16-byte granule).
+__host__ __device__ __forceinline__ int64_t lay_byte(const Lay& L, int64_t pix, int32_t c) {
+  return lay_chunk(L, pix, c) * L.kb + static_cast<int64_t>(c % L.cpc) * (L.kb / L.cpc);
 }
 
 // quant_code when the clip bounds lie inside int32 (every realize site:

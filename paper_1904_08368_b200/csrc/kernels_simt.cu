@@ -44,45 +44,50 @@ __device__ __forceinline__ Pix decode_pix(int64_t pix, int32_t H, int32_t W) {
 // channel padding of the last chunk.
 __global__ void k_input_convert(const float* __restrict__ x, int N, int C, int H, int W, void* out, int fmt,
                                 Lay L, int s2d_pad, float pre_mul, QDev q) {
+  const int eb = L.kb / L.cpc;
+  const int gpc = L.kb / 16;       // 16-byte granules per chunk
+  const int cpg = 16 / eb;         // channels per granule
   const int planes = L.kind == LAY_S2D ? (4 * C + L.cpc - 1) / L.cpc : (C + L.cpc - 1) / L.cpc;
   const int64_t grid_pix = L.kind == LAY_S2D ? static_cast<int64_t>(N) * L.Hq * L.Wq
                                              : static_cast<int64_t>(N) * (H + 2 * kPad) * (W + 2 * kPad);
-  const int64_t total = static_cast<int64_t>(planes) * grid_pix;
+  const int64_t total = static_cast<int64_t>(planes) * gpc * grid_pix;
   GRID_STRIDE(i, total) {
     int64_t pix = i % grid_pix;
-    int32_t pl = static_cast<int32_t>(i / grid_pix);
+    int64_t t = i / grid_pix;
+    const int gr = static_cast<int>(t % gpc);
+    const int32_t pl = static_cast<int32_t>(t / gpc);
     float v[16];
     bool live[16];
-    int64_t dst_chunk;
+    int64_t dst_byte;
     if (L.kind == LAY_S2D) {
       // s2d pixel (n, si, sj), channel sc = (py*2 + px)*C + c  <-  x[n][c][2si+py-pad][2sj+px-pad]
       int32_t sj = static_cast<int32_t>(pix % L.Wq);
-      int64_t t = pix / L.Wq;
-      int32_t si = static_cast<int32_t>(t % L.Hq);
-      int32_t n = static_cast<int32_t>(t / L.Hq);
+      int64_t t2 = pix / L.Wq;
+      int32_t si = static_cast<int32_t>(t2 % L.Hq);
+      int32_t n = static_cast<int32_t>(t2 / L.Hq);
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
-        int sc = pl * L.cpc + k;
+        int sc = pl * L.cpc + gr * cpg + k;
         int ph = sc / C, c = sc - ph * C;
         int y = 2 * si + (ph >> 1) - s2d_pad, xx = 2 * sj + (ph & 1) - s2d_pad;
-        live[k] = k < L.cpc && sc < 4 * C && y >= 0 && y < H && xx >= 0 && xx < W;
+        live[k] = k < cpg && sc < 4 * C && y >= 0 && y < H && xx >= 0 && xx < W;
         v[k] = live[k] ? x[((static_cast<int64_t>(n) * C + c) * H + y) * W + xx] : 0.f;
       }
-      dst_chunk = pl * L.Pp + pix;
+      dst_byte = (pl * L.Pp + pix) * L.kb + gr * 16;
     } else {
       Pix p = decode_pix(pix, H, W);
-      int32_t c0 = pl * L.cpc;
+      int32_t c0 = pl * L.cpc + gr * cpg;
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
-        live[k] = k < L.cpc && !p.border && c0 + k < C;
+        live[k] = k < cpg && !p.border && c0 + k < C;
         v[k] = live[k] ? x[((static_cast<int64_t>(p.n) * C + c0 + k) * H + p.h) * W + p.w] : 0.f;
       }
-      dst_chunk = lay_chunk(L, pix, c0);
+      dst_byte = lay_chunk(L, pix, pl * L.cpc) * L.kb + gr * 16;
     }
 #pragma unroll
     for (int k = 0; k < 16; ++k)
       if (pre_mul != 0.f && live[k]) v[k] = __fmul_rn(v[k], pre_mul);
-    char* dst = static_cast<char*>(out) + dst_chunk * 16;
+    char* dst = static_cast<char*>(out) + dst_byte;
     if (fmt == FMT_F32) {
       *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
     } else if (fmt == FMT_BF16) {
@@ -153,7 +158,8 @@ __global__ void k_zero_border(void* buf, Lay L, int N) {
       wp = (r & 1) ? Wp - 1 : 0;
     }
     int64_t pix = (static_cast<int64_t>(n) * Hp + hp) * Wp + wp;
-    reinterpret_cast<int4*>(buf)[lay_chunk(L, pix, plane * L.cpc)] = make_int4(0, 0, 0, 0);
+    int4* dst = reinterpret_cast<int4*>(static_cast<char*>(buf) + lay_chunk(L, pix, plane * L.cpc) * L.kb);
+    for (int g = 0; g < L.kb / 16; ++g) dst[g] = make_int4(0, 0, 0, 0);
   }
 }
 
@@ -167,7 +173,8 @@ __global__ void k_zero_border(void* buf, Lay L, int N) {
 __global__ void k_weight_prep(const float* __restrict__ w, int O, int I, int KH, int KW, int Cs, int wl,
                               const float* __restrict__ oc_scale, float scalar, int fmt, int quant, QDev q,
                               void* out) {
-  const int cpc = fmt == FMT_I8 ? 16 : 8;
+  // WL_TC / WL_S2D: Cs carries the chunk width in bytes (16, 64 or 128)
+  const int cpc = (wl == WL_ROWS ? 16 : Cs) / (fmt == FMT_I8 ? 1 : 2);
   const int TA = (KH + 1) / 2;
   const int planes = wl == WL_S2D ? (4 * I + cpc - 1) / cpc : (I + cpc - 1) / cpc;
   int64_t total;
@@ -440,9 +447,10 @@ __global__ void k_dwconv(const void* __restrict__ x, int xfmt, const float* __re
 // (padded taps skipped, like the reference's bounds test).  Also emits the
 // consumers' second copy (int8 codes or bf16) when requested.
 __global__ void k_maxpool(const void* __restrict__ x, int xfmt, ConvGeom g, OutDev out) {
-  const int cpc = g.in.cpc;
-  const uint32_t planes = static_cast<uint32_t>((g.C + cpc - 1) / cpc);
-  const uint32_t total = planes * g.N * g.OH * g.OW;
+  const int eb = xfmt == FMT_F32 ? 4 : 2;
+  const int cpg = 16 / eb;  // channels per 16-byte granule
+  const uint32_t grans = static_cast<uint32_t>((g.C + cpg - 1) / cpg);
+  const uint32_t total = grans * g.N * g.OH * g.OW;
   const int Hp = g.H + 2 * kPad, Wp = g.W + 2 * kPad;
   const int OHp = g.OH + 2 * kPad, OWp = g.OW + 2 * kPad;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
@@ -450,11 +458,14 @@ __global__ void k_maxpool(const void* __restrict__ x, int xfmt, ConvGeom g, OutD
     const int ow = static_cast<int>(i - t * g.OW);
     uint32_t t2 = t / g.OH;
     const int oh = static_cast<int>(t - t2 * g.OH);
-    const uint32_t plane = t2 / g.N;
-    const int n = static_cast<int>(t2 - plane * g.N);
+    const uint32_t gran = t2 / g.N;
+    const int n = static_cast<int>(t2 - gran * g.N);
+    const int c0 = static_cast<int>(gran) * cpg;
     const int h0 = oh * g.sh - g.ph, w0 = ow * g.sw - g.pw;  // logical window origin
+    // taps are consecutive pixels of one chunk plane: byte stride g.in.kb
     const char* src = static_cast<const char*>(x) +
-                      (static_cast<int64_t>(plane) * g.in.Pp + (static_cast<int64_t>(n) * Hp + h0 + kPad) * Wp + w0 + kPad) * 16;
+                      lay_byte(g.in, (static_cast<int64_t>(n) * Hp + h0 + kPad) * Wp + w0 + kPad, c0);
+    const int64_t row = static_cast<int64_t>(Wp) * g.in.kb;
     float acc[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) acc[k] = 0.f;
@@ -463,7 +474,7 @@ __global__ void k_maxpool(const void* __restrict__ x, int xfmt, ConvGeom g, OutD
       const bool hv = h0 + kh >= 0 && h0 + kh < g.H;
       for (int kw = 0; kw < g.KW; ++kw) {
         if (!hv || w0 + kw < 0 || w0 + kw >= g.W) continue;
-        const char* p = src + (kh * Wp + kw) * 16;
+        const char* p = src + kh * row + kw * g.in.kb;
         float v[8];
         if (xfmt == FMT_F32) {
           float4 f = __ldg(reinterpret_cast<const float4*>(p));
@@ -484,7 +495,7 @@ __global__ void k_maxpool(const void* __restrict__ x, int xfmt, ConvGeom g, OutD
       }
     }
     const int64_t pix = (static_cast<int64_t>(n) * OHp + oh + kPad) * OWp + ow + kPad;
-    char* dst = static_cast<char*>(out.primary) + (static_cast<int64_t>(plane) * out.plan.Pp + pix) * 16;
+    char* dst = static_cast<char*>(out.primary) + lay_byte(out.plan, pix, c0);
     if (out.primary_fmt == FMT_F32) {
       *reinterpret_cast<float4*>(dst) = make_float4(acc[0], acc[1], acc[2], acc[3]);
     } else {
@@ -495,14 +506,13 @@ __global__ void k_maxpool(const void* __restrict__ x, int xfmt, ConvGeom g, OutD
       *reinterpret_cast<uint4*>(dst) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
     }
     if (out.side) {
-      const int c0 = static_cast<int>(plane) * cpc;
-      if (out.side_fmt == FMT_I8 && cpc == 4 && c0 + 4 <= g.C) {
+      if (out.side_fmt == FMT_I8 && cpg == 4 && c0 + 4 <= g.C) {
         uint32_t u = 0;
 #pragma unroll
         for (int k = 0; k < 4; ++k) u |= (static_cast<uint32_t>(quant_code_fast(acc[k], out.side_q)) & 0xff) << (8 * k);
-        *reinterpret_cast<uint32_t*>(static_cast<char*>(out.side) + lay_chunk(out.slay, pix, c0) * 16 + (c0 % 16)) = u;
+        *reinterpret_cast<uint32_t*>(static_cast<char*>(out.side) + lay_byte(out.slay, pix, c0)) = u;
       } else {
-        for (int k = 0; k < cpc && c0 + k < g.C; ++k) {
+        for (int k = 0; k < cpg && c0 + k < g.C; ++k) {
           int64_t so = lay_off(out.slay, pix, c0 + k);
           if (out.side_fmt == FMT_I8) static_cast<int8_t*>(out.side)[so] = static_cast<int8_t>(quant_code(acc[k], out.side_q));
           else static_cast<uint16_t*>(out.side)[so] = f32_to_bf16(acc[k]);
@@ -636,7 +646,7 @@ void launch_input_convert(const float* x, int N, int C, int H, int W, void* out,
   int planes = L.kind == LAY_S2D ? (4 * C + L.cpc - 1) / L.cpc : (C + L.cpc - 1) / L.cpc;
   int64_t grid_pix = L.kind == LAY_S2D ? static_cast<int64_t>(N) * L.Hq * L.Wq
                                        : static_cast<int64_t>(N) * (H + 2 * kPad) * (W + 2 * kPad);
-  k_input_convert<<<grid_stride_blocks(planes * grid_pix), kThreads, 0, s>>>(x, N, C, H, W, out, fmt, L, s2d_pad,
+  k_input_convert<<<grid_stride_blocks(planes * (L.kb / 16) * grid_pix), kThreads, 0, s>>>(x, N, C, H, W, out, fmt, L, s2d_pad,
                                                                             pre_mul, q);
 }
 
@@ -654,7 +664,7 @@ void launch_zero_border(void* buf, const Lay& L, int N, cudaStream_t s) {
 
 void launch_weight_prep(const float* w, int O, int I, int KH, int KW, int Cs, int wl, const float* oc_scale,
                         float scalar, int fmt, int quant, QDev q, void* out, cudaStream_t s) {
-  int cpc = fmt == FMT_I8 ? 16 : 8;
+  int cpc = (wl == WL_ROWS ? 16 : Cs) / (fmt == FMT_I8 ? 1 : 2);
   int TA = (KH + 1) / 2;
   int planes = wl == WL_S2D ? (4 * I + cpc - 1) / cpc : (I + cpc - 1) / cpc;
   int64_t total;
@@ -693,7 +703,8 @@ void launch_dwconv(const void* x, int xfmt, const float* w, const ConvGeom& g, i
 }
 
 void launch_maxpool(const void* x, int xfmt, const ConvGeom& g, const OutDev& out, cudaStream_t s) {
-  int64_t total = static_cast<int64_t>(g.N) * g.OH * g.OW * ((g.C + g.in.cpc - 1) / g.in.cpc);
+  int cpg = xfmt == FMT_F32 ? 4 : 8;
+  int64_t total = static_cast<int64_t>(g.N) * g.OH * g.OW * ((g.C + cpg - 1) / cpg);
   k_maxpool<<<grid_stride_blocks(total), kThreads, 0, s>>>(x, xfmt, g, out);
 }
 
