@@ -140,6 +140,16 @@ void mr_exec_destroy(mr_exec_t ex);
 
 const char* mr_last_error_message(void);
 
+/* Host-only compile check (no device touched): parses the fused module and
+ * lowers every Primitive group exactly as mr_exec_create does, then returns a
+ * JSON description of the lowered groups (kind, anchor attrs, prologue and
+ * epilogue op lists) in *json (valid until the next call on this thread).
+ * The error contract matches mr_exec_create's (MR_ERR_SYNTAX,
+ * MR_ERR_UNSUPPORTED_GROUP ...).  Mirrors what FuseOps' consumer learns from
+ * the reference's per-group type check (passes.cpp:452-486). */
+mr_status mr_module_lower(const char* fused_module_text, int64_t batch, int32_t n_data_inputs,
+                          const char** json);
+
 /* Library build identification (arch, kernels compiled). */
 const char* mr_build_info(void);
 

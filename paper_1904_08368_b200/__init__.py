@@ -33,7 +33,7 @@ MR_FLOAT = 2
 EXPORTS = [
     "mr_exec_default_options", "mr_exec_create", "mr_exec_set_weights", "mr_exec_run",
     "mr_exec_run_host", "mr_exec_output_shape", "mr_exec_describe", "mr_exec_launch_count",
-    "mr_exec_profile", "mr_exec_destroy", "mr_last_error_message", "mr_build_info",
+    "mr_exec_profile", "mr_exec_destroy", "mr_last_error_message", "mr_module_lower", "mr_build_info",
 ]
 
 
@@ -81,6 +81,8 @@ def lib():
         L.mr_exec_destroy.argtypes = [ctypes.c_void_p]
         L.mr_last_error_message.restype = ctypes.c_char_p
         L.mr_build_info.restype = ctypes.c_char_p
+        L.mr_module_lower.argtypes = [ctypes.c_char_p, ctypes.c_int64, ctypes.c_int32,
+                                      ctypes.POINTER(ctypes.c_char_p)]
         _lib = L
     return _lib
 
@@ -99,6 +101,15 @@ def _tensor(ptr: int, shape: Sequence[int]) -> Tensor:
     t.type_code = MR_FLOAT
     t.bits = 32
     return t
+
+
+def lower(fused_text: str, batch: int = 1, n_data_inputs: int = 1) -> dict:
+    """Host-only parse + lowering of a fused module (no device needed):
+    the group list mr_exec_create would compile, or BackendError with the
+    same status (MR_ERR_SYNTAX = 6, MR_ERR_UNSUPPORTED_GROUP = 100 ...)."""
+    out = ctypes.c_char_p()
+    _check(lib().mr_module_lower(fused_text.encode(), int(batch), int(n_data_inputs), ctypes.byref(out)))
+    return json.loads(out.value.decode())
 
 
 class Executor:

@@ -1002,6 +1002,28 @@ void prepare_weights(Exec& ex, cudaStream_t s) {
   }
 }
 
+std::string program_json(const Program& P) {
+  static const char* kinds[] = {"conv2d", "dense", "max_pool2d", "depthwise_conv2d"};
+  std::ostringstream os;
+  os << "{\"int8\": " << (P.any_quant ? "true" : "false") << ", \"n_params\": " << P.n_params
+     << ", \"result_shape\": " << dims_str(P.values[P.result_value].shape) << ", \"groups\": [";
+  for (size_t gi = 0; gi < P.groups.size(); ++gi) {
+    const GroupDesc& g = P.groups[gi];
+    std::string d = describe_group(P, g);
+    std::string esc;
+    for (char c : d) esc += (c == '"' ? '\'' : c);
+    os << (gi ? ", " : "") << "{\"name\": \"" << g.name << "\", \"anchor\": \"" << kinds[static_cast<int>(g.kind)]
+       << "\", \"desc\": \"" << esc << "\", \"data_quant\": " << (g.data.quant ? "true" : "false")
+       << ", \"weight_quant\": " << (g.weight.quant ? "true" : "false") << ", \"kernel\": ["
+       << g.kh << ", " << g.kw << "], \"strides\": [" << g.sh << ", " << g.sw << "], \"padding\": [" << g.ph << ", "
+       << g.pw << "], \"epilogue\": [";
+    for (size_t i = 0; i < g.epi.size(); ++i) os << (i ? ", " : "") << static_cast<int>(g.epi[i].kind);
+    os << "], \"in_shape\": " << dims_str(g.in_shape) << ", \"out_shape\": " << dims_str(g.out_shape) << "}";
+  }
+  os << "]}";
+  return os.str();
+}
+
 void make_describe(Exec& ex) {
   std::ostringstream os;
   const Program& P = ex.P;
@@ -1270,6 +1292,18 @@ int32_t mr_exec_profile(mr_exec_t h, const mr_tensor* inputs, mr_tensor* output,
 void mr_exec_destroy(mr_exec_t h) { delete reinterpret_cast<Exec*>(h); }
 
 const char* mr_last_error_message(void) { return g_last_error.c_str(); }
+
+mr_status mr_module_lower(const char* text, int64_t batch, int32_t n_data_inputs, const char** json) {
+  static thread_local std::string out;
+  API_BEGIN
+  if (!text || !json) fail(MR_ERR_INVALID_ARGUMENT, "null argument");
+  if (batch < 1) fail(MR_ERR_INVALID_ARGUMENT, "batch must be >= 1");
+  Module m = parse_fused_module(text);
+  Program P = lower_module(m, batch, n_data_inputs);
+  out = program_json(P);
+  *json = out.c_str();
+  API_END
+}
 
 const char* mr_build_info(void) { return MRB200_BUILD_INFO; }
 
