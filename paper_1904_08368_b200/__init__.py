@@ -22,7 +22,7 @@ from typing import Dict, List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libmrb200.so")
+LIB_PATH = os.environ.get("MRB200_LIB") or os.path.join(_HERE, "_lib", "libmrb200.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "mrb200.h")
 
 MR_FLOAT_BF16 = 0

@@ -105,6 +105,9 @@ struct TcArgs {
   // pooled row is written instead of the conv output
   int32_t pool, pkh, pkw, psh, psw, pph, ppw, poh, pow, band, stage_stride, relu_last;
   float acc_scale;
+  FastDiv fd_wg, fd_hg;    // M-grid decode (pixel -> n, y, x)
+  FastDiv fd_swp, fd_shp;  // side output PHASE decode (padded grid)
+  FastDiv fd_pow;          // fused pool: item -> (granule, pooled column)
   int32_t dbg;  // MRB200_TC_DBG (timing experiments only): 1 skip epilogue math, 2 hoisted descriptors, 4 no MMAs,
                 //   16 CTA-0 timestamps of the fused-pool epilogue
   unsigned long long* stamps;
@@ -135,10 +138,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "{\n"
       ".reg .pred p;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(0x989680u)  // suspend-time hint: the warp sleeps until the phase flips
       : "memory");
 }
 
@@ -245,7 +248,8 @@ struct RowDst {
 // Byte offset of the 16-byte granule holding channel c (chunk-plane stride
 // `pstride` and base `cbase` in chunk units, so PHASE sub-grids fit too).
 __device__ __forceinline__ int64_t gran_byte(const Lay& L, int64_t cbase, int64_t pstride, int c) {
-  return ((c / L.cpc) * pstride + cbase) * L.kb + static_cast<int64_t>(c % L.cpc) * (L.kb / L.cpc);
+  const int lg = lay_lg(L);
+  return ((c >> lg) * pstride + cbase) * L.kb + static_cast<int64_t>(c & (L.cpc - 1)) * (L.kb >> lg);
 }
 
 __device__ __forceinline__ void st16(void* base, int64_t byte, uint4 v) {
@@ -649,7 +653,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         const OutDev& o = a.out;
         const int granules = a.bn / 4;
         for (int it = threadIdx.x - 64; it < ((a.dbg & 1) ? 0 : a.pow * granules); it += kEpiWarps * 32) {
-          const int g4 = it / a.pow, pw = it - g4 * a.pow;  // pixel-fastest: coalesced stores
+          const int g4 = static_cast<int>(fdiv(static_cast<uint32_t>(it), a.fd_pow)), pw = it - g4 * a.pow;  // pixel-fastest: coalesced stores
           const int c0 = g4 * 4;
           const int x0 = pw * a.psw - a.ppw;
           float mx[4] = {0.f, 0.f, 0.f, 0.f};
@@ -721,7 +725,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       int cur_sb = -1;
       RowDst d;
       bool valid = false;
-      for (int item = slice; item < a.sub * chunks; item += 4) {
+      // each warp of a lane quarter takes a contiguous run of items, so a
+      // sub-tile's row decode is done once per warp
+      const int n_items = a.sub * chunks, per = (n_items + 3) >> 2;
+      const int it_end = min(n_items, (slice + 1) * per);
+      for (int item = slice * per; item < it_end; ++item) {
         const int sb = item / chunks;
         const int c = (item - sb * chunks) * 16;
         if (sb != cur_sb) {
@@ -731,9 +739,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           d.border = false;
           d.pix = 0;
           if (valid) {
-            const uint32_t t = q / static_cast<uint32_t>(a.Wg);
+            const uint32_t t = fdiv(q, a.fd_wg);
             const int x = static_cast<int>(q - t * static_cast<uint32_t>(a.Wg));
-            const uint32_t n32 = t / static_cast<uint32_t>(a.Hg);
+            const uint32_t n32 = fdiv(t, a.fd_hg);
             const int y = static_cast<int>(t - n32 * static_cast<uint32_t>(a.Hg));
             const int n = static_cast<int>(n32);
             if (a.out_mode == OUT_SAME) {
@@ -746,9 +754,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             if (a.out.side) {
               if (sl.kind == LAY_PHASE) {
                 const uint32_t p32 = static_cast<uint32_t>(d.pix);
-                const uint32_t tt = p32 / static_cast<uint32_t>(sl.Wp);
+                const uint32_t tt = fdiv(p32, a.fd_swp);
                 const int wp = static_cast<int>(p32 - tt * static_cast<uint32_t>(sl.Wp));
-                const uint32_t nn = tt / static_cast<uint32_t>(sl.Hp);
+                const uint32_t nn = fdiv(tt, a.fd_shp);
                 const int hp = static_cast<int>(tt - nn * static_cast<uint32_t>(sl.Hp));
                 d.side_base = static_cast<int64_t>((hp & 1) * 2 + (wp & 1)) * sl.Pp +
                               (static_cast<int64_t>(nn) * sl.Hq + hp / 2) * sl.Wq + wp / 2;
@@ -897,6 +905,8 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
   }
   a.kb = kb;
   a.Pg = static_cast<int64_t>(a.N) * a.Hg * a.Wg;
+  a.fd_wg = make_fastdiv(static_cast<uint32_t>(a.Wg));
+  a.fd_hg = make_fastdiv(static_cast<uint32_t>(a.Hg));
   if (a.Pg + kTileM >= (int64_t(1) << 31)) return false;
   int dmin = 1 << 30, dmax = -(1 << 30);
   for (const Tap& t : taps) {
@@ -999,6 +1009,7 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
     a.ppw = sp.ppw;
     a.poh = sp.poh;
     a.pow = sp.pow;
+    a.fd_pow = make_fastdiv(static_cast<uint32_t>(sp.pow));
     a.band = sp.pkh;
     const int sub = (a.band * a.Wg + kTileM - 1) / kTileM;
     a.stage_stride = (sub * kTileM + 1) | 1;  // float4 elements per granule plane (odd: spread banks)
@@ -1198,6 +1209,10 @@ bool tc_conv_launch(TcConvPlan* p, const void* x, const Lay& xl, const void* w, 
   a.stamps = stamps;
   a.epi = epi;
   a.out = out;
+  if (out.side && out.slay.kind == LAY_PHASE) {
+    a.fd_swp = make_fastdiv(static_cast<uint32_t>(out.slay.Wp));
+    a.fd_shp = make_fastdiv(static_cast<uint32_t>(out.slay.Hp));
+  }
   const int sig = epi_signature(epi, out);
 #define MRB_TC_LAUNCH(EB_, SIG_)                                                                          \
   do {                                                                                                    \

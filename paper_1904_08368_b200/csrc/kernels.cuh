@@ -82,7 +82,29 @@ struct OutDev {
   QDev side_q;
 };
 
+// Division by a launch-constant divisor d for dividends n < 2^31 as a
+// multiply-high and a shift (round-up magic number: s = ceil(log2 d),
+// m = ceil(2^(31+s) / d) < 2^32; exact for every n < 2^31).
+struct FastDiv {
+  uint32_t d, m;
+  int32_t s;  // -1: d == 1
+};
+
+inline FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f{d, 0u, -1};
+  if (d <= 1) return f;
+  int s = 0;
+  while ((1ull << s) < d) ++s;
+  f.s = s;
+  f.m = static_cast<uint32_t>(((1ull << (31 + s)) + d - 1) / d);
+  return f;
+}
+
 #ifdef __CUDACC__
+
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
+  return f.s < 0 ? n : (__umulhi(n, f.m) >> (f.s - 1));
+}
 
 __device__ __forceinline__ float bf16_to_f32(uint16_t h) { return __uint_as_float(static_cast<uint32_t>(h) << 16); }
 
@@ -118,10 +140,20 @@ __device__ __forceinline__ int32_t quant_code(float v, const QDev& q) {
   return cast_int_ref(t, q.is_signed);
 }
 
+// log2(cpc): chunk widths are powers of two (kb in {16, 64, 128} bytes over
+// 1/2/4-byte elements), so channel -> (plane, lane) is a shift and a mask.
+__host__ __device__ __forceinline__ int32_t lay_lg(const Lay& L) {
+#ifdef __CUDA_ARCH__
+  return 31 - __clz(L.cpc);
+#else
+  return __builtin_ctz(static_cast<unsigned>(L.cpc));
+#endif
+}
+
 // Chunk index (16-byte units) of the chunk holding channel c of the padded
 // pixel pix (NORMAL-grid linear index) in layout L.
 __host__ __device__ __forceinline__ int64_t lay_chunk(const Lay& L, int64_t pix, int32_t c) {
-  const int64_t plane = c / L.cpc;
+  const int64_t plane = c >> lay_lg(L);
   if (L.kind == LAY_PHASE) {
     int32_t wp = static_cast<int32_t>(pix % L.Wp);
     int64_t t = pix / L.Wp;
@@ -135,12 +167,12 @@ __host__ __device__ __forceinline__ int64_t lay_chunk(const Lay& L, int64_t pix,
 
 __host__ __device__ __forceinline__ int64_t lay_off(const Lay& L, int64_t pix, int32_t c) {
   if (L.cpc == 0) return pix * L.C + c;
-  return lay_chunk(L, pix, c) * L.cpc + (c % L.cpc);
+  return lay_chunk(L, pix, c) * L.cpc + (c & (L.cpc - 1));
 }
 
 // Byte offset of channel c (c % (16 / eb) == 0 for a 16-byte granule).
 __host__ __device__ __forceinline__ int64_t lay_byte(const Lay& L, int64_t pix, int32_t c) {
-  return lay_chunk(L, pix, c) * L.kb + static_cast<int64_t>(c % L.cpc) * (L.kb / L.cpc);
+  return lay_chunk(L, pix, c) * L.kb + static_cast<int64_t>(c & (L.cpc - 1)) * (L.kb >> lay_lg(L));
 }
 
 // quant_code when the clip bounds lie inside int32 (every realize site:
