@@ -171,25 +171,43 @@ def time_ours(precision, batch, steps, warmup, rank, world, local):
     ms_step = ms / steps
     value = batch * world * steps / (ms / 1e3)
 
-    # e2e through the public API from pinned host memory (H2D + run + D2H per step)
+    # e2e through the public API from pinned host memory: every step uploads its
+    # input (H2D), runs, and reads back its logits (D2H).  Streaming form
+    # (mr_exec_submit_host): step i+1's upload overlaps step i's kernels.
     x_pin = torch.from_numpy(x_host).pin_memory()
     y_pin = torch.empty(ex.output_shape, dtype=torch.float32).pin_memory()
     xn, yn = x_pin.numpy(), y_pin.numpy()
     for _ in range(max(1, warmup)):
-        ex.run_host_into(xn, yn, sh)
+        ex.submit_host(xn, yn, sh)
+    ex.sync()
     torch.cuda.synchronize()
     barrier(world)
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
     e2.record(stream)
     for _ in range(steps):
-        ex.run_host_into(xn, yn, sh)
+        ex.submit_host(xn, yn, sh)
     e3.record(stream)
+    ex.sync()
     torch.cuda.synchronize()
+    wall_e2e = time.perf_counter() - t0
     barrier(world)
     ms_e2e = max_over_ranks(e2.elapsed_time(e3), world)
+    # the same through the blocking call (H2D, run, D2H, synchronize per step)
+    e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    nsync = max(1, steps // 4)
+    e4.record(stream)
+    for _ in range(nsync):
+        ex.run_host_into(xn, yn, sh)
+    e5.record(stream)
+    torch.cuda.synchronize()
+    ms_sync = max_over_ranks(e4.elapsed_time(e5), world)
     e2e = {"value": batch * world * steps / (ms_e2e / 1e3), "unit": UNIT,
            "h2d_bytes_per_step": int(x_host.nbytes), "d2h_bytes_per_step": int(np.prod(ex.output_shape) * 4),
-           "ms_per_step": ms_e2e / steps}
+           "ms_per_step": ms_e2e / steps, "api": "mr_exec_submit_host x K + mr_exec_sync (pinned host buffers)",
+           "wall_ms_per_step": 1e3 * wall_e2e / steps,
+           "blocking_call": {"value": batch * world * nsync / (ms_sync / 1e3), "ms_per_step": ms_sync / nsync,
+                             "api": "mr_exec_run_host per step"}}
 
     # per-launch device times (CUDA events between launches on the same stream)
     desc = ex.describe()

@@ -122,6 +122,18 @@ mr_status mr_exec_run_host(mr_exec_t ex, const mr_tensor* inputs, mr_tensor* out
                            void* stream);
 
 /* Shape of @main's result at the bound batch. */
+/* Asynchronous end-to-end call for streaming inference: enqueues the H2D copy
+ * of inputs[0] (HOST float32, pinned for true asynchrony) into one of two
+ * device stages on an internal copy stream, the run on `stream` once that
+ * copy lands, and the D2H of the result into output->data (HOST) on `stream`,
+ * then returns without waiting.  Consecutive submissions pipeline: batch
+ * i+1's upload overlaps batch i's kernels.  Host buffers must stay untouched
+ * until mr_exec_sync returns.  Results are identical to mr_exec_run_host. */
+mr_status mr_exec_submit_host(mr_exec_t ex, const mr_tensor* inputs, mr_tensor* output, void* stream);
+
+/* Waits for every mr_exec_submit_host issued since the last sync. */
+mr_status mr_exec_sync(mr_exec_t ex);
+
 mr_status mr_exec_output_shape(mr_exec_t ex, mr_tensor* shape_only);
 
 /* JSON description of the lowered program: groups, kernels, formats, arena

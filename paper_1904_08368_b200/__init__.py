@@ -32,7 +32,7 @@ MR_FLOAT = 2
 # every symbol include/mrb200.h declares
 EXPORTS = [
     "mr_exec_default_options", "mr_exec_create", "mr_exec_set_weights", "mr_exec_run",
-    "mr_exec_run_host", "mr_exec_output_shape", "mr_exec_describe", "mr_exec_launch_count",
+    "mr_exec_run_host", "mr_exec_submit_host", "mr_exec_sync", "mr_exec_output_shape", "mr_exec_describe", "mr_exec_launch_count",
     "mr_exec_profile", "mr_exec_destroy", "mr_last_error_message", "mr_module_lower", "mr_build_info",
 ]
 
@@ -70,6 +70,9 @@ def lib():
         L.mr_exec_run.argtypes = [ctypes.c_void_p, ctypes.POINTER(Tensor), ctypes.POINTER(Tensor), ctypes.c_void_p]
         L.mr_exec_run_host.argtypes = [ctypes.c_void_p, ctypes.POINTER(Tensor), ctypes.POINTER(Tensor),
                                        ctypes.c_void_p]
+        L.mr_exec_submit_host.argtypes = [ctypes.c_void_p, ctypes.POINTER(Tensor), ctypes.POINTER(Tensor),
+                                          ctypes.c_void_p]
+        L.mr_exec_sync.argtypes = [ctypes.c_void_p]
         L.mr_exec_output_shape.argtypes = [ctypes.c_void_p, ctypes.POINTER(Tensor)]
         L.mr_exec_describe.argtypes = [ctypes.c_void_p]
         L.mr_exec_describe.restype = ctypes.c_char_p
@@ -177,6 +180,17 @@ class Executor:
         tout = _tensor(out.ctypes.data, out.shape)
         _check(lib().mr_exec_run_host(self._h, ctypes.byref(tin), ctypes.byref(tout), ctypes.c_void_p(stream)))
         return out
+
+    def submit_host(self, x: np.ndarray, out: np.ndarray, stream: int = 0) -> None:
+        """Asynchronous end to end (mr_exec_submit_host): H2D of x (pinned for
+        overlap) on an internal copy stream, run, D2H into out; no wait.
+        Keep x and out alive and untouched until sync()."""
+        tin = _tensor(x.ctypes.data, x.shape)
+        tout = _tensor(out.ctypes.data, out.shape)
+        _check(lib().mr_exec_submit_host(self._h, ctypes.byref(tin), ctypes.byref(tout), ctypes.c_void_p(stream)))
+
+    def sync(self) -> None:
+        _check(lib().mr_exec_sync(self._h))
 
     def profile_device(self, x_ptr: int, x_shape: Sequence[int], out_ptr: int, stream: int = 0) -> List[float]:
         tin = _tensor(x_ptr, x_shape)

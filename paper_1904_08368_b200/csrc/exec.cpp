@@ -108,12 +108,25 @@ struct Exec {
   bool weights_ready = false;
   // io
   const float* cur_input = nullptr;
-  const float* graph_input = nullptr;
   float* out_internal = nullptr;  // result buffer (NCHW float32)
   int64_t out_elems = 0;
   std::vector<int64_t> out_shape;
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t graph_exec = nullptr;
+  // captured launch lists, one per input buffer address (the input pointer is
+  // baked into the graph): the caller's buffer and the two pipeline stages
+  struct GraphEnt {
+    const float* in;
+    cudaGraph_t g;
+    cudaGraphExec_t e;
+  };
+  std::vector<GraphEnt> graphs;
+  // asynchronous host pipeline (mr_exec_submit_host): double-buffered input
+  // stages filled on copy_stream while the previous batch computes
+  cudaStream_t copy_stream = nullptr;
+  float* stage[2] = {nullptr, nullptr};
+  cudaEvent_t loaded[2] = {nullptr, nullptr}, consumed[2] = {nullptr, nullptr}, fresh = nullptr;
+  int64_t submitted = 0;
+  bool pipe_fresh = true;
+  cudaStream_t pipe_stream = nullptr;
   float* host_stage_in = nullptr;
   float* host_stage_out = nullptr;
   float* dev_in = nullptr;
@@ -121,9 +134,26 @@ struct Exec {
   std::string describe;
   std::vector<TcConvPlan*> tc_plans;
 
+  void drop_graphs() {
+    for (auto& g : graphs) {
+      cudaGraphExecDestroy(g.e);
+      cudaGraphDestroy(g.g);
+    }
+    graphs.clear();
+  }
+
   ~Exec() {
-    if (graph_exec) cudaGraphExecDestroy(graph_exec);
-    if (graph) cudaGraphDestroy(graph);
+    drop_graphs();
+    if (copy_stream) {
+      cudaStreamSynchronize(copy_stream);
+      cudaStreamDestroy(copy_stream);
+    }
+    for (int i = 0; i < 2; ++i) {
+      if (stage[i]) cudaFree(stage[i]);
+      if (loaded[i]) cudaEventDestroy(loaded[i]);
+      if (consumed[i]) cudaEventDestroy(consumed[i]);
+    }
+    if (fresh) cudaEventDestroy(fresh);
     for (auto* p : tc_plans) tc_conv_destroy(p);
     if (arena) cudaFree(arena);
     for (void* p : param_dev) if (p) cudaFree(p);
@@ -1059,26 +1089,34 @@ void run_launches(Exec& ex, cudaStream_t s) {
   for (auto& L : ex.launches) L.fn(s);
 }
 
-void ensure_graph(Exec& ex, cudaStream_t s) {
-  if (ex.graph_exec && ex.graph_input == ex.cur_input) return;
-  if (ex.graph_exec) {
-    cudaGraphExecDestroy(ex.graph_exec);
-    ex.graph_exec = nullptr;
-  }
-  if (ex.graph) {
-    cudaGraphDestroy(ex.graph);
-    ex.graph = nullptr;
+cudaGraphExec_t ensure_graph(Exec& ex) {
+  for (auto& g : ex.graphs)
+    if (g.in == ex.cur_input) return g.e;
+  if (ex.graphs.size() >= 4) {  // bounded cache: drop the oldest capture
+    cudaGraphExecDestroy(ex.graphs.front().e);
+    cudaGraphDestroy(ex.graphs.front().g);
+    ex.graphs.erase(ex.graphs.begin());
   }
   cudaStream_t cap = nullptr;
   CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
   CK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
   run_launches(ex, cap);
-  cudaError_t ce = cudaStreamEndCapture(cap, &ex.graph);
+  Exec::GraphEnt ent{ex.cur_input, nullptr, nullptr};
+  cudaError_t ce = cudaStreamEndCapture(cap, &ent.g);
   cudaStreamDestroy(cap);
   if (ce != cudaSuccess) fail(MR_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
-  CK(cudaGraphInstantiate(&ex.graph_exec, ex.graph, 0));
-  ex.graph_input = ex.cur_input;
-  (void)s;
+  CK(cudaGraphInstantiate(&ent.e, ent.g, 0));
+  ex.graphs.push_back(ent);
+  return ent.e;
+}
+
+void run_body(Exec& ex, cudaStream_t s) {
+  if (ex.opt.use_cuda_graph) {
+    CK(cudaGraphLaunch(ensure_graph(ex), s));
+  } else {
+    run_launches(ex, s);
+    CK(cudaGetLastError());
+  }
 }
 
 int64_t numel(const mr_tensor& t) {
@@ -1186,10 +1224,7 @@ mr_status mr_exec_set_weights(mr_exec_t h, int32_t n, const mr_tensor* w) {
   prepare_weights(ex, nullptr);
   CK(cudaDeviceSynchronize());
   ex.weights_ready = true;
-  if (ex.graph_exec) {  // weights live at fixed addresses only after the first set
-    cudaGraphExecDestroy(ex.graph_exec);
-    ex.graph_exec = nullptr;
-  }
+  ex.drop_graphs();  // weights live at fixed addresses only after the first set
   make_describe(ex);
   API_END
 }
@@ -1203,13 +1238,7 @@ mr_status mr_exec_run(mr_exec_t h, const mr_tensor* inputs, mr_tensor* output, v
   if (numel(*output) != ex.out_elems) fail(MR_ERR_TYPE_MISMATCH, "output size mismatch");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   ex.cur_input = static_cast<const float*>(inputs[0].data);
-  if (ex.opt.use_cuda_graph) {
-    ensure_graph(ex, s);
-    CK(cudaGraphLaunch(ex.graph_exec, s));
-  } else {
-    run_launches(ex, s);
-    CK(cudaGetLastError());
-  }
+  run_body(ex, s);
   CK(cudaMemcpyAsync(output->data, ex.out_internal, static_cast<size_t>(ex.out_elems) * 4, cudaMemcpyDeviceToDevice, s));
   API_END
 }
@@ -1230,15 +1259,61 @@ mr_status mr_exec_run_host(mr_exec_t h, const mr_tensor* inputs, mr_tensor* outp
   CK(cudaMemcpyAsync(ex.dev_in, inputs[0].data, static_cast<size_t>(n_in) * 4, cudaMemcpyHostToDevice, s));
   ex.cur_input = ex.dev_in;
   if (!ex.weights_ready) fail(MR_ERR_INVALID_ARGUMENT, "mr_exec_set_weights first");
-  if (ex.opt.use_cuda_graph) {
-    ensure_graph(ex, s);
-    CK(cudaGraphLaunch(ex.graph_exec, s));
-  } else {
-    run_launches(ex, s);
-    CK(cudaGetLastError());
-  }
+  run_body(ex, s);
   CK(cudaMemcpyAsync(output->data, ex.out_internal, static_cast<size_t>(ex.out_elems) * 4, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  API_END
+}
+
+mr_status mr_exec_submit_host(mr_exec_t h, const mr_tensor* inputs, mr_tensor* output, void* stream) {
+  API_BEGIN
+  Exec& ex = *reinterpret_cast<Exec*>(h);
+  if (!ex.weights_ready) fail(MR_ERR_INVALID_ARGUMENT, "mr_exec_set_weights first");
+  check_input(ex, inputs);
+  if (!output || !output->data) fail(MR_ERR_INVALID_ARGUMENT, "null output");
+  if (numel(*output) != ex.out_elems) fail(MR_ERR_TYPE_MISMATCH, "output size mismatch");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (!ex.pipe_fresh && s != ex.pipe_stream) fail(MR_ERR_INVALID_ARGUMENT, "mr_exec_sync before switching streams");
+  const int64_t n_in = numel(inputs[0]);
+  if (!ex.copy_stream) {
+    CK(cudaStreamCreateWithFlags(&ex.copy_stream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaMalloc(&ex.stage[i], static_cast<size_t>(n_in) * 4));
+      CK(cudaEventCreateWithFlags(&ex.loaded[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ex.consumed[i], cudaEventDisableTiming));
+    }
+    CK(cudaEventCreateWithFlags(&ex.fresh, cudaEventDisableTiming));
+  }
+  const int b = static_cast<int>(ex.submitted & 1);
+  if (ex.pipe_fresh) {
+    // the first upload after a sync is ordered after the work already on `stream`
+    CK(cudaEventRecord(ex.fresh, s));
+    CK(cudaStreamWaitEvent(ex.copy_stream, ex.fresh, 0));
+    ex.pipe_fresh = false;
+    ex.pipe_stream = s;
+  }
+  if (ex.submitted >= 2) CK(cudaStreamWaitEvent(ex.copy_stream, ex.consumed[b], 0));  // stage b's last reader done
+  CK(cudaMemcpyAsync(ex.stage[b], inputs[0].data, static_cast<size_t>(n_in) * 4, cudaMemcpyHostToDevice,
+                     ex.copy_stream));
+  CK(cudaEventRecord(ex.loaded[b], ex.copy_stream));
+  CK(cudaStreamWaitEvent(s, ex.loaded[b], 0));
+  ex.cur_input = ex.stage[b];
+  run_body(ex, s);
+  CK(cudaEventRecord(ex.consumed[b], s));
+  CK(cudaMemcpyAsync(output->data, ex.out_internal, static_cast<size_t>(ex.out_elems) * 4, cudaMemcpyDeviceToHost, s));
+  ++ex.submitted;
+  API_END
+}
+
+mr_status mr_exec_sync(mr_exec_t h) {
+  API_BEGIN
+  Exec& ex = *reinterpret_cast<Exec*>(h);
+  if (!ex.pipe_fresh) {  // (the stream may be the legacy default stream, handle 0)
+    if (ex.copy_stream) CK(cudaStreamSynchronize(ex.copy_stream));
+    CK(cudaStreamSynchronize(ex.pipe_stream));
+  }
+  ex.pipe_fresh = true;
+  ex.pipe_stream = nullptr;
   API_END
 }
 

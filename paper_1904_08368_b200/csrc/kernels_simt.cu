@@ -115,88 +115,99 @@ __global__ void k_input_convert(const float* __restrict__ x, int N, int C, int H
 }
 
 // ---- boundary for the stem: NCHW float32 -> LAY_S2D -------------------------------
-// One block per (image n, s2d row si).  The s2d row reads input rows
-// y = 2*si + {0, 1} - pad of every channel: the block stages those 2*C rows in
-// shared memory with coalesced loads (each input row is read exactly once over
-// the grid), then each thread emits whole s2d pixels (contiguous 16-byte
-// granules).  Channel sc = (py*2 + px)*C + c of s2d pixel (si, sj) holds
+// Persistent: each block walks s2d rows (n, si) with stride gridDim.x.  An s2d
+// row reads input rows y = 2*si + {0, 1} - pad of every channel; the block
+// stages those 2*C rows in shared memory with cp.async (16-byte, zero-filled
+// outside the image), prefetching the next row into the other buffer while
+// it emits the current one as whole s2d pixels (contiguous 16-byte granules).
+// Channel sc = (py*2 + px)*C + c of s2d pixel (si, sj) holds
 // x[n][c][2si+py-pad][2sj+px-pad], zero outside the image (padded taps).
-__global__ void k_input_s2d(const float* __restrict__ x, int C, int H, int W, void* out, int fmt, Lay L, int pad,
-                            float pre_mul, QDev q) {
-  extern __shared__ float rows[];  // [C][2][W]
-  const int si = blockIdx.x % L.Hq;
-  const int n = blockIdx.x / L.Hq;
-  const int y0 = 2 * si - pad;
-  // all of a thread's row loads are issued before any is consumed (memory-level
-  // parallelism); W % 4 == 0 is checked by the launcher
+__device__ __forceinline__ void s2d_prefetch(float* buf, const float* __restrict__ x, int n, int si, int C, int H,
+                                             int W, int pad) {
   const int W4 = W >> 2, total4 = 2 * C * W4;
-  for (int base = 0; base < total4; base += 4 * blockDim.x) {
-    float4 v[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int i = base + k * blockDim.x + threadIdx.x;
-      v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (i < total4) {
-        const int cr = i / W4, x4 = i - cr * W4, y = y0 + (cr & 1), c = cr >> 1;
-        if (y >= 0 && y < H) v[k] = __ldg(reinterpret_cast<const float4*>(x + ((static_cast<int64_t>(n) * C + c) * H + y) * W) + x4);
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int i = base + k * blockDim.x + threadIdx.x;
-      if (i < total4) {
-        float4 t = v[k];
-        if (pre_mul != 0.f) {  // only in-image values are scaled; padding stays +0
-          const int y = y0 + ((i / W4) & 1);
-          if (y >= 0 && y < H) t = make_float4(__fmul_rn(t.x, pre_mul), __fmul_rn(t.y, pre_mul), __fmul_rn(t.z, pre_mul), __fmul_rn(t.w, pre_mul));
-        }
-        reinterpret_cast<float4*>(rows)[i] = t;
-      }
-    }
+  for (int i = threadIdx.x; i < total4; i += blockDim.x) {
+    const int cr = i / W4, x4 = i - cr * W4, y = 2 * si - pad + (cr & 1), c = cr >> 1;
+    const bool in = y >= 0 && y < H;
+    const float* src = x + ((static_cast<int64_t>(n) * C + c) * H + (in ? y : 0)) * W + 4 * x4;
+    const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(buf + 4 * i));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(in ? 16 : 0) : "memory");
   }
-  __syncthreads();
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(128) k_input_s2d(const float* __restrict__ x, int N, int C, int H, int W, void* out,
+                                                   int fmt, Lay L, int pad, float pre_mul, QDev q) {
+  extern __shared__ __align__(16) float rows[];  // 2 x [C][2][W]
+  const int stride = 2 * C * W;
+  const int n_rows = N * L.Hq;
   const int eb = L.kb >> lay_lg(L);
   const int gpc = L.kb / 16, cpg = 16 / eb;
   const int planes = (4 * C + L.cpc - 1) / L.cpc;
-  const bool row_ok[2] = {y0 >= 0 && y0 < H, y0 + 1 >= 0 && y0 + 1 < H};
-  for (int sj = threadIdx.x; sj < L.Wq; sj += blockDim.x) {
-    const int64_t pix = (static_cast<int64_t>(n) * L.Hq + si) * L.Wq + sj;
+  const bool fast_q = q.lo > -2147483648.f && q.hi < 2147483648.f;  // realize clips: [-128, 127] / [0, 255]
+  // per granule channel (pl, gr, k): staged row offset, column shift, row parity, liveness
+  __shared__ int2 ktab[64];
+  for (int i = threadIdx.x; i < planes * gpc * 16 && i < 64; i += blockDim.x) {
+    const int k = i & 15, pg = i >> 4;
+    const int sc = (pg / gpc) * L.cpc + (pg % gpc) * cpg + k;
+    const int ph = sc / C, c = sc - ph * C, r = (ph >> 1) & 1;
+    const bool ok = k < cpg && sc < 4 * C;
+    ktab[i] = make_int2((c * 2 + r) * W, (((ph & 1) - pad + 64) << 2) | (r << 1) | (ok ? 1 : 0));
+  }
+  if (blockIdx.x < n_rows) s2d_prefetch(rows, x, blockIdx.x / L.Hq, blockIdx.x % L.Hq, C, H, W, pad);
+  int it = 0;
+  for (int row = blockIdx.x; row < n_rows; row += gridDim.x, ++it) {
+    const int n = row / L.Hq, si = row - n * L.Hq;
+    const int nxt = row + gridDim.x;
+    if (nxt < n_rows) {
+      s2d_prefetch(rows + ((it + 1) & 1) * stride, x, nxt / L.Hq, nxt % L.Hq, C, H, W, pad);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const float* cur = rows + (it & 1) * stride;
+    const int y0 = 2 * si - pad;
+    const bool row_ok0 = y0 >= 0 && y0 < H, row_ok1 = y0 + 1 >= 0 && y0 + 1 < H;
     for (int pl = 0; pl < planes; ++pl)
       for (int gr = 0; gr < gpc; ++gr) {
-        float v[16];
-        bool live[16];
+        for (int sj = threadIdx.x; sj < L.Wq; sj += blockDim.x) {
+          const int64_t pix = (static_cast<int64_t>(n) * L.Hq + si) * L.Wq + sj;
+          float v[16];
+          bool live[16];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          const int sc = pl * L.cpc + gr * cpg + k;
-          const int ph = sc / C, c = sc - ph * C;
-          const int r = (ph >> 1) & 1, xx = 2 * sj + (ph & 1) - pad;
-          live[k] = k < cpg && sc < 4 * C && row_ok[r] && xx >= 0 && xx < W;
-          v[k] = live[k] ? rows[(c * 2 + r) * W + xx] : 0.f;
-        }
-        char* dst = static_cast<char*>(out) + (pl * L.Pp + pix) * L.kb + gr * 16;
-        uint32_t w4[4];
-        if (fmt == FMT_F32) {
-          *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
-          continue;
-        } else if (fmt == FMT_BF16) {
-#pragma unroll
-          for (int h = 0; h < 4; ++h)
-            w4[h] = static_cast<uint32_t>(f32_to_bf16(v[2 * h])) | (static_cast<uint32_t>(f32_to_bf16(v[2 * h + 1])) << 16);
-        } else {
-#pragma unroll
-          for (int h = 0; h < 4; ++h) {
-            uint32_t u = 0;
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-              const int k = 4 * h + b;
-              const int32_t code = live[k] ? quant_code(v[k], q) : 0;
-              u |= (static_cast<uint32_t>(code) & 0xff) << (8 * b);
-            }
-            w4[h] = u;
+          for (int k = 0; k < 16; ++k) {
+            const int2 t = ktab[(pl * gpc + gr) * 16 + k];
+            const int xx = 2 * sj + (t.y >> 2) - 64;
+            live[k] = (t.y & 1) && ((t.y & 2) ? row_ok1 : row_ok0) && xx >= 0 && xx < W;
+            v[k] = live[k] ? cur[t.x + xx] : 0.f;
+            if (live[k] && pre_mul != 0.f) v[k] = __fmul_rn(v[k], pre_mul);
           }
+          char* dst = static_cast<char*>(out) + (pl * L.Pp + pix) * L.kb + gr * 16;
+          uint32_t w4[4];
+          if (fmt == FMT_F32) {
+            *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+            continue;
+          } else if (fmt == FMT_BF16) {
+#pragma unroll
+            for (int h = 0; h < 4; ++h)
+              w4[h] = static_cast<uint32_t>(f32_to_bf16(v[2 * h])) | (static_cast<uint32_t>(f32_to_bf16(v[2 * h + 1])) << 16);
+          } else {
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              uint32_t u = 0;
+#pragma unroll
+              for (int b = 0; b < 4; ++b) {
+                const int k = 4 * h + b;
+                const int32_t code = !live[k] ? 0 : fast_q ? quant_code_fast(v[k], q) : quant_code(v[k], q);
+                u |= (static_cast<uint32_t>(code) & 0xff) << (8 * b);
+              }
+              w4[h] = u;
+            }
+          }
+          *reinterpret_cast<uint4*>(dst) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
         }
-        *reinterpret_cast<uint4*>(dst) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
       }
+    __syncthreads();  // `cur` is refilled by the prefetch two rows ahead
   }
 }
 
@@ -729,9 +740,18 @@ unsigned grid_stride_blocks(int64_t total) {
 
 void launch_input_convert(const float* x, int N, int C, int H, int W, void* out, int fmt, const Lay& L,
                           int s2d_pad, float pre_mul, QDev q, cudaStream_t s) {
-  if (L.kind == LAY_S2D && 2 * C * W * 4 <= 48 * 1024 && W % 4 == 0 &&
+  const int s2d_planes = (4 * C + L.cpc - 1) / L.cpc;
+  if (L.kind == LAY_S2D && 2 * 2 * C * W * 4 <= 40 * 1024 && W % 4 == 0 && s2d_planes * (L.kb / 16) <= 4 &&
       reinterpret_cast<uintptr_t>(x) % 16 == 0) {
-    k_input_s2d<<<N * L.Hq, 128, 2 * C * W * sizeof(float), s>>>(x, C, H, W, out, fmt, L, s2d_pad, pre_mul, q);
+    static int sms = [] {
+      int d = 0, v = 0;
+      cudaGetDevice(&d);
+      cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+      return v > 0 ? v : 148;
+    }();
+    const int rows = N * L.Hq;
+    k_input_s2d<<<std::min(rows, sms * 8), 128, 2 * 2 * C * W * sizeof(float), s>>>(x, N, C, H, W, out, fmt, L,
+                                                                                  s2d_pad, pre_mul, q);
     return;
   }
   int planes = L.kind == LAY_S2D ? (4 * C + L.cpc - 1) / L.cpc : (C + L.cpc - 1) / L.cpc;

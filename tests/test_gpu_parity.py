@@ -85,3 +85,23 @@ def test_resnet18_bf16_full_size(gpu):
     y = ex.run_host(x)
     assert normwise(y, gold["fp32"]) <= BF16_TOL
     assert np.array_equal(np.argmax(y, 1), np.argmax(gold["fp32"], 1))
+
+
+@pytest.mark.gpu
+def test_submit_host_pipeline_matches_blocking(gpu):
+    """mr_exec_submit_host (double-buffered async H2D) returns exactly what the
+    blocking call returns, batch by batch, including across stage reuse."""
+    import torch
+    ex, src = setup("resnet18_tiny", "int8", 4)
+    gold = np.load(os.path.join(GOLD, "resnet18_tiny_b4.npz"))
+    xs = [modelzoo.make_inputs(src, 4, seed=s) for s in range(5)]
+    want = [ex.run_host(x) for x in xs]
+    assert np.array_equal(bits(want[0]), bits(gold["int8"]))
+    pins = [torch.from_numpy(x).pin_memory().numpy() for x in xs]
+    outs = [torch.empty(ex.output_shape, dtype=torch.float32).pin_memory().numpy() for _ in xs]
+    for _ in range(2):
+        for x, o in zip(pins, outs):
+            ex.submit_host(x, o)
+        ex.sync()
+        for o, w in zip(outs, want):
+            assert np.array_equal(bits(o), bits(w))
