@@ -208,6 +208,12 @@ __device__ __forceinline__ void umma_elect(uint32_t tmem_d, uint64_t adesc, uint
   }
 }
 
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\nselp.u32 %0, 1, 0, e;\n}\n" : "=r"(p));
+  return p != 0;
+}
+
 __device__ __forceinline__ void umma_commit_elect(uint64_t* bar) {
   asm volatile(
       "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
@@ -544,59 +550,58 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     }
   } else if (warp == 1) {
     // ===== MMA issuer =====
-    // The whole warp walks the loop (warp-uniform values); elect.sync inside
-    // the tcgen05.mma / commit asm picks the issuing lane.  A super-tile is
-    // `sub` 128-row M tiles that share every B descriptor: one stage wait,
-    // one accumulator wait and two commits per super-tile.
-    if (a.resident_b) mbar_wait(bfull, 0);
-    int stage = 0;
-    uint32_t phase = 0;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    const uint32_t smB_u = smem_u32(smB);
-    const uint32_t smA_u = smem_u32(smA);
-    const uint64_t hi = static_cast<uint64_t>(a.desc_hi) << 32;
-    const uint32_t sub_step16 = static_cast<uint32_t>(kTileM * a.kb) >> 4;  // 128 rows, in descriptor units
-    for (int mt = m_start; mt < a.m_tiles; mt += m_step) {
-      const int row0 = tile_row0(a, mt, msub);
-      const uint32_t shift16 = a.kb == 16 ? static_cast<uint32_t>(row0 - 8 * floor_div8(row0)) * 16 : 0u;
-      mbar_wait(&tempty[acc], acc_phase ^ 1);
-      tc_fence_after();
-      const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * a.sub * a.bn);
-      for (int ks = 0; ks < a.k_stages; ++ks) {
-        mbar_wait(&full[stage], phase);
+    // One elected thread walks the loop; every descriptor, TMEM address and
+    // step-table entry is warp-uniform, so it all lives in uniform registers
+    // (a handful of uniform adds per tcgen05.mma, no per-MMA loads).  A
+    // super-tile is `sub` 128-row M tiles sharing every B descriptor: one
+    // stage wait, one accumulator wait and two commits per super-tile.
+    if (elect_one()) {
+      if (a.resident_b) mbar_wait(bfull, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      const uint32_t smB_u = smem_u32(smB);
+      const uint32_t smA_u = smem_u32(smA);
+      const uint64_t hi = static_cast<uint64_t>(a.desc_hi) << 32;
+      const uint32_t idesc = a.idesc, bn = static_cast<uint32_t>(a.bn), sub = static_cast<uint32_t>(a.sub);
+      const uint32_t n_steps = static_cast<uint32_t>(a.n_steps);
+      const uint32_t sub_step16 = static_cast<uint32_t>(kTileM * a.kb) >> 4;  // 128 rows, in descriptor units
+      const bool no_mma = (a.dbg & 4) != 0;
+      for (int mt = m_start; mt < a.m_tiles; mt += m_step) {
+        const int row0 = tile_row0(a, mt, msub);
+        const uint32_t shift16 = a.kb == 16 ? static_cast<uint32_t>(row0 - 8 * floor_div8(row0)) * 16 : 0u;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t sA = smA_u + stage * a.a_stage_bytes + shift16;
-        const uint32_t sB = a.resident_b ? smB_u + ks * a.b_ks_stride : smB_u + stage * a.b_stage_bytes;
-        const uint32_t a16 = sA >> 4, b16 = sB >> 4;
-        if (a.dbg & 2) {
-          // timing experiment: same MMA count, one hoisted descriptor pair (wrong results)
-          const uint64_t bd = hi | (a.steps[0].b_lo + b16);
-          const uint64_t ad = hi | (a.steps[0].a_lo + a16);
-          const int n = a.n_steps * a.sub;
-#pragma unroll 1
-          for (int i = 0; i < n; ++i) umma_elect<EB>(tmem_d, ad, bd, a.idesc, (ks | i) != 0 ? 1u : 0u);
-        } else if (!(a.dbg & 4))
-        for (int st = 0; st < a.n_steps; ++st) {
-          const uint64_t bd = hi | (a.steps[st].b_lo + b16);
-          const uint32_t alo = a.steps[st].a_lo + a16;
-          const uint32_t accum = (ks | st) != 0 ? 1u : 0u;
-#pragma unroll 4
-          for (int sb = 0; sb < a.sub; ++sb)
-            umma_elect<EB>(tmem_d + static_cast<uint32_t>(sb * a.bn), hi | (alo + sb * sub_step16), bd, a.idesc, accum);
+        const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc) * sub * bn;
+        for (int ks = 0; ks < a.k_stages; ++ks) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sA = smA_u + stage * a.a_stage_bytes + shift16;
+          const uint32_t sB = a.resident_b ? smB_u + ks * a.b_ks_stride : smB_u + stage * a.b_stage_bytes;
+          const uint32_t a16 = sA >> 4, b16 = sB >> 4;
+          if (!no_mma)
+            for (uint32_t st = 0; st < n_steps; ++st) {
+              const uint64_t bd = hi | (a.steps[st].b_lo + b16);
+              const uint32_t alo = a.steps[st].a_lo + a16;
+              const uint32_t accum = (ks | st) != 0 ? 1u : 0u;
+              for (uint32_t sb = 0; sb < sub; ++sb)
+                umma<EB>(tmem_d + sb * bn, hi | (alo + sb * sub_step16), bd, idesc, accum);
+            }
+          umma_commit(&empty[stage]);  // frees the smem stage when these MMAs retire
+          if (++stage == a.n_stages) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
-        umma_commit_elect(&empty[stage]);  // frees the smem stage when these MMAs retire
-        if (++stage == a.n_stages) {
-          stage = 0;
-          phase ^= 1;
+        umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
         }
-      }
-      umma_commit_elect(&tfull[acc]);  // accumulator ready for the epilogue
-      if (++acc == 2) {
-        acc = 0;
-        acc_phase ^= 1;
       }
     }
+    __syncwarp();
   } else {
     // ===== epilogue warps =====
     // warp w (2..17): TMEM lane quarter w % 4 (hardware lane-access rule);

@@ -211,6 +211,93 @@ __global__ void __launch_bounds__(128) k_input_s2d(const float* __restrict__ x, 
   }
 }
 
+// Compile-time form of k_input_s2d for the common stem (C input channels,
+// padding PAD, CPC channels per 16-byte chunk: 16 int8 / 8 bf16): the channel
+// -> (row, column shift) map folds to constants and every tap is a branch-free
+// select, so the kernel stays memory-bound.  Same values as k_input_s2d.
+template <int C, int PAD, int CPC>
+__global__ void __launch_bounds__(128) k_input_s2d_ct(const float* __restrict__ x, int N, int H, int W, void* out,
+                                                      Lay L, float pre_mul, QDev q, FastDiv fd_w4) {
+  extern __shared__ __align__(16) float rows[];  // 2 x [C][2][W]
+  constexpr int PLANES = (4 * C + CPC - 1) / CPC;
+  const int stride = 2 * C * W;
+  const int n_rows = N * L.Hq;
+  const int W4 = W >> 2, total4 = 2 * C * W4;
+  const bool fast_q = q.lo > -2147483648.f && q.hi < 2147483648.f;
+  auto prefetch = [&](float* buf, int row) {
+    const int n = row / L.Hq, si = row - n * L.Hq;
+    for (int i = threadIdx.x; i < total4; i += blockDim.x) {
+      const int cr = static_cast<int>(fdiv(static_cast<uint32_t>(i), fd_w4)), x4 = i - cr * W4;
+      const int y = 2 * si - PAD + (cr & 1), c = cr >> 1;
+      const bool in = y >= 0 && y < H;
+      const float* src = x + ((static_cast<int64_t>(n) * C + c) * H + (in ? y : 0)) * W + 4 * x4;
+      const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(buf + 4 * i));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(in ? 16 : 0) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (blockIdx.x < n_rows) prefetch(rows, blockIdx.x);
+  int it = 0;
+  for (int row = blockIdx.x; row < n_rows; row += gridDim.x, ++it) {
+    const int n = row / L.Hq, si = row - n * L.Hq;
+    if (row + gridDim.x < n_rows) {
+      prefetch(rows + ((it + 1) & 1) * stride, row + gridDim.x);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const float* cur = rows + (it & 1) * stride;
+    const int y0 = 2 * si - PAD;
+    const bool rok[2] = {y0 >= 0 && y0 < H, y0 + 1 >= 0 && y0 + 1 < H};
+    for (int sj = threadIdx.x; sj < L.Wq; sj += blockDim.x) {
+      const int64_t pix = (static_cast<int64_t>(n) * L.Hq + si) * L.Wq + sj;
+      const int xb = 2 * sj - PAD;  // column of phase px = 0
+      const bool cok[2] = {xb >= 0 && xb < W, xb + 1 >= 0 && xb + 1 < W};
+      const int xc[2] = {min(max(xb, 0), W - 1), min(max(xb + 1, 0), W - 1)};
+#pragma unroll
+      for (int pl = 0; pl < PLANES; ++pl) {
+        float v[CPC];
+        bool live[CPC];
+#pragma unroll
+        for (int k = 0; k < CPC; ++k) {
+          const int sc = pl * CPC + k;
+          if (sc < 4 * C) {
+            const int ph = sc / C, c = sc % C, r = ph >> 1, px = ph & 1;
+            live[k] = rok[r] && cok[px];
+            const float t = cur[(c * 2 + r) * W + xc[px]];
+            v[k] = live[k] ? (pre_mul != 0.f ? __fmul_rn(t, pre_mul) : t) : 0.f;
+          } else {
+            live[k] = false;
+            v[k] = 0.f;
+          }
+        }
+        char* dst = static_cast<char*>(out) + (pl * L.Pp + pix) * 16;
+        uint32_t w4[4];
+        if constexpr (CPC == 8) {
+#pragma unroll
+          for (int h = 0; h < 4; ++h)
+            w4[h] = static_cast<uint32_t>(f32_to_bf16(v[2 * h])) | (static_cast<uint32_t>(f32_to_bf16(v[2 * h + 1])) << 16);
+        } else {
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            uint32_t u = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              const int k = 4 * h + b;
+              const int32_t code = !live[k] ? 0 : fast_q ? quant_code_fast(v[k], q) : quant_code(v[k], q);
+              u |= (static_cast<uint32_t>(code) & 0xff) << (8 * b);
+            }
+            w4[h] = u;
+          }
+        }
+        *reinterpret_cast<uint4*>(dst) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // ---- P16 / row-major -> NCHW float32 (@main result) -------------------------------
 // fmt FMT_I8: realize codes, the value is code * c2 (exact).
 __global__ void k_to_nchw(const void* __restrict__ x, int fmt, Lay L, float c2, float* __restrict__ y, int N, int C,
@@ -750,6 +837,15 @@ void launch_input_convert(const float* x, int N, int C, int H, int W, void* out,
       return v > 0 ? v : 148;
     }();
     const int rows = N * L.Hq;
+    const size_t smem = 2 * 2 * C * W * sizeof(float);
+    if (C == 3 && s2d_pad == 3 && L.kb == 16 && (fmt == FMT_I8 || fmt == FMT_BF16)) {
+      const FastDiv fd = make_fastdiv(static_cast<uint32_t>(W / 4));
+      if (fmt == FMT_I8)
+        k_input_s2d_ct<3, 3, 16><<<std::min(rows, sms * 8), 128, smem, s>>>(x, N, H, W, out, L, pre_mul, q, fd);
+      else
+        k_input_s2d_ct<3, 3, 8><<<std::min(rows, sms * 8), 128, smem, s>>>(x, N, H, W, out, L, pre_mul, q, fd);
+      return;
+    }
     k_input_s2d<<<std::min(rows, sms * 8), 128, 2 * 2 * C * W * sizeof(float), s>>>(x, N, C, H, W, out, fmt, L,
                                                                                   s2d_pad, pre_mul, q);
     return;
