@@ -71,7 +71,7 @@ inline int epi_signature(const EpiDev& e, const OutDev& o) {
   return SIG_ANY;
 }
 
-constexpr int kMaxSteps = 64;
+constexpr int kMaxSteps = 80;
 
 // One tcgen05.mma of a tile's K loop: byte offsets (relative to the A stage
 // base + row shift, and to the B stage / resident base) and the leading byte
@@ -88,6 +88,11 @@ struct TcArgs {
   int32_t N, Hg, Wg;
   int64_t Pg;  // N*Hg*Wg
   int32_t m_tiles, n_tiles, bn, Cc, pps, k_stages, sub0, subs, hg;
+  int8_t region_sg[8];  // A stage region -> TMA sub-grid coordinate (subs regions)
+  // TC_STEM_POOL: M rows are pooled pixels; per M tile 3 super-tiles (window
+  // row dy) of 3 sub-tiles (window column dx) over one A stage; step table
+  // [dy][dx][8 tap pairs]; the epilogue max-reduces the 9 accumulators
+  int32_t win;
   int32_t sub;         // 128-row M tiles per super-tile (share B descriptors and the pipeline handshakes)
   int32_t nbox, hbox;  // A TMA boxes per (plane, sub-grid) block and their height in TMA rows
   int32_t dmin;  // smallest tap row offset (tile row 0 + dmin = first halo row)
@@ -513,7 +518,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int msub = a.sub * kTileM;  // rows of a super-tile
+  const int msub = a.win ? kTileM : a.sub * kTileM;  // grid rows per M tile
   if (warp == 0) {
     if (lane == 0) {
       // ===== TMA producer =====
@@ -537,7 +542,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             for (int sg = 0; sg < a.subs; ++sg)
               for (int bx = 0; bx < a.nbox; ++bx)
                 tma_load_4d(dA + ((pl * a.subs + sg) * a.hg + bx * a.hbox) * row_bytes, &tmA, &full[stage], 0,
-                            r0 + bx * a.hbox, a.sub0 + sg, ks * a.pps + pl);
+                            r0 + bx * a.hbox, a.region_sg[sg], ks * a.pps + pl);
           if (!a.resident_b)
             tma_load_4d(smB + stage * a.b_stage_bytes, &tmB, &full[stage], 0, n_tile * a.bn / (a.kb == 16 ? 8 : 1),
                         ks * a.pps, 0);
@@ -568,6 +573,37 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       const uint32_t n_steps = static_cast<uint32_t>(a.n_steps);
       const uint32_t sub_step16 = static_cast<uint32_t>(kTileM * a.kb) >> 4;  // 128 rows, in descriptor units
       const bool no_mma = (a.dbg & 4) != 0;
+      if (a.win) {
+        // TC_STEM_POOL: one A stage per M tile, 3 window rows x 3 window columns
+        for (int mt = m_start; mt < a.m_tiles; mt += m_step) {
+          const int row0 = tile_row0(a, mt, msub);
+          const uint32_t shift16 = static_cast<uint32_t>(row0 - 8 * floor_div8(row0)) * 16;
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a16 = (smA_u + stage * a.a_stage_bytes + shift16) >> 4, b16 = smB_u >> 4;
+          for (uint32_t dy = 0; dy < 3; ++dy) {
+            mbar_wait(&tempty[acc], acc_phase ^ 1);
+            tc_fence_after();
+            const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc) * 3u * bn;
+            if (!no_mma)
+              for (uint32_t st = 0; st < 8; ++st) {
+                const uint64_t bd = hi | (a.steps[dy * 24 + st].b_lo + b16);
+                for (uint32_t dx = 0; dx < 3; ++dx)
+                  umma<EB>(tmem_d + dx * bn, hi | (a.steps[dy * 24 + dx * 8 + st].a_lo + a16), bd, idesc, st != 0);
+              }
+            umma_commit(&tfull[acc]);
+            if (++acc == 2) {
+              acc = 0;
+              acc_phase ^= 1;
+            }
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == a.n_stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      } else
       for (int mt = m_start; mt < a.m_tiles; mt += m_step) {
         const int row0 = tile_row0(a, mt, msub);
         const uint32_t shift16 = a.kb == 16 ? static_cast<uint32_t>(row0 - 8 * floor_div8(row0)) * 16 : 0u;
@@ -615,6 +651,73 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     float* stg = reinterpret_cast<float*>(smem_pool);
+    if constexpr (EB == 1) {
+      if (a.win) {
+        // TC_STEM_POOL epilogue: lane = pooled pixel, warp slice = 16-channel
+        // chunk.  The reference pools relu(bias + acc * s) with its ordered
+        // max over the valid window taps; bias_add / relu / (* s > 0) are
+        // monotone, so the max is taken on the int32 accumulators of the
+        // valid taps (padded conv positions skipped) and the epilogue is
+        // applied once to the winner -- the same float.
+        const int c = slice * 16;
+        for (int mt = m_start; mt < a.m_tiles; mt += m_step) {
+          const uint32_t q = static_cast<uint32_t>(mt) * kTileM + row;
+          const uint32_t t = fdiv(q, a.fd_wg);
+          const int j = static_cast<int>(q - t * static_cast<uint32_t>(a.Wg));
+          const uint32_t n32 = fdiv(t, a.fd_hg);
+          const int i = static_cast<int>(t - n32 * static_cast<uint32_t>(a.Hg));
+          const int n = static_cast<int>(n32), pp = i - 1, pq = j - 1;
+          const bool vpool = n < a.N && pp >= 0 && pp < a.poh && pq >= 0 && pq < a.pow;
+          int32_t mx[16];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) mx[k] = INT32_MIN;
+          for (int dy = 0; dy < 3; ++dy) {
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const int y = 2 * pp - 1 + dy;
+            const bool yok = vpool && y >= 0 && y < a.OH;
+#pragma unroll
+            for (int dx = 0; dx < 3; ++dx) {
+              uint32_t raw[16];
+              tmem_ld16(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+                            static_cast<uint32_t>((acc * 3 + dx) * a.bn + c), raw);
+              const int x = 2 * pq - 1 + dx;
+              if (yok && x >= 0 && x < a.OW) {
+#pragma unroll
+                for (int k = 0; k < 16; ++k) mx[k] = max(mx[k], static_cast<int32_t>(raw[k]));
+              }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (++acc == 2) {
+              acc = 0;
+              acc_phase ^= 1;
+            }
+          }
+          if (vpool && !(a.dbg & 1)) {
+            RowDst d;
+            d.border = false;
+            d.pix = (static_cast<int64_t>(n) * (a.poh + 2 * kPad) + pp + kPad) * (a.pow + 2 * kPad) + pq + kPad;
+            if (a.out.side && sl.kind == LAY_PHASE) {
+              const uint32_t p32 = static_cast<uint32_t>(d.pix);
+              const uint32_t tt = fdiv(p32, a.fd_swp);
+              const int wp = static_cast<int>(p32 - tt * static_cast<uint32_t>(sl.Wp));
+              const uint32_t nn = fdiv(tt, a.fd_shp);
+              const int hp = static_cast<int>(tt - nn * static_cast<uint32_t>(sl.Hp));
+              d.side_base = static_cast<int64_t>((hp & 1) * 2 + (wp & 1)) * sl.Pp +
+                            (static_cast<int64_t>(nn) * sl.Hq + hp / 2) * sl.Wq + wp / 2;
+              d.side_pstride = 4 * sl.Pp;
+            } else {
+              d.side_base = d.pix;
+              d.side_pstride = sl.Pp;
+            }
+            epilogue_chunk<EB, SIG>(a, reinterpret_cast<const uint32_t*>(mx), d, n_tile * a.bn + c);
+          }
+        }
+        goto epilogue_done;
+      }
+    }
     for (int mt = m_start; mt < a.m_tiles; mt += m_step) {
       if ((a.dbg & 16) && a.pool && blockIdx.x == 0 && threadIdx.x == 64 && (mt - m_start) / m_step < 16)
         a.stamps[((mt - m_start) / m_step) * 8 + 5] = clock64();
@@ -788,6 +891,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       }
     }
   }
+epilogue_done:
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -905,9 +1009,37 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
       if (pair_taps && (TA & 1)) return false;
       break;
     }
+    case TC_STEM_POOL: {
+      // int8 7x7/s2/p3 stem + 3x3/s2/p1 max_pool2d over LAY_S2DP: M grid =
+      // the phase sub-grid raster (pooled pixel (p, q) at (p+1, q+1)); the
+      // 16 s2d taps (ty, tx) are paired along tx (K = 2 x 16 bytes)
+      if (eb != 1 || sp.KH != 7 || sp.KW != 7 || 4 * sp.C > 16 || !sp.pool) return false;
+      if (sp.pkh != 3 || sp.pkw != 3 || sp.psh != 2 || sp.psw != 2 || sp.pph != 1 || sp.ppw != 1) return false;
+      kb = 16;
+      const int hs = (sp.H + 6 + 1) / 2, ws = (sp.W + 6 + 1) / 2;
+      a.Hg = (hs + 3) / 2 + 1;  // == make_lay(LAY_S2DP) (exec.cpp)
+      a.Wg = (ws + 3) / 2 + 1;
+      if (a.Hg < sp.poh + 3 || a.Wg < sp.pow + 3) return false;
+      a.out_mode = OUT_REMAP;
+      a.OH = sp.OH;
+      a.OW = sp.OW;
+      a.poh = sp.poh;
+      a.pow = sp.pow;
+      cc = 1;
+      pair_taps = true;
+      a.win = 1;
+      a.subs = 6;  // [row phase][col phase 0, col phase 1, col phase 0 again]
+      const int8_t rs[6] = {0, 1, 0, 2, 3, 2};
+      for (int i = 0; i < 6; ++i) a.region_sg[i] = rs[i];
+      for (int ta = 0; ta < 4; ++ta)
+        for (int tb = 0; tb < 4; ++tb) taps.push_back({0, 0});  // B layout only; A offsets below
+      break;
+    }
     default:
       return false;
   }
+  if (!a.win)
+    for (int i = 0; i < a.subs && i < 8; ++i) a.region_sg[i] = static_cast<int8_t>(a.sub0 + i);
   a.kb = kb;
   a.Pg = static_cast<int64_t>(a.N) * a.Hg * a.Wg;
   a.fd_wg = make_fastdiv(static_cast<uint32_t>(a.Wg));
@@ -917,6 +1049,10 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
   for (const Tap& t : taps) {
     dmin = std::min(dmin, t.delta);
     dmax = std::max(dmax, t.delta + (pair_taps ? 1 : 0));
+  }
+  if (a.win) {  // A offsets fl(v/2)*Wg + fl(u/2), v, u in [-1, 4] (+1 row: the odd-u second half)
+    dmin = -a.Wg - 1;
+    dmax = 2 * a.Wg + 2;
   }
   a.dmin = dmin;
   const int ntaps = static_cast<int>(taps.size());
@@ -941,7 +1077,7 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
   // A rows per (sub-grid, plane) block for a super-tile of `sub` M tiles,
   // split into <= 256-row TMA boxes (rows aligned for the swizzle atom)
   auto geom = [&](int sub, int* hg, int* nbox, int* hbox) {
-    int need = kTileM * sub + dmax - dmin;
+    int need = kTileM * (a.win ? 1 : sub) + dmax - dmin;
     if (kb == 16) need = (7 + need + 7) / 8;
     const int align = kb == 16 ? 1 : 1024 / kb;
     *nbox = (need + 255) / 256;
@@ -1001,7 +1137,9 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
     }
     return false;
   };
-  if (sp.pool) {
+  if (a.win) {
+    found = sp.OC % 64 == 0 && try_cfg(64, 3, true);
+  } else if (sp.pool) {
     // fused max_pool2d: one super-tile = the pkh conv rows of one pooled row,
     // whole channel range in one N tile, staging in shared memory
     if (a.out_mode != OUT_REMAP || sp.OC > 256) return false;
@@ -1032,7 +1170,8 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
     }
   }
   if (!found) return false;
-  a.m_tiles = a.pool ? sp.N * sp.poh : static_cast<int>((a.Pg + kTileM * a.sub - 1) / (kTileM * a.sub));
+  a.m_tiles = a.pool ? sp.N * sp.poh
+                     : static_cast<int>((a.Pg + kTileM * (a.win ? 1 : a.sub) - 1) / (kTileM * (a.win ? 1 : a.sub)));
   const int rows_bytes = a.hg * row_bytes;
   a.Cc = cc;
   a.k_stages = cc / a.pps;
@@ -1082,6 +1221,24 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
           a.steps[a.n_steps++] = m;
         }
   }
+  if (a.win) {
+    // [dy][dx][ty][tx pair]: v = dy + ty - 1, u = dx + 2k - 1; tap (ty, 2k) reads region
+    // (v&1, u&1) at fl(v/2)*Wg + fl(u/2); tap (ty, 2k+1) the next column region (LBO)
+    a.n_steps = 0;
+    for (int dy = 0; dy < 3; ++dy)
+      for (int dx = 0; dx < 3; ++dx)
+        for (int ty = 0; ty < 4; ++ty)
+          for (int k = 0; k < 2; ++k) {
+            const int v = dy + ty - 1, u = dx + 2 * k - 1;
+            const int vb = v & 1, ub = u & 1, fv = v >> 1, fu = u >> 1;  // arithmetic shifts: floor
+            MmaStep m;
+            m.a_off = static_cast<uint32_t>(vb * 3 + ub) * a_sub + static_cast<uint32_t>(fv * a.Wg + fu - dmin) * 16;
+            m.a_lbo = a_sub + static_cast<uint32_t>(ub) * 16;
+            m.b_off = static_cast<uint32_t>(ty * 4 + 2 * k) * b_plane;
+            m.b_lbo = b_plane;
+            a.steps[a.n_steps++] = m;
+          }
+  }
   for (int i = 0; i < a.n_steps; ++i) {
     MmaStep& m = a.steps[i];
     m.a_lo = ((m.a_off >> 4) & 0x3FFF) | (((m.a_lbo >> 4) & 0x3FFF) << 16);
@@ -1116,7 +1273,7 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
 // same representation already fixed it).
 static bool choose(TcConvPlan& p) {
   const TcConvSpec keep = p.spec;
-  if (p.spec.kind == TC_STEM_S2D) return choose_kb(p, 16);
+  if (p.spec.kind == TC_STEM_S2D || p.spec.kind == TC_STEM_POOL) return choose_kb(p, 16);
   const int forced = p.spec.kb;
   for (int kb : {128, 64}) {
     if (forced && kb != forced) continue;
@@ -1166,7 +1323,7 @@ static bool encode_maps(TcConvPlan& p, const void* x, const Lay& xl, const void*
   const cuuint64_t row_bytes = kb == 16 ? 128 : kb;
   const cuuint64_t rows = kb == 16 ? static_cast<cuuint64_t>(xl.Pp / 8) : static_cast<cuuint64_t>(xl.Pp);
   {
-    const cuuint64_t tsubs = xl.kind == LAY_PHASE ? 4 : 1;
+    const cuuint64_t tsubs = xl.kind == LAY_PHASE || xl.kind == LAY_S2DP ? 4 : 1;
     cuuint64_t dims[4] = {row_bytes, rows, tsubs, static_cast<cuuint64_t>(a.Cc)};
     cuuint64_t strides[3] = {row_bytes, static_cast<cuuint64_t>(xl.Pp) * kb, static_cast<cuuint64_t>(xl.Pp) * kb * tsubs};
     cuuint32_t box[4] = {static_cast<cuuint32_t>(row_bytes), static_cast<cuuint32_t>(a.hbox), 1, 1};
@@ -1203,6 +1360,9 @@ bool tc_conv_launch(TcConvPlan* p, const void* x, const Lay& xl, const void* w, 
   }
   TcArgs a = p->args;
   a.acc_scale = acc_scale;
+  // TC_STEM_POOL takes the window max on the accumulators: exact only when the
+  // accumulator -> float map is non-decreasing
+  if (a.win && !(acc_scale > 0.f)) return false;
   a.relu_last = epi.n_ops > 0 && epi.op[epi.n_ops - 1] == E_RELU;
   static const int dbg = [] {
     const char* e = std::getenv("MRB200_TC_DBG");
@@ -1260,7 +1420,7 @@ void tc_conv_destroy(TcConvPlan* p) { delete p; }
 
 const char* tc_conv_describe(const TcConvPlan* p, char* buf, int n) {
   const TcArgs& a = p->args;
-  static const char* kinds[] = {"s1", "s2-phase", "stem-s2d"};
+  static const char* kinds[] = {"s1", "s2-phase", "stem-s2d", "stem-pool"};
   std::snprintf(buf, n,
                 "tcgen05 %s %s %dx(M128)xN%d kb=%d taps=%d steps=%d grid=%dx%d rows=%dx%d pps=%d stages=%d B=%s ctas=%d smem=%zu",
                 p->spec.elem_bytes == 1 ? "i8" : "bf16", kinds[p->spec.kind], a.sub, a.bn, a.kb, p->spec.taps, a.n_steps,

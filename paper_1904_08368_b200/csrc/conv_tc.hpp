@@ -12,6 +12,8 @@ enum TcKind : int {
   TC_S1 = 0,        // stride-1 3x3/pad-1 or 1x1 over a LAY_NORMAL input
   TC_S2_PHASE = 1,  // stride-2 3x3/pad-1 or 1x1 over a LAY_PHASE input
   TC_STEM_S2D = 2,  // KxK stride-2 stem over the LAY_S2D network input
+  TC_STEM_POOL = 3, // 7x7/s2 stem fused with a 3x3/s2/p1 max_pool2d over the LAY_S2DP input:
+                    // M rows = pooled pixels, the 9 window taps = 3 super-tiles x 3 sub-tiles
 };
 
 struct TcConvSpec {

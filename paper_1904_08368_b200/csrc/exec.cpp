@@ -207,10 +207,17 @@ Lay make_lay(const std::vector<int64_t>& s, int fmt, int kind, int s2d_pad = 0, 
       L.Hq = (L.Hp + 1) / 2;
       L.Wq = (L.Wp + 1) / 2;
       L.Pp = round_up(s[0] * L.Hq * L.Wq, 8);
-    } else {  // LAY_S2D: 4*C s2d channels on a ceil((H+2p)/2) grid
+    } else if (kind == LAY_S2D) {  // 4*C s2d channels on a ceil((H+2p)/2) grid
       L.C = static_cast<int32_t>(4 * s[1]);
       L.Hq = static_cast<int32_t>((s[2] + 2 * s2d_pad + 1) / 2);
       L.Wq = static_cast<int32_t>((s[3] + 2 * s2d_pad + 1) / 2);
+      L.Pp = round_up(s[0] * L.Hq * L.Wq, 8);
+    } else {  // LAY_S2DP: the s2d grid shifted by 2, split into 4 phase sub-grids
+      L.C = static_cast<int32_t>(4 * s[1]);
+      const int32_t hs = static_cast<int32_t>((s[2] + 2 * s2d_pad + 1) / 2);
+      const int32_t ws = static_cast<int32_t>((s[3] + 2 * s2d_pad + 1) / 2);
+      L.Hq = (hs + 3) / 2 + 1;
+      L.Wq = (ws + 3) / 2 + 1;
       L.Pp = round_up(s[0] * L.Hq * L.Wq, 8);
     }
   } else {
@@ -223,7 +230,7 @@ Lay make_lay(const std::vector<int64_t>& s, int fmt, int kind, int s2d_pad = 0, 
 int64_t lay_elems(const Lay& L) {
   if (L.cpc == 0) return L.Pp * L.C;
   int64_t planes = (L.C + L.cpc - 1) / L.cpc;
-  return planes * (L.kind == LAY_PHASE ? 4 : 1) * L.Pp * L.cpc;
+  return planes * (L.kind == LAY_PHASE || L.kind == LAY_S2DP ? 4 : 1) * L.Pp * L.cpc;
 }
 
 
@@ -232,7 +239,7 @@ int64_t lay_elems(const Lay& L) {
 int want_rep(Exec& ex, int v, int fmt, const QParams* q, int kind = LAY_NORMAL, int s2d_pad = 0, int kb = 0) {
   auto& rs = ex.reps[v];
   if (ex.P.values[v].shape.size() != 4) kind = LAY_NORMAL;
-  if (fmt == FMT_F32 || kind == LAY_S2D) kb = 16;
+  if (fmt == FMT_F32 || kind == LAY_S2D || kind == LAY_S2DP) kb = 16;
   for (size_t i = 0; i < rs.size(); ++i) {
     const Rep& r = rs[i];
     if (r.nchw_user) continue;
@@ -324,8 +331,13 @@ void decide_tc(Exec& ex) {
           fs.ppw = static_cast<int>(pg.pw);
           fs.poh = static_cast<int>(pg.out_shape[2]);
           fs.pow = static_cast<int>(pg.out_shape[3]);
-          if (tc_conv_plan_ok(fs)) {
-            sp = fs;
+          // int8, 3-channel 7x7/s2/p3 stem + 3x3/s2/p1 pool: the pool window
+          // is part of the GEMM's M (TC_STEM_POOL); otherwise staged pooling
+          TcConvSpec wp = fs;
+          wp.kind = TC_STEM_POOL;
+          const bool win_ok = sp.elem_bytes == 1 && sp.C == 3 && g.ph == 3 && tc_conv_plan_ok(wp);
+          if (win_ok || tc_conv_plan_ok(fs)) {
+            sp = win_ok ? wp : fs;
             ex.fused_pool[gi] = pj;
             ex.fused_away[pj] = 1;
           }
@@ -414,7 +426,7 @@ GroupIO resolve_inputs(Exec& ex, int gi) {
   int kind = LAY_NORMAL, s2d_pad = 0, kb = 0;
   if (path == P_CONV_I8_TC || path == P_CONV_BF16_TC) {
     const TcConvSpec& sp = ex.group_tc[gi];
-    kind = sp.kind == TC_S2_PHASE ? LAY_PHASE : sp.kind == TC_STEM_S2D ? LAY_S2D : LAY_NORMAL;
+    kind = sp.kind == TC_S2_PHASE ? LAY_PHASE : sp.kind == TC_STEM_S2D ? LAY_S2D : sp.kind == TC_STEM_POOL ? LAY_S2DP : LAY_NORMAL;
     s2d_pad = static_cast<int>(g.ph);
     kb = sp.kb;
   }
@@ -616,7 +628,7 @@ void build(Exec& ex) {
       int fmt = rep.fmt;
       Lay lay = rep.lay;
       int s2d_pad = 0;
-      if (lay.kind == LAY_S2D)
+      if (lay.kind == LAY_S2D || lay.kind == LAY_S2DP)
         for (int c : vi.consumers)
           if (P.groups[c].data.value == static_cast<int>(v)) s2d_pad = static_cast<int>(P.groups[c].ph);
       Exec* e = &ex;
@@ -965,7 +977,7 @@ void prepare_weights(Exec& ex, cudaStream_t s) {
     }
     int fmt, cs;
     int wl = WL_ROWS;
-    if (path == P_CONV_I8_TC || path == P_CONV_BF16_TC) wl = ex.group_tc[gi].kind == TC_STEM_S2D ? WL_S2D : WL_TC;
+    if (path == P_CONV_I8_TC || path == P_CONV_BF16_TC) wl = ex.group_tc[gi].kind == TC_STEM_S2D || ex.group_tc[gi].kind == TC_STEM_POOL ? WL_S2D : WL_TC;
     if (w.quant) {
       fmt = FMT_I8;
       cs = static_cast<int>(round_up(I, 4));

@@ -34,6 +34,12 @@ struct QDev {
 //               (n * Hq + hp / 2) * Wq + wp / 2; sub-grids of Pp pixels
 //   LAY_S2D     the network input in space-to-depth form for a 7x7/s2 stem
 //               (written by input_convert, read by the stem tcgen05 conv only)
+//   LAY_S2DP    LAY_S2D shifted by 2 s2d pixels (zero rows/columns on top and
+//               left) and split into its 4 stride-2 phase sub-grids of Hq x Wq:
+//               s2d pixel (si, sj) -> sub-grid ((si+2)&1)*2 + ((sj+2)&1),
+//               position (n*Hq + (si+2)/2)*Wq + (sj+2)/2, sub-grid stride Pp.
+//               Read by the fused stem + 3x3/s2 max_pool2d kernel, whose M
+//               rows are pooled pixels (conv_tc.cu TC_STEM_POOL).
 // A pixel's kb-byte chunk is one row of a tcgen05 operand tile: kb = 128 / 64
 // rows are TMA-loaded with the matching 128B / 64B swizzle, and a stride-1
 // 3x3 conv reads its 9 taps as 9 row shifts of one contiguous pixel range
@@ -41,7 +47,7 @@ struct QDev {
 // tensor (float32 residual stream: warp-coalesced epilogue loads) and for the
 // 16-byte stem input.  Plane strides are padded to a multiple of 8 pixels.
 // Borders hold zeros.  cpc == 0 marks a plain row-major [N, C] tensor (pix = n).
-enum LayKind : int32_t { LAY_NORMAL = 0, LAY_PHASE = 1, LAY_S2D = 2 };
+enum LayKind : int32_t { LAY_NORMAL = 0, LAY_PHASE = 1, LAY_S2D = 2, LAY_S2DP = 3 };
 
 struct Lay {
   int32_t cpc;

@@ -6,6 +6,9 @@
 // Activations use the padded P16 layout (kernels.cuh).
 #include <cuda_runtime.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "kernels.cuh"
 #include "launch.hpp"
 
@@ -215,17 +218,22 @@ __global__ void __launch_bounds__(128) k_input_s2d(const float* __restrict__ x, 
 // padding PAD, CPC channels per 16-byte chunk: 16 int8 / 8 bf16): the channel
 // -> (row, column shift) map folds to constants and every tap is a branch-free
 // select, so the kernel stays memory-bound.  Same values as k_input_s2d.
-template <int C, int PAD, int CPC>
+// PHASED writes LAY_S2DP: the s2d grid is walked from (-2, -2) over the
+// 2*Hq x 2*Wq extent of the 4 phase sub-grids (every position written, zeros
+// outside the image), so no separate border pass is needed.
+template <int C, int PAD, int CPC, bool PHASED>
 __global__ void __launch_bounds__(128) k_input_s2d_ct(const float* __restrict__ x, int N, int H, int W, void* out,
                                                       Lay L, float pre_mul, QDev q, FastDiv fd_w4) {
   extern __shared__ __align__(16) float rows[];  // 2 x [C][2][W]
   constexpr int PLANES = (4 * C + CPC - 1) / CPC;
+  constexpr int OFF = PHASED ? 2 : 0;                  // s2d index = grid index - OFF
+  const int GR = PHASED ? 2 * L.Hq : L.Hq, GC = PHASED ? 2 * L.Wq : L.Wq;  // walked grid
   const int stride = 2 * C * W;
-  const int n_rows = N * L.Hq;
+  const int n_rows = N * GR;
   const int W4 = W >> 2, total4 = 2 * C * W4;
   const bool fast_q = q.lo > -2147483648.f && q.hi < 2147483648.f;
   auto prefetch = [&](float* buf, int row) {
-    const int n = row / L.Hq, si = row - n * L.Hq;
+    const int n = row / GR, si = row - n * GR - OFF;
     for (int i = threadIdx.x; i < total4; i += blockDim.x) {
       const int cr = static_cast<int>(fdiv(static_cast<uint32_t>(i), fd_w4)), x4 = i - cr * W4;
       const int y = 2 * si - PAD + (cr & 1), c = cr >> 1;
@@ -239,7 +247,7 @@ __global__ void __launch_bounds__(128) k_input_s2d_ct(const float* __restrict__ 
   if (blockIdx.x < n_rows) prefetch(rows, blockIdx.x);
   int it = 0;
   for (int row = blockIdx.x; row < n_rows; row += gridDim.x, ++it) {
-    const int n = row / L.Hq, si = row - n * L.Hq;
+    const int n = row / GR, gi = row - n * GR, si = gi - OFF;
     if (row + gridDim.x < n_rows) {
       prefetch(rows + ((it + 1) & 1) * stride, row + gridDim.x);
       asm volatile("cp.async.wait_group 1;" ::: "memory");
@@ -250,8 +258,11 @@ __global__ void __launch_bounds__(128) k_input_s2d_ct(const float* __restrict__ 
     const float* cur = rows + (it & 1) * stride;
     const int y0 = 2 * si - PAD;
     const bool rok[2] = {y0 >= 0 && y0 < H, y0 + 1 >= 0 && y0 + 1 < H};
-    for (int sj = threadIdx.x; sj < L.Wq; sj += blockDim.x) {
-      const int64_t pix = (static_cast<int64_t>(n) * L.Hq + si) * L.Wq + sj;
+    for (int gj = threadIdx.x; gj < GC; gj += blockDim.x) {
+      const int sj = gj - OFF;
+      const int64_t pix = PHASED ? static_cast<int64_t>((gi & 1) * 2 + (gj & 1)) * L.Pp +
+                                       (static_cast<int64_t>(n) * L.Hq + (gi >> 1)) * L.Wq + (gj >> 1)
+                                 : (static_cast<int64_t>(n) * L.Hq + si) * L.Wq + sj;
       const int xb = 2 * sj - PAD;  // column of phase px = 0
       const bool cok[2] = {xb >= 0 && xb < W, xb + 1 >= 0 && xb + 1 < W};
       const int xc[2] = {min(max(xb, 0), W - 1), min(max(xb + 1, 0), W - 1)};
@@ -272,7 +283,7 @@ __global__ void __launch_bounds__(128) k_input_s2d_ct(const float* __restrict__ 
             v[k] = 0.f;
           }
         }
-        char* dst = static_cast<char*>(out) + (pl * L.Pp + pix) * 16;
+        char* dst = static_cast<char*>(out) + (pl * (PHASED ? 4 : 1) * L.Pp + pix) * 16;
         uint32_t w4[4];
         if constexpr (CPC == 8) {
 #pragma unroll
@@ -827,6 +838,24 @@ unsigned grid_stride_blocks(int64_t total) {
 
 void launch_input_convert(const float* x, int N, int C, int H, int W, void* out, int fmt, const Lay& L,
                           int s2d_pad, float pre_mul, QDev q, cudaStream_t s) {
+  if (L.kind == LAY_S2DP) {
+    // only the int8 3-channel pad-3 stem is planned onto LAY_S2DP (exec.cpp decide_tc)
+    static int sms2 = [] {
+      int d = 0, v = 0;
+      cudaGetDevice(&d);
+      cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+      return v > 0 ? v : 148;
+    }();
+    if (!(C == 3 && s2d_pad == 3 && fmt == FMT_I8 && W % 4 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0)) {
+      std::fprintf(stderr, "mrb200: LAY_S2DP input conversion needs an int8 3-channel pad-3 stem\n");
+      std::abort();
+    }
+    const FastDiv fd = make_fastdiv(static_cast<uint32_t>(W / 4));
+    const int rows = N * 2 * L.Hq;
+    k_input_s2d_ct<3, 3, 16, true><<<std::min(rows, sms2 * 8), 128, 2 * 2 * C * W * sizeof(float), s>>>(
+        x, N, H, W, out, L, pre_mul, q, fd);
+    return;
+  }
   const int s2d_planes = (4 * C + L.cpc - 1) / L.cpc;
   if (L.kind == LAY_S2D && 2 * 2 * C * W * 4 <= 40 * 1024 && W % 4 == 0 && s2d_planes * (L.kb / 16) <= 4 &&
       reinterpret_cast<uintptr_t>(x) % 16 == 0) {
@@ -841,9 +870,9 @@ void launch_input_convert(const float* x, int N, int C, int H, int W, void* out,
     if (C == 3 && s2d_pad == 3 && L.kb == 16 && (fmt == FMT_I8 || fmt == FMT_BF16)) {
       const FastDiv fd = make_fastdiv(static_cast<uint32_t>(W / 4));
       if (fmt == FMT_I8)
-        k_input_s2d_ct<3, 3, 16><<<std::min(rows, sms * 8), 128, smem, s>>>(x, N, H, W, out, L, pre_mul, q, fd);
+        k_input_s2d_ct<3, 3, 16, false><<<std::min(rows, sms * 8), 128, smem, s>>>(x, N, H, W, out, L, pre_mul, q, fd);
       else
-        k_input_s2d_ct<3, 3, 8><<<std::min(rows, sms * 8), 128, smem, s>>>(x, N, H, W, out, L, pre_mul, q, fd);
+        k_input_s2d_ct<3, 3, 8, false><<<std::min(rows, sms * 8), 128, smem, s>>>(x, N, H, W, out, L, pre_mul, q, fd);
       return;
     }
     k_input_s2d<<<std::min(rows, sms * 8), 128, 2 * 2 * C * W * sizeof(float), s>>>(x, N, C, H, W, out, fmt, L,
