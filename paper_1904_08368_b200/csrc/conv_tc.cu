@@ -38,6 +38,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
 #include <vector>
 
@@ -72,6 +73,8 @@ inline int epi_signature(const EpiDev& e, const OutDev& o) {
 }
 
 constexpr int kMaxSteps = 80;
+constexpr int kVecSlots = 2;   // staged per-channel vectors
+constexpr int kVecArea = (kVecSlots + 1) * 256 * 4 + 16;  // + b*c1 for the short requantize + flag
 
 // One tcgen05.mma of a tile's K loop: byte offsets (relative to the A stage
 // base + row shift, and to the B stage / resident base) and the leading byte
@@ -93,6 +96,16 @@ struct TcArgs {
   // row dy) of 3 sub-tiles (window column dx) over one A stage; step table
   // [dy][dx][8 tap pairs]; the epilogue max-reduces the 9 accumulators
   int32_t win;
+  // per-CTA shared-memory copies of the epilogue's per-channel vectors
+  // (bias / channel scale): slot of op k (-1: read global), byte offset of the
+  // area from the barrier block
+  int8_t vec_slot[kMaxEpi];
+  int32_t vec_off;
+  // exact short requantize (SIG_BIAS_RELU_REQ): acc_scale and the requant c1
+  // are powers of two, so (acc*s + b)*c1 == fma(acc, s*c1, b*c1) exactly
+  int32_t p2;
+  float p2_scale;  // s * c1
+  int32_t p2_hi;
   int32_t sub;         // 128-row M tiles per super-tile (share B descriptors and the pipeline handshakes)
   int32_t nbox, hbox;  // A TMA boxes per (plane, sub-grid) block and their height in TMA rows
   int32_t dmin;  // smallest tap row offset (tile row 0 + dmin = first halo row)
@@ -300,7 +313,8 @@ __device__ __forceinline__ void epilogue_values(const TcArgs& a, const uint32_t*
 }
 
 template <int EB, int SIG>
-__device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* raw, const RowDst& d, int c0) {
+__device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* raw, const RowDst& d, int c0,
+                                               const float* s_vec, bool p2ok, int cl) {
   const OutDev& o = a.out;
   const int pf = o.primary_fmt;
   const int peb = pf == FMT_F32 ? 4 : pf == FMT_BF16 ? 2 : 1;  // 16-byte granules per 16 channels
@@ -321,12 +335,20 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
     code[i] = 0;
   }
   const EpiDev& e = a.epi;
-  auto vec16 = [&](const float* base, float (&t)[16]) {
-    const float4* p = reinterpret_cast<const float4*>(base + c0);
+  auto vec16k = [&](int k, float (&t)[16]) {
+    float4 f[4];
+    if (a.vec_slot[k] >= 0) {  // staged in shared memory (plain loads: __ldg is global-only)
+      const float4* p = reinterpret_cast<const float4*>(s_vec + a.vec_slot[k] * 256 + cl);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) f[j] = p[j];
+    } else {
+      const float4* p = reinterpret_cast<const float4*>(e.vec[k] + c0);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) f[j] = __ldg(p + j);
+    }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      float4 f = __ldg(p + j);
-      t[4 * j] = f.x; t[4 * j + 1] = f.y; t[4 * j + 2] = f.z; t[4 * j + 3] = f.w;
+      t[4 * j] = f[j].x; t[4 * j + 1] = f[j].y; t[4 * j + 2] = f[j].z; t[4 * j + 3] = f[j].w;
     }
   };
   auto res16 = [&](int k, float (&t)[16]) {
@@ -358,7 +380,7 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
         for (int i = 0; i < 16; ++i) v[i] = __fmul_rn(v[i], e.s[k]);
       } else if (op == E_MULC || op == E_BIAS) {
         float t[16];
-        vec16(e.vec[k], t);
+        vec16k(k, t);
         if (op == E_MULC) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] = __fmul_rn(v[i], t[i]);
@@ -388,8 +410,31 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
     }
   } else {
     // op 0 is always bias_add for the specialised signatures
+    if constexpr (SIG == SIG_BIAS_RELU_REQ && EB == 1) {
+      if (p2ok) {
+        // code = clip(rint(relu(acc*s + b) * c1)) == clamp(rni(fma(acc, s*c1, b*c1)), 0, hi):
+        // acc*s and *c1 are exact (powers of two, |acc| < 2^24 by the exactness bound),
+        // so the fma rounds once exactly where fadd did; relu/rint/clip become integer clamps
+        const float4* bp = reinterpret_cast<const float4*>(s_vec + kVecSlots * 256 + cl);
+        float bb[16];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float4 f = bp[j];
+          bb[4 * j] = f.x; bb[4 * j + 1] = f.y; bb[4 * j + 2] = f.z; bb[4 * j + 3] = f.w;
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int r = __float2int_rn(__fmaf_rn(static_cast<float>(static_cast<int32_t>(raw[i])), a.p2_scale, bb[i]));
+          code[i] = min(max(r, 0), a.p2_hi);
+        }
+        st16(o.primary, gran_byte(o.plan, d.pix, o.plan.Pp, c0),
+             make_uint4(pack4_i8(code[0], code[1], code[2], code[3]), pack4_i8(code[4], code[5], code[6], code[7]),
+                        pack4_i8(code[8], code[9], code[10], code[11]), pack4_i8(code[12], code[13], code[14], code[15])));
+        return;
+      }
+    }
     float t[16];
-    vec16(e.vec[0], t);
+    vec16k(0, t);
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __fadd_rn(v[i], t[i]);
     if constexpr (SIG == SIG_BIAS_RES_RELU) {
@@ -512,6 +557,28 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(tmem_cols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // stage this CTA's per-channel epilogue vectors (and b*c1) in shared memory
+  float* s_vec = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + a.vec_off);
+  int* s_p2ok = reinterpret_cast<int*>(s_vec + (kVecSlots + 1) * 256);
+  {
+    const int c0 = (blockIdx.x % a.n_tiles) * a.bn;
+    if (!(a.dbg & 128))
+    for (int k = 0; k < a.epi.n_ops; ++k)
+      if (a.vec_slot[k] >= 0)
+        for (int i = threadIdx.x; i < a.bn; i += blockDim.x) s_vec[a.vec_slot[k] * 256 + i] = a.epi.vec[k][c0 + i];
+    int ok = 1;
+    if (a.p2 && !(a.dbg & 128)) {
+      const float c1 = a.epi.q[2].c1;
+      for (int i = threadIdx.x; i < a.bn; i += blockDim.x) {
+        const float b = a.epi.vec[0][c0 + i];
+        const float r = __fmul_rn(b, c1);
+        ok &= (isfinite(r) && __fdiv_rn(r, c1) == b) ? 1 : 0;  // exact scaling by the power of two
+        s_vec[kVecSlots * 256 + i] = r;
+      }
+    }
+    ok = __syncthreads_and(ok);
+    if (threadIdx.x == 0) *s_p2ok = ok;
   }
   tc_fence_before();
   __syncthreads();
@@ -651,6 +718,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     float* stg = reinterpret_cast<float*>(smem_pool);
+    const bool p2ok = a.p2 && *s_p2ok && !(a.dbg & 64);
     if constexpr (EB == 1) {
       if (a.win) {
         // TC_STEM_POOL epilogue: lane = pooled pixel, warp slice = 16-channel
@@ -712,7 +780,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
               d.side_base = d.pix;
               d.side_pstride = sl.Pp;
             }
-            epilogue_chunk<EB, SIG>(a, reinterpret_cast<const uint32_t*>(mx), d, n_tile * a.bn + c);
+            epilogue_chunk<EB, SIG>(a, reinterpret_cast<const uint32_t*>(mx), d, n_tile * a.bn + c, s_vec, p2ok, c);
           }
         }
         goto epilogue_done;
@@ -837,9 +905,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       // sub-tile's row decode is done once per warp
       const int n_items = a.sub * chunks, per = (n_items + 3) >> 2;
       const int it_end = min(n_items, (slice + 1) * per);
+      const int lgc = 31 - __clz(chunks);  // chunks = bn / 16 is a power of two
       for (int item = slice * per; item < it_end; ++item) {
-        const int sb = item / chunks;
-        const int c = (item - sb * chunks) * 16;
+        const int sb = item >> lgc;
+        const int c = (item & (chunks - 1)) * 16;
         if (sb != cur_sb) {
           cur_sb = sb;
           const uint32_t q = static_cast<uint32_t>(mt * a.sub + sb) * kTileM + row;  // grids < 2^31 pixels
@@ -880,7 +949,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                                static_cast<uint32_t>((acc * a.sub + sb) * a.bn + c);
         uint32_t raw[16];
         tmem_ld16(taddr, raw);  // warp-collective: every lane executes it
-        if (valid && !(a.dbg & 1)) epilogue_chunk<EB, SIG>(a, raw, d, n_tile * a.bn + c);
+        if (valid && !(a.dbg & 1)) epilogue_chunk<EB, SIG>(a, raw, d, n_tile * a.bn + c, s_vec, p2ok, c);
       }
       tc_fence_before();
       __syncwarp();
@@ -1056,7 +1125,8 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
   }
   a.dmin = dmin;
   const int ntaps = static_cast<int>(taps.size());
-  int barrier_bytes = 256;
+  int barrier_bytes = 256 + kVecArea;  // mbarriers + staged epilogue vectors
+  a.vec_off = 256;
   const int ksteps = kb / 32 > 0 ? kb / 32 : 1;  // 32-byte MMA K steps per chunk row
   const int row_bytes = kb == 16 ? 128 : kb;     // TMA row: 8 pixels (kb 16) or one pixel
   auto steps_for = [&](int pps) {
@@ -1159,6 +1229,7 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
     const int staging = (sp.OC / 4) * a.stage_stride * 16;
     // the staging buffer shares the budget with the pipeline
     barrier_bytes += staging;
+    a.vec_off = 256 + staging;
     found = try_cfg(sp.OC, sub, true);
     if (!found || a.n_stages < 2) return false;
   } else {
@@ -1353,6 +1424,14 @@ static bool encode_maps(TcConvPlan& p, const void* x, const Lay& xl, const void*
   return true;
 }
 
+static int dbg_env() {
+  static const int d = [] {
+    const char* e = std::getenv("MRB200_TC_DBG");
+    return e ? std::atoi(e) : 0;
+  }();
+  return d;
+}
+
 bool tc_conv_launch(TcConvPlan* p, const void* x, const Lay& xl, const void* w, float acc_scale, const EpiDev& epi,
                     const OutDev& out, cudaStream_t s) {
   if (p->map_x != x || p->map_w != w) {
@@ -1363,6 +1442,14 @@ bool tc_conv_launch(TcConvPlan* p, const void* x, const Lay& xl, const void* w, 
   // TC_STEM_POOL takes the window max on the accumulators: exact only when the
   // accumulator -> float map is non-decreasing
   if (a.win && !(acc_scale > 0.f)) return false;
+  {
+    int slots = 0;
+    for (int k = 0; k < kMaxEpi; ++k) {
+      a.vec_slot[k] = -1;
+      if (!(dbg_env() & 128) && k < epi.n_ops && (epi.op[k] == E_BIAS || epi.op[k] == E_MULC) && slots < kVecSlots && a.bn <= 256)
+        a.vec_slot[k] = static_cast<int8_t>(slots++);
+    }
+  }
   a.relu_last = epi.n_ops > 0 && epi.op[epi.n_ops - 1] == E_RELU;
   static const int dbg = [] {
     const char* e = std::getenv("MRB200_TC_DBG");
@@ -1379,6 +1466,19 @@ bool tc_conv_launch(TcConvPlan* p, const void* x, const Lay& xl, const void* w, 
     a.fd_shp = make_fastdiv(static_cast<uint32_t>(out.slay.Hp));
   }
   const int sig = epi_signature(epi, out);
+  auto pow2 = [](float f) {
+    int e = 0;
+    return f > 0.f && std::isfinite(f) && std::frexp(f, &e) == 0.5f;
+  };
+  a.p2 = 0;
+  if (sig == SIG_BIAS_RELU_REQ && p->spec.elem_bytes == 1 && pow2(acc_scale) && pow2(epi.q[2].c1)) {
+    const float S = acc_scale * epi.q[2].c1;
+    if (pow2(S) && std::fabs(S) >= 1e-30f && std::fabs(S) <= 1e30f) {
+      a.p2 = 1;
+      a.p2_scale = S;
+      a.p2_hi = static_cast<int32_t>(epi.q[2].hi);
+    }
+  }
 #define MRB_TC_LAUNCH(EB_, SIG_)                                                                          \
   do {                                                                                                    \
     cudaFuncSetAttribute(k_conv_tc<EB_, SIG_>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p->smem)); \

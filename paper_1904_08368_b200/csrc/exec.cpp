@@ -71,6 +71,9 @@ struct Buffer {
   int first = 0, last = 0;  // launch indices
   int64_t offset = -1;
   std::string what;
+  // zero border forever: its producer writes only interior pixels, so the
+  // buffer gets arena space of its own (never aliased) zeroed once at build
+  bool zero_border = false;
 };
 
 struct LaunchRec {
@@ -106,6 +109,7 @@ struct Exec {
   std::vector<int> fused_pool;              // conv group -> its max_pool2d consumer executed in-kernel, or -1
   std::vector<char> fused_away;             // group executed inside another group's launch
   bool weights_ready = false;
+  int64_t zero_bytes = 0;  // arena prefix of the zero-border buffers
   // io
   const float* cur_input = nullptr;
   float* out_internal = nullptr;  // result buffer (NCHW float32)
@@ -504,11 +508,20 @@ struct Builder {
 };
 
 void assign_offsets(Exec& ex) {
-  std::vector<int> order(ex.bufs.size());
-  for (size_t i = 0; i < order.size(); ++i) order[i] = static_cast<int>(i);
+  // dedicated, never-aliased region for the zero-border buffers (zeroed once)
+  int64_t base = 0;
+  for (Buffer& b : ex.bufs)
+    if (b.zero_border) {
+      b.offset = base;
+      base += round_up(std::max<int64_t>(b.bytes, 1), 256);
+    }
+  ex.zero_bytes = base;
+  std::vector<int> order;
+  for (size_t i = 0; i < ex.bufs.size(); ++i)
+    if (!ex.bufs[i].zero_border) order.push_back(static_cast<int>(i));
   std::sort(order.begin(), order.end(), [&](int a, int b) { return ex.bufs[a].bytes > ex.bufs[b].bytes; });
   std::vector<int> placed;
-  int64_t top = 0;
+  int64_t top = base;
   for (int id : order) {
     Buffer& b = ex.bufs[id];
     int64_t size = round_up(std::max<int64_t>(b.bytes, 1), 256);
@@ -520,7 +533,7 @@ void assign_offsets(Exec& ex) {
       busy.emplace_back(q.offset, q.offset + round_up(std::max<int64_t>(q.bytes, 1), 256));
     }
     std::sort(busy.begin(), busy.end());
-    int64_t off = 0;
+    int64_t off = base;
     for (auto& [s, e] : busy) {
       if (off + size <= s) break;
       off = std::max(off, e);
@@ -852,19 +865,9 @@ void build(Exec& ex) {
     bool tc_same = (path == P_CONV_I8_TC || path == P_CONV_BF16_TC) && ex.group_tc[gi].kind == TC_S1;
     const auto& zshape = fp >= 0 ? P.groups[fp].out_shape : g.out_shape;
     if (!tc_same && !has_sum && zshape.size() == 4) {
-      for (int b2 : {obuf, sbuf}) {
-        if (b2 < 0) continue;
-        LaunchRec Z;
-        Z.name = "%" + g.name;
-        Z.kernel = "zero_border";
-        Lay zl = b2 == obuf ? orep.lay : ex.reps[ov][side_rep[sgi]].lay;
-        int N = static_cast<int>(zshape[0]), H = static_cast<int>(zshape[2]), W = static_cast<int>(zshape[3]);
-        int64_t border = (zl.C + zl.cpc - 1) / zl.cpc * static_cast<int64_t>(N) * (2 * (W + 2) + 2 * H) * 16;
-        Z.bytes = static_cast<double>(border);
-        Z.fn = [e, b2, zl, N](cudaStream_t s) { launch_zero_border(e->ptr(b2), zl, N, s); };
-        ex.launches.push_back(Z);
-        ++B.launch_idx;
-      }
+      // interior-only producer: keep the padding ring zero without a per-run pass
+      for (int b2 : {obuf, sbuf})
+        if (b2 >= 0) ex.bufs[b2].zero_border = true;
     }
     if (has_sum) {
       LaunchRec S;
@@ -918,6 +921,7 @@ void build(Exec& ex) {
 
   assign_offsets(ex);
   CK(cudaMalloc(&ex.arena, static_cast<size_t>(std::max<int64_t>(ex.arena_bytes, 256))));
+  if (ex.zero_bytes) CK(cudaMemset(ex.arena, 0, static_cast<size_t>(ex.zero_bytes)));
 }
 
 }  // namespace mrb200

@@ -741,7 +741,7 @@ __global__ void k_sum_hw(const float* __restrict__ x, Lay L, int N, int H, int W
 //   mode 0: int8 codes, dp4a, int32 acc * acc_scale (exact)
 //   mode 1: float32 strict, sequential k (kernels.cpp:618-623), weights [M][K]
 //   mode 2: bf16 weights, fp32 FMA accumulate
-constexpr int kDenseRows = 16;
+constexpr int kDenseRows = 8;
 
 __global__ void __launch_bounds__(256) k_dense(const float* __restrict__ x, int N, int K, int Kp,
                                                const void* __restrict__ w, int M, int mode, float pre_mul, int quant,
@@ -767,7 +767,19 @@ __global__ void __launch_bounds__(256) k_dense(const float* __restrict__ x, int 
 #pragma unroll
     for (int r = 0; r < kDenseRows; ++r) acc[r] = 0;
     const int32_t* wt = static_cast<const int32_t*>(w);
-    for (int kw = 0; kw < Kp / 4; ++kw) {
+    const int KW = Kp / 4;
+    int kw = 0;
+    for (; kw + 8 <= KW; kw += 8) {  // 8 weight words in flight per thread
+      int32_t wv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) wv[u] = __ldg(wt + static_cast<int64_t>(kw + u) * M + j);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int r = 0; r < kDenseRows; ++r)
+          acc[r] = __dp4a(*reinterpret_cast<const int32_t*>(scode + r * Kp + (kw + u) * 4), wv[u], acc[r]);
+    }
+    for (; kw < KW; ++kw) {
       const int32_t wv = __ldg(wt + static_cast<int64_t>(kw) * M + j);
 #pragma unroll
       for (int r = 0; r < kDenseRows; ++r)
@@ -788,7 +800,17 @@ __global__ void __launch_bounds__(256) k_dense(const float* __restrict__ x, int 
     const uint16_t* wt = static_cast<const uint16_t*>(w);
 #pragma unroll
     for (int r = 0; r < kDenseRows; ++r) res[r] = 0.0f;
-    for (int k = 0; k < K; ++k) {
+    int k = 0;
+    for (; k + 8 <= K; k += 8) {
+      float wv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) wv[u] = bf16_to_f32(__ldg(wt + static_cast<int64_t>(k + u) * M + j));
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int r = 0; r < kDenseRows; ++r) res[r] = __fmaf_rn(srow[r * Kp + k + u], wv[u], res[r]);
+    }
+    for (; k < K; ++k) {
       const float wv = bf16_to_f32(__ldg(wt + static_cast<int64_t>(k) * M + j));
 #pragma unroll
       for (int r = 0; r < kDenseRows; ++r) res[r] = __fmaf_rn(srow[r * Kp + k], wv, res[r]);
