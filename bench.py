@@ -141,11 +141,11 @@ def load(precision):
     return mrb, modelzoo, text, meta, src, wl
 
 
-def time_ours(precision, batch, steps, warmup, rank, world, local):
+def time_ours(precision, batch, steps, warmup, rank, world, local, graph=True):
     """Device-resident throughput + e2e + per-launch profile for one precision."""
     import torch
     mrb, modelzoo, text, meta, src, wl = load(precision)
-    ex = mrb.Executor(text, batch=batch, device=local)
+    ex = mrb.Executor(text, batch=batch, device=local, use_cuda_graph=graph)
     ex.set_weights(wl)
     x_host = modelzoo.make_inputs(src, batch, seed=rank)
     x_dev = torch.from_numpy(x_host).to(f"cuda:{local}")
@@ -227,7 +227,8 @@ def roofline(res, precision, pk):
     # aggregate by kernel family
     fam = {}
     for L, ms in zip(desc["launches"], per):
-        f = fam.setdefault(L["kernel"], {"ms": 0.0, "bytes": 0.0, "flops": 0.0, "n": 0})
+        # "conv_i8_tcgen05+max_pool" (the fused stem) is the same kernel family
+        f = fam.setdefault(L["kernel"].split("+")[0], {"ms": 0.0, "bytes": 0.0, "flops": 0.0, "n": 0})
         f["ms"] += ms
         f["bytes"] += L["bytes"]
         f["flops"] += L["flops"]
@@ -249,8 +250,8 @@ def roofline(res, precision, pk):
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
         t = json.load(open(tf)).get(precision, {}).get(name)
-        if t is not None:
-            traffic = t
+        if t is not None:  # DRAM bytes of the family per step (ncu), same unit as `algorithmic.bytes`
+            traffic = t["bytes_per_step"]
     # whole-step roofline: sum over launches of max(bytes/BW, flops/peak)
     t_roof = sum(max(L["bytes"] / (hbm * 1e9), L["flops"] / (tc * 1e12)) for L in desc["launches"])
     return {"kernel": name, "launches": f["n"], "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
@@ -259,6 +260,21 @@ def roofline(res, precision, pk):
             "algorithmic": {"bytes": f["bytes"], "ops": f["flops"], "avg_ms": f["ms"] / f["n"]},
             "step_roofline_ms": t_roof * 1e3, "step_profiled_ms": total_ms,
             "step_frac": (t_roof * 1e3) / total_ms}
+
+
+def per_launch_table(res, precision, pk):
+    """Every launch of one step: algorithmic bytes / ops, live device time and
+    its own roofline fraction (max of the HBM and tensor-pipe bounds)."""
+    hbm = pk["hbm_gbs"] * 1e9
+    tc = pk["bf16_tflops"] * 1e12 * (2.0 if precision == "int8" else 1.0)
+    out = []
+    for L, ms in zip(res["desc"]["launches"], res["per_launch_ms"]):
+        t_roof = max(L["bytes"] / hbm, L["flops"] / tc)
+        out.append({"launch": L["name"], "kernel": L["kernel"], "bytes": L["bytes"], "ops": L["flops"],
+                    "ms": round(ms, 4), "roof_ms": round(t_roof * 1e3, 4),
+                    "bound": "hbm" if L["bytes"] / hbm >= L["flops"] / tc else "tensor",
+                    "frac": round(t_roof * 1e3 / ms, 3) if ms > 0 else None})
+    return out
 
 
 def cpu_reference(precision, images, procs, timeout=900):
@@ -313,6 +329,9 @@ def main():
     ap.add_argument("--batch", type=int, default=BATCH_PER_GPU, help="images per GPU per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-bf16", action="store_true")
+    ap.add_argument("--no-cuda-graph", action="store_true",
+                    help="replay the launch list without a CUDA graph (for ncu launch lists: ncu cannot replay "
+                         "the captured graph)")
     args = ap.parse_args()
     rank, world, local = dist_env()
     warmup = max(args.warmup, 3)
@@ -353,11 +372,11 @@ def main():
     else:
         torch.cuda.set_device(local)
     pk = peaks()
-    res = time_ours("int8", args.batch, args.steps, warmup, rank, world, local)
+    res = time_ours("int8", args.batch, args.steps, warmup, rank, world, local, not args.no_cuda_graph)
     roof = roofline(res, "int8", pk)
     bf16 = None
     if not args.no_bf16:
-        rb = time_ours("fp32", args.batch, args.steps, warmup, rank, world, local)
+        rb = time_ours("fp32", args.batch, args.steps, warmup, rank, world, local, not args.no_cuda_graph)
         bf16 = {"value": rb["value"], "unit": UNIT, "ms_per_step": rb["ms_step"], "e2e": rb["e2e"],
                 "roofline": roofline(rb, "bf16", pk), "gpu_launches": rb["launches"] * args.steps,
                 "module": "models/resnet18_fp32.fused.rly (bf16 operands, fp32 accumulate)"}
@@ -375,7 +394,8 @@ def main():
                 "config": config, "e2e": res["e2e"], "gpu_launches": res["launches"] * args.steps,
                 "clocks": res["clocks"], "roofline": roof, "cpu_baseline": cpu, "bf16": bf16,
                 "per_group_ms": {L["name"] + ":" + L["kernel"]: round(ms, 4)
-                                 for L, ms in zip(res["desc"]["launches"], res["per_launch_ms"])}}
+                                 for L, ms in zip(res["desc"]["launches"], res["per_launch_ms"])},
+                "per_launch": per_launch_table(res, "int8", pk)}
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
