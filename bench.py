@@ -395,7 +395,8 @@ def main():
                 "clocks": res["clocks"], "roofline": roof, "cpu_baseline": cpu, "bf16": bf16,
                 "per_group_ms": {L["name"] + ":" + L["kernel"]: round(ms, 4)
                                  for L, ms in zip(res["desc"]["launches"], res["per_launch_ms"])},
-                "per_launch": per_launch_table(res, "int8", pk)}
+                "per_launch": per_launch_table(res, "int8", pk),
+                "plans": {g["name"]: g["kernel"] + (": " + g["plan"] if g["plan"] else "") for g in res["desc"]["groups"]}}
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

@@ -43,6 +43,7 @@
 #include <vector>
 
 #include "conv_tc.hpp"
+#include "launch.hpp"
 
 namespace mrb200 {
 
@@ -126,8 +127,8 @@ struct TcArgs {
   FastDiv fd_wg, fd_hg;    // M-grid decode (pixel -> n, y, x)
   FastDiv fd_swp, fd_shp;  // side output PHASE decode (padded grid)
   FastDiv fd_pow;          // fused pool: item -> (granule, pooled column)
-  int32_t dbg;  // MRB200_TC_DBG (timing experiments only): 1 skip epilogue math, 2 hoisted descriptors, 4 no MMAs,
-                //   16 CTA-0 timestamps of the fused-pool epilogue
+  int32_t dbg;  // MRB200_TC_DBG (timing experiments only, wrong results): 1 skip epilogue math, 4 no MMAs,
+                //   16 CTA-0 timestamps of the fused-pool epilogue, 1024 kernel phase times (globaltimer)
   unsigned long long* stamps;
   EpiDev epi;
   OutDev out;
@@ -533,6 +534,13 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  auto gtime = [] {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+  };
+  if ((a.dbg & 1024) && threadIdx.x == 0) atomicMin(&a.stamps[0], gtime());
+  pdl_trigger();  // the next launch may start its own prologue as SMs free up
   const int n_tile = blockIdx.x % a.n_tiles;
   const int m_start = blockIdx.x / a.n_tiles;
   const int m_step = gridDim.x / a.n_tiles;
@@ -552,6 +560,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+    // resident weights are static (prepared at set_weights): load them before
+    // waiting for the previous kernel
+    if (a.resident_b) {
+      mbar_expect_tx(bfull, a.b_res_bytes);
+      tma_load_4d(smB, &tmB, bfull, 0, n_tile * a.bn / (a.kb == 16 ? 8 : 1), 0, 0);
+    }
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -584,15 +598,13 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // activations (A, residuals, outputs) belong to the previous kernels from here on
+  if ((a.dbg & 1024) && threadIdx.x == 0) atomicMax(&a.stamps[1], gtime());
 
   const int msub = a.win ? kTileM : a.sub * kTileM;  // grid rows per M tile
   if (warp == 0) {
     if (lane == 0) {
       // ===== TMA producer =====
-      if (a.resident_b) {
-        mbar_expect_tx(bfull, a.b_res_bytes);
-        tma_load_4d(smB, &tmB, bfull, 0, n_tile * a.bn / (a.kb == 16 ? 8 : 1), 0, 0);
-      }
       const int row_bytes = a.kb == 16 ? 128 : a.kb;
       int stage = 0;
       uint32_t phase = 0;
@@ -602,7 +614,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         const int r0 = a.kb == 16 ? floor_div8(row0) : row0;
         for (int ks = 0; ks < a.k_stages; ++ks) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], a.a_stage_bytes + (a.resident_b ? 0 : a.b_stage_bytes));
+          const bool load_b = !a.resident_b;
+          mbar_expect_tx(&full[stage], a.a_stage_bytes + (load_b ? a.b_stage_bytes : 0));
           // A stage layout [pps][subs][hg rows][row]: one box per (plane, sub-grid, row block)
           uint8_t* dA = smA + stage * a.a_stage_bytes;
           for (int pl = 0; pl < a.pps; ++pl)
@@ -610,7 +623,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
               for (int bx = 0; bx < a.nbox; ++bx)
                 tma_load_4d(dA + ((pl * a.subs + sg) * a.hg + bx * a.hbox) * row_bytes, &tmA, &full[stage], 0,
                             r0 + bx * a.hbox, a.region_sg[sg], ks * a.pps + pl);
-          if (!a.resident_b)
+          if (load_b)
             tma_load_4d(smB + stage * a.b_stage_bytes, &tmB, &full[stage], 0, n_tile * a.bn / (a.kb == 16 ? 8 : 1),
                         ks * a.pps, 0);
           if (++stage == a.n_stages) {
@@ -961,6 +974,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     }
   }
 epilogue_done:
+  if ((a.dbg & 1024) && threadIdx.x == 64) atomicMax(&a.stamps[3], gtime());
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -1457,14 +1471,33 @@ bool tc_conv_launch(TcConvPlan* p, const void* x, const Lay& xl, const void* w, 
   }();
   a.dbg = dbg;
   static unsigned long long* stamps = nullptr;
-  if ((dbg & 16) && !stamps) cudaMalloc(&stamps, 8 * 16 * 8);
+  if ((dbg & (16 | 1024)) && !stamps) cudaMalloc(&stamps, 8 * 16 * 8);
   a.stamps = stamps;
+  if (dbg & 1024) {
+    unsigned long long init[4] = {~0ull, 0ull, ~0ull, 0ull};
+    cudaMemcpyAsync(stamps, init, sizeof(init), cudaMemcpyHostToDevice, s);
+  }
   a.epi = epi;
   a.out = out;
   if (out.side && out.slay.kind == LAY_PHASE) {
     a.fd_swp = make_fastdiv(static_cast<uint32_t>(out.slay.Wp));
     a.fd_shp = make_fastdiv(static_cast<uint32_t>(out.slay.Hp));
   }
+  struct StampPrint {  // dbg 1024: kernel phase times (globaltimer ns) of this launch
+    cudaStream_t s;
+    unsigned long long* st;
+    TcConvPlan* p;
+    bool on;
+    ~StampPrint() {
+      if (!on) return;
+      unsigned long long h[4];
+      cudaStreamSynchronize(s);
+      cudaMemcpy(h, st, sizeof(h), cudaMemcpyDeviceToHost);
+      char buf[256];
+      std::fprintf(stderr, "TCSTAMP prologue %.2f us, end %.2f us | %s\n", (h[1] - h[0]) / 1e3, (h[3] - h[0]) / 1e3,
+                   tc_conv_describe(p, buf, sizeof(buf)));
+    }
+  } stamp_print{s, stamps, p, (dbg & 1024) != 0};
   const int sig = epi_signature(epi, out);
   auto pow2 = [](float f) {
     int e = 0;
@@ -1482,7 +1515,7 @@ bool tc_conv_launch(TcConvPlan* p, const void* x, const Lay& xl, const void* w, 
 #define MRB_TC_LAUNCH(EB_, SIG_)                                                                          \
   do {                                                                                                    \
     cudaFuncSetAttribute(k_conv_tc<EB_, SIG_>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p->smem)); \
-    k_conv_tc<EB_, SIG_><<<p->grid, kThreadsTc, p->smem, s>>>(p->tmA, p->tmB, a);                       \
+    pdl_launch(k_conv_tc<EB_, SIG_>, p->grid, kThreadsTc, p->smem, s, p->tmA, p->tmB, a);                 \
   } while (0)
 #define MRB_TC_SIGS(EB_)                                          \
   switch (sig) {                                                  \

@@ -108,6 +108,12 @@ inline FastDiv make_fastdiv(uint32_t d) {
 
 #ifdef __CUDACC__
 
+// Programmatic dependent launch: every graph kernel lets the next one start
+// its independent prologue at once (trigger) and waits for the previous
+// kernel's results before touching activations (wait; a no-op without PDL).
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
   return f.s < 0 ? n : (__umulhi(n, f.m) >> (f.s - 1));
 }

@@ -47,6 +47,8 @@ __device__ __forceinline__ Pix decode_pix(int64_t pix, int32_t H, int32_t W) {
 // channel padding of the last chunk.
 __global__ void k_input_convert(const float* __restrict__ x, int N, int C, int H, int W, void* out, int fmt,
                                 Lay L, int s2d_pad, float pre_mul, QDev q) {
+  pdl_trigger();
+  pdl_wait();
   const int eb = L.kb / L.cpc;
   const int gpc = L.kb / 16;       // 16-byte granules per chunk
   const int cpg = 16 / eb;         // channels per granule
@@ -140,6 +142,8 @@ __device__ __forceinline__ void s2d_prefetch(float* buf, const float* __restrict
 
 __global__ void __launch_bounds__(128) k_input_s2d(const float* __restrict__ x, int N, int C, int H, int W, void* out,
                                                    int fmt, Lay L, int pad, float pre_mul, QDev q) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ __align__(16) float rows[];  // 2 x [C][2][W]
   const int stride = 2 * C * W;
   const int n_rows = N * L.Hq;
@@ -224,6 +228,8 @@ __global__ void __launch_bounds__(128) k_input_s2d(const float* __restrict__ x, 
 template <int C, int PAD, int CPC, bool PHASED>
 __global__ void __launch_bounds__(128) k_input_s2d_ct(const float* __restrict__ x, int N, int H, int W, void* out,
                                                       Lay L, float pre_mul, QDev q, FastDiv fd_w4) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ __align__(16) float rows[];  // 2 x [C][2][W]
   constexpr int PLANES = (4 * C + CPC - 1) / CPC;
   constexpr int OFF = PHASED ? 2 : 0;                  // s2d index = grid index - OFF
@@ -313,6 +319,8 @@ __global__ void __launch_bounds__(128) k_input_s2d_ct(const float* __restrict__ 
 // fmt FMT_I8: realize codes, the value is code * c2 (exact).
 __global__ void k_to_nchw(const void* __restrict__ x, int fmt, Lay L, float c2, float* __restrict__ y, int N, int C,
                           int H, int W, int is4d) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t total = static_cast<int64_t>(N) * C * H * W;
   GRID_STRIDE(i, total) {
     int w = static_cast<int>(i % W);
@@ -331,6 +339,8 @@ __global__ void k_to_nchw(const void* __restrict__ x, int fmt, Lay L, float c2, 
 // ---- zero the one-pixel border of a P16 buffer (after producers that write
 // interior pixels only) -- NORMAL or PHASE layout -----------------------------------
 __global__ void k_zero_border(void* buf, Lay L, int N) {
+  pdl_trigger();
+  pdl_wait();
   const int32_t Hp = L.Hp, Wp = L.Wp, H = Hp - 2 * kPad;
   const int32_t per = 2 * Wp + 2 * H;  // border pixels per image
   const int planes = (L.C + L.cpc - 1) / L.cpc;
@@ -460,6 +470,8 @@ __device__ __forceinline__ OutPix decode_out(int64_t m, const ConvGeom& g) {
 // quanta (checked statically at weight load).
 __global__ void __launch_bounds__(256) k_conv_i8_simt(const int8_t* __restrict__ x, const int8_t* __restrict__ w,
                                                       ConvGeom g, float acc_scale, EpiDev epi, OutDev out) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ int32_t As[8][64 + 4];
   __shared__ int32_t Bs[8][64 + 4];
   const int64_t M = static_cast<int64_t>(g.N) * g.OH * g.OW;
@@ -527,6 +539,8 @@ __global__ void __launch_bounds__(256) k_conv_i8_simt(const int8_t* __restrict__
 // ---- convolution, bf16 operands, fp32 accumulate (CUDA cores) --------------------
 __global__ void __launch_bounds__(256) k_conv_bf16_simt(const uint16_t* __restrict__ x, const uint16_t* __restrict__ w,
                                                         ConvGeom g, EpiDev epi, OutDev out) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float As[16][64 + 4];
   __shared__ float Bs[16][64 + 4];
   const int64_t M = static_cast<int64_t>(g.N) * g.OH * g.OW;
@@ -592,6 +606,8 @@ __global__ void __launch_bounds__(256) k_conv_bf16_simt(const uint16_t* __restri
 // (kernels.cpp:681-701), product and sum each rounded (no FMA).
 __global__ void k_conv_f32_strict(const float* __restrict__ x, const float* __restrict__ w, ConvGeom g,
                                   EpiDev epi, OutDev out) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t total = static_cast<int64_t>(g.N) * g.OH * g.OW * g.OC;
   GRID_STRIDE(i, total) {
     int oc = static_cast<int>(i % g.OC);
@@ -616,6 +632,8 @@ __global__ void k_conv_f32_strict(const float* __restrict__ x, const float* __re
 // ---- depthwise convolution (float; reference order kh -> kw) ---------------------
 __global__ void k_dwconv(const void* __restrict__ x, int xfmt, const float* __restrict__ w, ConvGeom g, int strict,
                          EpiDev epi, OutDev out) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t total = static_cast<int64_t>(g.N) * g.OH * g.OW * g.C;
   GRID_STRIDE(i, total) {
     int c = static_cast<int>(i % g.C);
@@ -642,6 +660,8 @@ __global__ void k_dwconv(const void* __restrict__ x, int xfmt, const float* __re
 // (padded taps skipped, like the reference's bounds test).  Also emits the
 // consumers' second copy (int8 codes or bf16) when requested.
 __global__ void k_maxpool(const void* __restrict__ x, int xfmt, ConvGeom g, OutDev out) {
+  pdl_trigger();
+  pdl_wait();
   const int eb = xfmt == FMT_F32 ? 4 : 2;
   const int cpg = 16 / eb;  // channels per 16-byte granule
   const uint32_t grans = static_cast<uint32_t>((g.C + cpg - 1) / cpg);
@@ -721,6 +741,8 @@ __global__ void k_maxpool(const void* __restrict__ x, int xfmt, ConvGeom g, OutD
 // reduce_impl (kernels.cpp:519-566) visits the input row-major, so for a fixed
 // (n, c) the terms arrive in (h, w) order.  Input P16 float32, output [N, C].
 __global__ void k_sum_hw(const float* __restrict__ x, Lay L, int N, int H, int W, int C, float* __restrict__ y) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t total = static_cast<int64_t>(N) * C;
   GRID_STRIDE(i, total) {
     int c = static_cast<int>(i % C);
@@ -746,6 +768,8 @@ constexpr int kDenseRows = 8;
 __global__ void __launch_bounds__(256) k_dense(const float* __restrict__ x, int N, int K, int Kp,
                                                const void* __restrict__ w, int M, int mode, float pre_mul, int quant,
                                                QDev q, float acc_scale, EpiDev epi, OutDev out) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ float srow[];  // [kDenseRows][Kp] floats (mode 1/2) or bytes (mode 0)
   const int n0 = blockIdx.y * kDenseRows;
   int8_t* scode = reinterpret_cast<int8_t*>(srow);
@@ -849,6 +873,18 @@ __global__ void k_dense_weight_t(const float* __restrict__ w, int M, int K, int 
   }
 }
 
+}  // namespace
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("MRB200_NO_PDL");
+    return !(e && std::atoi(e));
+  }();
+  return on;
+}
+
+namespace {
+
 unsigned grid_stride_blocks(int64_t total) {
   int64_t b = (total + kThreads - 1) / kThreads;
   if (b > 148 * 32) b = 148 * 32;
@@ -874,7 +910,7 @@ void launch_input_convert(const float* x, int N, int C, int H, int W, void* out,
     }
     const FastDiv fd = make_fastdiv(static_cast<uint32_t>(W / 4));
     const int rows = N * 2 * L.Hq;
-    k_input_s2d_ct<3, 3, 16, true><<<std::min(rows, sms2 * 8), 128, 2 * 2 * C * W * sizeof(float), s>>>(
+    pdl_launch(k_input_s2d_ct<3, 3, 16, true>, std::min(rows, sms2 * 8), 128, 2 * 2 * C * W * sizeof(float), s, 
         x, N, H, W, out, L, pre_mul, q, fd);
     return;
   }
@@ -892,32 +928,32 @@ void launch_input_convert(const float* x, int N, int C, int H, int W, void* out,
     if (C == 3 && s2d_pad == 3 && L.kb == 16 && (fmt == FMT_I8 || fmt == FMT_BF16)) {
       const FastDiv fd = make_fastdiv(static_cast<uint32_t>(W / 4));
       if (fmt == FMT_I8)
-        k_input_s2d_ct<3, 3, 16, false><<<std::min(rows, sms * 8), 128, smem, s>>>(x, N, H, W, out, L, pre_mul, q, fd);
+        pdl_launch(k_input_s2d_ct<3, 3, 16, false>, std::min(rows, sms * 8), 128, smem, s, x, N, H, W, out, L, pre_mul, q, fd);
       else
-        k_input_s2d_ct<3, 3, 8, false><<<std::min(rows, sms * 8), 128, smem, s>>>(x, N, H, W, out, L, pre_mul, q, fd);
+        pdl_launch(k_input_s2d_ct<3, 3, 8, false>, std::min(rows, sms * 8), 128, smem, s, x, N, H, W, out, L, pre_mul, q, fd);
       return;
     }
-    k_input_s2d<<<std::min(rows, sms * 8), 128, 2 * 2 * C * W * sizeof(float), s>>>(x, N, C, H, W, out, fmt, L,
+    pdl_launch(k_input_s2d, std::min(rows, sms * 8), 128, 2 * 2 * C * W * sizeof(float), s, x, N, C, H, W, out, fmt, L,
                                                                                   s2d_pad, pre_mul, q);
     return;
   }
   int planes = L.kind == LAY_S2D ? (4 * C + L.cpc - 1) / L.cpc : (C + L.cpc - 1) / L.cpc;
   int64_t grid_pix = L.kind == LAY_S2D ? static_cast<int64_t>(N) * L.Hq * L.Wq
                                        : static_cast<int64_t>(N) * (H + 2 * kPad) * (W + 2 * kPad);
-  k_input_convert<<<grid_stride_blocks(planes * (L.kb / 16) * grid_pix), kThreads, 0, s>>>(x, N, C, H, W, out, fmt, L, s2d_pad,
+  pdl_launch(k_input_convert, grid_stride_blocks(planes * (L.kb / 16) * grid_pix), kThreads, 0, s, x, N, C, H, W, out, fmt, L, s2d_pad,
                                                                             pre_mul, q);
 }
 
 void launch_to_nchw(const void* x, int fmt, const Lay& L, float c2, float* y, int N, int C, int H, int W, int is4d,
                     cudaStream_t s) {
   int64_t total = static_cast<int64_t>(N) * C * H * W;
-  k_to_nchw<<<grid_stride_blocks(total), kThreads, 0, s>>>(x, fmt, L, c2, y, N, C, H, W, is4d);
+  pdl_launch(k_to_nchw, grid_stride_blocks(total), kThreads, 0, s, x, fmt, L, c2, y, N, C, H, W, is4d);
 }
 
 void launch_zero_border(void* buf, const Lay& L, int N, cudaStream_t s) {
   int planes = (L.C + L.cpc - 1) / L.cpc;
   int64_t total = static_cast<int64_t>(planes) * N * (2 * L.Wp + 2 * (L.Hp - 2 * kPad));
-  k_zero_border<<<grid_stride_blocks(total), kThreads, 0, s>>>(buf, L, N);
+  pdl_launch(k_zero_border, grid_stride_blocks(total), kThreads, 0, s, buf, L, N);
 }
 
 void launch_weight_prep(const float* w, int O, int I, int KH, int KW, int Cs, int wl, const float* oc_scale,
@@ -938,37 +974,37 @@ void launch_conv_i8_simt(const int8_t* x, const int8_t* w, const ConvGeom& g, fl
                          const EpiDev& epi, const OutDev& out, cudaStream_t s) {
   int64_t M = static_cast<int64_t>(g.N) * g.OH * g.OW;
   dim3 grid(static_cast<unsigned>((M + 63) / 64), static_cast<unsigned>((g.OC + 63) / 64));
-  k_conv_i8_simt<<<grid, 256, 0, s>>>(x, w, g, acc_scale, epi, out);
+  pdl_launch(k_conv_i8_simt, grid, 256, 0, s, x, w, g, acc_scale, epi, out);
 }
 
 void launch_conv_bf16_simt(const uint16_t* x, const uint16_t* w, const ConvGeom& g, const EpiDev& epi,
                            const OutDev& out, cudaStream_t s) {
   int64_t M = static_cast<int64_t>(g.N) * g.OH * g.OW;
   dim3 grid(static_cast<unsigned>((M + 63) / 64), static_cast<unsigned>((g.OC + 63) / 64));
-  k_conv_bf16_simt<<<grid, 256, 0, s>>>(x, w, g, epi, out);
+  pdl_launch(k_conv_bf16_simt, grid, 256, 0, s, x, w, g, epi, out);
 }
 
 void launch_conv_f32_strict(const float* x, const float* w, const ConvGeom& g, const EpiDev& epi,
                             const OutDev& out, cudaStream_t s) {
   int64_t total = static_cast<int64_t>(g.N) * g.OH * g.OW * g.OC;
-  k_conv_f32_strict<<<grid_stride_blocks(total), kThreads, 0, s>>>(x, w, g, epi, out);
+  pdl_launch(k_conv_f32_strict, grid_stride_blocks(total), kThreads, 0, s, x, w, g, epi, out);
 }
 
 void launch_dwconv(const void* x, int xfmt, const float* w, const ConvGeom& g, int strict, const EpiDev& epi,
                    const OutDev& out, cudaStream_t s) {
   int64_t total = static_cast<int64_t>(g.N) * g.OH * g.OW * g.C;
-  k_dwconv<<<grid_stride_blocks(total), kThreads, 0, s>>>(x, xfmt, w, g, strict, epi, out);
+  pdl_launch(k_dwconv, grid_stride_blocks(total), kThreads, 0, s, x, xfmt, w, g, strict, epi, out);
 }
 
 void launch_maxpool(const void* x, int xfmt, const ConvGeom& g, const OutDev& out, cudaStream_t s) {
   int cpg = xfmt == FMT_F32 ? 4 : 8;
   int64_t total = static_cast<int64_t>(g.N) * g.OH * g.OW * ((g.C + cpg - 1) / cpg);
-  k_maxpool<<<grid_stride_blocks(total), kThreads, 0, s>>>(x, xfmt, g, out);
+  pdl_launch(k_maxpool, grid_stride_blocks(total), kThreads, 0, s, x, xfmt, g, out);
 }
 
 void launch_sum_hw(const float* x, const Lay& L, int N, int H, int W, int C, float* y, cudaStream_t s) {
   int64_t total = static_cast<int64_t>(N) * C;
-  k_sum_hw<<<grid_stride_blocks(total), kThreads, 0, s>>>(x, L, N, H, W, C, y);
+  pdl_launch(k_sum_hw, grid_stride_blocks(total), kThreads, 0, s, x, L, N, H, W, C, y);
 }
 
 void launch_dense_weight_t(const float* w, int M, int K, int Kp, const float* oc_scale, float scalar, int fmt,
@@ -982,7 +1018,7 @@ void launch_dense(const float* x, int N, int K, int Kp, const void* w, int M, in
   dim3 grid(static_cast<unsigned>((M + 255) / 256), static_cast<unsigned>((N + kDenseRows - 1) / kDenseRows));
   size_t smem = (mode == 0 ? static_cast<size_t>(Kp) : static_cast<size_t>(Kp) * sizeof(float)) * kDenseRows;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  k_dense<<<grid, 256, smem, s>>>(x, N, K, Kp, w, M, mode, pre_mul, quant, q, acc_scale, epi, out);
+  pdl_launch(k_dense, grid, 256, smem, s, x, N, K, Kp, w, M, mode, pre_mul, quant, q, acc_scale, epi, out);
 }
 
 }  // namespace mrb200

@@ -9,6 +9,25 @@
 
 namespace mrb200 {
 
+// Launches a graph kernel with programmatic stream serialization (PDL): it may
+// start while its predecessor drains; the kernel calls pdl_wait() before
+// reading or writing activations.  MRB200_NO_PDL=1 launches plainly.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline void pdl_launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 enum WeightLayout : int { WL_ROWS = 0, WL_TC = 1, WL_S2D = 2 };
 
 void launch_input_convert(const float* x, int N, int C, int H, int W, void* out, int fmt, const Lay& L,
