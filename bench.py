@@ -37,12 +37,24 @@ BATCH_PER_GPU = 256
 
 
 def peaks():
+    """HBM and bf16 from the driver's MEASURED_PEAKS.json; the int8 tensor peak
+    (no cuBLAS int8 figure there) from our tcgen05 kind::i8 microbenchmark
+    (tests/tc_peak.cu -> profiles/tc_peak.json, N=256), else 2x bf16."""
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
-                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]), "source": "measured"}
-    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+        pk = {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+              "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]), "source": "measured"}
+    else:
+        pk = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+    tp = os.path.join(ROOT, "profiles", "tc_peak.json")
+    if os.path.exists(tp):
+        pk["i8_tops"] = json.load(open(tp))["i8_tops"]["256"]
+        pk["i8_source"] = "tcgen05 kind::i8 microbenchmark, N=256 (profiles/tc_peak.json)"
+    else:
+        pk["i8_tops"] = 2.0 * pk["bf16_tflops"]
+        pk["i8_source"] = "2x measured bf16 (estimate)"
+    return pk
 
 
 class ClockSampler:
@@ -236,7 +248,7 @@ def roofline(res, precision, pk):
     top = max(fam.items(), key=lambda kv: kv[1]["ms"])
     name, f = top
     hbm = pk["hbm_gbs"]
-    tc = pk["bf16_tflops"] * (2.0 if precision == "int8" else 1.0)  # int8 = 2x measured bf16 (estimate)
+    tc = pk["i8_tops"] if precision == "int8" else pk["bf16_tflops"]
     t_mem = f["bytes"] / (hbm * 1e9)
     t_tc = f["flops"] / (tc * 1e12)
     bound = "hbm" if t_mem >= t_tc else "tensor"
@@ -256,7 +268,7 @@ def roofline(res, precision, pk):
     t_roof = sum(max(L["bytes"] / (hbm * 1e9), L["flops"] / (tc * 1e12)) for L in desc["launches"])
     return {"kernel": name, "launches": f["n"], "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
             "frac": achieved / peak, "traffic": traffic, "share_of_step": f["ms"] / total_ms,
-            "peak_source": pk["source"] + ("" if precision != "int8" else "; int8 tensor peak = 2x measured bf16 (estimate)"),
+            "peak_source": pk["source"] + ("" if precision != "int8" else "; int8 tensor peak: " + pk["i8_source"]),
             "algorithmic": {"bytes": f["bytes"], "ops": f["flops"], "avg_ms": f["ms"] / f["n"]},
             "step_roofline_ms": t_roof * 1e3, "step_profiled_ms": total_ms,
             "step_frac": (t_roof * 1e3) / total_ms}
@@ -266,7 +278,7 @@ def per_launch_table(res, precision, pk):
     """Every launch of one step: algorithmic bytes / ops, live device time and
     its own roofline fraction (max of the HBM and tensor-pipe bounds)."""
     hbm = pk["hbm_gbs"] * 1e9
-    tc = pk["bf16_tflops"] * 1e12 * (2.0 if precision == "int8" else 1.0)
+    tc = (pk["i8_tops"] if precision == "int8" else pk["bf16_tflops"]) * 1e12
     out = []
     for L, ms in zip(res["desc"]["launches"], res["per_launch_ms"]):
         t_roof = max(L["bytes"] / hbm, L["flops"] / tc)
