@@ -218,3 +218,21 @@ void mro_max_pool2d_f32(const float* x, float* y, int64_t N, int64_t C, int64_t 
           y[((n * C + c) * OH + oh) * OW + ow] = acc;
         }
 }
+
+void mro_dwconv2d_f32(const float* x, const float* w, float* y, int64_t N, int64_t C, int64_t H, int64_t W,
+                      int64_t KH, int64_t KW, int64_t sh, int64_t sw, int64_t ph, int64_t pw) {
+  const int64_t OH = (H - KH + 2 * ph) / sh + 1, OW = (W - KW + 2 * pw) / sw + 1;
+  for (int64_t n = 0; n < N; ++n)
+    for (int64_t c = 0; c < C; ++c)
+      for (int64_t oh = 0; oh < OH; ++oh)
+        for (int64_t ow = 0; ow < OW; ++ow) {
+          float acc = 0.0f;
+          for (int64_t kh = 0; kh < KH; ++kh)
+            for (int64_t kw = 0; kw < KW; ++kw) {
+              const int64_t h = oh * sh - ph + kh, ww = ow * sw - pw + kw;
+              if (h < 0 || h >= H || ww < 0 || ww >= W) continue;
+              acc += x[((n * C + c) * H + h) * W + ww] * w[(c * KH + kh) * KW + kw];
+            }
+          y[((n * C + c) * OH + oh) * OW + ow] = acc;
+        }
+}

@@ -51,6 +51,7 @@ def lib():
         L.mro_sum_f32.argtypes = [P, P, P, I, P]
         L.mro_max_pool2d_f32.argtypes = [P, P] + [I64] * 10
         L.mro_simq_f32.argtypes = [P, P, I64, ctypes.c_double, I, I]
+        L.mro_dwconv2d_f32.argtypes = [P, P, P] + [I64] * 10
         L.mro_set_threads(os.cpu_count() or 1)
         _lib = L
     return _lib
@@ -165,6 +166,25 @@ def op_max_pool2d(x, win, strides=(1, 1), padding=(0, 0)):
     return y
 
 
+def op_depthwise_conv2d(x, win, w, strides=(1, 1), padding=(0, 0)):
+    x, w = _f32(x), _f32(w)
+    N, C, H, W = x.shape
+    KH, KW = w.shape[2], w.shape[3]
+    sh, sw = strides
+    ph, pw = padding
+    OH, OW = (H - KH + 2 * ph) // sh + 1, (W - KW + 2 * pw) // sw + 1
+    y = np.empty((N, C, OH, OW), np.float32)
+    lib().mro_dwconv2d_f32(_p(x), _p(w), _p(y), N, C, H, W, KH, KW, sh, sw, ph, pw)
+    return y
+
+
+def op_reshape(x, newshape):
+    """kernels.cpp:390-397: a view (same row-major data, new shape)."""
+    if isinstance(x, IntTensor):
+        return IntTensor(x.vals.reshape(tuple(newshape)), x.dtype)
+    return _f32(x).reshape(tuple(int(d) for d in newshape))
+
+
 def op_dense(x, w):
     x, w = _f32(x), _f32(w)
     n, k = x.shape
@@ -216,6 +236,8 @@ OPS = {
     "conv2d": op_conv2d,
     "nn.conv2d": op_conv2d,
     "max_pool2d": op_max_pool2d,
+    "depthwise_conv2d": op_depthwise_conv2d,
+    "reshape": op_reshape,
     "dense": op_dense,
     "nn.dense": op_dense,
     "bias_add": op_bias_add,

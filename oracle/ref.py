@@ -91,16 +91,17 @@ class RunResult:
 
 
 def run(fused_text: str, images: np.ndarray, weights: Sequence[np.ndarray], timeout=None,
-        workdir: str = None) -> RunResult:
-    """interp(@main) once per image (batch-1 calls) -> stacked float32 output."""
+        workdir: str = None, whole_batch: bool = False) -> RunResult:
+    """interp(@main) once per image (batch-1 calls) -> stacked float32 output;
+    whole_batch: one call over the batch (static-batch modules: reshape heads)."""
     with tempfile.TemporaryDirectory(dir=workdir) as d:
         src = os.path.join(d, "fused.rly")
         wf, xf, of = (os.path.join(d, n) for n in ("w.bin", "x.bin", "out.bin"))
         open(src, "w").write(fused_text)
         write_tensors(wf, weights)
         write_tensors(xf, [images])
-        p = _call(["run", src, wf, xf, of], timeout=timeout)
-        secs = [float(l.split()[2]) for l in p.stderr.splitlines() if l.startswith("image ")]
+        p = _call(["runall" if whole_batch else "run", src, wf, xf, of], timeout=timeout)
+        secs = [float(l.split()[-1]) for l in p.stderr.splitlines() if l.startswith(("image ", "batch "))]
         return RunResult(read_tensors(of)[0].copy(), secs)
 
 

@@ -306,7 +306,10 @@ int usage() {
                "  mr_ref run FUSED.rly WEIGHTS.bin IMAGES.bin OUT.bin\n"
                "      interp(@main) once per image of IMAGES.bin's first tensor ([B,...] ->\n"
                "      batch-1 calls), WEIGHTS.bin = the remaining @main args in order;\n"
-               "      per-image seconds on stderr as 'image i t'\n");
+               "      per-image seconds on stderr as 'image i t'\n"
+               "  mr_ref runall FUSED.rly WEIGHTS.bin IMAGES.bin OUT.bin\n"
+               "      one interp(@main) over the whole batch (static-batch modules, e.g. a\n"
+               "      reshape to (B, C*H*W)); seconds on stderr as 'batch t'\n");
   return 2;
 }
 
@@ -339,6 +342,22 @@ int main(int argc, char** argv) {
         if ((s = find_scale(fn)) != 0) break;
       if (s == 0) diag_throw(DiagCode::Internal, "no simulated_quantize site");
       std::printf("%d\n", static_cast<int>(std::lround(std::log2(s))));
+      return 0;
+    }
+    if (cmd == "runall" && argc == 6) {
+      ModuleEnv m = parse_module(read_file(argv[2]), argv[2], ext_registry());
+      std::vector<TensorLiteral> weights = read_tensors(argv[3]);
+      std::vector<TensorLiteral> images = read_tensors(argv[4]);
+      if (images.size() != 1) diag_throw(DiagCode::Internal, "IMAGES.bin must hold one tensor");
+      std::vector<ValueRef> args{make_tensor_value(images[0])};
+      for (auto& w : weights) args.push_back(make_tensor_value(std::move(w)));
+      InterpOptions opts;
+      opts.fuel = INT64_MAX / 2;
+      double t0 = now_s();
+      ValueRef r = interp(m, "main", args, opts);
+      std::fprintf(stderr, "batch %.6f\n", now_s() - t0);
+      TensorLiteral out = tens(r);
+      write_tensors(argv[5], {&out});
       return 0;
     }
     if (cmd == "run" && argc == 6) {

@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -273,6 +274,15 @@ int want_rep(Exec& ex, int v, int fmt, const QParams* q, int kind = LAY_NORMAL, 
 // tcgen05 formulation per conv group, decided at compile time from the
 // geometry: stride-1 halo (3x3/1x1), stride-2 over phase-split inputs, or
 // the space-to-depth stem; anything else runs on the CUDA-core kernel.
+// A tail op after the element epilogue (sum over HW or flatten): the anchor
+// kernel writes the float32 pre-tail tensor, a second launch finishes it.
+bool g_has_sum(const GroupDesc& g) {
+  if (g.epi.empty()) return false;
+  for (const auto& e : g.epi)
+    if (e.kind == EpiKind::Flatten) return true;
+  return g.epi.back().kind == EpiKind::SumHW;
+}
+
 void decide_tc(Exec& ex) {
   Program& P = ex.P;
   std::map<int, int> phase_kb;
@@ -283,7 +293,7 @@ void decide_tc(Exec& ex) {
     int& path = ex.group_path[gi];
     const GroupDesc& g = P.groups[gi];
     if (path != P_CONV_I8_TC && path != P_CONV_BF16_TC) continue;
-    bool has_sum = !g.epi.empty() && g.epi.back().kind == EpiKind::SumHW;
+    bool has_sum = g_has_sum(g);
     const auto& os = has_sum ? g.pre_sum_shape : g.out_shape;
     TcConvSpec sp{};
     sp.elem_bytes = path == P_CONV_I8_TC ? 1 : 2;
@@ -390,7 +400,14 @@ void plan(Exec& ex, bool use_tc) {
   for (size_t gi = 0; gi < P.groups.size(); ++gi) {
     const GroupDesc& g = P.groups[gi];
     const ValueInfo& ov = P.values[g.out_value];
-    if (ov.quantized) {
+    bool flat = false;
+    for (const auto& e : g.epi) flat = flat || e.kind == EpiKind::Flatten;
+    if (flat || (ov.quantized && ov.shape.size() == 2)) {
+      // the flatten tail / a dense epilogue writes row-major float32; a trailing
+      // realize chain leaves code * c2 there, the reference's exact value, and a
+      // dense consumer re-quantizes it exactly (GroupIO::requant_data)
+      want_rep(ex, g.out_value, FMT_F32, nullptr);
+    } else if (ov.quantized) {
       want_rep(ex, g.out_value, FMT_I8, &ov.q);
     } else if (g.kind == GroupKind::Dense || ov.shape.size() == 2) {
       want_rep(ex, g.out_value, FMT_F32, nullptr);
@@ -415,6 +432,10 @@ struct GroupIO {
   int data_rep = -1;
   std::vector<int> res_rep;  // per epi op (Residual only)
   float data_scale = 1.f;    // c2 of the data codes (int8)
+  // dense over a realized (coded) value: the float rep holds code * c2 exactly;
+  // the prologue re-quantizes with the same chain (c1 * c2 == 1: the codes come back exactly)
+  bool requant_data = false;
+  QParams requant_q;
 };
 
 namespace {
@@ -445,8 +466,14 @@ GroupIO resolve_inputs(Exec& ex, int gi) {
   } else if (g.kind == GroupKind::Dense) {
     if (dv.shape.size() != 2) fail(MR_ERR_UNSUPPORTED_GROUP, "group %" + g.name + ": dense over a 4-D value");
     io.data_rep = want_rep(ex, g.data.value, FMT_F32, nullptr);
-    if (g.data.quant) io.data_scale = g.data.q.c2;
-    else if (dv.quantized) fail(MR_ERR_UNSUPPORTED_GROUP, "group %" + g.name + ": dense over a coded value");
+    if (g.data.quant) {
+      io.data_scale = g.data.q.c2;
+    } else if (dv.quantized) {
+      if (!(dv.q.c1 * dv.q.c2 == 1.f)) fail(MR_ERR_UNSUPPORTED_GROUP, "group %" + g.name + ": dense over a coded value");
+      io.requant_data = true;
+      io.requant_q = dv.q;
+      io.data_scale = dv.q.c2;
+    }
   } else if (path == P_CONV_F32 || path == P_CONV_BF16_SIMT || path == P_CONV_BF16_TC) {
     if (g.data.pre_mul != 0.f) fail(MR_ERR_UNSUPPORTED_GROUP, "group %" + g.name + ": scaled conv input");
     io.data_rep = want_rep(ex, g.data.value, ffmt, nullptr, kind, s2d_pad, kb);
@@ -469,7 +496,6 @@ GroupIO resolve_inputs(Exec& ex, int gi) {
 namespace mrb200 {
 namespace {
 
-bool g_has_sum(const GroupDesc& g) { return !g.epi.empty() && g.epi.back().kind == EpiKind::SumHW; }
 
 struct Builder {
   Exec& ex;
@@ -566,7 +592,8 @@ EpiDev make_epi(Exec& ex, int gi, const GroupIO& io, int upto) {
       case EpiKind::Relu: e.op[n] = E_RELU; break;
       case EpiKind::Requant: e.op[n] = E_REQ; e.q[n] = to_qdev(op.q); break;
       case EpiKind::Clip: e.op[n] = E_CLIP; e.s[n] = op.lo; e.s2[n] = op.hi; break;
-      case EpiKind::SumHW: fail(MR_ERR_INTERNAL, "SumHW inside the element epilogue");
+      case EpiKind::SumHW:
+      case EpiKind::Flatten: fail(MR_ERR_INTERNAL, "tail op inside the element epilogue");
     }
     ++n;
   }
@@ -672,8 +699,15 @@ void build(Exec& ex) {
     int sbuf = side_rep[sgi] >= 0 ? B.buffer_for(ov, side_rep[sgi], "%" + oname + ":codes") : -1;
     const Rep& orep = ex.reps[ov][0];
 
-    bool has_sum = !g.epi.empty() && g.epi.back().kind == EpiKind::SumHW;
+    bool has_sum = g_has_sum(g);
     int n_elem_ops = static_cast<int>(g.epi.size()) - (has_sum ? 1 : 0);
+    int flatten_at = -1;  // reshape tail (+ the consumer's realize chain after it)
+    for (size_t i = 0; i < g.epi.size(); ++i)
+      if (g.epi[i].kind == EpiKind::Flatten) flatten_at = static_cast<int>(i);
+    if (flatten_at >= 0) {
+      has_sum = true;
+      n_elem_ops = flatten_at;
+    }
     EpiDev epi = make_epi(ex, static_cast<int>(gi), gio, n_elem_ops);
     OutDev out{};
     int pre_sum_buf = -1;
@@ -764,7 +798,7 @@ void build(Exec& ex) {
       int n = 0, vi = 0;
       for (size_t i = 0; i < gg.epi.size() && n < d.n_ops; ++i) {
         const EpiOp& op = gg.epi[i];
-        if (op.kind == EpiKind::SumHW) continue;
+        if (op.kind == EpiKind::SumHW || op.kind == EpiKind::Flatten) continue;
         if (op.kind == EpiKind::Bias) d.vec[n] = static_cast<const float*>(e->param_dev[e->P.values[op.value].param_index]);
         if (op.kind == EpiKind::MulChannel) d.vec[n] = static_cast<const float*>(e->group_vecs[gidx][1 + vi++]);
         ++n;
@@ -775,7 +809,7 @@ void build(Exec& ex) {
       const GroupDesc& gg = e->P.groups[gidx];
       int n = 0;
       for (size_t i = 0; i < gg.epi.size() && n < d.n_ops; ++i) {
-        if (gg.epi[i].kind == EpiKind::SumHW) continue;
+        if (gg.epi[i].kind == EpiKind::SumHW || gg.epi[i].kind == EpiKind::Flatten) continue;
         if (gg.epi[i].kind == EpiKind::Residual) {
           const Rep& r = e->reps[gg.epi[i].value][gio.res_rep[i]];
           d.res[n] = e->ptr(r.buf);
@@ -831,8 +865,8 @@ void build(Exec& ex) {
         int M = static_cast<int>(g.out_shape[1]);
         int mode = path == P_DENSE_I8 ? 0 : path == P_DENSE_F32 ? 1 : 2;
         float pre = g.data.pre_mul;
-        int quant = g.data.quant ? 1 : 0;
-        QDev q = to_qdev(g.data.q);
+        int quant = g.data.quant || gio.requant_data ? 1 : 0;
+        QDev q = to_qdev(g.data.quant ? g.data.q : gio.requant_q);
         L.fn = [e, gidx, dbuf, N, K, M, mode, pre, quant, q, acc_scale, outdev, epidev](cudaStream_t s) {
           EpiDev d = epidev();
           launch_dense(static_cast<const float*>(e->ptr(dbuf)), N, K, e->group_kp[gidx], e->group_w[gidx], M, mode,
@@ -869,7 +903,26 @@ void build(Exec& ex) {
       for (int b2 : {obuf, sbuf})
         if (b2 >= 0) ex.bufs[b2].zero_border = true;
     }
-    if (has_sum) {
+    if (has_sum && flatten_at >= 0) {
+      // reshape view: the P16 float32 tensor -> row-major [N, C*H*W] (NCHW order)
+      LaunchRec S;
+      S.name = "%" + g.name;
+      S.kernel = "flatten";
+      const auto& ps = g.pre_sum_shape;
+      S.bytes = 8.0 * ps[0] * ps[1] * ps[2] * ps[3];
+      int N = static_cast<int>(ps[0]), C = static_cast<int>(ps[1]), H = static_cast<int>(ps[2]),
+          W = static_cast<int>(ps[3]);
+      B.use(pre_sum_buf);
+      if (orep.fmt != FMT_F32) fail(MR_ERR_UNSUPPORTED_GROUP, "group %" + g.name + ": flattened value must be float32");
+      const bool rq = flatten_at + 1 < static_cast<int>(g.epi.size());  // trailing realize chain
+      const QDev q = rq ? to_qdev(g.epi.back().q) : QDev{};
+      S.fn = [e, pre_sum_buf, pre_lay, obuf, N, C, H, W, rq, q](cudaStream_t s) {
+        launch_to_nchw(e->ptr(pre_sum_buf), FMT_F32, pre_lay, 1.f, static_cast<float*>(e->ptr(obuf)), N, C, H, W, 1, s,
+                       rq ? &q : nullptr);
+      };
+      ex.launches.push_back(S);
+      ++B.launch_idx;
+    } else if (has_sum) {
       LaunchRec S;
       S.name = "%" + g.name;
       S.kernel = "sum_hw";
@@ -1102,7 +1155,18 @@ void make_describe(Exec& ex) {
 }
 
 void run_launches(Exec& ex, cudaStream_t s) {
-  for (auto& L : ex.launches) L.fn(s);
+  static const bool sync_debug = [] {
+    const char* e = std::getenv("MRB200_SYNC_DEBUG");
+    return e && std::atoi(e);
+  }();
+  for (auto& L : ex.launches) {
+    L.fn(s);
+    if (sync_debug) {  // debugging only: name the launch that faults
+      cudaError_t err = cudaStreamSynchronize(s);
+      if (err == cudaSuccess) err = cudaGetLastError();
+      if (err != cudaSuccess) fail(MR_ERR_CUDA, "launch " + L.name + " (" + L.kernel + "): " + cudaGetErrorString(err));
+    }
+  }
 }
 
 cudaGraphExec_t ensure_graph(Exec& ex) {

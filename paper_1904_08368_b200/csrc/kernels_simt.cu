@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(128) k_input_s2d_ct(const float* __restrict__ 
 // ---- P16 / row-major -> NCHW float32 (@main result) -------------------------------
 // fmt FMT_I8: realize codes, the value is code * c2 (exact).
 __global__ void k_to_nchw(const void* __restrict__ x, int fmt, Lay L, float c2, float* __restrict__ y, int N, int C,
-                          int H, int W, int is4d) {
+                          int H, int W, int is4d, int rq, QDev q) {
   pdl_trigger();
   pdl_wait();
   const int64_t total = static_cast<int64_t>(N) * C * H * W;
@@ -331,8 +331,12 @@ __global__ void k_to_nchw(const void* __restrict__ x, int fmt, Lay L, float c2, 
     int n = static_cast<int>(t / C);
     int64_t pix = is4d ? pad_pix(n, h, w, H, W) : n;
     int64_t src = lay_off(L, pix, c);
-    if (fmt == FMT_I8) y[i] = __fmul_rn(static_cast<float>(static_cast<const int8_t*>(x)[src]), c2);
-    else y[i] = load_fmt(x, fmt, src);
+    float v;
+    if (fmt == FMT_I8) v = __fmul_rn(static_cast<float>(static_cast<const int8_t*>(x)[src]), c2);
+    else v = load_fmt(x, fmt, src);
+    // rq: a realize chain after a flatten (quantize.cpp:181-201): code then code * c2
+    if (rq) v = __fmul_rn(static_cast<float>(quant_code(v, q)), q.c2);
+    y[i] = v;
   }
 }
 
@@ -711,14 +715,19 @@ __global__ void k_maxpool(const void* __restrict__ x, int xfmt, ConvGeom g, OutD
     }
     const int64_t pix = (static_cast<int64_t>(n) * OHp + oh + kPad) * OWp + ow + kPad;
     char* dst = static_cast<char*>(out.primary) + lay_byte(out.plan, pix, c0);
-    if (out.primary_fmt == FMT_F32) {
-      *reinterpret_cast<float4*>(dst) = make_float4(acc[0], acc[1], acc[2], acc[3]);
-    } else {
-      uint32_t w4[4];
-#pragma unroll
-      for (int b = 0; b < 4; ++b)
-        w4[b] = static_cast<uint32_t>(f32_to_bf16(acc[2 * b])) | (static_cast<uint32_t>(f32_to_bf16(acc[2 * b + 1])) << 16);
-      *reinterpret_cast<uint4*>(dst) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+    // 4-channel pieces at their own addresses: the input granule (cpg = 4 or 8
+    // channels) and the output's (4 fp32 / 8 bf16) need not coincide
+    (void)dst;
+    for (int s4 = 0; s4 < cpg / 4 && c0 + 4 * s4 < g.C; ++s4) {
+      char* d4 = static_cast<char*>(out.primary) + lay_byte(out.plan, pix, c0 + 4 * s4);
+      const float* a4 = acc + 4 * s4;
+      if (out.primary_fmt == FMT_F32) {
+        *reinterpret_cast<float4*>(d4) = make_float4(a4[0], a4[1], a4[2], a4[3]);
+      } else {
+        *reinterpret_cast<uint2*>(d4) =
+            make_uint2(static_cast<uint32_t>(f32_to_bf16(a4[0])) | (static_cast<uint32_t>(f32_to_bf16(a4[1])) << 16),
+                       static_cast<uint32_t>(f32_to_bf16(a4[2])) | (static_cast<uint32_t>(f32_to_bf16(a4[3])) << 16));
+      }
     }
     if (out.side) {
       if (out.side_fmt == FMT_I8 && cpg == 4 && c0 + 4 <= g.C) {
@@ -764,81 +773,94 @@ __global__ void k_sum_hw(const float* __restrict__ x, Lay L, int N, int H, int W
 //   mode 1: float32 strict, sequential k (kernels.cpp:618-623), weights [M][K]
 //   mode 2: bf16 weights, fp32 FMA accumulate
 constexpr int kDenseRows = 8;
+constexpr int kDenseK = 2048;  // K chunk staged in shared memory (a multiple of 4)
 
 __global__ void __launch_bounds__(256) k_dense(const float* __restrict__ x, int N, int K, int Kp,
                                                const void* __restrict__ w, int M, int mode, float pre_mul, int quant,
                                                QDev q, float acc_scale, EpiDev epi, OutDev out) {
   pdl_trigger();
   pdl_wait();
-  extern __shared__ float srow[];  // [kDenseRows][Kp] floats (mode 1/2) or bytes (mode 0)
+  extern __shared__ float srow[];  // [kDenseRows][ks] floats (mode 1/2) or bytes (mode 0)
+  const int ks = min(Kp, kDenseK);  // row stride of the staged chunk (== the launcher's allocation)
   const int n0 = blockIdx.y * kDenseRows;
   int8_t* scode = reinterpret_cast<int8_t*>(srow);
-  for (int idx = threadIdx.x; idx < kDenseRows * Kp; idx += blockDim.x) {
-    int r = idx / Kp, k = idx - r * Kp;
-    int n = n0 + r;
-    bool live = n < N && k < K;
-    float v = live ? x[static_cast<int64_t>(n) * K + k] : 0.f;
-    if (pre_mul != 0.f && live) v = __fmul_rn(v, pre_mul);
-    if (mode == 0) scode[idx] = live ? static_cast<int8_t>(quant ? quant_code(v, q) : static_cast<int32_t>(v)) : 0;
-    else srow[idx] = v;
-  }
-  __syncthreads();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= M) return;
+  const bool jv = j < M;
+  int acc[kDenseRows];
   float res[kDenseRows];
-  if (mode == 0) {
-    int acc[kDenseRows];
 #pragma unroll
-    for (int r = 0; r < kDenseRows; ++r) acc[r] = 0;
-    const int32_t* wt = static_cast<const int32_t*>(w);
-    const int KW = Kp / 4;
-    int kw = 0;
-    for (; kw + 8 <= KW; kw += 8) {  // 8 weight words in flight per thread
-      int32_t wv[8];
+  for (int r = 0; r < kDenseRows; ++r) {
+    acc[r] = 0;
+    res[r] = 0.0f;
+  }
+  // K in chunks of kDenseK (the row prologue is staged per chunk); the
+  // accumulation order over k is the same sequential order as one pass
+  for (int k0 = 0; k0 < Kp; k0 += kDenseK) {
+    const int kc = min(kDenseK, Kp - k0);
+    __syncthreads();  // the previous chunk is consumed
+    for (int idx = threadIdx.x; idx < kDenseRows * kc; idx += blockDim.x) {
+      const int r = idx / kc, kk = idx - r * kc, k = k0 + kk;
+      const int n = n0 + r;
+      const bool live = n < N && k < K;
+      float v = live ? x[static_cast<int64_t>(n) * K + k] : 0.f;
+      if (pre_mul != 0.f && live) v = __fmul_rn(v, pre_mul);
+      if (mode == 0) scode[r * ks + kk] = live ? static_cast<int8_t>(quant ? quant_code(v, q) : static_cast<int32_t>(v)) : 0;
+      else srow[r * ks + kk] = v;
+    }
+    __syncthreads();
+    if (!jv) continue;
+    if (mode == 0) {
+      const int32_t* wt = static_cast<const int32_t*>(w) + static_cast<int64_t>(k0 / 4) * M + j;
+      const int KW = kc / 4;  // Kp and kDenseK are multiples of 4
+      int kw = 0;
+      for (; kw + 8 <= KW; kw += 8) {  // 8 weight words in flight per thread
+        int32_t wv[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) wv[u] = __ldg(wt + static_cast<int64_t>(kw + u) * M + j);
+        for (int u = 0; u < 8; ++u) wv[u] = __ldg(wt + static_cast<int64_t>(kw + u) * M);
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+          for (int r = 0; r < kDenseRows; ++r)
+            acc[r] = __dp4a(*reinterpret_cast<const int32_t*>(scode + r * ks + (kw + u) * 4), wv[u], acc[r]);
+      }
+      for (; kw < KW; ++kw) {
+        const int32_t wv = __ldg(wt + static_cast<int64_t>(kw) * M);
 #pragma unroll
         for (int r = 0; r < kDenseRows; ++r)
-          acc[r] = __dp4a(*reinterpret_cast<const int32_t*>(scode + r * Kp + (kw + u) * 4), wv[u], acc[r]);
-    }
-    for (; kw < KW; ++kw) {
-      const int32_t wv = __ldg(wt + static_cast<int64_t>(kw) * M + j);
+          acc[r] = __dp4a(*reinterpret_cast<const int32_t*>(scode + r * ks + kw * 4), wv, acc[r]);
+      }
+    } else if (mode == 1) {
+      const float* wr = static_cast<const float*>(w) + static_cast<int64_t>(j) * K + k0;
+      const int kend = min(kc, K - k0);
+      for (int kk = 0; kk < kend; ++kk) {
+        const float wv = wr[kk];
 #pragma unroll
-      for (int r = 0; r < kDenseRows; ++r)
-        acc[r] = __dp4a(*reinterpret_cast<const int32_t*>(scode + r * Kp + kw * 4), wv, acc[r]);
+        for (int r = 0; r < kDenseRows; ++r) res[r] = __fadd_rn(res[r], __fmul_rn(srow[r * ks + kk], wv));
+      }
+    } else {
+      const uint16_t* wt = static_cast<const uint16_t*>(w) + static_cast<int64_t>(k0) * M + j;
+      const int kend = min(kc, K - k0);
+      int kk = 0;
+      for (; kk + 8 <= kend; kk += 8) {
+        float wv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) wv[u] = bf16_to_f32(__ldg(wt + static_cast<int64_t>(kk + u) * M));
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+          for (int r = 0; r < kDenseRows; ++r) res[r] = __fmaf_rn(srow[r * ks + kk + u], wv[u], res[r]);
+      }
+      for (; kk < kend; ++kk) {
+        const float wv = bf16_to_f32(__ldg(wt + static_cast<int64_t>(kk) * M));
+#pragma unroll
+        for (int r = 0; r < kDenseRows; ++r) res[r] = __fmaf_rn(srow[r * ks + kk], wv, res[r]);
+      }
     }
+  }
+  if (!jv) return;
+  if (mode == 0) {
 #pragma unroll
     for (int r = 0; r < kDenseRows; ++r) res[r] = __fmul_rn(static_cast<float>(acc[r]), acc_scale);
-  } else if (mode == 1) {
-    const float* wr = static_cast<const float*>(w) + static_cast<int64_t>(j) * K;
-#pragma unroll
-    for (int r = 0; r < kDenseRows; ++r) res[r] = 0.0f;
-    for (int k = 0; k < K; ++k) {
-      const float wv = wr[k];
-#pragma unroll
-      for (int r = 0; r < kDenseRows; ++r) res[r] = __fadd_rn(res[r], __fmul_rn(srow[r * Kp + k], wv));
-    }
-  } else {
-    const uint16_t* wt = static_cast<const uint16_t*>(w);
-#pragma unroll
-    for (int r = 0; r < kDenseRows; ++r) res[r] = 0.0f;
-    int k = 0;
-    for (; k + 8 <= K; k += 8) {
-      float wv[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) wv[u] = bf16_to_f32(__ldg(wt + static_cast<int64_t>(k + u) * M + j));
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-#pragma unroll
-        for (int r = 0; r < kDenseRows; ++r) res[r] = __fmaf_rn(srow[r * Kp + k + u], wv[u], res[r]);
-    }
-    for (; k < K; ++k) {
-      const float wv = bf16_to_f32(__ldg(wt + static_cast<int64_t>(k) * M + j));
-#pragma unroll
-      for (int r = 0; r < kDenseRows; ++r) res[r] = __fmaf_rn(srow[r * Kp + k], wv, res[r]);
-    }
   }
 #pragma unroll
   for (int r = 0; r < kDenseRows; ++r) {
@@ -945,9 +967,10 @@ void launch_input_convert(const float* x, int N, int C, int H, int W, void* out,
 }
 
 void launch_to_nchw(const void* x, int fmt, const Lay& L, float c2, float* y, int N, int C, int H, int W, int is4d,
-                    cudaStream_t s) {
+                    cudaStream_t s, const QDev* rq) {
   int64_t total = static_cast<int64_t>(N) * C * H * W;
-  pdl_launch(k_to_nchw, grid_stride_blocks(total), kThreads, 0, s, x, fmt, L, c2, y, N, C, H, W, is4d);
+  pdl_launch(k_to_nchw, grid_stride_blocks(total), kThreads, 0, s, x, fmt, L, c2, y, N, C, H, W, is4d, rq ? 1 : 0,
+             rq ? *rq : QDev{});
 }
 
 void launch_zero_border(void* buf, const Lay& L, int N, cudaStream_t s) {
@@ -1016,7 +1039,8 @@ void launch_dense_weight_t(const float* w, int M, int K, int Kp, const float* oc
 void launch_dense(const float* x, int N, int K, int Kp, const void* w, int M, int mode, float pre_mul,
                   int quant, QDev q, float acc_scale, const EpiDev& epi, const OutDev& out, cudaStream_t s) {
   dim3 grid(static_cast<unsigned>((M + 255) / 256), static_cast<unsigned>((N + kDenseRows - 1) / kDenseRows));
-  size_t smem = (mode == 0 ? static_cast<size_t>(Kp) : static_cast<size_t>(Kp) * sizeof(float)) * kDenseRows;
+  const size_t kc = static_cast<size_t>(std::min(Kp, kDenseK));
+  size_t smem = (mode == 0 ? kc : kc * sizeof(float)) * kDenseRows;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   pdl_launch(k_dense, grid, 256, smem, s, x, N, K, Kp, w, M, mode, pre_mul, quant, q, acc_scale, epi, out);
 }

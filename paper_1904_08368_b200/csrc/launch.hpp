@@ -33,7 +33,7 @@ enum WeightLayout : int { WL_ROWS = 0, WL_TC = 1, WL_S2D = 2 };
 void launch_input_convert(const float* x, int N, int C, int H, int W, void* out, int fmt, const Lay& L,
                           int s2d_pad, float pre_mul, QDev q, cudaStream_t s);
 void launch_to_nchw(const void* x, int fmt, const Lay& L, float c2, float* y, int N, int C, int H, int W, int is4d,
-                    cudaStream_t s);
+                    cudaStream_t s, const QDev* rq = nullptr);
 void launch_zero_border(void* buf, const Lay& L, int N, cudaStream_t s);
 void launch_weight_prep(const float* w, int O, int I, int KH, int KW, int Cs, int wl, const float* oc_scale,
                         float scalar, int fmt, int quant, QDev q, void* out, cudaStream_t s);

@@ -350,6 +350,10 @@ Program lower_module(const Module& m, int64_t batch, int n_data_inputs) {
       if (c->callee_is_var) unsupported(g.name, "call in epilogue");
       const std::string& o = c->name;
       if (!g.epi.empty() && g.epi.back().kind == EpiKind::SumHW) unsupported(g.name, "ops after sum");
+      // after a flatten only the realize chain of the consumer's input (matched above; run by
+      // the flatten tail) may follow
+      for (const auto& e : g.epi)
+        if (e.kind == EpiKind::Flatten) unsupported(g.name, "ops after reshape");
       auto other = [&]() -> ExprP {
         if (c->args.size() != 2) unsupported(g.name, o + " arity");
         return c->args[1 - pos];
@@ -408,6 +412,16 @@ Program lower_module(const Module& m, int64_t batch, int n_data_inputs) {
         g.pre_sum_shape = shape;
         shape = {shape[0], shape[1]};
         g.epi.push_back(EpiOp{EpiKind::SumHW});
+      } else if (o == "reshape") {
+        // the flatten a classifier head needs: [N,C,H,W] -> [N, C*H*W] (row-major view)
+        auto ns = attr_ints(c->attrs, "newshape", {});
+        if (shape.size() != 4 || ns.size() != 2 || ns[0] != shape[0] || ns[1] != shape[1] * shape[2] * shape[3])
+          unsupported(g.name, "only the [N,C,H,W] -> [N,C*H*W] reshape is fused");
+        if (!g.epi.empty() && g.epi.back().kind == EpiKind::Requant)
+          unsupported(g.name, "reshape of realize codes");
+        g.pre_sum_shape = shape;
+        shape = {ns[0], ns[1]};
+        g.epi.push_back(EpiOp{EpiKind::Flatten});
       } else {
         unsupported(g.name, "epilogue operator " + o);
       }
@@ -468,7 +482,7 @@ std::string describe_group(const Program& p, const GroupDesc& g) {
     if (g.weight.quant) os << " Q[" << g.weight.q.c1 << "," << g.weight.q.c2 << "]";
   }
   os << ")";
-  static const char* names[] = {"", "mul", "mulc", "bias", "add", "relu", "Q", "clip", "sum"};
+  static const char* names[] = {"", "mul", "mulc", "bias", "add", "relu", "Q", "clip", "sum", "flatten"};
   for (const auto& e : g.epi) os << " -> " << names[static_cast<int>(e.kind)];
   return os.str();
 }

@@ -40,6 +40,8 @@ enum class EpiKind : int32_t {
   Requant = 6,     // the 6-op realize chain               quantize.cpp:181-201
   Clip = 7,        // clip(v, lo, hi)                      kernels.cpp:296-316
   SumHW = 8,       // sum(v, axis=(2,3)), must be last     kernels.cpp:519-575
+  Flatten = 9,     // reshape [N,C,H,W] -> [N, C*H*W] (a view: row-major NCHW order), must be last
+                   //                                      kernels.cpp:390-397
 };
 
 struct EpiOp {

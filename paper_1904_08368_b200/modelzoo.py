@@ -89,7 +89,7 @@ class _Builder:
         return "meta[Constant][%d]" % (len(self.meta) - 1)
 
     # layers ---------------------------------------------------------------
-    def conv_bn(self, x, cin, cout, k, stride, pad, tag, relu=True, bn=True):
+    def conv_bn(self, x, cin, cout, k, stride, pad, tag, relu=True, bn=True, act=None):
         w = self.param("w_" + tag, (cout, cin, k, k), "conv_w")
         y = self.let("conv2d(%s, %s, strides=(%d, %d), padding=(%d, %d))" % (x, w, stride, stride, pad, pad))
         if bn:
@@ -97,6 +97,8 @@ class _Builder:
             y = self.let("multiply(%s, %s)" % (y, self.meta_const(gamma, (cout, 1, 1))))
         b = self.param("b_" + tag, (cout,), "bias")
         y = self.let("bias_add(%s, %s)" % (y, b))
+        if act is not None:
+            return self.act(y, act)
         if relu:
             y = self.let("relu(%s)" % y)
         return y
@@ -112,6 +114,27 @@ class _Builder:
         y = self.let("bias_add(%s, %s)" % (y, b))
         if relu:
             y = self.let("relu(%s)" % y)
+        return y
+
+    def depthwise_bn(self, x, c, k, stride, pad, tag, act="relu6"):
+        """depthwise_conv2d (extension op, registered on the reference's
+        OpRegistry by oracle/ref_harness.cpp) + folded BN (channel multiply
+        left in the epilogue: fold-scale folds only conv2d) + bias + relu6."""
+        win = self.param("win_" + tag, (c, c, k, k), "window")
+        w = self.param("w_" + tag, (c, 1, k, k), "dw_w")
+        y = self.let("depthwise_conv2d(%s, %s, %s, strides=(%d, %d), padding=(%d, %d))"
+                     % (x, win, w, stride, stride, pad, pad))
+        gamma = self.rng.uniform(0.5, 1.5, size=(c,)).astype(np.float32)
+        y = self.let("multiply(%s, %s)" % (y, self.meta_const(gamma, (c, 1, 1))))
+        b = self.param("b_" + tag, (c,), "bias")
+        y = self.let("bias_add(%s, %s)" % (y, b))
+        return self.act(y, act)
+
+    def act(self, y, act):
+        if act == "relu":
+            return self.let("relu(%s)" % y)
+        if act == "relu6":
+            return self.let("clip(%s, a_min=0.0, a_max=6.0)" % y)
         return y
 
     def finish(self, name, result, input_shape, num_classes):
@@ -156,7 +179,69 @@ def resnet18(image: int = 224, num_classes: int = 1000, seed: int = 1,
     return b.finish("resnet18", out, (3, image, image), num_classes)
 
 
-MODELS = {"resnet18": resnet18}
+def mobilenet_v1(image: int = 224, num_classes: int = 1000, seed: int = 1, alpha: float = 1.0) -> ModelSource:
+    """MobileNet-v1: 3x3/s2 stem, 13 x {depthwise
+    3x3 + BN + relu6, pointwise 1x1 + BN + relu6}, global average (sum x 1/HW)
+    + dense."""
+    b = _Builder(seed)
+    c = lambda v: max(8, int(v * alpha))  # noqa: E731
+    x = b.param("x", ("?n", 3, image, image), "input")
+    y = b.conv_bn(x, 3, c(32), 3, 2, 1, "stem", act="relu6")
+    hw = (image + 2 - 3) // 2 + 1
+    cin = c(32)
+    cfg = [(64, 1), (128, 2), (128, 1), (256, 2), (256, 1), (512, 2)] + [(512, 1)] * 5 + [(1024, 2), (1024, 1)]
+    for i, (cout, st) in enumerate(cfg):
+        y = b.depthwise_bn(y, cin, 3, st, 1, "dw%d" % i)
+        y = b.conv_bn(y, cin, c(cout), 1, 1, 0, "pw%d" % i, act="relu6")
+        hw = (hw + 2 - 3) // st + 1
+        cin = c(cout)
+    g = b.let("sum(%s, axis=(2, 3))" % y)
+    g = b.let("multiply(%s, const %s)" % (g, fmt_f32(1.0 / (hw * hw))))
+    out = b.dense(g, cin, num_classes, "fc")
+    return b.finish("mobilenet_v1", out, (3, image, image), num_classes)
+
+
+def vgg16(image: int = 224, num_classes: int = 1000, seed: int = 1, batch: int = 1,
+          widths=(64, 128, 256, 512, 512), fc: int = 4096) -> ModelSource:
+    """VGG-16 (config C4): 13 x conv3x3 + bias + relu, 5 x max_pool 2x2/s2,
+    flatten (reshape: static batch) + dense 4096 + relu, dense 4096 + relu,
+    dense classes."""
+    bld = _Builder(seed)
+    x = bld.param("x", (batch, 3, image, image), "input")
+    y, cin, hw = x, 3, image
+    reps = (2, 2, 3, 3, 3)
+    for si, (cout, r) in enumerate(zip(widths, reps)):
+        for j in range(r):
+            y = bld.conv_bn(y, cin, cout, 3, 1, 1, "c%d_%d" % (si + 1, j + 1), bn=False)
+            cin = cout
+        y = bld.max_pool(y, cin, 2, 2, 0, "p%d" % (si + 1))
+        hw //= 2
+    flat = cin * hw * hw
+    y = bld.let("reshape(%s, newshape=(%d, %d))" % (y, batch, flat))
+    y = bld.dense(y, flat, fc, "fc6", relu=True)
+    y = bld.dense(y, fc, fc, "fc7", relu=True)
+    out = bld.dense(y, fc, num_classes, "fc8")
+    src = bld.finish("vgg16", out, (3, image, image), num_classes)
+    return src
+
+
+def dqn(num_actions: int = 18, seed: int = 1, batch: int = 1) -> ModelSource:
+    """Nature DQN (config C4): x [N,4,84,84] scaled by 1/255, conv 8x8/s4
+    4->32, conv 4x4/s2 32->64, conv 3x3/s1 64->64 (bias + relu each), flatten
+    (static batch) + dense 512 + relu, dense actions."""
+    bld = _Builder(seed)
+    x = bld.param("x", (batch, 4, 84, 84), "input")
+    y = bld.let("multiply(%s, const %s)" % (x, fmt_f32(1.0 / 255.0)))
+    y = bld.conv_bn(y, 4, 32, 8, 4, 0, "c1", bn=False)
+    y = bld.conv_bn(y, 32, 64, 4, 2, 0, "c2", bn=False)
+    y = bld.conv_bn(y, 64, 64, 3, 1, 0, "c3", bn=False)
+    y = bld.let("reshape(%s, newshape=(%d, %d))" % (y, batch, 64 * 7 * 7))
+    y = bld.dense(y, 3136, 512, "fc1", relu=True)
+    out = bld.dense(y, 512, num_actions, "fc2")
+    return bld.finish("dqn", out, (4, 84, 84), num_actions)
+
+
+MODELS = {"resnet18": resnet18, "mobilenet_v1": mobilenet_v1, "vgg16": vgg16, "dqn": dqn}
 
 
 def make_weights(src: ModelSource, seed: int = 1) -> Dict[str, np.ndarray]:
@@ -167,7 +252,7 @@ def make_weights(src: ModelSource, seed: int = 1) -> Dict[str, np.ndarray]:
         if p.kind == "input":
             continue
         shape = tuple(int(d) for d in p.shape)
-        if p.kind in ("conv_w", "dense_w"):
+        if p.kind in ("conv_w", "dense_w", "dw_w"):
             fan_in = int(np.prod(shape[1:]))
             out[p.name] = (rng.standard_normal(shape) * np.sqrt(2.0 / fan_in)).astype(np.float32)
         elif p.kind == "bias":
@@ -182,4 +267,7 @@ def make_weights(src: ModelSource, seed: int = 1) -> Dict[str, np.ndarray]:
 def make_inputs(src: ModelSource, batch: int, seed: int = 0) -> np.ndarray:
     """Synthetic images x ~ U[0,1), NCHW float32."""
     rng = np.random.Generator(np.random.PCG64(seed))
-    return rng.random((batch,) + tuple(src.input_shape), dtype=np.float32)
+    x = rng.random((batch,) + tuple(src.input_shape), dtype=np.float32)
+    if src.name == "dqn":  # Atari frames: integer pixel values in [0, 255]
+        x = np.floor(x * 256.0).astype(np.float32)
+    return x

@@ -29,10 +29,13 @@ def sha(a):
 def make(name, batch):
     res = {}
     for prec in ("int8", "fp32"):
+        if not os.path.exists(os.path.join(ROOT, "models", "%s_%s.fused.rly" % (name, prec))):
+            continue
         text, meta, src = mrb.load_model(name, prec)
         w = modelzoo.make_weights(src, seed=meta["weights_seed"])
         x = modelzoo.make_inputs(src, batch, seed=0)
-        r = ref.run(text, x, ref.weight_list(src, w))
+        static = "batch" in meta["builder_kwargs"]  # static-batch module (reshape head)
+        r = ref.run(text, x, ref.weight_list(src, w), whole_batch=static)
         res[prec] = r.out
         res[prec + "_seconds"] = np.asarray(r.seconds)
     res["x_sha256"] = np.asarray(sha(x))
@@ -42,5 +45,6 @@ def make(name, batch):
 
 
 if __name__ == "__main__":
-    make("resnet18_tiny", 4)
-    make("resnet18", 2)
+    todo = {"resnet18_tiny": 4, "resnet18": 2, "mobilenet_v1": 2, "dqn": 2, "vgg16": 2}
+    for name in sys.argv[1:] or list(todo):
+        make(name, todo[name])

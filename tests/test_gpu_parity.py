@@ -105,3 +105,30 @@ def test_submit_host_pipeline_matches_blocking(gpu):
         ex.sync()
         for o, w in zip(outs, want):
             assert np.array_equal(bits(o), bits(w))
+
+
+# ---- BASELINE.json configs[2..3]: MobileNet-v1 (depthwise), VGG-16, DQN (flatten heads) ----
+OTHER = [("mobilenet_v1", "int8"), ("mobilenet_v1", "fp32"), ("dqn", "int8"), ("dqn", "fp32"), ("vgg16", "fp32")]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,prec", OTHER)
+def test_other_models(gpu, name, prec):
+    """int8 modules bit-exact; float modules in bf16 mode within the normwise
+    tolerance + top-1 agreement, against the reference interpreter (b2)."""
+    gold = np.load(os.path.join(GOLD, "%s_b2.npz" % name))
+    ex, src = setup(name, prec, 2)
+    y = ex.run_host(modelzoo.make_inputs(src, 2, seed=0))
+    if prec == "int8":
+        assert np.array_equal(bits(y), bits(gold["int8"])), int(np.sum(bits(y) != bits(gold["int8"])))
+    else:
+        assert normwise(y, gold["fp32"]) <= BF16_TOL, normwise(y, gold["fp32"])
+        assert np.array_equal(np.argmax(y, 1), np.argmax(gold["fp32"], 1))
+
+
+@pytest.mark.gpu
+def test_dqn_fp32_strict_bitexact(gpu):
+    gold = np.load(os.path.join(GOLD, "dqn_b2.npz"))
+    ex, src = setup("dqn", "fp32", 2, float_mode=mrb.MR_FLOAT_FP32_STRICT)
+    y = ex.run_host(modelzoo.make_inputs(src, 2, seed=0))
+    assert np.array_equal(bits(y), bits(gold["fp32"])), np.max(np.abs(y - gold["fp32"]))

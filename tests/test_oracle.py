@@ -175,3 +175,15 @@ def test_port_matches_live_reference_small_module():
         mine = port.run_module(SMALL, [x, w, b, r])
         theirs = ref.run(SMALL, x, [w, b, r]).out  # first @main param = the data input
         assert np.array_equal(bits(mine), bits(theirs)), trial
+
+
+@pytest.mark.parametrize("name,prec", [("mobilenet_v1", "int8"), ("mobilenet_v1", "fp32"), ("dqn", "int8"),
+                                       ("dqn", "fp32"), ("vgg16", "fp32")])
+def test_port_matches_reference_golden_other_models(name, prec):
+    """depthwise_conv2d (MobileNet), the flatten reshape + large dense heads
+    (VGG-16, DQN): the port against the reference's own outputs."""
+    path = os.path.join(GOLD, "%s_b2.npz" % name)
+    if not os.path.exists(path):
+        pytest.skip("golden not generated")
+    text, x, wl = _golden_case(name, 2, prec)
+    assert np.array_equal(bits(port.run_weights(text, x, wl)), bits(np.load(path)[prec]))
