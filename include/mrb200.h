@@ -49,6 +49,7 @@ typedef enum mr_status {
   MR_ERR_META_INDEX = 7,
   MR_ERR_TYPE_MISMATCH = 9,
   MR_ERR_ARITY_MISMATCH = 13,
+  MR_ERR_CALIBRATION_FAILED = 15,
   MR_ERR_UNCALIBRATED = 16,
   MR_ERR_INTERNAL = 24,
   /* backend-specific */
@@ -161,6 +162,19 @@ const char* mr_last_error_message(void);
  * the reference's per-group type check (passes.cpp:452-486). */
 mr_status mr_module_lower(const char* fused_module_text, int64_t batch, int32_t n_data_inputs,
                           const char** json);
+
+/* GPU calibration sweep: the global power-of-two
+ * scale the reference's quant_calibrate (quantize.cpp:138-177) picks -- the
+ * first k in [k_min, k_max] (the reference: [-16, 16]) such that no quantize
+ * site of the module at rho = 2^k sees |nearbyint(x / rho * 2^(bits-sign))|
+ * above 2^(bits-1), over the weights and every calibration batch.
+ * `fused_module_text` is a realized + fused module at ANY global scale (the
+ * sweep rewrites every site, as with_global_scale does, quantize.cpp:123-134);
+ * inputs[i] is calibration batch i (HOST float32, opts->batch images each).
+ * Fails with MR_ERR_CALIBRATION_FAILED when every k overflows. */
+mr_status mr_calibrate(const char* fused_module_text, const mr_exec_options* opts, int32_t n_weights,
+                       const mr_tensor* weights, int32_t n_sets, const mr_tensor* inputs, int32_t k_min,
+                       int32_t k_max, int32_t* k_out, int32_t* trials_out);
 
 /* Library build identification (arch, kernels compiled). */
 const char* mr_build_info(void);

@@ -33,7 +33,7 @@ MR_FLOAT = 2
 EXPORTS = [
     "mr_exec_default_options", "mr_exec_create", "mr_exec_set_weights", "mr_exec_run",
     "mr_exec_run_host", "mr_exec_submit_host", "mr_exec_sync", "mr_exec_output_shape", "mr_exec_describe", "mr_exec_launch_count",
-    "mr_exec_profile", "mr_exec_destroy", "mr_last_error_message", "mr_module_lower", "mr_build_info",
+    "mr_exec_profile", "mr_exec_destroy", "mr_last_error_message", "mr_module_lower", "mr_calibrate", "mr_build_info",
 ]
 
 
@@ -84,6 +84,9 @@ def lib():
         L.mr_exec_destroy.argtypes = [ctypes.c_void_p]
         L.mr_last_error_message.restype = ctypes.c_char_p
         L.mr_build_info.restype = ctypes.c_char_p
+        L.mr_calibrate.argtypes = [ctypes.c_char_p, ctypes.POINTER(Options), ctypes.c_int32, ctypes.POINTER(Tensor),
+                                   ctypes.c_int32, ctypes.POINTER(Tensor), ctypes.c_int32, ctypes.c_int32,
+                                   ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]
         L.mr_module_lower.argtypes = [ctypes.c_char_p, ctypes.c_int64, ctypes.c_int32,
                                       ctypes.POINTER(ctypes.c_char_p)]
         _lib = L
@@ -113,6 +116,25 @@ def lower(fused_text: str, batch: int = 1, n_data_inputs: int = 1) -> dict:
     out = ctypes.c_char_p()
     _check(lib().mr_module_lower(fused_text.encode(), int(batch), int(n_data_inputs), ctypes.byref(out)))
     return json.loads(out.value.decode())
+
+
+def calibrate(fused_int8_text: str, weights: Sequence[np.ndarray], batches: Sequence[np.ndarray],
+              k_min: int = -16, k_max: int = 16, device: int = 0):
+    """GPU calibration sweep (mr_calibrate): the global scale exponent k the
+    reference's quant_calibrate would pick for these weights and calibration
+    batches.  Returns (k, trials)."""
+    batches = [np.ascontiguousarray(b, np.float32) for b in batches]
+    ws = [np.ascontiguousarray(w, np.float32) for w in weights]
+    opts = Options()
+    lib().mr_exec_default_options(ctypes.byref(opts))
+    opts.device = device
+    opts.batch = int(batches[0].shape[0])
+    wt = (Tensor * max(1, len(ws)))(*[_tensor(w.ctypes.data, w.shape) for w in ws])
+    xt = (Tensor * len(batches))(*[_tensor(b.ctypes.data, b.shape) for b in batches])
+    k, trials = ctypes.c_int32(0), ctypes.c_int32(0)
+    _check(lib().mr_calibrate(fused_int8_text.encode(), ctypes.byref(opts), len(ws), wt, len(batches), xt,
+                              int(k_min), int(k_max), ctypes.byref(k), ctypes.byref(trials)))
+    return int(k.value), int(trials.value)
 
 
 class Executor:

@@ -428,6 +428,12 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
           const int r = __float2int_rn(__fmaf_rn(static_cast<float>(static_cast<int32_t>(raw[i])), a.p2_scale, bb[i]));
           code[i] = min(max(r, 0), a.p2_hi);
         }
+        if (e.q[2].ovf) {  // calibration: the rounded site value max(r, 0) must not exceed 128
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (__float2int_rn(__fmaf_rn(static_cast<float>(static_cast<int32_t>(raw[i])), a.p2_scale, bb[i])) > 128)
+              atomicOr(e.q[2].ovf, 1);
+        }
         st16(o.primary, gran_byte(o.plan, d.pix, o.plan.Pp, c0),
              make_uint4(pack4_i8(code[0], code[1], code[2], code[3]), pack4_i8(code[4], code[5], code[6], code[7]),
                         pack4_i8(code[8], code[9], code[10], code[11]), pack4_i8(code[12], code[13], code[14], code[15])));
@@ -454,6 +460,7 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
       const QDev qd = e.q[2];
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
+        quant_observe(v[i], qd);
         float t = fminf(rintf(__fmul_rn(v[i], qd.c1)), qd.hi);
         code[i] = __float2int_rz(t);
       }

@@ -47,7 +47,28 @@ namespace {
 
 int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 
-QDev to_qdev(const QParams& q) { return QDev{q.c1, q.lo, q.hi, q.c2, q.is_signed ? 1 : 0}; }
+// Set while a calibration trial executor is built and its weights prepared:
+// every QDev then carries the trial's device overflow flag (mr_calibrate).
+thread_local int32_t* g_calib_ovf = nullptr;
+
+QDev to_qdev(const QParams& q) { return QDev{q.c1, q.lo, q.hi, q.c2, q.is_signed ? 1 : 0, g_calib_ovf}; }
+
+// The module with every quantize site at global scale rho = 2^k
+// (with_global_scale, quantize.cpp:123-134): realize's constants are
+// c1 = 2^(bits-sign) / rho and c2 = rho / 2^(bits-sign) (quantize.cpp:181-201).
+void rescale_sites(Program& P, int k) {
+  auto fix = [k](QParams& q) {
+    const int e = (q.is_signed ? 7 : 8) - k;
+    q.c1 = std::ldexp(1.0f, e);
+    q.c2 = std::ldexp(1.0f, -e);
+  };
+  for (auto& v : P.values) fix(v.q);
+  for (auto& g : P.groups) {
+    fix(g.data.q);
+    fix(g.weight.q);
+    for (auto& e : g.epi) fix(e.q);
+  }
+}
 
 bool is_pow2(float v) {
   if (!(v > 0.f) || !std::isfinite(v)) return false;
@@ -1250,6 +1271,22 @@ using namespace mrb200;
   }                                                   \
   return MR_OK;
 
+namespace mrb200 {
+namespace {
+std::unique_ptr<Exec> make_exec(Program P, const mr_exec_options& o) {
+  auto ex = std::make_unique<Exec>();
+  ex->opt = o;
+  ex->P = std::move(P);
+  if (ex->opt.n_data_inputs != 1) fail(MR_ERR_UNSUPPORTED_GROUP, "exactly one data input is supported");
+  build(*ex);
+  upload_group_constants(*ex);
+  ex->param_dev.assign(ex->P.n_params, nullptr);
+  make_describe(*ex);
+  return ex;
+}
+}  // namespace
+}  // namespace mrb200
+
 extern "C" {
 
 void mr_exec_default_options(mr_exec_options* o) {
@@ -1266,19 +1303,13 @@ mr_status mr_exec_create(const char* text, const mr_exec_options* opts, mr_exec_
   API_BEGIN
   if (!text || !out) fail(MR_ERR_INVALID_ARGUMENT, "null argument");
   *out = nullptr;
-  auto ex = std::make_unique<Exec>();
-  mr_exec_default_options(&ex->opt);
-  if (opts) ex->opt = *opts;
-  if (ex->opt.batch < 1) fail(MR_ERR_INVALID_ARGUMENT, "batch must be >= 1");
-  CK(cudaSetDevice(ex->opt.device));
+  mr_exec_options o;
+  mr_exec_default_options(&o);
+  if (opts) o = *opts;
+  if (o.batch < 1) fail(MR_ERR_INVALID_ARGUMENT, "batch must be >= 1");
+  CK(cudaSetDevice(o.device));
   Module m = parse_fused_module(text);
-  ex->P = lower_module(m, ex->opt.batch, ex->opt.n_data_inputs);
-  if (ex->opt.n_data_inputs != 1) fail(MR_ERR_UNSUPPORTED_GROUP, "exactly one data input is supported");
-  build(*ex);
-  upload_group_constants(*ex);
-  ex->param_dev.assign(ex->P.n_params, nullptr);
-  make_describe(*ex);
-  *out = reinterpret_cast<mr_exec_t>(ex.release());
+  *out = reinterpret_cast<mr_exec_t>(make_exec(lower_module(m, o.batch, o.n_data_inputs), o).release());
   API_END
 }
 
@@ -1457,6 +1488,69 @@ mr_status mr_module_lower(const char* text, int64_t batch, int32_t n_data_inputs
   Program P = lower_module(m, batch, n_data_inputs);
   out = program_json(P);
   *json = out.c_str();
+  API_END
+}
+
+mr_status mr_calibrate(const char* text, const mr_exec_options* opts, int32_t n_weights, const mr_tensor* weights,
+                       int32_t n_sets, const mr_tensor* inputs, int32_t k_min, int32_t k_max, int32_t* k_out,
+                       int32_t* trials_out) {
+  struct Flag {  // device overflow flag, freed on every exit path
+    int32_t* p = nullptr;
+    ~Flag() {
+      if (p) cudaFree(p);
+    }
+  } flag_mem;
+  API_BEGIN
+  if (!text || !k_out || (n_sets > 0 && !inputs)) fail(MR_ERR_INVALID_ARGUMENT, "null argument");
+  if (n_sets < 1) fail(MR_ERR_CALIBRATION_FAILED, "calibration requires a non-empty input set");
+  mr_exec_options o;
+  mr_exec_default_options(&o);
+  if (opts) o = *opts;
+  o.use_cuda_graph = 0;
+  CK(cudaSetDevice(o.device));
+  const Program P0 = lower_module(parse_fused_module(text), o.batch, o.n_data_inputs);
+  if (!P0.any_quant) fail(MR_ERR_INVALID_ARGUMENT, "module has no quantize sites");
+  CK(cudaMalloc(&flag_mem.p, sizeof(int32_t)));
+  int32_t* flag = flag_mem.p;
+  std::vector<float> out;
+  for (int k = k_min; k <= k_max; ++k) {
+    if (trials_out) *trials_out = k - k_min + 1;
+    Program P = P0;
+    rescale_sites(P, k);
+    CK(cudaMemset(flag, 0, sizeof(int32_t)));
+    g_calib_ovf = flag;  // every QDev of this trial reports overflow
+    std::unique_ptr<Exec> ex;
+    try {
+      ex = make_exec(std::move(P), o);
+      mr_exec_t h = reinterpret_cast<mr_exec_t>(ex.get());
+      mr_status st = mr_exec_set_weights(h, n_weights, weights);  // weight sites
+      if (st != MR_OK) throw Status{static_cast<int>(st), g_last_error};
+      int32_t ovf = 0;
+      CK(cudaMemcpy(&ovf, flag, sizeof(ovf), cudaMemcpyDeviceToHost));
+      out.resize(static_cast<size_t>(ex->out_elems));
+      mr_tensor res{};
+      res.data = out.data();
+      res.ndim = static_cast<int32_t>(ex->out_shape.size());
+      for (int i = 0; i < res.ndim; ++i) res.shape[i] = ex->out_shape[i];
+      res.type_code = MR_FLOAT;
+      res.bits = 32;
+      for (int32_t b = 0; b < n_sets && !ovf; ++b) {  // activation sites, one calibration batch at a time
+        st = mr_exec_run_host(h, &inputs[b], &res, nullptr);
+        if (st != MR_OK) throw Status{static_cast<int>(st), g_last_error};
+        CK(cudaMemcpy(&ovf, flag, sizeof(ovf), cudaMemcpyDeviceToHost));
+      }
+      g_calib_ovf = nullptr;
+      if (!ovf) {
+        *k_out = k;
+        return MR_OK;
+      }
+    } catch (...) {
+      g_calib_ovf = nullptr;
+      throw;
+    }
+  }
+  fail(MR_ERR_CALIBRATION_FAILED, "no power-of-two scale in [2^" + std::to_string(k_min) + ", 2^" +
+                                      std::to_string(k_max) + "] avoids overflow");
   API_END
 }
 

@@ -21,6 +21,11 @@ enum Fmt : int32_t { FMT_F32 = 0, FMT_BF16 = 1, FMT_I8 = 2 };
 struct QDev {
   float c1, lo, hi, c2;
   int32_t is_signed;
+  // calibration (mr_calibrate): when set, every quantization of a value x
+  // raises *ovf if the site would overflow -- quant_calibrate's observer,
+  // |nearbyint(x / rho * 2^(bits-sign))| > 2^(bits-1) (signed) or outside
+  // [0, 2^bits] (unsigned) (quantize.cpp:149-161)
+  int32_t* ovf;
 };
 
 // Physical layout of an activation tensor ("PK"): channels are split into
@@ -144,8 +149,18 @@ __device__ __forceinline__ int32_t cast_int_ref(float v, int32_t is_signed) {
   return is_signed ? static_cast<int32_t>(static_cast<int8_t>(lo8)) : lo8;
 }
 
+// quant_calibrate's overflow test on the value entering a quantize site.
+// x / rho * 2^(bits-sign) in double == v * c1 in float here (c1 is a power of
+// two), so the rounded products agree.
+__device__ __forceinline__ void quant_observe(float v, const QDev& q) {
+  if (q.ovf) {
+    const float t = rintf(__fmul_rn(v, q.c1));
+    if (q.is_signed ? fabsf(t) > 128.f : (t < 0.f || t > 256.f)) atomicOr(q.ovf, 1);
+  }
+}
 // The realize chain's integer code: cast(clip(round(v * c1), lo, hi)).
 __device__ __forceinline__ int32_t quant_code(float v, const QDev& q) {
+  quant_observe(v, q);
   float t = __fmul_rn(v, q.c1);
   t = rintf(t);
   t = clip_ref(t, q.lo, q.hi);
@@ -192,6 +207,7 @@ __host__ __device__ __forceinline__ int64_t lay_byte(const Lay& L, int64_t pix, 
 // cast is exact and the wrap to 8 bits is a plain narrowing.  NaN: clip keeps
 // NaN, cvt.rzi gives 0 == the reference's INT64_MIN & 0xff.
 __device__ __forceinline__ int32_t quant_code_fast(float v, const QDev& q) {
+  quant_observe(v, q);
   float t = clip_ref(rintf(__fmul_rn(v, q.c1)), q.lo, q.hi);
   int32_t k = __float2int_rz(t);
   return q.is_signed ? static_cast<int32_t>(static_cast<int8_t>(k)) : (k & 0xff);

@@ -132,3 +132,33 @@ def test_dqn_fp32_strict_bitexact(gpu):
     ex, src = setup("dqn", "fp32", 2, float_mode=mrb.MR_FLOAT_FP32_STRICT)
     y = ex.run_host(modelzoo.make_inputs(src, 2, seed=0))
     assert np.array_equal(bits(y), bits(gold["fp32"])), np.max(np.abs(y - gold["fp32"]))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["resnet18_tiny", "resnet18", "mobilenet_v1", "dqn"])
+def test_gpu_calibration_matches_reference(gpu, name):
+    """mr_calibrate picks the same global scale as the
+    reference's quant_calibrate (quantize.cpp:138-177) on the same weights and
+    calibration images (models/<name>.json, written by oracle/build_models.py)."""
+    import time
+    text, meta, src = mrb.load_model(name, "int8")
+    cal = meta["calibration"]
+    w = modelzoo.make_weights(src, seed=meta["weights_seed"])
+    x = modelzoo.make_inputs(src, cal["images"], seed=cal["inputs_seed"])
+    t0 = time.time()
+    k, trials = mrb.calibrate(text, [w[p.name] for p in src.params if p.kind != "input"], [x])
+    print(name, "k", k, "trials", trials, "gpu seconds %.3f" % (time.time() - t0),
+          "reference seconds", cal["seconds"])
+    assert k == cal["k"]
+    assert trials == k + 17  # every k below overflowed
+
+
+@pytest.mark.gpu
+def test_gpu_calibration_fails_like_reference(gpu):
+    """A range where every scale overflows fails with CalibrationFailed."""
+    text, meta, src = mrb.load_model("resnet18_tiny", "int8")
+    w = modelzoo.make_weights(src, seed=meta["weights_seed"])
+    x = modelzoo.make_inputs(src, 1, seed=0)
+    with pytest.raises(mrb.BackendError) as e:
+        mrb.calibrate(text, [w[p.name] for p in src.params if p.kind != "input"], [x], k_min=-16, k_max=-10)
+    assert e.value.code == 15  # MR_ERR_CALIBRATION_FAILED (DiagCode::CalibrationFailed + 1)
