@@ -313,7 +313,7 @@ __device__ __forceinline__ void epilogue_values(const TcArgs& a, const uint32_t*
   }
 }
 
-template <int EB, int SIG>
+template <int EB, int SIG, bool CAL>
 __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* raw, const RowDst& d, int c0,
                                                const float* s_vec, bool p2ok, int cl) {
   const OutDev& o = a.out;
@@ -401,7 +401,7 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
         const QDev qd = e.q[k];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          code[i] = quant_code(v[i], qd);
+          code[i] = quant_code_t<CAL>(v[i], qd);
           v[i] = __fmul_rn(static_cast<float>(code[i]), qd.c2);
         }
       } else if (op == E_CLIP) {
@@ -428,7 +428,7 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
           const int r = __float2int_rn(__fmaf_rn(static_cast<float>(static_cast<int32_t>(raw[i])), a.p2_scale, bb[i]));
           code[i] = min(max(r, 0), a.p2_hi);
         }
-        if (e.q[2].ovf) {  // calibration: the rounded site value max(r, 0) must not exceed 128
+        if (CAL && e.q[2].ovf) {  // calibration: the rounded site value max(r, 0) must not exceed 128
 #pragma unroll
           for (int i = 0; i < 16; ++i)
             if (__float2int_rn(__fmaf_rn(static_cast<float>(static_cast<int32_t>(raw[i])), a.p2_scale, bb[i])) > 128)
@@ -460,7 +460,7 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
       const QDev qd = e.q[2];
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
-        quant_observe(v[i], qd);
+        if constexpr (CAL) quant_observe(v[i], qd);
         float t = fminf(rintf(__fmul_rn(v[i], qd.c1)), qd.hi);
         code[i] = __float2int_rz(t);
       }
@@ -492,7 +492,7 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
     if (o.side_fmt == FMT_I8) {
       int sc[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) sc[i] = quant_code_fast(v[i], o.side_q);
+      for (int i = 0; i < 16; ++i) sc[i] = quant_code_fast_t<CAL>(v[i], o.side_q);
       st16(o.side, gran_byte(o.slay, d.side_base, d.side_pstride, c0),
            make_uint4(pack4_i8(sc[0], sc[1], sc[2], sc[3]), pack4_i8(sc[4], sc[5], sc[6], sc[7]),
                       pack4_i8(sc[8], sc[9], sc[10], sc[11]), pack4_i8(sc[12], sc[13], sc[14], sc[15])));
@@ -521,7 +521,7 @@ __device__ __forceinline__ int tile_start(const TcArgs& a, int mt, int msub) {
 }
 __device__ __forceinline__ int tile_row0(const TcArgs& a, int mt, int msub) { return tile_start(a, mt, msub) + a.dmin; }
 
-template <int EB, int SIG>
+template <int EB, int SIG, bool CAL>
 __global__ void __launch_bounds__(kThreadsTc, 1)
     k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -800,7 +800,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
               d.side_base = d.pix;
               d.side_pstride = sl.Pp;
             }
-            epilogue_chunk<EB, SIG>(a, reinterpret_cast<const uint32_t*>(mx), d, n_tile * a.bn + c, s_vec, p2ok, c);
+            epilogue_chunk<EB, SIG, CAL>(a, reinterpret_cast<const uint32_t*>(mx), d, n_tile * a.bn + c, s_vec, p2ok, c);
           }
         }
         goto epilogue_done;
@@ -900,7 +900,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             if (o.side_fmt == FMT_I8) {
               uint32_t u = 0;
 #pragma unroll
-              for (int k = 0; k < 4; ++k) u |= (static_cast<uint32_t>(quant_code_fast(mx[k], o.side_q)) & 0xff) << (8 * k);
+              for (int k = 0; k < 4; ++k) u |= (static_cast<uint32_t>(quant_code_fast_t<CAL>(mx[k], o.side_q)) & 0xff) << (8 * k);
               *reinterpret_cast<uint32_t*>(sbase) = u;
             } else {
               *reinterpret_cast<uint2*>(sbase) =
@@ -969,7 +969,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                                static_cast<uint32_t>((acc * a.sub + sb) * a.bn + c);
         uint32_t raw[16];
         tmem_ld16(taddr, raw);  // warp-collective: every lane executes it
-        if (valid && !(a.dbg & 1)) epilogue_chunk<EB, SIG>(a, raw, d, n_tile * a.bn + c, s_vec, p2ok, c);
+        if (valid && !(a.dbg & 1)) epilogue_chunk<EB, SIG, CAL>(a, raw, d, n_tile * a.bn + c, s_vec, p2ok, c);
       }
       tc_fence_before();
       __syncwarp();
@@ -1519,23 +1519,31 @@ bool tc_conv_launch(TcConvPlan* p, const void* x, const Lay& xl, const void* w, 
       a.p2_hi = static_cast<int32_t>(epi.q[2].hi);
     }
   }
-#define MRB_TC_LAUNCH(EB_, SIG_)                                                                          \
+#define MRB_TC_LAUNCH(EB_, SIG_, CAL_)                                                                    \
   do {                                                                                                    \
-    cudaFuncSetAttribute(k_conv_tc<EB_, SIG_>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p->smem)); \
-    pdl_launch(k_conv_tc<EB_, SIG_>, p->grid, kThreadsTc, p->smem, s, p->tmA, p->tmB, a);                 \
+    cudaFuncSetAttribute(k_conv_tc<EB_, SIG_, CAL_>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
+                         static_cast<int>(p->smem));                                                      \
+    pdl_launch(k_conv_tc<EB_, SIG_, CAL_>, p->grid, kThreadsTc, p->smem, s, p->tmA, p->tmB, a);           \
   } while (0)
-#define MRB_TC_SIGS(EB_)                                          \
-  switch (sig) {                                                  \
-    case SIG_BIAS: MRB_TC_LAUNCH(EB_, SIG_BIAS); break;           \
-    case SIG_BIAS_RELU: MRB_TC_LAUNCH(EB_, SIG_BIAS_RELU); break; \
-    case SIG_BIAS_RELU_REQ: MRB_TC_LAUNCH(EB_, SIG_BIAS_RELU_REQ); break; \
-    case SIG_BIAS_RES_RELU: MRB_TC_LAUNCH(EB_, SIG_BIAS_RES_RELU); break; \
-    default: MRB_TC_LAUNCH(EB_, SIG_ANY); break;                  \
+#define MRB_TC_SIGS(EB_, CAL_)                                                  \
+  switch (sig) {                                                                \
+    case SIG_BIAS: MRB_TC_LAUNCH(EB_, SIG_BIAS, CAL_); break;                   \
+    case SIG_BIAS_RELU: MRB_TC_LAUNCH(EB_, SIG_BIAS_RELU, CAL_); break;         \
+    case SIG_BIAS_RELU_REQ: MRB_TC_LAUNCH(EB_, SIG_BIAS_RELU_REQ, CAL_); break; \
+    case SIG_BIAS_RES_RELU: MRB_TC_LAUNCH(EB_, SIG_BIAS_RES_RELU, CAL_); break; \
+    default: MRB_TC_LAUNCH(EB_, SIG_ANY, CAL_); break;                          \
   }
+  // a calibration run (mr_calibrate) carries overflow flags in its QDevs
+  bool cal = out.side && out.side_q.ovf;
+  for (int k = 0; k < epi.n_ops; ++k) cal = cal || (epi.op[k] == E_REQ && epi.q[k].ovf);
   if (p->spec.elem_bytes == 1) {
-    MRB_TC_SIGS(1)
+    if (cal) {
+      MRB_TC_SIGS(1, true)
+    } else {
+      MRB_TC_SIGS(1, false)
+    }
   } else {
-    MRB_TC_SIGS(2)
+    MRB_TC_SIGS(2, false)
   }
 #undef MRB_TC_SIGS
 #undef MRB_TC_LAUNCH

@@ -159,8 +159,16 @@ __device__ __forceinline__ void quant_observe(float v, const QDev& q) {
   }
 }
 // The realize chain's integer code: cast(clip(round(v * c1), lo, hi)).
-__device__ __forceinline__ int32_t quant_code(float v, const QDev& q) {
-  quant_observe(v, q);
+// CAL = false compiles the calibration observer out (hot kernels are
+// instantiated both ways; the launchers pick CAL only for a calibration run).
+template <bool CAL>
+__device__ __forceinline__ int32_t quant_code_t(float v, const QDev& q);
+
+__device__ __forceinline__ int32_t quant_code(float v, const QDev& q) { return quant_code_t<true>(v, q); }
+
+template <bool CAL>
+__device__ __forceinline__ int32_t quant_code_t(float v, const QDev& q) {
+  if constexpr (CAL) quant_observe(v, q);
   float t = __fmul_rn(v, q.c1);
   t = rintf(t);
   t = clip_ref(t, q.lo, q.hi);
@@ -206,12 +214,15 @@ __host__ __device__ __forceinline__ int64_t lay_byte(const Lay& L, int64_t pix, 
 // [-128, 127] or [0, 255]): the clipped value is integral, so the truncating
 // cast is exact and the wrap to 8 bits is a plain narrowing.  NaN: clip keeps
 // NaN, cvt.rzi gives 0 == the reference's INT64_MIN & 0xff.
-__device__ __forceinline__ int32_t quant_code_fast(float v, const QDev& q) {
-  quant_observe(v, q);
+template <bool CAL>
+__device__ __forceinline__ int32_t quant_code_fast_t(float v, const QDev& q) {
+  if constexpr (CAL) quant_observe(v, q);
   float t = clip_ref(rintf(__fmul_rn(v, q.c1)), q.lo, q.hi);
   int32_t k = __float2int_rz(t);
   return q.is_signed ? static_cast<int32_t>(static_cast<int8_t>(k)) : (k & 0xff);
 }
+
+__device__ __forceinline__ int32_t quant_code_fast(float v, const QDev& q) { return quant_code_fast_t<true>(v, q); }
 
 __device__ __forceinline__ float load_fmt(const void* p, int32_t fmt, int64_t i) {
   if (fmt == FMT_F32) return static_cast<const float*>(p)[i];
