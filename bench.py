@@ -391,7 +391,8 @@ def main():
         rb = time_ours("fp32", args.batch, args.steps, warmup, rank, world, local, not args.no_cuda_graph)
         bf16 = {"value": rb["value"], "unit": UNIT, "ms_per_step": rb["ms_step"], "e2e": rb["e2e"],
                 "roofline": roofline(rb, "bf16", pk), "gpu_launches": rb["launches"] * args.steps,
-                "module": "models/resnet18_fp32.fused.rly (bf16 operands, fp32 accumulate)"}
+                "module": "models/resnet18_fp32.fused.rly (bf16 operands, fp32 accumulate)",
+                "per_launch": per_launch_table(rb, "bf16", pk)}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:

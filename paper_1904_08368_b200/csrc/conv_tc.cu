@@ -73,7 +73,7 @@ inline int epi_signature(const EpiDev& e, const OutDev& o) {
   return SIG_ANY;
 }
 
-constexpr int kMaxSteps = 80;
+constexpr int kMaxSteps = 144;  // bf16 TC_STEM_POOL: 9 window positions x 16 taps
 constexpr int kVecSlots = 2;   // staged per-channel vectors
 constexpr int kVecArea = (kVecSlots + 1) * 256 * 4 + 16;  // + b*c1 for the short requantize + flag
 
@@ -97,6 +97,7 @@ struct TcArgs {
   // row dy) of 3 sub-tiles (window column dx) over one A stage; step table
   // [dy][dx][8 tap pairs]; the epilogue max-reduces the 9 accumulators
   int32_t win;
+  int32_t win_spt;  // TC_STEM_POOL MMA steps per window position (8 int8 tap pairs, 16 bf16 taps)
   // per-CTA shared-memory copies of the epilogue's per-channel vectors
   // (bias / channel scale): slot of op k (-1: read global), byte offset of the
   // area from the barrier block
@@ -672,11 +673,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             mbar_wait(&tempty[acc], acc_phase ^ 1);
             tc_fence_after();
             const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc) * 3u * bn;
+            const uint32_t spt = static_cast<uint32_t>(a.win_spt);
             if (!no_mma)
-              for (uint32_t st = 0; st < 8; ++st) {
-                const uint64_t bd = hi | (a.steps[dy * 24 + st].b_lo + b16);
+              for (uint32_t st = 0; st < spt; ++st) {
+                const uint64_t bd = hi | (a.steps[dy * 3 * spt + st].b_lo + b16);
                 for (uint32_t dx = 0; dx < 3; ++dx)
-                  umma<EB>(tmem_d + dx * bn, hi | (a.steps[dy * 24 + dx * 8 + st].a_lo + a16), bd, idesc, st != 0);
+                  umma<EB>(tmem_d + dx * bn, hi | (a.steps[(dy * 3 + dx) * spt + st].a_lo + a16), bd, idesc, st != 0);
               }
             umma_commit(&tfull[acc]);
             if (++acc == 2) {
@@ -739,7 +741,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     uint32_t acc_phase = 0;
     float* stg = reinterpret_cast<float*>(smem_pool);
     const bool p2ok = a.p2 && *s_p2ok && !(a.dbg & 64);
-    if constexpr (EB == 1) {
+    {
       if (a.win) {
         // TC_STEM_POOL epilogue: lane = pooled pixel, warp slice = 16-channel
         // chunk.  The reference pools relu(bias + acc * s) with its ordered
@@ -756,9 +758,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           const int i = static_cast<int>(t - n32 * static_cast<uint32_t>(a.Hg));
           const int n = static_cast<int>(n32), pp = i - 1, pq = j - 1;
           const bool vpool = n < a.N && pp >= 0 && pp < a.poh && pq >= 0 && pq < a.pow;
-          int32_t mx[16];
+          // int8: int32 accumulators, bf16: fp32 (the max of the valid taps; -inf / INT32_MIN seeds)
+          uint32_t mx[16];
 #pragma unroll
-          for (int k = 0; k < 16; ++k) mx[k] = INT32_MIN;
+          for (int k = 0; k < 16; ++k) mx[k] = EB == 1 ? 0x80000000u : 0xff800000u;
           for (int dy = 0; dy < 3; ++dy) {
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
@@ -772,7 +775,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
               const int x = 2 * pq - 1 + dx;
               if (yok && x >= 0 && x < a.OW) {
 #pragma unroll
-                for (int k = 0; k < 16; ++k) mx[k] = max(mx[k], static_cast<int32_t>(raw[k]));
+                for (int k = 0; k < 16; ++k) {
+                  if constexpr (EB == 1)
+                    mx[k] = static_cast<uint32_t>(max(static_cast<int32_t>(mx[k]), static_cast<int32_t>(raw[k])));
+                  else
+                    mx[k] = __uint_as_float(mx[k]) < __uint_as_float(raw[k]) ? raw[k] : mx[k];
+                }
               }
             }
             tc_fence_before();
@@ -800,7 +808,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
               d.side_base = d.pix;
               d.side_pstride = sl.Pp;
             }
-            epilogue_chunk<EB, SIG, CAL>(a, reinterpret_cast<const uint32_t*>(mx), d, n_tile * a.bn + c, s_vec, p2ok, c);
+            epilogue_chunk<EB, SIG, CAL>(a, mx, d, n_tile * a.bn + c, s_vec, p2ok, c);
           }
         }
         goto epilogue_done;
@@ -1103,7 +1111,7 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
       // int8 7x7/s2/p3 stem + 3x3/s2/p1 max_pool2d over LAY_S2DP: M grid =
       // the phase sub-grid raster (pooled pixel (p, q) at (p+1, q+1)); the
       // 16 s2d taps (ty, tx) are paired along tx (K = 2 x 16 bytes)
-      if (eb != 1 || sp.KH != 7 || sp.KW != 7 || 4 * sp.C > 16 || !sp.pool) return false;
+      if (sp.KH != 7 || sp.KW != 7 || 4 * sp.C * eb > 32 || !sp.pool) return false;
       if (sp.pkh != 3 || sp.pkw != 3 || sp.psh != 2 || sp.psw != 2 || sp.pph != 1 || sp.ppw != 1) return false;
       kb = 16;
       const int hs = (sp.H + 6 + 1) / 2, ws = (sp.W + 6 + 1) / 2;
@@ -1115,12 +1123,20 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
       a.OW = sp.OW;
       a.poh = sp.poh;
       a.pow = sp.pow;
-      cc = 1;
-      pair_taps = true;
       a.win = 1;
-      a.subs = 6;  // [row phase][col phase 0, col phase 1, col phase 0 again]
-      const int8_t rs[6] = {0, 1, 0, 2, 3, 2};
-      for (int i = 0; i < 6; ++i) a.region_sg[i] = rs[i];
+      if (eb == 1) {  // 12 s2d codes in one 16-byte chunk; K = two adjacent taps
+        cc = 1;
+        pair_taps = true;
+        a.win_spt = 8;
+        a.subs = 6;  // [row phase][col phase 0, col phase 1, col phase 0 again]
+        const int8_t rs[6] = {0, 1, 0, 2, 3, 2};
+        for (int i = 0; i < 6; ++i) a.region_sg[i] = rs[i];
+      } else {  // 12 s2d bf16 channels in two 16-byte planes; K = one tap over both planes
+        cc = 2;
+        a.win_spt = 16;
+        a.subs = 4;  // [row phase][col phase]
+        for (int i = 0; i < 4; ++i) a.region_sg[i] = static_cast<int8_t>(i);
+      }
       for (int ta = 0; ta < 4; ++ta)
         for (int tb = 0; tb < 4; ++tb) taps.push_back({0, 0});  // B layout only; A offsets below
       break;
@@ -1314,20 +1330,29 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
         }
   }
   if (a.win) {
-    // [dy][dx][ty][tx pair]: v = dy + ty - 1, u = dx + 2k - 1; tap (ty, 2k) reads region
-    // (v&1, u&1) at fl(v/2)*Wg + fl(u/2); tap (ty, 2k+1) the next column region (LBO)
+    // [dy][dx][step]: v = dy + ty - 1, u = dx + tx - 1; tap (ty, tx) reads region (v&1, u&1)
+    // at fl(v/2)*Wg + fl(u/2).  int8: steps pair (ty, 2k), (ty, 2k+1), the second half in
+    // the next column region (LBO); bf16: one tap per step, K over the two chunk planes (LBO)
     a.n_steps = 0;
     for (int dy = 0; dy < 3; ++dy)
       for (int dx = 0; dx < 3; ++dx)
         for (int ty = 0; ty < 4; ++ty)
-          for (int k = 0; k < 2; ++k) {
-            const int v = dy + ty - 1, u = dx + 2 * k - 1;
+          for (int k = 0; k < (eb == 1 ? 2 : 4); ++k) {
+            const int tx = eb == 1 ? 2 * k : k;
+            const int v = dy + ty - 1, u = dx + tx - 1;
             const int vb = v & 1, ub = u & 1, fv = v >> 1, fu = u >> 1;  // arithmetic shifts: floor
             MmaStep m;
-            m.a_off = static_cast<uint32_t>(vb * 3 + ub) * a_sub + static_cast<uint32_t>(fv * a.Wg + fu - dmin) * 16;
-            m.a_lbo = a_sub + static_cast<uint32_t>(ub) * 16;
-            m.b_off = static_cast<uint32_t>(ty * 4 + 2 * k) * b_plane;
-            m.b_lbo = b_plane;
+            if (eb == 1) {
+              m.a_off = static_cast<uint32_t>(vb * 3 + ub) * a_sub + static_cast<uint32_t>(fv * a.Wg + fu - dmin) * 16;
+              m.a_lbo = a_sub + static_cast<uint32_t>(ub) * 16;
+              m.b_off = static_cast<uint32_t>(ty * 4 + tx) * b_plane;
+              m.b_lbo = b_plane;
+            } else {
+              m.a_off = static_cast<uint32_t>(vb * 2 + ub) * a_sub + static_cast<uint32_t>(fv * a.Wg + fu - dmin) * 16;
+              m.a_lbo = a_plane;
+              m.b_off = static_cast<uint32_t>((ty * 4 + tx) * bplanes) * b_plane;
+              m.b_lbo = b_plane;
+            }
             a.steps[a.n_steps++] = m;
           }
   }
@@ -1355,7 +1380,7 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
   if (per_n > a.m_tiles) per_n = a.m_tiles;
   p.grid = per_n * a.n_tiles;
   int body = a.resident_b ? a.b_res_bytes : a.b_stage_bytes * a.n_stages;
-  p.smem = 1024 + body + a.a_stage_bytes * a.n_stages + barrier_bytes + kMaxSteps * 8;
+  p.smem = 1024 + body + a.a_stage_bytes * a.n_stages + barrier_bytes;
   return true;
 }
 

@@ -370,7 +370,7 @@ void decide_tc(Exec& ex) {
           // is part of the GEMM's M (TC_STEM_POOL); otherwise staged pooling
           TcConvSpec wp = fs;
           wp.kind = TC_STEM_POOL;
-          const bool win_ok = sp.elem_bytes == 1 && sp.C == 3 && g.ph == 3 && tc_conv_plan_ok(wp);
+          const bool win_ok = sp.C == 3 && g.ph == 3 && tc_conv_plan_ok(wp);
           if (win_ok || tc_conv_plan_ok(fs)) {
             sp = win_ok ? wp : fs;
             ex.fused_pool[gi] = pj;

@@ -927,12 +927,18 @@ void launch_input_convert(const float* x, int N, int C, int H, int W, void* out,
       cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
       return v > 0 ? v : 148;
     }();
-    if (!(C == 3 && s2d_pad == 3 && fmt == FMT_I8 && W % 4 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0)) {
-      std::fprintf(stderr, "mrb200: LAY_S2DP input conversion needs an int8 3-channel pad-3 stem\n");
+    if (!(C == 3 && s2d_pad == 3 && (fmt == FMT_I8 || fmt == FMT_BF16) && W % 4 == 0 &&
+          reinterpret_cast<uintptr_t>(x) % 16 == 0)) {
+      std::fprintf(stderr, "mrb200: LAY_S2DP input conversion needs a 3-channel pad-3 stem (int8 / bf16)\n");
       std::abort();
     }
     const FastDiv fd = make_fastdiv(static_cast<uint32_t>(W / 4));
     const int rows = N * 2 * L.Hq;
+    if (fmt == FMT_BF16) {
+      pdl_launch(k_input_s2d_ct<3, 3, 8, true, false>, std::min(rows, sms2 * 8), 128, 2 * 2 * C * W * sizeof(float), s, x,
+                 N, H, W, out, L, pre_mul, q, fd);
+      return;
+    }
     pdl_launch(q.ovf ? k_input_s2d_ct<3, 3, 16, true, true> : k_input_s2d_ct<3, 3, 16, true, false>, std::min(rows, sms2 * 8), 128, 2 * 2 * C * W * sizeof(float), s, 
         x, N, H, W, out, L, pre_mul, q, fd);
     return;
