@@ -1064,7 +1064,7 @@ void prepare_weights(Exec& ex, cudaStream_t s) {
       cs = I;
     } else {
       fmt = FMT_BF16;
-      cs = I;
+      cs = g.kind == GroupKind::Dense ? static_cast<int>(round_up(I, 8)) : I;  // dense: [K/8][M][8] (k_dense)
     }
     int64_t n;
     if (fmt == FMT_F32) {

@@ -839,22 +839,20 @@ __global__ void __launch_bounds__(256) k_dense(const float* __restrict__ x, int 
         for (int r = 0; r < kDenseRows; ++r) res[r] = __fadd_rn(res[r], __fmul_rn(srow[r * ks + kk], wv));
       }
     } else {
-      const uint16_t* wt = static_cast<const uint16_t*>(w) + static_cast<int64_t>(k0) * M + j;
-      const int kend = min(kc, K - k0);
-      int kk = 0;
-      for (; kk + 8 <= kend; kk += 8) {
-        float wv[8];
+      // [K/8][M][8] bf16: one 16-byte load = 8 consecutive k of column j (padding rows are zero)
+      const uint4* wt = reinterpret_cast<const uint4*>(w) + static_cast<int64_t>(k0 / 8) * M + j;
+      for (int kk = 0; kk < kc; kk += 8) {
+        const uint4 u = __ldg(wt + static_cast<int64_t>(kk / 8) * M);
+        const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-        for (int u = 0; u < 8; ++u) wv[u] = bf16_to_f32(__ldg(wt + static_cast<int64_t>(kk + u) * M));
+        for (int h = 0; h < 4; ++h) {
+          const float w0 = __uint_as_float(w4[h] << 16), w1 = __uint_as_float(w4[h] & 0xffff0000u);
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-#pragma unroll
-          for (int r = 0; r < kDenseRows; ++r) res[r] = __fmaf_rn(srow[r * ks + kk + u], wv[u], res[r]);
-      }
-      for (; kk < kend; ++kk) {
-        const float wv = bf16_to_f32(__ldg(wt + static_cast<int64_t>(kk) * M));
-#pragma unroll
-        for (int r = 0; r < kDenseRows; ++r) res[r] = __fmaf_rn(srow[r * ks + kk], wv, res[r]);
+          for (int r = 0; r < kDenseRows; ++r) {
+            res[r] = __fmaf_rn(srow[r * ks + kk + 2 * h], w0, res[r]);
+            res[r] = __fmaf_rn(srow[r * ks + kk + 2 * h + 1], w1, res[r]);
+          }
+        }
       }
     }
   }
@@ -879,7 +877,7 @@ __global__ void k_dense_weight_t(const float* __restrict__ w, int M, int K, int 
   const int64_t total = static_cast<int64_t>(M) * Kp;
   GRID_STRIDE(i, total) {
     int j = static_cast<int>(i % M);
-    int k = static_cast<int>(i / M);  // out index: [k][j] (bf16) / [k/4][j][k%4] (int8)
+    int k = static_cast<int>(i / M);  // out index: [k/8][j][k%8] (bf16) / [k/4][j][k%4] (int8)
     float v = 0.f;
     bool live = k < K;
     if (live) {
@@ -891,7 +889,7 @@ __global__ void k_dense_weight_t(const float* __restrict__ w, int M, int K, int 
       int32_t code = live ? (quant ? quant_code(v, q) : static_cast<int32_t>(v)) : 0;
       static_cast<int8_t*>(out)[(static_cast<int64_t>(k / 4) * M + j) * 4 + (k & 3)] = static_cast<int8_t>(code);
     } else {
-      static_cast<uint16_t*>(out)[static_cast<int64_t>(k) * M + j] = live ? f32_to_bf16(v) : 0;
+      static_cast<uint16_t*>(out)[(static_cast<int64_t>(k / 8) * M + j) * 8 + (k & 7)] = live ? f32_to_bf16(v) : 0;
     }
   }
 }
