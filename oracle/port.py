@@ -139,8 +139,14 @@ def op_cast(x, dtype: str):
 
 
 def op_conv2d(x, w, strides=(1, 1), padding=(0, 0), layout="NCHW"):
+    if layout == "NHWC":
+        # kernels.cpp:640-716 walks the same (n, oc, oh, ow, ic, kh, kw) loops for
+        # NHWC/HWIO, only the indexing differs: same sums, same order
+        y = op_conv2d(np.ascontiguousarray(np.transpose(_f32(x), (0, 3, 1, 2))),
+                      np.ascontiguousarray(np.transpose(_f32(w), (3, 2, 0, 1))), strides, padding)
+        return np.ascontiguousarray(np.transpose(y, (0, 2, 3, 1)))
     if layout != "NCHW":
-        raise NotImplementedError("oracle conv2d: NCHW only")
+        raise NotImplementedError("oracle conv2d: NCHW / NHWC only")
     x, w = _f32(x), _f32(w)
     N, C, H, W = x.shape
     OC, IC, KH, KW = w.shape
@@ -176,6 +182,13 @@ def op_depthwise_conv2d(x, win, w, strides=(1, 1), padding=(0, 0)):
     y = np.empty((N, C, OH, OW), np.float32)
     lib().mro_dwconv2d_f32(_p(x), _p(w), _p(y), N, C, H, W, KH, KW, sh, sw, ph, pw)
     return y
+
+
+def op_transpose(x, axes):
+    """kernels.cpp:399-431: a fresh tensor with permuted axes (values unchanged)."""
+    if isinstance(x, IntTensor):
+        return IntTensor(np.ascontiguousarray(np.transpose(x.vals, tuple(axes))), x.dtype)
+    return np.ascontiguousarray(np.transpose(_f32(x), tuple(int(a) for a in axes)))
 
 
 def op_reshape(x, newshape):
@@ -238,6 +251,7 @@ OPS = {
     "max_pool2d": op_max_pool2d,
     "depthwise_conv2d": op_depthwise_conv2d,
     "reshape": op_reshape,
+    "transpose": op_transpose,
     "dense": op_dense,
     "nn.dense": op_dense,
     "bias_add": op_bias_add,

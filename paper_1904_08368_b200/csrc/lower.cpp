@@ -118,6 +118,13 @@ bool match_requant(const std::vector<ExprP>& ch, size_t i, QParams* q) {
 
 int64_t out_dim(int64_t in, int64_t k, int64_t s, int64_t p) { return (in - k + 2 * p) / s + 1; }
 
+// transpose(x, axes=perm): the layout pass's relabelings (passes.cpp:481-486,
+// rewrites.cpp:440-467) are data movement only; physical layouts here do not
+// depend on the logical axis order, so they are folded away during lowering.
+bool is_transpose(const ExprP& e, std::initializer_list<int64_t> perm) {
+  return is_call(e, "transpose") && attr_ints(e->attrs, "axes", {}) == std::vector<int64_t>(perm);
+}
+
 }  // namespace
 
 Program lower_module(const Module& m, int64_t batch, int n_data_inputs) {
@@ -193,12 +200,23 @@ Program lower_module(const Module& m, int64_t batch, int n_data_inputs) {
     const ExprP& A = b.let_of[anchor];
     b.visited.insert(anchor);
     const ValueInfo* data_vi = nullptr;
+    bool data_nhwc = false, weight_hwio = false, anchor_nhwc = false;  // layout-pass relabels
 
     // ---- prologues ----
     auto data_operand = [&](const ExprP& arg) {
       Traced t = trace(b, arg);
       if (t.value < 0) unsupported(g.name, "constant data operand");
       g.data.value = t.value;
+      data_nhwc = P.values[t.value].nhwc_view;
+      for (size_t k = 0; k < t.chain.size();) {  // NCHW -> NHWC relabels commute with the realize chain
+        if (is_transpose(t.chain[k], {0, 2, 3, 1})) {
+          if (data_nhwc) unsupported(g.name, "transpose of an NHWC value");
+          data_nhwc = true;
+          t.chain.erase(t.chain.begin() + static_cast<long>(k));
+        } else {
+          ++k;
+        }
+      }
       size_t i = 0;
       float s;
       if (i < t.chain.size() && is_call(t.chain[i], "multiply") && !match_requant(t.chain, i, &g.data.q) &&
@@ -224,6 +242,15 @@ Program lower_module(const Module& m, int64_t batch, int n_data_inputs) {
       } else {
         g.weight.constant = t.lit->f32();
         g.weight.shape = t.lit->shape;
+      }
+      weight_hwio = false;
+      for (size_t k = 0; k < t.chain.size();) {  // OIHW -> HWIO relabel (NHWC conv weights)
+        if (is_transpose(t.chain[k], {2, 3, 1, 0})) {
+          weight_hwio = true;
+          t.chain.erase(t.chain.begin() + static_cast<long>(k));
+        } else {
+          ++k;
+        }
       }
       size_t i = 0;
       while (i < t.chain.size() && is_call(t.chain[i], "multiply") && !match_requant(t.chain, i, &g.weight.q)) {
@@ -255,16 +282,20 @@ Program lower_module(const Module& m, int64_t batch, int n_data_inputs) {
     const std::string& op = A->name;
     if (op == "conv2d" || op == "depthwise_conv2d") {
       g.kind = op == "conv2d" ? GroupKind::Conv : GroupKind::DwConv;
-      if (attr_str(A->attrs, "layout", "NCHW") != "NCHW") unsupported(g.name, "only NCHW conv2d layout");
+      const std::string lay = attr_str(A->attrs, "layout", "NCHW");
+      if (lay != "NCHW" && !(lay == "NHWC" && op == "conv2d")) unsupported(g.name, "conv2d layout " + lay);
+      anchor_nhwc = lay == "NHWC";
       size_t want = op == "conv2d" ? 2 : 3;
       if (A->args.size() != want) unsupported(g.name, op + " arity");
       data_operand(A->args[0]);
+      if (data_nhwc != anchor_nhwc) unsupported(g.name, "conv2d data layout does not match its layout attribute");
       if (op == "depthwise_conv2d") {
         Traced win = trace(b, A->args[1]);
         if (win.value < 0 || !win.chain.empty()) unsupported(g.name, "window operand");
         g.window_value = win.value;
       }
       weight_operand(A->args.back());
+      if (weight_hwio != anchor_nhwc) unsupported(g.name, "conv2d weight layout does not match its layout attribute");
       auto st = attr_ints(A->attrs, "strides", {1, 1});
       auto pd = attr_ints(A->attrs, "padding", {0, 0});
       if (st.size() != 2 || pd.size() != 2) unsupported(g.name, "strides/padding");
@@ -336,6 +367,8 @@ Program lower_module(const Module& m, int64_t batch, int n_data_inputs) {
     }
     std::vector<int64_t> shape = g.out_shape;
     int64_t C = shape.size() >= 2 ? shape[1] : 1;
+    bool back_to_nchw = false, out_nhwc = false;
+    if (g.kind != GroupKind::Conv && data_nhwc) unsupported(g.name, op + " over an NHWC value");
     for (size_t i = 0; i < epi_calls.size();) {
       QParams q;
       if (match_requant(epi_calls, i, &q)) {
@@ -350,6 +383,19 @@ Program lower_module(const Module& m, int64_t batch, int n_data_inputs) {
       if (c->callee_is_var) unsupported(g.name, "call in epilogue");
       const std::string& o = c->name;
       if (!g.epi.empty() && g.epi.back().kind == EpiKind::SumHW) unsupported(g.name, "ops after sum");
+      if (o == "transpose") {
+        if (anchor_nhwc && !back_to_nchw && g.epi.empty() && is_transpose(c, {0, 3, 1, 2})) {
+          back_to_nchw = true;  // NHWC conv result back to NCHW: a relabel
+        } else if (!out_nhwc && (!anchor_nhwc || back_to_nchw) && is_transpose(c, {0, 2, 3, 1}) && shape.size() == 4) {
+          out_nhwc = true;  // the value is handed to NHWC consumers: a relabel
+        } else {
+          unsupported(g.name, "transpose in the epilogue");
+        }
+        ++i;
+        continue;
+      }
+      if (anchor_nhwc && !back_to_nchw) unsupported(g.name, "epilogue op on the NHWC conv result");
+      if (out_nhwc) unsupported(g.name, "op after the NHWC relabel (only a realize chain may follow)");
       // after a flatten only the realize chain of the consumer's input (matched above; run by
       // the flatten tail) may follow
       for (const auto& e : g.epi)
@@ -380,6 +426,7 @@ Program lower_module(const Module& m, int64_t batch, int n_data_inputs) {
         EpiOp e{EpiKind::Residual};
         e.value = b.param_value[r->name];
         if (P.values[e.value].shape != shape) unsupported(g.name, "broadcasting add in epilogue");
+        if (P.values[e.value].nhwc_view) unsupported(g.name, "residual operand is NHWC-relabelled");
         g.epi.push_back(e);
       } else if (o == "multiply") {
         ExprP k = other();
@@ -431,10 +478,12 @@ Program lower_module(const Module& m, int64_t batch, int n_data_inputs) {
     for (const auto& name : b.order)
       if (!b.visited.count(name)) unsupported(g.name, "binding %" + name + " is outside the prologue/anchor/epilogue pattern");
 
+    if (anchor_nhwc && !back_to_nchw) unsupported(g.name, "NHWC conv result never returns to NCHW");
     int ov = add_value(out);
     int gi = static_cast<int>(P.groups.size());
     P.values[ov].producer = gi;
     P.values[ov].shape = g.out_shape;
+    P.values[ov].nhwc_view = out_nhwc;
     if (!g.epi.empty() && g.epi.back().kind == EpiKind::Requant) {
       P.values[ov].quantized = true;
       P.values[ov].q = g.epi.back().q;
@@ -465,6 +514,7 @@ Program lower_module(const Module& m, int64_t batch, int n_data_inputs) {
     P.result_value = value_of["__result__"];
   }
   P.values[P.result_value].is_result = true;
+  if (P.values[P.result_value].nhwc_view) unsupported("@main", "an NHWC-relabelled result");
   if (P.groups.empty()) bad(MR_ERR_UNSUPPORTED_GROUP, "module has no Primitive group");
   return P;
 }

@@ -64,6 +64,10 @@ struct ValueInfo {
   QParams q;
   std::vector<int> consumers;  // groups reading it
   bool is_result = false;
+  // layout pass (passes.cpp:481-486): the reference value is the NHWC
+  // transpose of this NCHW tensor (its producer ended in transpose(0,2,3,1));
+  // only NHWC conv2d consumers read it (data layouts here are physical)
+  bool nhwc_view = false;
 };
 
 enum class GroupKind { Conv, Dense, MaxPool, DwConv };

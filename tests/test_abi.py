@@ -124,3 +124,11 @@ def test_product_does_not_import_oracle():
                 src = open(os.path.join(dirpath, f), errors="ignore").read()
                 bad = re.findall(r"from oracle|import oracle|libmr_oracle|mr_oracle\.h|\bmro_\w+|\bmr_ref\b|oracle/_ref", src)
                 assert not bad, (f, bad)
+
+
+@pytest.mark.parametrize("prec", ["int8", "fp32"])
+def test_lower_layout_pass_module(prec):
+    """the layout=NHWC pass output lowers to the same 22 groups."""
+    text, _, _ = mrb.load_model("resnet18_tiny_nhwc", prec)
+    d = mrb.lower(text, 4)
+    assert len(d["groups"]) == 22 and d["result_shape"] == [4, 10]

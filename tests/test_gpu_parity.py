@@ -162,3 +162,15 @@ def test_gpu_calibration_fails_like_reference(gpu):
     with pytest.raises(mrb.BackendError) as e:
         mrb.calibrate(text, [w[p.name] for p in src.params if p.kind != "input"], [x], k_min=-16, k_max=-10)
     assert e.value.code == 15  # MR_ERR_CALIBRATION_FAILED (DiagCode::CalibrationFailed + 1)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,batch,prec,fm", [("resnet18_tiny", 4, "int8", 0), ("resnet18_tiny", 4, "fp32", 1),
+                                                ("dqn", 2, "int8", 0)])
+def test_layout_pass_modules_bitexact(gpu, name, batch, prec, fm):
+    """The layout=NHWC pass output runs through the same
+    executor and matches the reference bit for bit."""
+    gold = np.load(os.path.join(GOLD, "%s_b%d.npz" % (name, batch)))
+    ex, src = setup(name + "_nhwc", prec, batch, float_mode=fm)
+    y = ex.run_host(modelzoo.make_inputs(src, batch, seed=0))
+    assert np.array_equal(bits(y), bits(gold[prec])), int(np.sum(bits(y) != bits(gold[prec])))

@@ -187,3 +187,17 @@ def test_port_matches_reference_golden_other_models(name, prec):
         pytest.skip("golden not generated")
     text, x, wl = _golden_case(name, 2, prec)
     assert np.array_equal(bits(port.run_weights(text, x, wl)), bits(np.load(path)[prec]))
+
+
+@pytest.mark.parametrize("name,batch,prec", [("resnet18_tiny", 4, "int8"), ("resnet18_tiny", 4, "fp32"),
+                                             ("dqn", 2, "int8"), ("dqn", 2, "fp32")])
+def test_port_layout_pass_modules(name, batch, prec):
+    """The layout=NHWC pass output (transposes + NHWC conv2d) evaluates to the
+    reference's NCHW results bit for bit (oracle/build_models: same k)."""
+    import paper_1904_08368_b200 as mrb
+    from paper_1904_08368_b200 import modelzoo
+    text, meta, src = mrb.load_model(name + "_nhwc", prec)
+    w = modelzoo.make_weights(src, seed=meta["weights_seed"])
+    x = modelzoo.make_inputs(src, batch, seed=0)
+    y = port.run_weights(text, x, [w[p.name] for p in src.params if p.kind != "input"])
+    assert np.array_equal(bits(y), bits(np.load(os.path.join(GOLD, "%s_b%d.npz" % (name, batch)))[prec]))
