@@ -132,3 +132,20 @@ def test_lower_layout_pass_module(prec):
     text, _, _ = mrb.load_model("resnet18_tiny_nhwc", prec)
     d = mrb.lower(text, 4)
     assert len(d["groups"]) == 22 and d["result_shape"] == [4, 10]
+
+
+def test_combine_conv_is_identity_on_baseline_models():
+    """the reference's combine-conv pass finds no
+    same-geometry parallel conv2d pairs in the BASELINE models, so its output
+    lowers to the same groups as the plain pipeline (concat / split groups would
+    be rejected at compile time with MR_ERR_UNSUPPORTED_GROUP)."""
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("oracle/_ref/mr_ref not built (needs /root/reference)")
+    from paper_1904_08368_b200 import modelzoo
+    for src in (modelzoo.resnet18(image=32, num_classes=10, widths=(32, 32, 64, 64)), modelzoo.dqn(batch=2),
+                modelzoo.mobilenet_v1(image=32)):
+        plain = ref.compile(src.text, "fold-scale,fold,dce,fuse", 0)
+        comb = ref.compile(src.text, "fold-scale,fold,dce,combine-conv,fuse", 0)
+        a, b = mrb.lower(plain, 2), mrb.lower(comb, 2)
+        assert [g["desc"] for g in a["groups"]] == [g["desc"] for g in b["groups"]]
