@@ -144,10 +144,13 @@ def barrier(world):
         dist.barrier()
 
 
+MODEL = "resnet18"  # --model: another BASELINE config as a side measurement (not the contract line)
+
+
 def load(precision):
     import paper_1904_08368_b200 as mrb
     from paper_1904_08368_b200 import modelzoo
-    text, meta, src = mrb.load_model("resnet18", precision)
+    text, meta, src = mrb.load_model(MODEL, precision)
     w = modelzoo.make_weights(src, seed=meta["weights_seed"])
     wl = [w[p.name] for p in src.params if p.kind != "input"]
     return mrb, modelzoo, text, meta, src, wl
@@ -341,12 +344,16 @@ def main():
     ap.add_argument("--batch", type=int, default=BATCH_PER_GPU, help="images per GPU per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-bf16", action="store_true")
+    ap.add_argument("--model", default="resnet18",
+                    help="models/<name>: resnet18 (the contract workload) or mobilenet_v1 (side measurement)")
     ap.add_argument("--no-cuda-graph", action="store_true",
                     help="replay the launch list without a CUDA graph (for ncu launch lists: ncu cannot replay "
                          "the captured graph)")
     args = ap.parse_args()
     rank, world, local = dist_env()
     warmup = max(args.warmup, 3)
+    global MODEL
+    MODEL = args.model
 
     config = {"workload": "resnet18_int8_b%d" % args.batch, "model": "ResNet-18 (fused, 22 Primitive groups)",
               "batch_per_gpu": args.batch, "global_batch": args.batch * world, "image": [3, 224, 224],

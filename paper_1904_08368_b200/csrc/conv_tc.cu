@@ -1392,7 +1392,9 @@ static bool choose(TcConvPlan& p) {
   const TcConvSpec keep = p.spec;
   if (p.spec.kind == TC_STEM_S2D || p.spec.kind == TC_STEM_POOL) return choose_kb(p, 16);
   const int forced = p.spec.kb;
-  for (int kb : {128, 64}) {
+  // 16-byte chunks (8-pixel no-swizzle rows, K over two planes) for channel
+  // counts that fill no 64-byte chunk (e.g. 32 int8 channels)
+  for (int kb : {128, 64, 16}) {
     if (forced && kb != forced) continue;
     p.spec = keep;
     if (choose_kb(p, kb)) {

@@ -338,12 +338,20 @@ void decide_tc(Exec& ex) {
       auto pk = phase_kb.find(g.data.value);  // one phase-split copy per value
       if (pk != phase_kb.end()) sp.kb = pk->second;
       ok = tc_conv_plan_ok(sp);
-    } else if (g.sh == 2 && g.sw == 2 && g.kh == g.kw && (g.kh & 1) && g.ph == g.kh / 2 && g.pw == g.kw / 2 &&
-               P.values[g.data.value].is_data) {
-      sp.kind = TC_STEM_S2D;
-      sp.Hs = static_cast<int>((sp.H + 2 * g.ph + 1) / 2);
-      sp.Ws = static_cast<int>((sp.W + 2 * g.pw + 1) / 2);
-      ok = tc_conv_plan_ok(sp);
+    }
+    if (!ok && g.sh == 2 && g.sw == 2 && g.kh == g.kw && (g.kh & 1) && g.ph == g.kh / 2 && g.pw == g.kw / 2 &&
+        P.values[g.data.value].is_data) {
+      // a stride-2 stem over the network input (e.g. 3x3/s2 on 3 channels, which
+      // fills no chunk for the phase formulation): space-to-depth
+      TcConvSpec s2 = sp;
+      s2.kind = TC_STEM_S2D;
+      s2.kb = 0;
+      s2.Hs = static_cast<int>((sp.H + 2 * g.ph + 1) / 2);
+      s2.Ws = static_cast<int>((sp.W + 2 * g.pw + 1) / 2);
+      if (tc_conv_plan_ok(s2)) {
+        sp = s2;
+        ok = true;
+      }
     }
     if (ok && sp.kind == TC_STEM_S2D) {
       // cross-group fusion: conv -> max_pool2d when the

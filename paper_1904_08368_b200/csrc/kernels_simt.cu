@@ -658,6 +658,255 @@ __global__ void k_dwconv(const void* __restrict__ x, int xfmt, const float* __re
   }
 }
 
+// ---- depthwise conv, bandwidth path --------------------------------------------------
+// One thread per (output pixel, 16-byte input granule: 4 fp32 / 8 bf16 channels),
+// output column fastest (coalesced 16-byte tap loads; the 3 input rows of a
+// warp are L1-resident).  The taps are fixed byte offsets into the zero-padded
+// input (padding <= kPad), so no bounds tests: adding a padded tap's exact
+// zero product leaves the sum bit-identical to the reference's skip (the
+// accumulator starts at +0, kernels.cpp:684-701 / ref_harness
+// k_depthwise_conv2d).  strict: fmul then fadd per tap in kh -> kw order.
+__global__ void __launch_bounds__(256) k_dwconv_fast(const void* __restrict__ x, int xfmt, const float* __restrict__ w,
+                                                     ConvGeom g, int strict, EpiDev epi, OutDev out, FastDiv fd_ow,
+                                                     FastDiv fd_oh, FastDiv fd_n) {
+  pdl_trigger();
+  pdl_wait();
+  const int eb = xfmt == FMT_F32 ? 4 : 2;
+  const int cpg = 16 / eb;
+  const uint32_t grans = static_cast<uint32_t>(g.C / cpg);
+  const uint32_t total = grans * g.N * g.OH * g.OW;
+  const int Wp = g.W + 2 * kPad, Hp = g.H + 2 * kPad;
+  const int OWp = g.OW + 2 * kPad, OHp = g.OH + 2 * kPad;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const uint32_t t = fdiv(i, fd_ow);
+    const int ow = static_cast<int>(i - t * static_cast<uint32_t>(g.OW));
+    const uint32_t t2 = fdiv(t, fd_oh);
+    const int oh = static_cast<int>(t - t2 * static_cast<uint32_t>(g.OH));
+    const uint32_t gran = fdiv(t2, fd_n);
+    const int n = static_cast<int>(t2 - gran * static_cast<uint32_t>(g.N));
+    const int c0 = static_cast<int>(gran) * cpg;
+    const int64_t pin = (static_cast<int64_t>(n) * Hp + oh * g.sh - g.ph + kPad) * Wp + ow * g.sw - g.pw + kPad;
+    const char* src = static_cast<const char*>(x) + lay_byte(g.in, pin, c0);
+    const int64_t row = static_cast<int64_t>(Wp) * g.in.kb;
+    float acc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k] = 0.0f;
+    for (int kh = 0; kh < g.KH; ++kh)
+      for (int kw = 0; kw < g.KW; ++kw) {
+        const char* p = src + kh * row + kw * g.in.kb;
+        float v[8];
+        if (xfmt == FMT_F32) {
+          const float4 f = __ldg(reinterpret_cast<const float4*>(p));
+          v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+          v[4] = v[5] = v[6] = v[7] = 0.f;
+        } else {
+          const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+          const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            v[2 * b] = __uint_as_float(w4[b] << 16);
+            v[2 * b + 1] = __uint_as_float(w4[b] & 0xffff0000u);
+          }
+        }
+        const int tap = kh * g.KW + kw;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          if (k >= cpg) break;
+          const float wv = __ldg(w + static_cast<int64_t>(c0 + k) * g.KH * g.KW + tap);
+          acc[k] = strict ? __fadd_rn(acc[k], __fmul_rn(v[k], wv)) : __fmaf_rn(v[k], wv, acc[k]);
+        }
+      }
+    const int64_t pix = (static_cast<int64_t>(n) * OHp + oh + kPad) * OWp + ow + kPad;
+    // epilogue + stores in 4-channel pieces (each lies inside one output chunk)
+    for (int s4 = 0; s4 < cpg / 4; ++s4) {
+      float r[4];
+      int32_t code[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        code[k] = 0;
+        r[k] = apply_epi(epi, acc[4 * s4 + k], pix, c0 + 4 * s4 + k, &code[k]);
+      }
+      char* d4 = static_cast<char*>(out.primary) + lay_byte(out.plan, pix, c0 + 4 * s4);
+      if (out.primary_fmt == FMT_F32) {
+        *reinterpret_cast<float4*>(d4) = make_float4(r[0], r[1], r[2], r[3]);
+      } else if (out.primary_fmt == FMT_BF16) {
+        *reinterpret_cast<uint2*>(d4) =
+            make_uint2(static_cast<uint32_t>(f32_to_bf16(r[0])) | (static_cast<uint32_t>(f32_to_bf16(r[1])) << 16),
+                       static_cast<uint32_t>(f32_to_bf16(r[2])) | (static_cast<uint32_t>(f32_to_bf16(r[3])) << 16));
+      } else {
+        uint32_t u = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) u |= (static_cast<uint32_t>(code[k]) & 0xff) << (8 * k);
+        *reinterpret_cast<uint32_t*>(d4) = u;
+      }
+      if (out.side) {
+        char* s4p = static_cast<char*>(out.side) + lay_byte(out.slay, pix, c0 + 4 * s4);
+        if (out.side_fmt == FMT_I8) {
+          uint32_t u = 0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) u |= (static_cast<uint32_t>(quant_code(r[k], out.side_q)) & 0xff) << (8 * k);
+          *reinterpret_cast<uint32_t*>(s4p) = u;
+        } else {
+          *reinterpret_cast<uint2*>(s4p) =
+              make_uint2(static_cast<uint32_t>(f32_to_bf16(r[0])) | (static_cast<uint32_t>(f32_to_bf16(r[1])) << 16),
+                         static_cast<uint32_t>(f32_to_bf16(r[2])) | (static_cast<uint32_t>(f32_to_bf16(r[3])) << 16));
+        }
+      }
+    }
+  }
+}
+
+// Register-blocked depthwise 3x3 (stride 1 or 2, pad <= 1): one thread = 4
+// channels x 4 consecutive output columns.  The 36 weights stay in registers,
+// the input columns of the 4 outputs are loaded once per input row (6 / 9
+// loads per row), the epilogue's ops are interpreted once per thread over the
+// 16 values with their per-channel vectors hoisted.  Same per-output order and
+// arithmetic as k_dwconv_fast (and the reference).
+template <int SW>
+__global__ void __launch_bounds__(256) k_dw3x3_rb(const void* __restrict__ x, int xfmt, const float* __restrict__ w,
+                                                  ConvGeom g, int strict, EpiDev epi, OutDev out, FastDiv fd_owq,
+                                                  FastDiv fd_oh, FastDiv fd_n) {
+  pdl_trigger();
+  pdl_wait();
+  constexpr int OUTS = 4, NCOL = (OUTS - 1) * SW + 3;
+  const int owq = (g.OW + OUTS - 1) / OUTS;
+  const uint32_t pieces = static_cast<uint32_t>(g.C / 4);
+  const uint32_t total = pieces * g.N * g.OH * owq;
+  const int Wp = g.W + 2 * kPad, Hp = g.H + 2 * kPad;
+  const int OWp = g.OW + 2 * kPad, OHp = g.OH + 2 * kPad;
+  const bool f32 = xfmt == FMT_F32;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const uint32_t t = fdiv(i, fd_owq);
+    const int oq = static_cast<int>(i - t * static_cast<uint32_t>(owq));
+    const uint32_t t2 = fdiv(t, fd_oh);
+    const int oh = static_cast<int>(t - t2 * static_cast<uint32_t>(g.OH));
+    const uint32_t pc = fdiv(t2, fd_n);
+    const int n = static_cast<int>(t2 - pc * static_cast<uint32_t>(g.N));
+    const int c0 = static_cast<int>(pc) * 4, ow0 = oq * OUTS;
+    float wr[4][9];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int tp = 0; tp < 9; ++tp) wr[k][tp] = __ldg(w + static_cast<int64_t>(c0 + k) * 9 + tp);
+    float acc[OUTS][4];
+#pragma unroll
+    for (int o = 0; o < OUTS; ++o)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[o][k] = 0.0f;
+    const int ih0 = oh * g.sh - g.ph + kPad;  // padded input row of tap kh = 0
+    const int iw0 = ow0 * SW - g.pw + kPad;
+    const int64_t rowb = static_cast<int64_t>(Wp) * g.in.kb;
+    const char* base = static_cast<const char*>(x) + lay_byte(g.in, (static_cast<int64_t>(n) * Hp + ih0) * Wp, c0);
+#pragma unroll
+    for (int kh = 0; kh < 3; ++kh) {
+      float col[NCOL][4];
+#pragma unroll
+      for (int j = 0; j < NCOL; ++j) {
+        const int cw = min(iw0 + j, Wp - 1);  // columns past the row end only feed discarded outputs
+        const char* p = base + kh * rowb + static_cast<int64_t>(cw) * g.in.kb;
+        if (f32) {
+          const float4 f = __ldg(reinterpret_cast<const float4*>(p));
+          col[j][0] = f.x; col[j][1] = f.y; col[j][2] = f.z; col[j][3] = f.w;
+        } else {
+          const uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
+          col[j][0] = __uint_as_float(u.x << 16); col[j][1] = __uint_as_float(u.x & 0xffff0000u);
+          col[j][2] = __uint_as_float(u.y << 16); col[j][3] = __uint_as_float(u.y & 0xffff0000u);
+        }
+      }
+#pragma unroll
+      for (int kw = 0; kw < 3; ++kw)
+#pragma unroll
+        for (int o = 0; o < OUTS; ++o)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float xv = col[o * SW + kw][k], wv = wr[k][kh * 3 + kw];
+            acc[o][k] = strict ? __fadd_rn(acc[o][k], __fmul_rn(xv, wv)) : __fmaf_rn(xv, wv, acc[o][k]);
+          }
+    }
+    // epilogue: the op list once per thread over OUTS x 4 values
+    int32_t code[OUTS][4];
+#pragma unroll
+    for (int o = 0; o < OUTS; ++o)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) code[o][k] = 0;
+    for (int op = 0; op < epi.n_ops; ++op) {
+      const int kind = epi.op[op];
+      if (kind == E_MULC || kind == E_BIAS) {
+        const float4 v4 = *reinterpret_cast<const float4*>(epi.vec[op] + c0);
+        const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+        for (int o = 0; o < OUTS; ++o)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) acc[o][k] = kind == E_MULC ? __fmul_rn(acc[o][k], vv[k]) : __fadd_rn(acc[o][k], vv[k]);
+      } else if (kind == E_MULS) {
+#pragma unroll
+        for (int o = 0; o < OUTS; ++o)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) acc[o][k] = __fmul_rn(acc[o][k], epi.s[op]);
+      } else if (kind == E_RELU) {
+#pragma unroll
+        for (int o = 0; o < OUTS; ++o)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) acc[o][k] = relu_ref(acc[o][k]);
+      } else if (kind == E_CLIP) {
+#pragma unroll
+        for (int o = 0; o < OUTS; ++o)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) acc[o][k] = clip_ref(acc[o][k], epi.s[op], epi.s2[op]);
+      } else if (kind == E_REQ) {
+        const QDev q = epi.q[op];
+#pragma unroll
+        for (int o = 0; o < OUTS; ++o)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            code[o][k] = quant_code(acc[o][k], q);
+            acc[o][k] = __fmul_rn(static_cast<float>(code[o][k]), q.c2);
+          }
+      } else {  // E_RES: per element through the generic path
+#pragma unroll
+        for (int o = 0; o < OUTS; ++o) {
+          const int64_t pix = (static_cast<int64_t>(n) * OHp + oh + kPad) * OWp + min(ow0 + o, g.OW - 1) + kPad;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            acc[o][k] = __fadd_rn(acc[o][k], load_fmt(epi.res[op], epi.res_fmt[op], lay_off(epi.res_lay[op], pix, c0 + k)));
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < OUTS; ++o) {
+      if (ow0 + o >= g.OW) break;
+      const int64_t pix = (static_cast<int64_t>(n) * OHp + oh + kPad) * OWp + ow0 + o + kPad;
+      char* d4 = static_cast<char*>(out.primary) + lay_byte(out.plan, pix, c0);
+      const float* r = acc[o];
+      if (out.primary_fmt == FMT_F32) {
+        *reinterpret_cast<float4*>(d4) = make_float4(r[0], r[1], r[2], r[3]);
+      } else if (out.primary_fmt == FMT_BF16) {
+        *reinterpret_cast<uint2*>(d4) =
+            make_uint2(static_cast<uint32_t>(f32_to_bf16(r[0])) | (static_cast<uint32_t>(f32_to_bf16(r[1])) << 16),
+                       static_cast<uint32_t>(f32_to_bf16(r[2])) | (static_cast<uint32_t>(f32_to_bf16(r[3])) << 16));
+      } else {
+        uint32_t u = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) u |= (static_cast<uint32_t>(code[o][k]) & 0xff) << (8 * k);
+        *reinterpret_cast<uint32_t*>(d4) = u;
+      }
+      if (out.side) {
+        char* s4p = static_cast<char*>(out.side) + lay_byte(out.slay, pix, c0);
+        if (out.side_fmt == FMT_I8) {
+          uint32_t u = 0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) u |= (static_cast<uint32_t>(quant_code(r[k], out.side_q)) & 0xff) << (8 * k);
+          *reinterpret_cast<uint32_t*>(s4p) = u;
+        } else {
+          *reinterpret_cast<uint2*>(s4p) =
+              make_uint2(static_cast<uint32_t>(f32_to_bf16(r[0])) | (static_cast<uint32_t>(f32_to_bf16(r[1])) << 16),
+                         static_cast<uint32_t>(f32_to_bf16(r[2])) | (static_cast<uint32_t>(f32_to_bf16(r[3])) << 16));
+        }
+      }
+    }
+  }
+}
+
 // ---- max pooling: max over valid taps, seeded with the first (harness kernel) ----
 // One thread per (output pixel, 16-byte chunk), output column fastest; 32-bit
 // index math; the window's taps are 16-byte loads from the padded P16 input
@@ -1020,6 +1269,33 @@ void launch_conv_f32_strict(const float* x, const float* w, const ConvGeom& g, c
 
 void launch_dwconv(const void* x, int xfmt, const float* w, const ConvGeom& g, int strict, const EpiDev& epi,
                    const OutDev& out, cudaStream_t s) {
+  const int cpg = xfmt == FMT_F32 ? 4 : 8;
+  const int ocpc = out.plan.cpc, scpc = out.side ? out.slay.cpc : 4;
+  const bool fast = g.ph <= kPad && g.pw <= kPad && g.C % cpg == 0 && g.in.kind == LAY_NORMAL && g.in.cpc % cpg == 0 &&
+                    out.plan.kind == LAY_NORMAL && ocpc % 4 == 0 && scpc % 4 == 0 && (xfmt == FMT_F32 || xfmt == FMT_BF16);
+  if (fast && g.KH == 3 && g.KW == 3 && g.sh == g.sw && (g.sw == 1 || g.sw == 2) && g.C % 4 == 0 &&
+      g.in.cpc % 4 == 0) {
+    const int owq = (g.OW + 3) / 4;
+    const int64_t tot = static_cast<int64_t>(g.C / 4) * g.N * g.OH * owq;
+    if (tot < (int64_t(1) << 31)) {
+      const FastDiv a = make_fastdiv(static_cast<uint32_t>(owq)), b = make_fastdiv(static_cast<uint32_t>(g.OH)),
+                    c = make_fastdiv(static_cast<uint32_t>(g.N));
+      if (g.sw == 1)
+        pdl_launch(k_dw3x3_rb<1>, grid_stride_blocks(tot), 256, 0, s, x, xfmt, w, g, strict, epi, out, a, b, c);
+      else
+        pdl_launch(k_dw3x3_rb<2>, grid_stride_blocks(tot), 256, 0, s, x, xfmt, w, g, strict, epi, out, a, b, c);
+      return;
+    }
+  }
+  if (fast) {
+    const int64_t tot = static_cast<int64_t>(g.C / cpg) * g.N * g.OH * g.OW;
+    if (tot < (int64_t(1) << 31)) {
+      pdl_launch(k_dwconv_fast, grid_stride_blocks(tot), 256, 0, s, x, xfmt, w, g, strict, epi, out,
+                 make_fastdiv(static_cast<uint32_t>(g.OW)), make_fastdiv(static_cast<uint32_t>(g.OH)),
+                 make_fastdiv(static_cast<uint32_t>(g.N)));
+      return;
+    }
+  }
   int64_t total = static_cast<int64_t>(g.N) * g.OH * g.OW * g.C;
   pdl_launch(k_dwconv, grid_stride_blocks(total), kThreads, 0, s, x, xfmt, w, g, strict, epi, out);
 }
