@@ -762,7 +762,10 @@ __global__ void __launch_bounds__(256) k_dwconv_fast(const void* __restrict__ x,
 // loads per row), the epilogue's ops are interpreted once per thread over the
 // 16 values with their per-channel vectors hoisted.  Same per-output order and
 // arithmetic as k_dwconv_fast (and the reference).
-template <int SW>
+// PL consecutive lanes take PL consecutive 4-channel pieces of the same
+// pixels (PL = 8: 32 channels), so each warp store covers whole 32-byte
+// sectors of the consumer's channel rows (no partial-sector write merges).
+template <int SW, int PL>
 __global__ void __launch_bounds__(256) k_dw3x3_rb(const void* __restrict__ x, int xfmt, const float* __restrict__ w,
                                                   ConvGeom g, int strict, EpiDev epi, OutDev out, FastDiv fd_owq,
                                                   FastDiv fd_oh, FastDiv fd_n) {
@@ -776,12 +779,14 @@ __global__ void __launch_bounds__(256) k_dw3x3_rb(const void* __restrict__ x, in
   const int OWp = g.OW + 2 * kPad, OHp = g.OH + 2 * kPad;
   const bool f32 = xfmt == FMT_F32;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const uint32_t t = fdiv(i, fd_owq);
-    const int oq = static_cast<int>(i - t * static_cast<uint32_t>(owq));
+    const uint32_t lo = i & (PL - 1), ii = i / PL;
+    const uint32_t t = fdiv(ii, fd_owq);
+    const int oq = static_cast<int>(ii - t * static_cast<uint32_t>(owq));
     const uint32_t t2 = fdiv(t, fd_oh);
     const int oh = static_cast<int>(t - t2 * static_cast<uint32_t>(g.OH));
-    const uint32_t pc = fdiv(t2, fd_n);
-    const int n = static_cast<int>(t2 - pc * static_cast<uint32_t>(g.N));
+    const uint32_t phi = fdiv(t2, fd_n);
+    const int n = static_cast<int>(t2 - phi * static_cast<uint32_t>(g.N));
+    const uint32_t pc = phi * PL + lo;
     const int c0 = static_cast<int>(pc) * 4, ow0 = oq * OUTS;
     float wr[4][9];
 #pragma unroll
@@ -1280,10 +1285,15 @@ void launch_dwconv(const void* x, int xfmt, const float* w, const ConvGeom& g, i
     if (tot < (int64_t(1) << 31)) {
       const FastDiv a = make_fastdiv(static_cast<uint32_t>(owq)), b = make_fastdiv(static_cast<uint32_t>(g.OH)),
                     c = make_fastdiv(static_cast<uint32_t>(g.N));
+      // bf16 inputs: sector-complete stores; fp32 inputs (4-channel planes): pixel-consecutive lanes
+      // keep the larger input reads coalesced
+      const bool pl8 = g.C % 32 == 0 && xfmt == FMT_BF16;
       if (g.sw == 1)
-        pdl_launch(k_dw3x3_rb<1>, grid_stride_blocks(tot), 256, 0, s, x, xfmt, w, g, strict, epi, out, a, b, c);
+        pdl_launch(pl8 ? k_dw3x3_rb<1, 8> : k_dw3x3_rb<1, 1>, grid_stride_blocks(tot), 256, 0, s, x, xfmt, w, g, strict,
+                   epi, out, a, b, c);
       else
-        pdl_launch(k_dw3x3_rb<2>, grid_stride_blocks(tot), 256, 0, s, x, xfmt, w, g, strict, epi, out, a, b, c);
+        pdl_launch(pl8 ? k_dw3x3_rb<2, 8> : k_dw3x3_rb<2, 1>, grid_stride_blocks(tot), 256, 0, s, x, xfmt, w, g, strict,
+                   epi, out, a, b, c);
       return;
     }
   }
