@@ -174,3 +174,12 @@ def test_layout_pass_modules_bitexact(gpu, name, batch, prec, fm):
     ex, src = setup(name + "_nhwc", prec, batch, float_mode=fm)
     y = ex.run_host(modelzoo.make_inputs(src, batch, seed=0))
     assert np.array_equal(bits(y), bits(gold[prec])), int(np.sum(bits(y) != bits(gold[prec])))
+
+
+@pytest.mark.gpu
+def test_resnet18_fp32_strict_full_size(gpu):
+    """fp32 in the reference's exact accumulation order (kernels.cpp:684-701), full size."""
+    gold = np.load(os.path.join(GOLD, "resnet18_b2.npz"))
+    ex, src = setup("resnet18", "fp32", 2, float_mode=mrb.MR_FLOAT_FP32_STRICT)
+    y = ex.run_host(modelzoo.make_inputs(src, 2, seed=0))
+    assert np.array_equal(bits(y), bits(gold["fp32"])), int(np.sum(bits(y) != bits(gold["fp32"])))
