@@ -176,6 +176,34 @@ mr_status mr_calibrate(const char* fused_module_text, const mr_exec_options* opt
                        const mr_tensor* weights, int32_t n_sets, const mr_tensor* inputs, int32_t k_min,
                        int32_t k_max, int32_t* k_out, int32_t* trials_out);
 
+/* ---- group level: one Primitive closure application ----------------------
+ * Replaces Interpreter::apply on a Primitive Closure (interp.cpp:86-101): the
+ * group `group` (its function name %fusedN or the value its call binds) of
+ * `fused_module_text`, compiled on its own with the same kernels the executor
+ * uses for it (opts->batch binds ?n of the module).  The group's operands are
+ * its call arguments (= fn params in order, fuse.cpp:296-302). */
+typedef struct mr_group_s* mr_group_t;
+
+mr_status mr_group_compile(const char* fused_module_text, const char* group, const mr_exec_options* opts,
+                           mr_group_t* out);
+
+/* Number of operands and the result's shape. */
+mr_status mr_group_signature(mr_group_t g, int32_t* n_operands, mr_tensor* out_shape);
+
+/* Applies the group: in[i] = argument i (DEVICE float32, row-major, the types
+ * the module binds), *out = DEVICE float32 result.  Stream-ordered, no sync.
+ * Weight operands (the @main weight params the group reads) are staged and
+ * their prologues (folded-BN multiply, weight realize chain) run when a weight
+ * operand's address differs from the previous launch; contents at an
+ * unchanged address are assumed unchanged (mr_group_reload forces a restage).
+ * Fails with MR_ERR_ARITY_MISMATCH / MR_ERR_TYPE_MISMATCH like apply(). */
+mr_status mr_group_launch(mr_group_t g, const mr_tensor* in, int32_t n_in, mr_tensor* out, void* stream);
+
+/* Forces the next mr_group_launch to restage the weight operands. */
+void mr_group_reload(mr_group_t g);
+
+void mr_group_destroy(mr_group_t g);
+
 /* Library build identification (arch, kernels compiled). */
 const char* mr_build_info(void);
 

@@ -507,13 +507,20 @@ def _eval(e, env: Dict[str, object], mod: Module):
         args = [_eval(a, env, mod) for a in e[2]]
         inner = dict(fn.env)
         inner.update(zip(fn.params, args))
-        return _eval(fn.body, inner, mod)
+        out = _eval(fn.body, inner, mod)
+        trace = getattr(mod, "trace", None)
+        if trace is not None and e[1][0] == "var":  # per-group record for the group-level tests
+            trace.append((e[1][1], args, out.vals if isinstance(out, IntTensor) else out))
+        return out
     raise ValueError(tag)
 
 
-def run_module(text_or_module, args: Sequence[np.ndarray]) -> np.ndarray:
-    """Evaluates @main on `args` (float32 arrays in parameter order)."""
+def run_module(text_or_module, args: Sequence[np.ndarray], trace: list = None) -> np.ndarray:
+    """Evaluates @main on `args` (float32 arrays in parameter order).  With
+    `trace` (a list), appends (function name, arguments, result) for every
+    closure application -- one entry per Primitive group of a fused module."""
     mod = parse_module(text_or_module) if isinstance(text_or_module, str) else text_or_module
+    mod.trace = trace
     if len(args) != len(mod.params):
         raise ValueError("run_module: %d arguments for %d parameters" % (len(args), len(mod.params)))
     env = {name: np.ascontiguousarray(a, np.float32) for name, a in zip(mod.params, args)}

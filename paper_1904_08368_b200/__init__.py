@@ -34,6 +34,7 @@ EXPORTS = [
     "mr_exec_default_options", "mr_exec_create", "mr_exec_set_weights", "mr_exec_run",
     "mr_exec_run_host", "mr_exec_submit_host", "mr_exec_sync", "mr_exec_output_shape", "mr_exec_describe", "mr_exec_launch_count",
     "mr_exec_profile", "mr_exec_destroy", "mr_last_error_message", "mr_module_lower", "mr_calibrate", "mr_build_info",
+    "mr_group_compile", "mr_group_signature", "mr_group_launch", "mr_group_reload", "mr_group_destroy",
 ]
 
 
@@ -89,6 +90,13 @@ def lib():
                                    ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]
         L.mr_module_lower.argtypes = [ctypes.c_char_p, ctypes.c_int64, ctypes.c_int32,
                                       ctypes.POINTER(ctypes.c_char_p)]
+        L.mr_group_compile.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(Options),
+                                       ctypes.POINTER(ctypes.c_void_p)]
+        L.mr_group_signature.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(Tensor)]
+        L.mr_group_launch.argtypes = [ctypes.c_void_p, ctypes.POINTER(Tensor), ctypes.c_int32, ctypes.POINTER(Tensor),
+                                      ctypes.c_void_p]
+        L.mr_group_reload.argtypes = [ctypes.c_void_p]
+        L.mr_group_destroy.argtypes = [ctypes.c_void_p]
         _lib = L
     return _lib
 
@@ -223,6 +231,43 @@ class Executor:
         if n < 0:
             raise BackendError(-1, lib().mr_last_error_message().decode())
         return [ms[i] for i in range(n)]
+
+
+class Group:
+    """One Primitive closure application (mr_group_*; interp.cpp:86-101):
+    group `name` (%fusedN or the value its call binds) of a fused module,
+    compiled alone.  launch() takes the call's arguments in order as DEVICE
+    float32 tensors (pointer, shape) and writes the result to a device buffer."""
+
+    def __init__(self, fused_text: str, name: str, batch: int = 1, device: int = 0,
+                 float_mode: int = MR_FLOAT_BF16, use_cuda_graph: bool = True, force_simt: bool = False):
+        L = lib()
+        opts = Options()
+        L.mr_exec_default_options(ctypes.byref(opts))
+        opts.device, opts.batch, opts.float_mode = device, batch, float_mode
+        opts.use_cuda_graph = 1 if use_cuda_graph else 0
+        opts.force_simt = 1 if force_simt else 0
+        h = ctypes.c_void_p()
+        _check(L.mr_group_compile(fused_text.encode(), name.encode(), ctypes.byref(opts), ctypes.byref(h)))
+        self._h = h
+        n, shp = ctypes.c_int32(0), Tensor()
+        _check(L.mr_group_signature(self._h, ctypes.byref(n), ctypes.byref(shp)))
+        self.n_operands = int(n.value)
+        self.output_shape = tuple(shp.shape[i] for i in range(shp.ndim))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.mr_group_destroy(h)
+            self._h = None
+
+    def launch(self, operands: Sequence[tuple], out_ptr: int, stream: int = 0) -> None:
+        ts = (Tensor * max(1, len(operands)))(*[_tensor(p, s) for p, s in operands])
+        tout = _tensor(out_ptr, self.output_shape)
+        _check(lib().mr_group_launch(self._h, ts, len(operands), ctypes.byref(tout), ctypes.c_void_p(stream)))
+
+    def reload(self) -> None:
+        lib().mr_group_reload(self._h)
 
 
 def build_info() -> str:

@@ -133,14 +133,14 @@ struct Exec {
   bool weights_ready = false;
   int64_t zero_bytes = 0;  // arena prefix of the zero-border buffers
   // io
-  const float* cur_input = nullptr;
+  std::vector<const float*> cur_inputs;  // one per data input (@main params 0 .. n_data_inputs-1)
   float* out_internal = nullptr;  // result buffer (NCHW float32)
   int64_t out_elems = 0;
   std::vector<int64_t> out_shape;
   // captured launch lists, one per input buffer address (the input pointer is
   // baked into the graph): the caller's buffer and the two pipeline stages
   struct GraphEnt {
-    const float* in;
+    std::vector<const float*> in;
     cudaGraph_t g;
     cudaGraphExec_t e;
   };
@@ -155,8 +155,8 @@ struct Exec {
   cudaStream_t pipe_stream = nullptr;
   float* host_stage_in = nullptr;
   float* host_stage_out = nullptr;
-  float* dev_in = nullptr;
-  int64_t in_elems = 0;
+  std::vector<float*> dev_in;    // mr_exec_run_host staging, one per data input
+  std::vector<int64_t> in_elems;
   std::string describe;
   std::vector<TcConvPlan*> tc_plans;
 
@@ -186,7 +186,8 @@ struct Exec {
     for (void* p : group_w) if (p) cudaFree(p);
     for (auto& v : group_vecs) for (void* p : v) if (p) cudaFree(p);
     if (out_internal) cudaFree(out_internal);
-    if (dev_in) cudaFree(dev_in);
+    for (float* p : dev_in)
+      if (p) cudaFree(p);
     if (host_stage_in) cudaFreeHost(host_stage_in);
     if (host_stage_out) cudaFreeHost(host_stage_out);
   }
@@ -682,10 +683,29 @@ void build(Exec& ex) {
   for (size_t v = 0; v < P.values.size(); ++v) {
     const ValueInfo& vi = P.values[v];
     if (!vi.is_data) continue;
-    if (vi.shape.size() != 4) fail(MR_ERR_UNSUPPORTED_GROUP, "data input %" + vi.name + " must be 4-D NCHW");
+    if (vi.shape.size() != 4 && vi.shape.size() != 2)
+      fail(MR_ERR_UNSUPPORTED_GROUP, "data input %" + vi.name + " must be NCHW or [N, K]");
     for (size_t r = 0; r < ex.reps[v].size(); ++r) {
       const Rep rep = ex.reps[v][r];
       if (rep.nchw_user) continue;
+      if (vi.shape.size() == 2) {  // row-major [N, K]: the caller's layout already; copy it in
+        if (rep.fmt != FMT_F32 || rep.lay.cpc != 0)
+          fail(MR_ERR_UNSUPPORTED_GROUP, "2-D data input %" + vi.name + " needs a float32 row-major representation");
+        int buf = B.buffer_for(static_cast<int>(v), static_cast<int>(r), vi.name + ":in");
+        LaunchRec L;
+        L.name = "%" + vi.name;
+        L.kernel = "input_copy";
+        const size_t bytes = static_cast<size_t>(vi.shape[0] * vi.shape[1]) * 4;
+        L.bytes = 2.0 * bytes;
+        Exec* e = &ex;
+        const int pidx = vi.param_index;
+        L.fn = [e, buf, bytes, pidx](cudaStream_t s) {
+          CK(cudaMemcpyAsync(e->ptr(buf), e->cur_inputs[pidx], bytes, cudaMemcpyDeviceToDevice, s));
+        };
+        ex.launches.push_back(L);
+        ++B.launch_idx;
+        continue;
+      }
       int buf = B.buffer_for(static_cast<int>(v), static_cast<int>(r), vi.name + ":in");
       LaunchRec L;
       L.name = "%" + vi.name;
@@ -701,8 +721,9 @@ void build(Exec& ex) {
         for (int c : vi.consumers)
           if (P.groups[c].data.value == static_cast<int>(v)) s2d_pad = static_cast<int>(P.groups[c].ph);
       Exec* e = &ex;
-      L.fn = [e, buf, N, C, H, W, fmt, lay, s2d_pad, q](cudaStream_t s) {
-        launch_input_convert(e->cur_input, N, C, H, W, e->ptr(buf), fmt, lay, s2d_pad, 0.f, q, s);
+      const int pidx = vi.param_index;  // data inputs are @main params 0 .. n_data_inputs-1
+      L.fn = [e, buf, N, C, H, W, fmt, lay, s2d_pad, q, pidx](cudaStream_t s) {
+        launch_input_convert(e->cur_inputs[pidx], N, C, H, W, e->ptr(buf), fmt, lay, s2d_pad, 0.f, q, s);
       };
       ex.launches.push_back(L);
       ++B.launch_idx;
@@ -1200,7 +1221,7 @@ void run_launches(Exec& ex, cudaStream_t s) {
 
 cudaGraphExec_t ensure_graph(Exec& ex) {
   for (auto& g : ex.graphs)
-    if (g.in == ex.cur_input) return g.e;
+    if (g.in == ex.cur_inputs) return g.e;
   if (ex.graphs.size() >= 4) {  // bounded cache: drop the oldest capture
     cudaGraphExecDestroy(ex.graphs.front().e);
     cudaGraphDestroy(ex.graphs.front().g);
@@ -1210,7 +1231,7 @@ cudaGraphExec_t ensure_graph(Exec& ex) {
   CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
   CK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
   run_launches(ex, cap);
-  Exec::GraphEnt ent{ex.cur_input, nullptr, nullptr};
+  Exec::GraphEnt ent{ex.cur_inputs, nullptr, nullptr};
   cudaError_t ce = cudaStreamEndCapture(cap, &ent.g);
   cudaStreamDestroy(cap);
   if (ce != cudaSuccess) fail(MR_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
@@ -1235,18 +1256,24 @@ int64_t numel(const mr_tensor& t) {
 }
 
 void check_input(const Exec& ex, const mr_tensor* inputs) {
-  if (!inputs || !inputs[0].data) fail(MR_ERR_INVALID_ARGUMENT, "null input");
-  const ValueInfo* dv = nullptr;
-  for (const auto& v : ex.P.values)
-    if (v.is_data) {
-      dv = &v;
-      break;
-    }
-  if (!dv) fail(MR_ERR_INVALID_ARGUMENT, "module has no data input");
-  if (inputs[0].ndim != static_cast<int>(dv->shape.size())) fail(MR_ERR_TYPE_MISMATCH, "input rank mismatch");
-  for (int i = 0; i < inputs[0].ndim; ++i)
-    if (inputs[0].shape[i] != dv->shape[i]) fail(MR_ERR_TYPE_MISMATCH, "input shape mismatch with the bound batch");
-  if (inputs[0].type_code != MR_FLOAT || inputs[0].bits != 32) fail(MR_ERR_TYPE_MISMATCH, "input must be float32");
+  if (!inputs) fail(MR_ERR_INVALID_ARGUMENT, "null input");
+  int seen = 0;
+  for (const auto& v : ex.P.values) {
+    if (!v.is_data) continue;
+    const mr_tensor& t = inputs[v.param_index];
+    if (!t.data) fail(MR_ERR_INVALID_ARGUMENT, "null input %" + v.name);
+    if (t.ndim != static_cast<int>(v.shape.size())) fail(MR_ERR_TYPE_MISMATCH, "input %" + v.name + " rank mismatch");
+    for (int i = 0; i < t.ndim; ++i)
+      if (t.shape[i] != v.shape[i]) fail(MR_ERR_TYPE_MISMATCH, "input %" + v.name + " shape mismatch with the bound batch");
+    if (t.type_code != MR_FLOAT || t.bits != 32) fail(MR_ERR_TYPE_MISMATCH, "input %" + v.name + " must be float32");
+    ++seen;
+  }
+  if (!seen) fail(MR_ERR_INVALID_ARGUMENT, "module has no data input");
+}
+
+void set_inputs(Exec& ex, const mr_tensor* inputs) {
+  ex.cur_inputs.assign(static_cast<size_t>(ex.opt.n_data_inputs), nullptr);
+  for (int k = 0; k < ex.opt.n_data_inputs; ++k) ex.cur_inputs[k] = static_cast<const float*>(inputs[k].data);
 }
 
 }  // namespace
@@ -1281,11 +1308,39 @@ using namespace mrb200;
 
 namespace mrb200 {
 namespace {
+// Binds the non-data @main params (w[i] = param n_data_inputs + i) and runs the
+// hoisted weight prologues.  `kind` is H2D for mr_exec_set_weights, D2D for the
+// group-level launch whose operands are device tensors.
+void load_weights(Exec& ex, int32_t n, const mr_tensor* w, cudaMemcpyKind kind) {
+  int expect = ex.P.n_params - ex.opt.n_data_inputs;
+  if (n != expect) fail(MR_ERR_ARITY_MISMATCH, "expected " + std::to_string(expect) + " weight tensors");
+  if (n && !w) fail(MR_ERR_INVALID_ARGUMENT, "null weights");
+  for (const auto& v : ex.P.values) {
+    if (v.param_index < 0 || v.is_data) continue;
+    const mr_tensor& t = w[v.param_index - ex.opt.n_data_inputs];
+    if (t.type_code != MR_FLOAT || t.bits != 32) fail(MR_ERR_TYPE_MISMATCH, "%" + v.name + " must be float32");
+    if (t.ndim != static_cast<int>(v.shape.size())) fail(MR_ERR_TYPE_MISMATCH, "%" + v.name + " rank mismatch");
+    for (int i = 0; i < t.ndim; ++i)
+      if (t.shape[i] != v.shape[i]) fail(MR_ERR_TYPE_MISMATCH, "%" + v.name + " shape mismatch");
+    int64_t bytes = numel(t) * 4;
+    if (bytes && !t.data) fail(MR_ERR_INVALID_ARGUMENT, "null tensor %" + v.name);
+    void*& dst = ex.param_dev[v.param_index];
+    if (!dst) CK(cudaMalloc(&dst, static_cast<size_t>(std::max<int64_t>(bytes, 4))));
+    if (bytes) CK(cudaMemcpy(dst, t.data, static_cast<size_t>(bytes), kind));
+  }
+  for (void* p : ex.group_w) if (p) cudaFree(p);
+  prepare_weights(ex, nullptr);
+  CK(cudaDeviceSynchronize());
+  ex.weights_ready = true;
+  ex.drop_graphs();  // weights live at fixed addresses only after the first set
+  make_describe(ex);
+}
+
 std::unique_ptr<Exec> make_exec(Program P, const mr_exec_options& o) {
   auto ex = std::make_unique<Exec>();
   ex->opt = o;
   ex->P = std::move(P);
-  if (ex->opt.n_data_inputs != 1) fail(MR_ERR_UNSUPPORTED_GROUP, "exactly one data input is supported");
+  if (ex->opt.n_data_inputs < 1) fail(MR_ERR_INVALID_ARGUMENT, "at least one data input");
   build(*ex);
   upload_group_constants(*ex);
   ex->param_dev.assign(ex->P.n_params, nullptr);
@@ -1325,26 +1380,7 @@ mr_status mr_exec_set_weights(mr_exec_t h, int32_t n, const mr_tensor* w) {
   API_BEGIN
   Exec& ex = *reinterpret_cast<Exec*>(h);
   CK(cudaSetDevice(ex.opt.device));
-  int expect = ex.P.n_params - ex.opt.n_data_inputs;
-  if (n != expect) fail(MR_ERR_ARITY_MISMATCH, "expected " + std::to_string(expect) + " weight tensors");
-  for (const auto& v : ex.P.values) {
-    if (v.param_index < 0 || v.is_data) continue;
-    const mr_tensor& t = w[v.param_index - ex.opt.n_data_inputs];
-    if (t.type_code != MR_FLOAT || t.bits != 32) fail(MR_ERR_TYPE_MISMATCH, "%" + v.name + " must be float32");
-    if (t.ndim != static_cast<int>(v.shape.size())) fail(MR_ERR_TYPE_MISMATCH, "%" + v.name + " rank mismatch");
-    for (int i = 0; i < t.ndim; ++i)
-      if (t.shape[i] != v.shape[i]) fail(MR_ERR_TYPE_MISMATCH, "%" + v.name + " shape mismatch");
-    int64_t bytes = numel(t) * 4;
-    void*& dst = ex.param_dev[v.param_index];
-    if (!dst) CK(cudaMalloc(&dst, static_cast<size_t>(std::max<int64_t>(bytes, 4))));
-    if (bytes) CK(cudaMemcpy(dst, t.data, static_cast<size_t>(bytes), cudaMemcpyHostToDevice));
-  }
-  for (void* p : ex.group_w) if (p) cudaFree(p);
-  prepare_weights(ex, nullptr);
-  CK(cudaDeviceSynchronize());
-  ex.weights_ready = true;
-  ex.drop_graphs();  // weights live at fixed addresses only after the first set
-  make_describe(ex);
+  load_weights(ex, n, w, cudaMemcpyHostToDevice);
   API_END
 }
 
@@ -1356,7 +1392,7 @@ mr_status mr_exec_run(mr_exec_t h, const mr_tensor* inputs, mr_tensor* output, v
   if (!output || !output->data) fail(MR_ERR_INVALID_ARGUMENT, "null output");
   if (numel(*output) != ex.out_elems) fail(MR_ERR_TYPE_MISMATCH, "output size mismatch");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  ex.cur_input = static_cast<const float*>(inputs[0].data);
+  set_inputs(ex, inputs);
   run_body(ex, s);
   CK(cudaMemcpyAsync(output->data, ex.out_internal, static_cast<size_t>(ex.out_elems) * 4, cudaMemcpyDeviceToDevice, s));
   API_END
@@ -1368,15 +1404,21 @@ mr_status mr_exec_run_host(mr_exec_t h, const mr_tensor* inputs, mr_tensor* outp
   check_input(ex, inputs);
   if (!output || !output->data) fail(MR_ERR_INVALID_ARGUMENT, "null output");
   if (numel(*output) != ex.out_elems) fail(MR_ERR_TYPE_MISMATCH, "output size mismatch");
-  int64_t n_in = numel(inputs[0]);
-  if (!ex.dev_in || ex.in_elems != n_in) {
-    if (ex.dev_in) cudaFree(ex.dev_in);
-    CK(cudaMalloc(&ex.dev_in, static_cast<size_t>(n_in) * 4));
-    ex.in_elems = n_in;
-  }
+  const int nd = ex.opt.n_data_inputs;
+  ex.dev_in.resize(static_cast<size_t>(nd), nullptr);
+  ex.in_elems.resize(static_cast<size_t>(nd), 0);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  CK(cudaMemcpyAsync(ex.dev_in, inputs[0].data, static_cast<size_t>(n_in) * 4, cudaMemcpyHostToDevice, s));
-  ex.cur_input = ex.dev_in;
+  ex.cur_inputs.assign(static_cast<size_t>(nd), nullptr);
+  for (int k = 0; k < nd; ++k) {
+    const int64_t n_in = numel(inputs[k]);
+    if (!ex.dev_in[k] || ex.in_elems[k] != n_in) {
+      if (ex.dev_in[k]) cudaFree(ex.dev_in[k]);
+      CK(cudaMalloc(&ex.dev_in[k], static_cast<size_t>(n_in) * 4));
+      ex.in_elems[k] = n_in;
+    }
+    CK(cudaMemcpyAsync(ex.dev_in[k], inputs[k].data, static_cast<size_t>(n_in) * 4, cudaMemcpyHostToDevice, s));
+    ex.cur_inputs[k] = ex.dev_in[k];
+  }
   if (!ex.weights_ready) fail(MR_ERR_INVALID_ARGUMENT, "mr_exec_set_weights first");
   run_body(ex, s);
   CK(cudaMemcpyAsync(output->data, ex.out_internal, static_cast<size_t>(ex.out_elems) * 4, cudaMemcpyDeviceToHost, s));
@@ -1393,6 +1435,7 @@ mr_status mr_exec_submit_host(mr_exec_t h, const mr_tensor* inputs, mr_tensor* o
   if (numel(*output) != ex.out_elems) fail(MR_ERR_TYPE_MISMATCH, "output size mismatch");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (!ex.pipe_fresh && s != ex.pipe_stream) fail(MR_ERR_INVALID_ARGUMENT, "mr_exec_sync before switching streams");
+  if (ex.opt.n_data_inputs != 1) fail(MR_ERR_INVALID_ARGUMENT, "mr_exec_submit_host streams one data input");
   const int64_t n_in = numel(inputs[0]);
   if (!ex.copy_stream) {
     CK(cudaStreamCreateWithFlags(&ex.copy_stream, cudaStreamNonBlocking));
@@ -1416,7 +1459,7 @@ mr_status mr_exec_submit_host(mr_exec_t h, const mr_tensor* inputs, mr_tensor* o
                      ex.copy_stream));
   CK(cudaEventRecord(ex.loaded[b], ex.copy_stream));
   CK(cudaStreamWaitEvent(s, ex.loaded[b], 0));
-  ex.cur_input = ex.stage[b];
+  ex.cur_inputs.assign(1, ex.stage[b]);
   run_body(ex, s);
   CK(cudaEventRecord(ex.consumed[b], s));
   CK(cudaMemcpyAsync(output->data, ex.out_internal, static_cast<size_t>(ex.out_elems) * 4, cudaMemcpyDeviceToHost, s));
@@ -1461,7 +1504,7 @@ int32_t mr_exec_profile(mr_exec_t h, const mr_tensor* inputs, mr_tensor* output,
     Exec& ex = *reinterpret_cast<Exec*>(h);
     check_input(ex, inputs);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    ex.cur_input = static_cast<const float*>(inputs[0].data);
+    set_inputs(ex, inputs);
     std::vector<cudaEvent_t> ev(ex.launches.size() + 1);
     for (auto& e : ev) CK(cudaEventCreate(&e));
     CK(cudaEventRecord(ev[0], s));
@@ -1561,6 +1604,90 @@ mr_status mr_calibrate(const char* text, const mr_exec_options* opts, int32_t n_
                                       std::to_string(k_max) + "] avoids overflow");
   API_END
 }
+
+struct mr_group_s {
+  std::unique_ptr<Exec> ex;
+  std::vector<int> perm;         // exec param k <- group operand perm[k]
+  int n_data = 0;                // exec params 0..n_data-1 are activations
+  int n_operands = 0;
+  std::vector<const void*> staged;  // weight operand addresses of the last staging
+};
+
+mr_status mr_group_compile(const char* text, const char* group, const mr_exec_options* opts, mr_group_t* out) {
+  API_BEGIN
+  if (!text || !group || !out) fail(MR_ERR_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  mr_exec_options o;
+  mr_exec_default_options(&o);
+  if (opts) o = *opts;
+  if (o.batch < 1) fail(MR_ERR_INVALID_ARGUMENT, "batch must be >= 1");
+  Module m = parse_fused_module(text);
+  auto g = std::make_unique<mr_group_s>();
+  GroupModule gm = extract_group_module(m, group, o.batch, o.n_data_inputs);
+  g->perm = gm.perm;
+  g->n_data = gm.n_data;
+  int n_ops = 0;
+  for (int p : g->perm) n_ops = std::max(n_ops, p + 1);
+  g->n_operands = n_ops;
+  Program gp = lower_module(gm.m, o.batch, g->n_data, &gm.coded);  // host-side errors before any device work
+  gp.any_quant = gp.any_quant || gm.module_quant;  // same float format as inside the whole module
+  CK(cudaSetDevice(o.device));
+  mr_exec_options go = o;
+  go.n_data_inputs = g->n_data;
+  g->ex = make_exec(std::move(gp), go);
+  *out = g.release();
+  API_END
+}
+
+mr_status mr_group_signature(mr_group_t g, int32_t* n_operands, mr_tensor* out_shape) {
+  API_BEGIN
+  if (!g) fail(MR_ERR_INVALID_ARGUMENT, "null group");
+  if (n_operands) *n_operands = g->n_operands;
+  if (out_shape) {
+    std::memset(out_shape, 0, sizeof(*out_shape));
+    out_shape->ndim = static_cast<int32_t>(g->ex->out_shape.size());
+    for (size_t i = 0; i < g->ex->out_shape.size(); ++i) out_shape->shape[i] = g->ex->out_shape[i];
+    out_shape->type_code = MR_FLOAT;
+    out_shape->bits = 32;
+  }
+  API_END
+}
+
+mr_status mr_group_launch(mr_group_t g, const mr_tensor* in, int32_t n_in, mr_tensor* out, void* stream) {
+  API_BEGIN
+  if (!g) fail(MR_ERR_INVALID_ARGUMENT, "null group");
+  Exec& ex = *g->ex;
+  if (n_in != g->n_operands)
+    fail(MR_ERR_ARITY_MISMATCH, "function expects " + std::to_string(g->n_operands) + " arguments, got " +
+                                    std::to_string(n_in));
+  if (!in) fail(MR_ERR_INVALID_ARGUMENT, "null operands");
+  CK(cudaSetDevice(ex.opt.device));
+  std::vector<mr_tensor> ordered(g->perm.size());
+  for (size_t k = 0; k < g->perm.size(); ++k) ordered[k] = in[g->perm[k]];
+  std::vector<const void*> addrs;
+  for (size_t k = static_cast<size_t>(g->n_data); k < ordered.size(); ++k) addrs.push_back(ordered[k].data);
+  if (!ex.weights_ready || addrs != g->staged) {
+    // weight staging is synchronous: order it after the caller's prior work
+    CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    load_weights(ex, static_cast<int32_t>(ordered.size()) - g->n_data, ordered.data() + g->n_data,
+                 cudaMemcpyDeviceToDevice);
+    g->staged = addrs;
+  }
+  check_input(ex, ordered.data());
+  if (!out || !out->data) fail(MR_ERR_INVALID_ARGUMENT, "null output");
+  if (numel(*out) != ex.out_elems) fail(MR_ERR_TYPE_MISMATCH, "output size mismatch");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  set_inputs(ex, ordered.data());
+  run_body(ex, s);
+  CK(cudaMemcpyAsync(out->data, ex.out_internal, static_cast<size_t>(ex.out_elems) * 4, cudaMemcpyDeviceToDevice, s));
+  API_END
+}
+
+void mr_group_reload(mr_group_t g) {
+  if (g) g->staged.clear();
+}
+
+void mr_group_destroy(mr_group_t g) { delete g; }
 
 const char* mr_build_info(void) { return MRB200_BUILD_INFO; }
 

@@ -127,7 +127,8 @@ bool is_transpose(const ExprP& e, std::initializer_list<int64_t> perm) {
 
 }  // namespace
 
-Program lower_module(const Module& m, int64_t batch, int n_data_inputs) {
+Program lower_module(const Module& m, int64_t batch, int n_data_inputs,
+                     const std::map<std::string, QParams>* coded_inputs) {
   Program P;
   std::map<std::string, int> value_of;
   auto add_value = [&](const std::string& name) {
@@ -149,6 +150,12 @@ Program lower_module(const Module& m, int64_t batch, int n_data_inputs) {
     if (mp.type.dtype != "float32")
       bad(MR_ERR_TYPE_MISMATCH, "@main parameter %" + mp.name + " is " + mp.type.dtype + "; only float32 is supported");
     for (const auto& d : mp.type.dims) P.values[v].shape.push_back(d.symbolic ? batch : d.value);
+    if (coded_inputs && coded_inputs->count(mp.name)) {
+      if (!P.values[v].is_data) bad(MR_ERR_INVALID_ARGUMENT, "coded input %" + mp.name + " is not a data input");
+      P.values[v].quantized = true;
+      P.values[v].q = coded_inputs->at(mp.name);
+      P.any_quant = true;
+    }
   }
   P.n_params = static_cast<int>(m.params.size());
 
@@ -517,6 +524,78 @@ Program lower_module(const Module& m, int64_t batch, int n_data_inputs) {
   if (P.values[P.result_value].nhwc_view) unsupported("@main", "an NHWC-relabelled result");
   if (P.groups.empty()) bad(MR_ERR_UNSUPPORTED_GROUP, "module has no Primitive group");
   return P;
+}
+
+GroupModule extract_group_module(const Module& m, const std::string& group, int64_t batch, int n_data_inputs) {
+  GroupModule out;
+  std::vector<int>* perm = &out.perm;
+  std::map<std::string, QParams>* coded = &out.coded;
+  const Program P = lower_module(m, batch, n_data_inputs);  // validates the module, binds the shapes
+  std::map<std::string, int> value_of;
+  for (size_t v = 0; v < P.values.size(); ++v) value_of[P.values[v].name] = static_cast<int>(v);
+  std::string key = group;
+  if (!key.empty() && key[0] == '%') key = key.substr(1);
+  std::map<std::string, ExprP> fns;
+  std::string fn_name, out_name;
+  ExprP call;
+  for (const auto& [name, e] : m.body->lets) {
+    if (e->kind == Expr::Fn) {
+      fns[name] = e;
+    } else if (e->kind == Expr::Call && e->callee_is_var && (e->name == key || name == key)) {
+      fn_name = e->name;
+      out_name = name;
+      call = e;
+    }
+  }
+  if (!call && m.body->result->kind == Expr::Call && m.body->result->name == key) {
+    fn_name = key;
+    out_name = "__result__";
+    call = m.body->result;
+  }
+  if (!call || !fns.count(fn_name)) bad(MR_ERR_UNBOUND_VARIABLE, "no Primitive group %" + key + " in @main");
+  const ExprP fn = fns[fn_name];
+  std::vector<std::string> data_args, weight_args;
+  std::map<std::string, int> first_pos;
+  for (size_t i = 0; i < call->args.size(); ++i) {
+    const std::string& a = call->args[i]->name;
+    if (first_pos.count(a)) continue;
+    first_pos[a] = static_cast<int>(i);
+    const ValueInfo& vi = P.values[value_of.at(a)];
+    if (vi.nhwc_view) unsupported(fn_name, "group-level call on an NHWC-relabelled operand %" + a);
+    (vi.producer >= 0 || vi.is_data ? data_args : weight_args).push_back(a);
+    if (vi.quantized) {
+      // the caller hands code * c2 as float32; the group re-derives the codes
+      // with the producer's chain, exact when c1 * c2 == 1 (power-of-two scales)
+      if (!(vi.q.c1 * vi.q.c2 == 1.f)) unsupported(fn_name, "coded operand %" + a + " with c1 * c2 != 1");
+      (*coded)[a] = vi.q;
+    }
+  }
+  if (data_args.empty()) unsupported(fn_name, "group has no activation operand");
+  out.module_quant = P.any_quant;
+  Module& g = out.m;
+  for (const auto* list : {&data_args, &weight_args}) {
+    for (const auto& a : *list) {
+      MainParam mp;
+      mp.name = a;
+      for (int64_t d : P.values[value_of.at(a)].shape) {
+        Dim dim;
+        dim.value = d;
+        mp.type.dims.push_back(dim);
+      }
+      g.params.push_back(mp);
+      perm->push_back(first_pos[a]);
+    }
+  }
+  out.n_data = static_cast<int>(data_args.size());
+  g.body = std::make_shared<Block>();
+  g.body->lets.emplace_back(fn_name, fn);
+  const std::string res = out_name == "__result__" ? "__group_result__" : out_name;
+  g.body->lets.emplace_back(res, call);
+  auto rv = std::make_shared<Expr>();
+  rv->kind = Expr::Var;
+  rv->name = res;
+  g.body->result = rv;
+  return out;
 }
 
 std::string describe_group(const Program& p, const GroupDesc& g) {

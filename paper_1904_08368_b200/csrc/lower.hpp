@@ -14,6 +14,7 @@
 #pragma once
 
 #include <cstdint>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -121,8 +122,27 @@ struct LowerError {
 };
 
 // Lowers the parsed fused module with the symbolic batch bound to `batch`.
-Program lower_module(const Module& m, int64_t batch, int n_data_inputs);
+// `coded_inputs` marks data params that carry realize-coded values (code * c2,
+// as another group's Requant epilogue leaves them) -- the group level's view
+// of an operand its producer quantized.
+Program lower_module(const Module& m, int64_t batch, int n_data_inputs,
+                     const std::map<std::string, QParams>* coded_inputs = nullptr);
 
 std::string describe_group(const Program& p, const GroupDesc& g);
+
+// One Primitive group of a fused module as a module of its own (the group
+// level of the boundary: one closure application,
+// interp.cpp:86-101).  `group` names the function (%fusedN) or the value its
+// call binds (%vN).
+struct GroupModule {
+  Module m;               // @main takes the group's distinct call arguments,
+                          // activations first (their shapes bound to the batch),
+                          // then the @main weight params
+  std::vector<int> perm;  // m's param k = the group's call argument perm[k]
+  int n_data = 0;         // activations among m's params
+  std::map<std::string, QParams> coded;  // activations the full module holds realize-coded
+  bool module_quant = false;             // the full module has quantize sites (float format choice)
+};
+GroupModule extract_group_module(const Module& m, const std::string& group, int64_t batch, int n_data_inputs);
 
 }  // namespace mrb200
