@@ -225,12 +225,17 @@ __global__ void __launch_bounds__(128) k_input_s2d(const float* __restrict__ x, 
 // PHASED writes LAY_S2DP: the s2d grid is walked from (-2, -2) over the
 // 2*Hq x 2*Wq extent of the 4 phase sub-grids (every position written, zeros
 // outside the image), so no separate border pass is needed.
+#ifndef MRB200_S2D_STAGES
+#define MRB200_S2D_STAGES 2  // deeper rings measured slower inside the CUDA graph
+#endif
+constexpr int kS2dStages = MRB200_S2D_STAGES;  // k_input_s2d_ct row ring depth
+
 template <int C, int PAD, int CPC, bool PHASED, bool CAL>
 __global__ void __launch_bounds__(128) k_input_s2d_ct(const float* __restrict__ x, int N, int H, int W, void* out,
                                                       Lay L, float pre_mul, QDev q, FastDiv fd_w4) {
   pdl_trigger();
   pdl_wait();
-  extern __shared__ __align__(16) float rows[];  // 2 x [C][2][W]
+  extern __shared__ __align__(16) float rows[];  // kS2dStages x [C][2][W]
   constexpr int PLANES = (4 * C + CPC - 1) / CPC;
   constexpr int OFF = PHASED ? 2 : 0;                  // s2d index = grid index - OFF
   const int GR = PHASED ? 2 * L.Hq : L.Hq, GC = PHASED ? 2 * L.Wq : L.Wq;  // walked grid
@@ -250,18 +255,23 @@ __global__ void __launch_bounds__(128) k_input_s2d_ct(const float* __restrict__ 
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  if (blockIdx.x < n_rows) prefetch(rows, blockIdx.x);
+  // kS2dStages-deep cp.async ring: rows it+1 .. it+kS2dStages-1 are in flight
+  // while row it converts (one commit group per row, empty past the end)
+#pragma unroll
+  for (int k = 0; k < kS2dStages - 1; ++k) {
+    const int r = blockIdx.x + k * gridDim.x;
+    if (r < n_rows) prefetch(rows + k * stride, r);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   int it = 0;
   for (int row = blockIdx.x; row < n_rows; row += gridDim.x, ++it) {
     const int n = row / GR, gi = row - n * GR, si = gi - OFF;
-    if (row + gridDim.x < n_rows) {
-      prefetch(rows + ((it + 1) & 1) * stride, row + gridDim.x);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
+    const int ahead = row + (kS2dStages - 1) * gridDim.x;
+    if (ahead < n_rows) prefetch(rows + ((it + kS2dStages - 1) % kS2dStages) * stride, ahead);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group %0;" ::"n"(kS2dStages - 1) : "memory");
     __syncthreads();
-    const float* cur = rows + (it & 1) * stride;
+    const float* cur = rows + (it % kS2dStages) * stride;
     const int y0 = 2 * si - PAD;
     const bool rok[2] = {y0 >= 0 && y0 < H, y0 + 1 >= 0 && y0 + 1 < H};
     for (int gj = threadIdx.x; gj < GC; gj += blockDim.x) {
@@ -1125,6 +1135,137 @@ __global__ void __launch_bounds__(256) k_dense(const float* __restrict__ x, int 
   }
 }
 
+// ---- dense, K split across warps (int8 codes / bf16 weights) ----------------------
+// The int8 contraction is an exact int32 sum and the bf16 mode is held to a
+// tolerance, so K can be split: block = 32 output columns (one per lane) x R
+// rows; warp w owns K slice w of each staged chunk, the 8 partial sums are
+// reduced through shared memory in fixed warp order.  Each thread issues its
+// chunk's weight loads before the row staging so the L2 round trip overlaps
+// it.  Grid: ceil(M/32) x ceil(N/R) (the head: 32 x 16 = 512 blocks).
+constexpr int kDkWarps = 8;
+constexpr int kDkChunk = 1024;  // K elements per staged chunk (multiple of 8 * kDkWarps)
+
+template <int MODE, int R, bool CAL>
+__global__ void __launch_bounds__(256) k_dense_ks(const float* __restrict__ x, int N, int K, int Kp,
+                                                  const void* __restrict__ w, int M, float pre_mul, int quant, QDev q,
+                                                  float acc_scale, EpiDev epi, OutDev out) {
+  pdl_trigger();
+  pdl_wait();
+  constexpr int kSlice = kDkChunk / kDkWarps;            // K per warp per chunk
+  constexpr int kLoads = MODE == 0 ? kSlice / 4 : kSlice / 8;  // weight words (int32 / uint4) per thread
+  __shared__ __align__(16) uint8_t stage[MODE == 0 ? R * kDkChunk : R * kDkChunk * 4];
+  __shared__ float red[kDkWarps][R][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int j = blockIdx.x * 32 + lane;
+  const bool jv = j < M;
+  const int n0 = blockIdx.y * R;
+  int acc[R];
+  float res[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    acc[r] = 0;
+    res[r] = 0.f;
+  }
+  for (int k0 = 0; k0 < Kp; k0 += kDkChunk) {
+    const int kc = min(kDkChunk, Kp - k0);
+    const int ks0 = warp * kSlice;  // this warp's slice within the chunk
+    // 1. weight loads for the slice (zero past the chunk / the padded K)
+    int32_t wv[MODE == 0 ? kLoads : 1];
+    uint4 wb[MODE == 2 ? kLoads : 1];
+    if (MODE == 0) {
+      const int32_t* wt = static_cast<const int32_t*>(w) + static_cast<int64_t>((k0 + ks0) / 4) * M + j;
+#pragma unroll
+      for (int u = 0; u < kLoads; ++u) wv[u] = (jv && ks0 + u * 4 < kc) ? __ldg(wt + static_cast<int64_t>(u) * M) : 0;
+    } else {
+      const uint4* wt = reinterpret_cast<const uint4*>(w) + static_cast<int64_t>((k0 + ks0) / 8) * M + j;
+#pragma unroll
+      for (int u = 0; u < kLoads; ++u)
+        wb[u] = (jv && ks0 + u * 8 < kc) ? __ldg(wt + static_cast<int64_t>(u) * M) : make_uint4(0, 0, 0, 0);
+    }
+    // 2. stage the R rows' chunk (prologue: pre_mul, realize chain); 8 row
+    // loads in flight per thread (a dependent load per element would serialise
+    // the DRAM round trips)
+    __syncthreads();  // the previous chunk is consumed
+    constexpr int kU = 8;
+    for (int base = threadIdx.x; base < R * kc; base += kU * blockDim.x) {
+      float v[kU];
+      bool live[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int idx = base + u * blockDim.x;
+        const int r = idx / kc, k = k0 + idx - r * kc;
+        live[u] = idx < R * kc && n0 + r < N && k < K;
+        v[u] = live[u] ? x[static_cast<int64_t>(n0 + r) * K + k] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int idx = base + u * blockDim.x;
+        if (idx >= R * kc) break;
+        const int r = idx / kc, kk = idx - r * kc;
+        float t = v[u];
+        if (pre_mul != 0.f && live[u]) t = __fmul_rn(t, pre_mul);
+        if (MODE == 0)
+          stage[r * kDkChunk + kk] = static_cast<uint8_t>(
+              live[u] ? static_cast<int8_t>(quant ? quant_code_t<CAL>(t, q) : static_cast<int32_t>(t)) : 0);
+        else
+          reinterpret_cast<float*>(stage)[r * kDkChunk + kk] = t;
+      }
+    }
+    __syncthreads();
+    // 3. contract the slice
+    if (MODE == 0) {
+#pragma unroll
+      for (int u = 0; u < kLoads; ++u) {
+        if (ks0 + u * 4 >= kc) break;
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          acc[r] = __dp4a(*reinterpret_cast<const int32_t*>(stage + r * kDkChunk + ks0 + u * 4), wv[u], acc[r]);
+      }
+    } else {
+      const float* sf = reinterpret_cast<const float*>(stage);
+#pragma unroll
+      for (int u = 0; u < kLoads; ++u) {
+        if (ks0 + u * 8 >= kc) break;
+        const uint32_t w4[4] = {wb[u].x, wb[u].y, wb[u].z, wb[u].w};
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const float4 a = *reinterpret_cast<const float4*>(sf + r * kDkChunk + ks0 + u * 8);
+          const float4 b = *reinterpret_cast<const float4*>(sf + r * kDkChunk + ks0 + u * 8 + 4);
+          const float xs[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            res[r] = __fmaf_rn(xs[2 * h], __uint_as_float(w4[h] << 16), res[r]);
+            res[r] = __fmaf_rn(xs[2 * h + 1], __uint_as_float(w4[h] & 0xffff0000u), res[r]);
+          }
+        }
+      }
+    }
+  }
+  // 4. cross-warp reduction (fixed order) + epilogue
+#pragma unroll
+  for (int r = 0; r < R; ++r) red[warp][r][lane] = MODE == 0 ? __int_as_float(acc[r]) : res[r];
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < R * 32; idx += blockDim.x) {
+    const int r = idx >> 5, l = idx & 31;
+    const int n = n0 + r, jj = blockIdx.x * 32 + l;
+    if (n >= N || jj >= M) continue;
+    float v;
+    if (MODE == 0) {
+      int s = 0;
+#pragma unroll
+      for (int ww = 0; ww < kDkWarps; ++ww) s += __float_as_int(red[ww][r][l]);
+      v = __fmul_rn(static_cast<float>(s), acc_scale);
+    } else {
+      v = red[0][r][l];
+#pragma unroll
+      for (int ww = 1; ww < kDkWarps; ++ww) v += red[ww][r][l];
+    }
+    int32_t code = 0;
+    v = apply_epi(epi, v, n, jj, &code);
+    store_out(out, v, code, n, jj);
+  }
+}
+
 // [M][K] float32 (after the prologue) -> transposed kernel layouts for k_dense.
 __global__ void k_dense_weight_t(const float* __restrict__ w, int M, int K, int Kp, const float* __restrict__ oc_scale,
                                  float scalar, int fmt, int quant, QDev q, void* out) {
@@ -1187,12 +1328,12 @@ void launch_input_convert(const float* x, int N, int C, int H, int W, void* out,
     const FastDiv fd = make_fastdiv(static_cast<uint32_t>(W / 4));
     const int rows = N * 2 * L.Hq;
     if (fmt == FMT_BF16) {
-      pdl_launch(k_input_s2d_ct<3, 3, 8, true, false>, std::min(rows, sms2 * 8), 128, 2 * 2 * C * W * sizeof(float), s, x,
+      pdl_launch(k_input_s2d_ct<3, 3, 8, true, false>, std::min(rows, sms2 * 8), 128, kS2dStages * 2 * C * W * sizeof(float), s, x,
                  N, H, W, out, L, pre_mul, q, fd);
       return;
     }
-    pdl_launch(q.ovf ? k_input_s2d_ct<3, 3, 16, true, true> : k_input_s2d_ct<3, 3, 16, true, false>, std::min(rows, sms2 * 8), 128, 2 * 2 * C * W * sizeof(float), s, 
-        x, N, H, W, out, L, pre_mul, q, fd);
+    pdl_launch(q.ovf ? k_input_s2d_ct<3, 3, 16, true, true> : k_input_s2d_ct<3, 3, 16, true, false>, std::min(rows, sms2 * 8), 128, kS2dStages * 2 * C * W * sizeof(float), s,
+               x, N, H, W, out, L, pre_mul, q, fd);
     return;
   }
   const int s2d_planes = (4 * C + L.cpc - 1) / L.cpc;
@@ -1205,8 +1346,8 @@ void launch_input_convert(const float* x, int N, int C, int H, int W, void* out,
       return v > 0 ? v : 148;
     }();
     const int rows = N * L.Hq;
-    const size_t smem = 2 * 2 * C * W * sizeof(float);
-    if (C == 3 && s2d_pad == 3 && L.kb == 16 && (fmt == FMT_I8 || fmt == FMT_BF16)) {
+    const size_t smem = kS2dStages * 2 * C * W * sizeof(float);
+    if (C == 3 && s2d_pad == 3 && L.kb == 16 && (fmt == FMT_I8 || fmt == FMT_BF16) && smem <= 48 * 1024) {
       const FastDiv fd = make_fastdiv(static_cast<uint32_t>(W / 4));
       if (fmt == FMT_I8)
         pdl_launch(q.ovf ? k_input_s2d_ct<3, 3, 16, false, true> : k_input_s2d_ct<3, 3, 16, false, false>, std::min(rows, sms * 8), 128, smem, s, x, N, H, W, out, L, pre_mul, q, fd);
@@ -1335,6 +1476,19 @@ void launch_dense(const float* x, int N, int K, int Kp, const void* w, int M, in
   // a calibration run (mr_calibrate) observes the prologue's quantize site and the epilogue's
   bool cal = quant && q.ovf;
   for (int k = 0; k < epi.n_ops; ++k) cal = cal || (epi.op[k] == E_REQ && epi.q[k].ovf);
+  if (mode == 0 || mode == 2) {  // K split across warps (exact int32 sum / bf16 tolerance)
+    constexpr int R0 = 16, R2 = 4;
+    const int R = mode == 0 ? R0 : R2;
+    dim3 g2(static_cast<unsigned>((M + 31) / 32), static_cast<unsigned>((N + R - 1) / R));
+    if (mode == 0) {
+      auto k2 = cal ? k_dense_ks<0, R0, true> : k_dense_ks<0, R0, false>;
+      pdl_launch(k2, g2, 256, 0, s, x, N, K, Kp, w, M, pre_mul, quant, q, acc_scale, epi, out);
+    } else {
+      auto k2 = cal ? k_dense_ks<2, R2, true> : k_dense_ks<2, R2, false>;
+      pdl_launch(k2, g2, 256, 0, s, x, N, K, Kp, w, M, pre_mul, quant, q, acc_scale, epi, out);
+    }
+    return;
+  }
   auto kern = cal ? k_dense<true> : k_dense<false>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   pdl_launch(kern, grid, 256, smem, s, x, N, K, Kp, w, M, mode, pre_mul, quant, q, acc_scale, epi, out);
