@@ -183,3 +183,25 @@ def test_resnet18_fp32_strict_full_size(gpu):
     ex, src = setup("resnet18", "fp32", 2, float_mode=mrb.MR_FLOAT_FP32_STRICT)
     y = ex.run_host(modelzoo.make_inputs(src, 2, seed=0))
     assert np.array_equal(bits(y), bits(gold["fp32"])), int(np.sum(bits(y) != bits(gold["fp32"])))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["resnet18", "mobilenet_v1"])
+def test_bf16_top1_agreement_b256(gpu, name):
+    """bf16 criterion at the benchmark batch (BASELINE north_star: logits
+    max|d|/max|ref| <= 1e-2 plus top-1 agreement; SURVEY.md 8(d) asks for the
+    exact agreement count): 256 images against the fp32 reference, here the
+    strict-fp32 executor, which the tests above pin bit for bit to the
+    reference interpreter.  Measured (seed 7): ResNet-18 and MobileNet-v1
+    counts are recorded in DESIGN.md; random-init logits have small top-1
+    margins, so the floor is 97 %."""
+    ref_ex, src = setup(name, "fp32", 256, float_mode=mrb.MR_FLOAT_FP32_STRICT)
+    bf_ex, _ = setup(name, "fp32", 256)
+    x = modelzoo.make_inputs(src, 256, seed=7)
+    r = ref_ex.run_host(x)
+    y = bf_ex.run_host(x)
+    agree = int(np.sum(np.argmax(y, 1) == np.argmax(r, 1)))
+    err = normwise(y, r)
+    print("%s bf16 vs fp32: top-1 agreement %d/256, normwise %.5f" % (name, agree, err))
+    assert agree >= 249  # >= 97 %
+    assert err <= BF16_TOL
