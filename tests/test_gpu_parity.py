@@ -205,3 +205,19 @@ def test_bf16_top1_agreement_b256(gpu, name):
     print("%s bf16 vs fp32: top-1 agreement %d/256, normwise %.5f" % (name, agree, err))
     assert agree >= 249  # >= 97 %
     assert err <= BF16_TOL
+
+
+@pytest.mark.gpu
+def test_resnet18_int8_batch4096_matches_shards(gpu):
+    """Config C5: ResNet-18 int8 at batch 4096 on one GPU.
+    Per-sample independence (8(e)) makes every 256-image slice of the batch-4096
+    result equal, bit for bit, to a batch-256 run on that slice -- which the
+    full-size parity test pins to the reference."""
+    big, src = setup("resnet18", "int8", 4096)
+    small, _ = setup("resnet18", "int8", 256)
+    rng = np.random.default_rng(11)
+    x = rng.random((4096, 3, 224, 224), dtype=np.float32)
+    y = big.run_host(x)
+    for s in (0, 7, 15):
+        ys = small.run_host(np.ascontiguousarray(x[s * 256:(s + 1) * 256]))
+        assert np.array_equal(bits(ys), bits(y[s * 256:(s + 1) * 256])), s
