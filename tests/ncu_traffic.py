@@ -16,7 +16,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def family(kname, prec):
     if "k_conv_tc" in kname:
         return "conv_i8_tcgen05" if prec == "int8" else "conv_bf16_tcgen05"
-    for key, fam in (("k_input", "input_convert"), ("k_dense(", "dense_i8" if prec == "int8" else "dense_bf16"),
+    for key, fam in (("k_input", "input_convert"), ("k_dense_ks", "dense_i8" if prec == "int8" else "dense_bf16"),
+                     ("k_dense<", "dense_i8" if prec == "int8" else "dense_bf16"),
                      ("k_sum_hw", "sum_hw"), ("k_to_nchw", "result_to_nchw"), ("k_maxpool", "max_pool")):
         if key in kname:
             return fam
