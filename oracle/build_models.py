@@ -45,7 +45,11 @@ CONFIGS = {
     "mobilenet_v1": (modelzoo.mobilenet_v1, {}),
     "vgg16": (modelzoo.vgg16, dict(batch=2)),
     "dqn": (modelzoo.dqn, dict(batch=2)),
+    # model interchange: weights embedded in the metadata
+    # pool (modelzoo.bind_weights), folded by the reference's own passes
+    "resnet18_small_const": (modelzoo.resnet18, dict(image=32, num_classes=10, widths=(16, 16, 32, 32))),
 }
+BIND = {"resnet18_small_const"}
 # float-only (BASELINE lists them as bf16 configs; an int8 calibration sweep of
 # the 224x224 VGG-16 in the reference interpreter takes about an hour)
 NO_INT8 = {"vgg16"}
@@ -55,6 +59,9 @@ def build(name: str, out_dir: str) -> dict:
     fn, kw = CONFIGS[name]
     src = fn(**kw)
     w = modelzoo.make_weights(src, seed=1)
+    if name in BIND:
+        src = modelzoo.bind_weights(src, w)
+        w = {p.name: w[p.name] for p in src.params if p.kind != "input"}
     batch = kw.get("batch", 1)  # static-batch modules calibrate on their own batch
     x = modelzoo.make_inputs(src, batch, seed=0)
     t0 = time.time()
@@ -69,6 +76,7 @@ def build(name: str, out_dir: str) -> dict:
     meta = {
         "name": name,
         "builder": fn.__name__,
+        "bind_weights": name in BIND,
         "builder_kwargs": {k2: list(v) if isinstance(v, tuple) else v for k2, v in kw.items()},
         "weights_seed": 1,
         "calibration": None if k is None else {"inputs_seed": 0, "images": batch, "k": k, "scale": 2.0 ** k,

@@ -382,8 +382,17 @@ def _parse_expr(p: _P):
         e = ("var", v)
     elif v == "const":
         p.next()
-        num = _parse_value(p)
-        e = ("const", np.asarray(num, np.float32))
+        if p.accept("("):  # tensor literal const(values, (dims), dtype) (printer.cpp:173-194)
+            vals = _parse_value(p)
+            p.expect(",")
+            shape = _parse_value(p)
+            p.expect(",")
+            p.next()  # dtype
+            p.expect(")")
+            e = ("const", np.asarray(vals, np.float32).reshape(shape))
+        else:
+            num = _parse_value(p)
+            e = ("const", np.asarray(num, np.float32))
     elif v == "meta":
         p.next()
         p.expect("[")

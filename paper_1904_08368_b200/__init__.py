@@ -287,4 +287,6 @@ def load_model(name: str, precision: str):
     builder = getattr(modelzoo, meta["builder"])
     kw = {k: tuple(v) if isinstance(v, list) else v for k, v in meta["builder_kwargs"].items()}
     src = builder(**kw)
+    if meta.get("bind_weights"):  # weights live in the module's metadata pool
+        src = modelzoo.bind_weights(src, modelzoo.make_weights(src, seed=meta["weights_seed"]))
     return text, meta, src

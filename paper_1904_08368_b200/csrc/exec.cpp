@@ -1312,11 +1312,11 @@ namespace {
 // hoisted weight prologues.  `kind` is H2D for mr_exec_set_weights, D2D for the
 // group-level launch whose operands are device tensors.
 void load_weights(Exec& ex, int32_t n, const mr_tensor* w, cudaMemcpyKind kind) {
-  int expect = ex.P.n_params - ex.opt.n_data_inputs;
+  int expect = ex.P.n_params - static_cast<int>(ex.P.hidden_data.size()) - ex.opt.n_data_inputs;
   if (n != expect) fail(MR_ERR_ARITY_MISMATCH, "expected " + std::to_string(expect) + " weight tensors");
   if (n && !w) fail(MR_ERR_INVALID_ARGUMENT, "null weights");
   for (const auto& v : ex.P.values) {
-    if (v.param_index < 0 || v.is_data) continue;
+    if (v.param_index < 0 || v.is_data || v.hidden >= 0) continue;
     const mr_tensor& t = w[v.param_index - ex.opt.n_data_inputs];
     if (t.type_code != MR_FLOAT || t.bits != 32) fail(MR_ERR_TYPE_MISMATCH, "%" + v.name + " must be float32");
     if (t.ndim != static_cast<int>(v.shape.size())) fail(MR_ERR_TYPE_MISMATCH, "%" + v.name + " rank mismatch");
@@ -1344,7 +1344,18 @@ std::unique_ptr<Exec> make_exec(Program P, const mr_exec_options& o) {
   build(*ex);
   upload_group_constants(*ex);
   ex->param_dev.assign(ex->P.n_params, nullptr);
+  // embedded weights (hidden parameters): uploaded once here
+  for (const auto& v : ex->P.values) {
+    if (v.hidden < 0) continue;
+    const auto& data = ex->P.hidden_data[static_cast<size_t>(v.hidden)];
+    void*& dst = ex->param_dev[v.param_index];
+    CK(cudaMalloc(&dst, std::max<size_t>(data.size() * 4, 4)));
+    if (!data.empty()) CK(cudaMemcpy(dst, data.data(), data.size() * 4, cudaMemcpyHostToDevice));
+  }
   make_describe(*ex);
+  // nothing left for mr_exec_set_weights to bind: prepare the weights now
+  if (ex->P.n_params - static_cast<int>(ex->P.hidden_data.size()) == ex->opt.n_data_inputs)
+    load_weights(*ex, 0, nullptr, cudaMemcpyHostToDevice);
   return ex;
 }
 }  // namespace

@@ -510,6 +510,15 @@ Program lower_module(const Module& m, int64_t batch, int n_data_inputs,
       fns[name] = e;
       continue;
     }
+    if (e->kind == Expr::Const) {  // an embedded weight: hidden parameter
+      if (e->lit.dtype != "float32") bad(MR_ERR_TYPE_MISMATCH, "@main constant %" + name + " is not float32");
+      const int v = add_value(name);
+      P.values[v].shape = e->lit.shape;
+      P.values[v].hidden = static_cast<int>(P.hidden_data.size());
+      P.values[v].param_index = P.n_params++;
+      P.hidden_data.push_back(e->lit.f32());
+      continue;
+    }
     handle_call(name, e);
   }
   const ExprP& res = m.body->result;

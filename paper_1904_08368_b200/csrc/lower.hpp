@@ -65,6 +65,10 @@ struct ValueInfo {
   QParams q;
   std::vector<int> consumers;  // groups reading it
   bool is_result = false;
+  // @main-level `let %t = <constant>` (weights embedded in the module's
+  // metadata pool, e.g. after `fold`): a hidden parameter the executor uploads
+  // itself, param_index >= the module's own parameter count
+  int hidden = -1;  // index into Program::hidden_data
   // layout pass (passes.cpp:481-486): the reference value is the NHWC
   // transpose of this NCHW tensor (its producer ended in transpose(0,2,3,1));
   // only NHWC conv2d consumers read it (data layouts here are physical)
@@ -112,7 +116,8 @@ struct Program {
   std::vector<ValueInfo> values;
   std::vector<GroupDesc> groups;  // in call (topological) order
   int result_value = -1;
-  int n_params = 0;
+  int n_params = 0;  // @main parameters + hidden constant parameters
+  std::vector<std::vector<float>> hidden_data;  // float32 literal per hidden parameter
   bool any_quant = false;
 };
 

@@ -271,3 +271,29 @@ def make_inputs(src: ModelSource, batch: int, seed: int = 0) -> np.ndarray:
     if src.name == "dqn":  # Atari frames: integer pixel values in [0, 255]
         x = np.floor(x * 256.0).astype(np.float32)
     return x
+
+
+def bind_weights(src: ModelSource, weights: Dict[str, np.ndarray],
+                 kinds=("conv_w", "dense_w", "bias", "dw_w")) -> ModelSource:
+    """Model interchange: the same network with its
+    weights embedded in the module's metadata pool (`let %w = meta[Constant][i]`,
+    printed like printer.cpp:173-194) instead of passed as @main parameters.
+    The reference's `fold` pass then hoists every weight prologue (folded-BN
+    multiply, the weight realize chain) into the constants at compile time."""
+    head, rest = src.text.split(") {\n", 1)
+    body, tail = rest.split("\n}\n", 1)
+    meta_lines = []
+    if tail.startswith("metadata {\n"):
+        meta_lines = tail[len("metadata {\n"):].rsplit("\n}", 1)[0].split("\n")
+    keep, lets = [], []
+    for p in src.params:
+        if p.kind not in kinds:
+            keep.append(p)
+            continue
+        vals = ", ".join(fmt_f32(v) for v in np.asarray(weights[p.name], np.float32).reshape(-1))
+        shp = "(" + ", ".join(str(d) for d in p.shape) + ")"
+        meta_lines.append("  const[%d] = const([%s], %s, float32);" % (len(meta_lines), vals, shp))
+        lets.append("  let %%%s = meta[Constant][%d];" % (p.name, len(meta_lines) - 1))
+    sig = ", ".join("%%%s: Tensor[(%s), float32]" % (p.name, ", ".join(str(d) for d in p.shape)) for p in keep)
+    text = "def @main(%s) {\n%s\n%s\n}\nmetadata {\n%s\n}\n" % (sig, "\n".join(lets), body, "\n".join(meta_lines))
+    return ModelSource(src.name + "_const", text, keep, src.input_shape, src.num_classes)

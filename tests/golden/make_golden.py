@@ -45,6 +45,6 @@ def make(name, batch):
 
 
 if __name__ == "__main__":
-    todo = {"resnet18_tiny": 4, "resnet18": 2, "mobilenet_v1": 2, "dqn": 2, "vgg16": 2}
+    todo = {"resnet18_tiny": 4, "resnet18": 2, "mobilenet_v1": 2, "dqn": 2, "vgg16": 2, "resnet18_small_const": 4}
     for name in sys.argv[1:] or list(todo):
         make(name, todo[name])

@@ -149,3 +149,17 @@ def test_combine_conv_is_identity_on_baseline_models():
         comb = ref.compile(src.text, "fold-scale,fold,dce,combine-conv,fuse", 0)
         a, b = mrb.lower(plain, 2), mrb.lower(comb, 2)
         assert [g["desc"] for g in a["groups"]] == [g["desc"] for g in b["groups"]]
+
+
+@pytest.mark.parametrize("prec", ["int8", "fp32"])
+def test_lower_weights_in_metadata(prec):
+    """Weights embedded as @main-level constants lower
+    to the same 22 groups; the constants become hidden parameters the executor
+    uploads itself, so only the data input and the pool window stay @main
+    arguments."""
+    text, meta, src = mrb.load_model("resnet18_small_const", prec)
+    d = mrb.lower(text, 4)
+    assert len(d["groups"]) == 22 and d["result_shape"] == [4, 10]
+    assert d["n_params"] > 2  # x, win_pool + the embedded weights
+    if prec == "int8":
+        assert all(x["weight_quant"] for x in d["groups"] if x["anchor"] != "max_pool2d")

@@ -221,3 +221,15 @@ def test_resnet18_int8_batch4096_matches_shards(gpu):
     for s in (0, 7, 15):
         ys = small.run_host(np.ascontiguousarray(x[s * 256:(s + 1) * 256]))
         assert np.array_equal(bits(ys), bits(y[s * 256:(s + 1) * 256])), s
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prec,fm", [("int8", 0), ("fp32", 1)])
+def test_weights_in_metadata_bitexact(gpu, prec, fm):
+    """Model interchange: a module with its weights in
+    the metadata pool runs with only the data input and the pool window bound;
+    int8 and fp32-strict match the reference bit for bit."""
+    gold = np.load(os.path.join(GOLD, "resnet18_small_const_b4.npz"))
+    ex, src = setup("resnet18_small_const", prec, 4, float_mode=fm)
+    y = ex.run_host(modelzoo.make_inputs(src, 4, seed=0))
+    assert np.array_equal(bits(y), bits(gold[prec])), int(np.sum(bits(y) != bits(gold[prec])))

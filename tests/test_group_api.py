@@ -66,7 +66,8 @@ def oracle_trace(name, prec, batch):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("name,prec,batch", [("resnet18_tiny", "int8", 2), ("resnet18_tiny", "fp32", 2),
-                                             ("mobilenet_v1", "int8", 2), ("dqn", "int8", 2)])
+                                             ("mobilenet_v1", "int8", 2), ("dqn", "int8", 2),
+                                             ("resnet18_small_const", "int8", 2)])
 def test_every_group_bitexact_through_group_api(gpu, name, prec, batch):
     """Each group of the module, launched alone on the oracle's own operands,
     reproduces the oracle's result for that group bit for bit (int8 realized

@@ -201,3 +201,20 @@ def test_port_layout_pass_modules(name, batch, prec):
     x = modelzoo.make_inputs(src, batch, seed=0)
     y = port.run_weights(text, x, [w[p.name] for p in src.params if p.kind != "input"])
     assert np.array_equal(bits(y), bits(np.load(os.path.join(GOLD, "%s_b%d.npz" % (name, batch)))[prec]))
+
+
+@pytest.mark.parametrize("prec", ["int8", "fp32"])
+def test_port_matches_reference_weights_in_metadata(prec):
+    """Model interchange: weights embedded in the
+    module (modelzoo.bind_weights, folded by the reference's passes; the
+    printer inlines small tensors as const(...) and pools the rest in the
+    metadata section) evaluate bit-identically to the reference's run."""
+    import paper_1904_08368_b200 as mrb
+    from paper_1904_08368_b200 import modelzoo
+    text, meta, src = mrb.load_model("resnet18_small_const", prec)
+    assert [p.kind for p in src.params] == ["input", "window"]
+    w = modelzoo.make_weights(src, seed=meta["weights_seed"])
+    x = modelzoo.make_inputs(src, 4, seed=0)
+    y = port.run_module(text, [x] + [w[p.name] for p in src.params if p.kind != "input"])
+    gold = np.load(os.path.join(GOLD, "resnet18_small_const_b4.npz"))
+    assert np.array_equal(bits(y), bits(gold[prec]))
