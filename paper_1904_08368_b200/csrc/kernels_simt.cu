@@ -775,16 +775,18 @@ __global__ void __launch_bounds__(256) k_dwconv_fast(const void* __restrict__ x,
 // PL consecutive lanes take PL consecutive 4-channel pieces of the same
 // pixels (PL = 8: 32 channels), so each warp store covers whole 32-byte
 // sectors of the consumer's channel rows (no partial-sector write merges).
+// Output pixels per thread along the row and the blocks-per-SM floor, per input
+// format (A/B builds on MobileNet-v1): bf16 (PL 8) 4 outputs, >= 2 blocks/SM;
+// fp32 (PL 1, the int8 modules' float path) 2 outputs, >= 3 blocks/SM.
+constexpr int dw_outs(int pl) { return pl == 8 ? 4 : 2; }
+constexpr int dw_minb(int pl) { return pl == 8 ? 2 : 3; }
 template <int SW, int PL>
-#ifndef MRB200_DW_MINB
-#define MRB200_DW_MINB 2  // >= 2 blocks per SM: 113 registers, +8 % on MobileNet-v1 (A/B builds)
-#endif
-__global__ void __launch_bounds__(256, MRB200_DW_MINB) k_dw3x3_rb(const void* __restrict__ x, int xfmt, const float* __restrict__ w,
+__global__ void __launch_bounds__(256, dw_minb(PL)) k_dw3x3_rb(const void* __restrict__ x, int xfmt, const float* __restrict__ w,
                                                   ConvGeom g, int strict, EpiDev epi, OutDev out, FastDiv fd_owq,
                                                   FastDiv fd_oh, FastDiv fd_n) {
   pdl_trigger();
   pdl_wait();
-  constexpr int OUTS = 4, NCOL = (OUTS - 1) * SW + 3;
+  constexpr int OUTS = dw_outs(PL), NCOL = (OUTS - 1) * SW + 3;
   const int owq = (g.OW + OUTS - 1) / OUTS;
   const uint32_t pieces = static_cast<uint32_t>(g.C / 4);
   const uint32_t total = pieces * g.N * g.OH * owq;
@@ -1424,14 +1426,15 @@ void launch_dwconv(const void* x, int xfmt, const float* w, const ConvGeom& g, i
                     out.plan.kind == LAY_NORMAL && ocpc % 4 == 0 && scpc % 4 == 0 && (xfmt == FMT_F32 || xfmt == FMT_BF16);
   if (fast && g.KH == 3 && g.KW == 3 && g.sh == g.sw && (g.sw == 1 || g.sw == 2) && g.C % 4 == 0 &&
       g.in.cpc % 4 == 0) {
-    const int owq = (g.OW + 3) / 4;
+    // bf16 inputs: sector-complete stores; fp32 inputs (4-channel planes): pixel-consecutive lanes
+    // keep the larger input reads coalesced
+    const bool pl8 = g.C % 32 == 0 && xfmt == FMT_BF16;
+    const int outs = pl8 ? dw_outs(8) : dw_outs(1);
+    const int owq = (g.OW + outs - 1) / outs;
     const int64_t tot = static_cast<int64_t>(g.C / 4) * g.N * g.OH * owq;
     if (tot < (int64_t(1) << 31)) {
       const FastDiv a = make_fastdiv(static_cast<uint32_t>(owq)), b = make_fastdiv(static_cast<uint32_t>(g.OH)),
                     c = make_fastdiv(static_cast<uint32_t>(g.N));
-      // bf16 inputs: sector-complete stores; fp32 inputs (4-channel planes): pixel-consecutive lanes
-      // keep the larger input reads coalesced
-      const bool pl8 = g.C % 32 == 0 && xfmt == FMT_BF16;
       if (g.sw == 1)
         pdl_launch(pl8 ? k_dw3x3_rb<1, 8> : k_dw3x3_rb<1, 1>, grid_stride_blocks(tot), 256, 0, s, x, xfmt, w, g, strict,
                    epi, out, a, b, c);
