@@ -1032,6 +1032,35 @@ __global__ void k_sum_hw(const float* __restrict__ x, Lay L, int N, int H, int W
   }
 }
 
+// Same sum, one warp per (image, 4-channel granule) of a NORMAL fp32 layout
+// with HW <= 64: the warp stages the granule's HW pixels (16 B each,
+// pixel-consecutive in the chunk plane: coalesced) in shared memory, then
+// lanes 0..3 each run one channel's sequential seeded sum in (h, w) order.
+__global__ void __launch_bounds__(256) k_sum_hw_warp(const float* __restrict__ x, Lay L, int N, int H, int W, int C,
+                                                     float* __restrict__ y) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ float4 st[8][64];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int HW = H * W, grans = C / 4;
+  const int64_t items = static_cast<int64_t>(N) * grans;
+  for (int64_t it = static_cast<int64_t>(blockIdx.x) * 8 + warp; it < items; it += static_cast<int64_t>(gridDim.x) * 8) {
+    const int n = static_cast<int>(it / grans), g = static_cast<int>(it - static_cast<int64_t>(n) * grans);
+    for (int p = lane; p < HW; p += 32) {
+      const int h = p / W, w = p - h * W;
+      st[warp][p] = *reinterpret_cast<const float4*>(x + lay_off(L, pad_pix(n, h, w, H, W), 4 * g));
+    }
+    __syncwarp();
+    if (lane < 4) {
+      const float* col = reinterpret_cast<const float*>(st[warp]) + lane;
+      float acc = col[0];
+      for (int p = 1; p < HW; ++p) acc = __fadd_rn(acc, col[4 * p]);
+      y[static_cast<int64_t>(n) * C + 4 * g + lane] = acc;
+    }
+    __syncwarp();
+  }
+}
+
 // ---- dense ----------------------------------------------------------------------------
 // Block = kDenseRows data rows x 256 outputs.  The rows get their prologue
 // (pre_mul, realize chain) once into shared memory; each thread owns one
@@ -1464,6 +1493,12 @@ void launch_maxpool(const void* x, int xfmt, const ConvGeom& g, const OutDev& ou
 }
 
 void launch_sum_hw(const float* x, const Lay& L, int N, int H, int W, int C, float* y, cudaStream_t s) {
+  if (H * W <= 64 && C % 4 == 0 && L.cpc >= 4 && L.cpc % 4 == 0 && L.kind == LAY_NORMAL && L.kb >= 16) {
+    const int64_t items = static_cast<int64_t>(N) * (C / 4);
+    pdl_launch(k_sum_hw_warp, static_cast<int>(std::min<int64_t>((items + 7) / 8, 148 * 8)), 256, 0, s, x, L, N, H, W,
+               C, y);
+    return;
+  }
   int64_t total = static_cast<int64_t>(N) * C;
   pdl_launch(k_sum_hw, grid_stride_blocks(total), kThreads, 0, s, x, L, N, H, W, C, y);
 }
