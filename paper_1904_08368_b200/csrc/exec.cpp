@@ -135,6 +135,7 @@ struct Exec {
   // io
   std::vector<const float*> cur_inputs;  // one per data input (@main params 0 .. n_data_inputs-1)
   float* out_internal = nullptr;  // result buffer (NCHW float32)
+  int out_alias_buf = -1;         // >= 0: out_internal is this arena buffer (row-major fp32 result)
   int64_t out_elems = 0;
   std::vector<int64_t> out_shape;
   // captured launch lists, one per input buffer address (the input pointer is
@@ -185,7 +186,7 @@ struct Exec {
     for (void* p : param_dev) if (p) cudaFree(p);
     for (void* p : group_w) if (p) cudaFree(p);
     for (auto& v : group_vecs) for (void* p : v) if (p) cudaFree(p);
-    if (out_internal) cudaFree(out_internal);
+    if (out_internal && out_alias_buf < 0) cudaFree(out_internal);
     for (float* p : dev_in)
       if (p) cudaFree(p);
     if (host_stage_in) cudaFreeHost(host_stage_in);
@@ -997,8 +998,16 @@ void build(Exec& ex) {
   ex.out_shape = rv.shape;
   ex.out_elems = 1;
   for (auto d : rv.shape) ex.out_elems *= d;
-  CK(cudaMalloc(&ex.out_internal, static_cast<size_t>(ex.out_elems) * 4));
-  {
+  // a float32 row-major [N, M] result (a dense head) already is the boundary
+  // layout: the executor reads it in place, no conversion launch
+  const bool alias_result = rr.fmt == FMT_F32 && !rr.has_q && rv.shape.size() == 2 && rr.lay.cpc == 0;
+  if (alias_result) {
+    ex.out_alias_buf = rr.buf;
+    B.use(rr.buf);  // keep it live to the end of the step
+  } else {
+    CK(cudaMalloc(&ex.out_internal, static_cast<size_t>(ex.out_elems) * 4));
+  }
+  if (!alias_result) {
     // NCHW float32 at the boundary; a realize-coded result is dequantized
     // (code * c2, exact) so the value equals the reference's float32 tensor.
     int rbuf = rr.buf;
@@ -1025,6 +1034,7 @@ void build(Exec& ex) {
   assign_offsets(ex);
   CK(cudaMalloc(&ex.arena, static_cast<size_t>(std::max<int64_t>(ex.arena_bytes, 256))));
   if (ex.zero_bytes) CK(cudaMemset(ex.arena, 0, static_cast<size_t>(ex.zero_bytes)));
+  if (ex.out_alias_buf >= 0) ex.out_internal = static_cast<float*>(ex.ptr(ex.out_alias_buf));
 }
 
 }  // namespace mrb200
