@@ -233,3 +233,28 @@ def test_weights_in_metadata_bitexact(gpu, prec, fm):
     ex, src = setup("resnet18_small_const", prec, 4, float_mode=fm)
     y = ex.run_host(modelzoo.make_inputs(src, 4, seed=0))
     assert np.array_equal(bits(y), bits(gold[prec])), int(np.sum(bits(y) != bits(gold[prec])))
+
+
+@pytest.mark.gpu
+def test_device_run_graph_and_profile_paths_agree(gpu):
+    """mr_exec_run on device buffers (CUDA-graph replay, one graph per input
+    address), the per-launch profile path and the host path return the same
+    bits; a second input buffer gets its own graph and the first still works."""
+    import torch
+    ex, src = setup("resnet18_tiny", "int8", 4)
+    gold = np.load(os.path.join(GOLD, "resnet18_tiny_b4.npz"))["int8"]
+    x = modelzoo.make_inputs(src, 4, seed=0)
+    xd = torch.from_numpy(x).cuda()
+    xd2 = xd.clone()
+    out = torch.empty(ex.output_shape, dtype=torch.float32, device="cuda")
+    for buf in (xd, xd2, xd):
+        out.zero_()
+        ex.run_device(buf.data_ptr(), buf.shape, out.data_ptr())
+        torch.cuda.synchronize()
+        assert np.array_equal(bits(out.cpu().numpy()), bits(gold))
+    ms = ex.profile_device(xd.data_ptr(), xd.shape, out.data_ptr())
+    torch.cuda.synchronize()
+    assert len(ms) == ex.launch_count() and all(t > 0 for t in ms)
+    assert np.array_equal(bits(out.cpu().numpy()), bits(gold))
+    d = ex.describe()
+    assert len(d["launches"]) == ex.launch_count()
