@@ -40,6 +40,7 @@
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "conv_tc.hpp"
@@ -705,14 +706,27 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           const uint32_t sA = smA_u + stage * a.a_stage_bytes + shift16;
           const uint32_t sB = a.resident_b ? smB_u + ks * a.b_ks_stride : smB_u + stage * a.b_stage_bytes;
           const uint32_t a16 = sA >> 4, b16 = sB >> 4;
-          if (!no_mma)
+          // the sub-tile count is a compile-time constant inside the step loop
+          // (the issue loop is on the critical path of the N=64 convs)
+          auto issue = [&](auto sub_c) {
+            constexpr uint32_t S = decltype(sub_c)::value;
             for (uint32_t st = 0; st < n_steps; ++st) {
               const uint64_t bd = hi | (a.steps[st].b_lo + b16);
               const uint32_t alo = a.steps[st].a_lo + a16;
               const uint32_t accum = (ks | st) != 0 ? 1u : 0u;
-              for (uint32_t sb = 0; sb < sub; ++sb)
+#pragma unroll
+              for (uint32_t sb = 0; sb < S; ++sb)
                 umma<EB>(tmem_d + sb * bn, hi | (alo + sb * sub_step16), bd, idesc, accum);
             }
+          };
+          if (!no_mma) {
+            switch (sub) {
+              case 1: issue(std::integral_constant<uint32_t, 1>{}); break;
+              case 2: issue(std::integral_constant<uint32_t, 2>{}); break;
+              case 3: issue(std::integral_constant<uint32_t, 3>{}); break;
+              default: issue(std::integral_constant<uint32_t, 4>{}); break;
+            }
+          }
           umma_commit(&empty[stage]);  // frees the smem stage when these MMAs retire
           if (++stage == a.n_stages) {
             stage = 0;
