@@ -93,6 +93,10 @@ struct TcArgs {
   int32_t N, Hg, Wg;
   int64_t Pg;  // N*Hg*Wg
   int32_t m_tiles, n_tiles, bn, Cc, pps, k_stages, sub0, subs, hg;
+  // streamed-weight 3x3 stride-1 convs: a stage holds ONE kernel row of taps
+  // (tap_groups = 3): 3x smaller weight stages, 3x deeper pipeline; the A rows of
+  // kernel row g start g * Wg pixels further
+  int32_t tap_groups;
   int8_t region_sg[8];  // A stage region -> TMA sub-grid coordinate (subs regions)
   // TC_STEM_POOL: M rows are pooled pixels; per M tile 3 super-tiles (window
   // row dy) of 3 sub-tiles (window column dx) over one A stage; step table
@@ -627,14 +631,16 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           mbar_expect_tx(&full[stage], a.a_stage_bytes + (load_b ? a.b_stage_bytes : 0));
           // A stage layout [pps][subs][hg rows][row]: one box per (plane, sub-grid, row block)
           uint8_t* dA = smA + stage * a.a_stage_bytes;
+          const int kc = ks / a.tap_groups, tg = ks - kc * a.tap_groups;  // chunk stage, kernel row
+          const int rg = r0 + tg * a.Wg;
           for (int pl = 0; pl < a.pps; ++pl)
             for (int sg = 0; sg < a.subs; ++sg)
               for (int bx = 0; bx < a.nbox; ++bx)
                 tma_load_4d(dA + ((pl * a.subs + sg) * a.hg + bx * a.hbox) * row_bytes, &tmA, &full[stage], 0,
-                            r0 + bx * a.hbox, a.region_sg[sg], ks * a.pps + pl);
+                            rg + bx * a.hbox, a.region_sg[sg], kc * a.pps + pl);
           if (load_b)
             tma_load_4d(smB + stage * a.b_stage_bytes, &tmB, &full[stage], 0, n_tile * a.bn / (a.kb == 16 ? 8 : 1),
-                        ks * a.pps, 0);
+                        kc * a.pps, tg * (a.tap_groups > 1 ? 3 : 0));
           if (++stage == a.n_stages) {
             stage = 0;
             phase ^= 1;
@@ -1211,6 +1217,9 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
   // (2 x sub x N <= 512 columns) and shared memory allow, resident weights
   // before streamed ones.
   bool found = false;
+  a.tap_groups = 1;
+  const bool trs_ok = sp.kind == TC_S1 && ntaps == 9 && kb >= 64 && !pair_taps && !a.win && !sp.pool &&
+                      !std::getenv("MRB200_NO_TAP_ROWS");
   auto try_cfg = [&](int cand, int sub, bool resident) {
     if (sp.OC % cand || 2 * sub * cand > 512) return false;
     int hg, nbox, hbox;
@@ -1237,6 +1246,32 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
         }
       }
       return false;
+    }
+    if (trs_ok) {  // one kernel row of taps per stage: A rows = the M tiles + 2 (dx = -1..1)
+      const int need = kTileM * sub + 2;
+      const int align = 1024 / kb;
+      const int nbox3 = (need + 255) / 256;
+      const int hbox3 = ((need + nbox3 - 1) / nbox3 + align - 1) / align * align;
+      for (int pps : {4, 2, 1}) {
+        if (cc % pps || 3 * pps * ksteps > kMaxSteps) continue;
+        const int bst = 3 * pps * cand * kb;
+        const int ast = pps * a.subs * nbox3 * hbox3 * row_bytes;
+        int ns = (kSmemBudget - barrier_bytes) / (ast + bst);
+        if (ns >= 3) {
+          a.resident_b = 0;
+          a.tap_groups = 3;
+          a.pps = pps;
+          a.b_stage_bytes = bst;
+          a.n_stages = ns > 8 ? 8 : ns;
+          a.bn = cand;
+          a.sub = sub;
+          a.hg = nbox3 * hbox3;
+          a.nbox = nbox3;
+          a.hbox = hbox3;
+          a.a_stage_bytes = ast;
+          return true;
+        }
+      }
     }
     for (int pps : {4, 2, 1}) {
       if (cc % pps || pair_taps || (kb == 16 && (pps & 1)) || steps_for(pps) > kMaxSteps) continue;
@@ -1296,7 +1331,7 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
                      : static_cast<int>((a.Pg + kTileM * (a.win ? 1 : a.sub) - 1) / (kTileM * (a.win ? 1 : a.sub)));
   const int rows_bytes = a.hg * row_bytes;
   a.Cc = cc;
-  a.k_stages = cc / a.pps;
+  a.k_stages = cc / a.pps * a.tap_groups;
   a.n_tiles = sp.OC / a.bn;
   // MMA step table (byte offsets; A relative to stage base [+ row shift for kb 16])
   const uint32_t a_sub = static_cast<uint32_t>(rows_bytes);
@@ -1331,12 +1366,15 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
   } else {
     // swizzled K-major: SBO = 8 rows x kb; the 32-byte K step is a start-address advance
     a.desc_hi = umma_desc_hi(8 * kb, kb == 128 ? 2 : 4);
-    for (int t = 0; t < ntaps; ++t)
+    // tap_groups 3: the stage holds one kernel row; its taps sit 0, 1, 2 rows from the stage base
+    const int stage_taps = a.tap_groups > 1 ? 3 : ntaps;
+    for (int t = 0; t < stage_taps; ++t)
       for (int kp = 0; kp < a.pps; ++kp)
         for (int kk = 0; kk < ksteps; ++kk) {
           MmaStep m;
+          const int rel = a.tap_groups > 1 ? t : taps[t].delta - dmin;
           m.a_off = static_cast<uint32_t>(kp) * a_plane + static_cast<uint32_t>(taps[t].sub) * a_sub +
-                    static_cast<uint32_t>(taps[t].delta - dmin) * kb + kk * 32;
+                    static_cast<uint32_t>(rel) * kb + kk * 32;
           m.a_lbo = 16;
           m.b_off = static_cast<uint32_t>(t * bplanes + kp) * b_plane + kk * 32;
           m.b_lbo = 16;
@@ -1474,7 +1512,8 @@ static bool encode_maps(TcConvPlan& p, const void* x, const Lay& xl, const void*
     cuuint64_t dims[4] = {brow, brows, static_cast<cuuint64_t>(a.Cc), static_cast<cuuint64_t>(p.spec.taps)};
     cuuint64_t strides[3] = {brow, static_cast<cuuint64_t>(OC) * kb, static_cast<cuuint64_t>(OC) * kb * a.Cc};
     cuuint32_t box[4] = {static_cast<cuuint32_t>(brow), static_cast<cuuint32_t>(kb == 16 ? a.bn / 8 : a.bn),
-                         static_cast<cuuint32_t>(a.resident_b ? a.Cc : a.pps), static_cast<cuuint32_t>(p.spec.taps)};
+                         static_cast<cuuint32_t>(a.resident_b ? a.Cc : a.pps),
+                         static_cast<cuuint32_t>(a.tap_groups > 1 ? p.spec.taps / a.tap_groups : p.spec.taps)};
     cuuint32_t es[4] = {1, 1, 1, 1};
     if (enc(&p.tmB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(w), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -1613,7 +1652,8 @@ const char* tc_conv_describe(const TcConvPlan* p, char* buf, int n) {
   std::snprintf(buf, n,
                 "tcgen05 %s %s %dx(M128)xN%d kb=%d taps=%d steps=%d grid=%dx%d rows=%dx%d pps=%d stages=%d B=%s ctas=%d smem=%zu",
                 p->spec.elem_bytes == 1 ? "i8" : "bf16", kinds[p->spec.kind], a.sub, a.bn, a.kb, p->spec.taps, a.n_steps,
-                a.Hg, a.Wg, a.nbox, a.hbox, a.pps, a.n_stages, a.resident_b ? "resident" : "streamed", p->grid, p->smem);
+                a.Hg, a.Wg, a.nbox, a.hbox, a.pps, a.n_stages,
+                a.resident_b ? "resident" : a.tap_groups > 1 ? "streamed-by-kernel-row" : "streamed", p->grid, p->smem);
   return buf;
 }
 
