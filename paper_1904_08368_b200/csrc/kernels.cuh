@@ -214,12 +214,38 @@ __host__ __device__ __forceinline__ int64_t lay_byte(const Lay& L, int64_t pix, 
 // [-128, 127] or [0, 255]): the clipped value is integral, so the truncating
 // cast is exact and the wrap to 8 bits is a plain narrowing.  NaN: clip keeps
 // NaN, cvt.rzi gives 0 == the reference's INT64_MIN & 0xff.
+// rint + clip to the 8-bit range + cast in ONE conversion: cvt.rni.sat.{s8,u8}.f32
+// (round to nearest even, saturate; NaN -> 0), equal to the reference chain
+// clip(rint(y), lo, hi) -> trunc -> wrap whenever [lo, hi] is exactly the
+// 8-bit range (every realize site: int8 [-128, 127], uint8 [0, 255]).
+__device__ __forceinline__ int32_t cvt_rn_sat_s8(float y) {
+  int32_t r;
+  asm("cvt.rni.sat.s8.f32 %0, %1;" : "=r"(r) : "f"(y));
+  return r;
+}
+__device__ __forceinline__ int32_t cvt_rn_sat_u8(float y) {
+  uint32_t r;
+  asm("cvt.rni.sat.u8.f32 %0, %1;" : "=r"(r) : "f"(y));
+  return static_cast<int32_t>(r);
+}
+
 template <bool CAL>
 __device__ __forceinline__ int32_t quant_code_fast_t(float v, const QDev& q) {
   if constexpr (CAL) quant_observe(v, q);
   float t = clip_ref(rintf(__fmul_rn(v, q.c1)), q.lo, q.hi);
   int32_t k = __float2int_rz(t);
   return q.is_signed ? static_cast<int32_t>(static_cast<int8_t>(k)) : (k & 0xff);
+}
+
+// quant_code_fast with the saturating conversion for the 8-bit ranges (the
+// network-input conversion; measured slower inside the conv epilogues)
+template <bool CAL>
+__device__ __forceinline__ int32_t quant_code_cvt_t(float v, const QDev& q) {
+  if (q.is_signed && q.lo == -128.f && q.hi == 127.f) {  // uniform branch
+    if constexpr (CAL) quant_observe(v, q);
+    return cvt_rn_sat_s8(__fmul_rn(v, q.c1));
+  }
+  return quant_code_fast_t<CAL>(v, q);
 }
 
 __device__ __forceinline__ int32_t quant_code_fast(float v, const QDev& q) { return quant_code_fast_t<true>(v, q); }

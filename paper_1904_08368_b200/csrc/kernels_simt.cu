@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(128) k_input_s2d_ct(const float* __restrict__ 
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
               const int k = 4 * h + b;
-              const int32_t code = !live[k] ? 0 : fast_q ? quant_code_fast_t<CAL>(v[k], q) : quant_code_t<CAL>(v[k], q);
+              const int32_t code = !live[k] ? 0 : fast_q ? quant_code_cvt_t<CAL>(v[k], q) : quant_code_t<CAL>(v[k], q);
               u |= (static_cast<uint32_t>(code) & 0xff) << (8 * b);
             }
             w4[h] = u;

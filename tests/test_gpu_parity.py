@@ -258,3 +258,26 @@ def test_device_run_graph_and_profile_paths_agree(gpu):
     assert np.array_equal(bits(out.cpu().numpy()), bits(gold))
     d = ex.describe()
     assert len(d["launches"]) == ex.launch_count()
+
+
+@pytest.mark.gpu
+def test_int8_input_quantization_edge_values(gpu):
+    """The realize chain at the input (multiply, rint, clip, cast to int8) on
+    ties, the clip boundaries, -0, huge values, infinities and NaN: the whole
+    int8 network matches the oracle (pinned to the reference) bit for bit."""
+    from oracle import port
+    ex, src = setup("resnet18_tiny", "int8", 4)
+    text, meta, _ = mrb.load_model("resnet18_tiny", "int8")
+    w = modelzoo.make_weights(src, seed=meta["weights_seed"])
+    x = modelzoo.make_inputs(src, 4, seed=3)
+    c1 = 2.0  # the module's input site scale (x * 2.0, see models/resnet18_tiny_int8.fused.rly)
+    assert "multiply(%x, const 2.0)" in text
+    edge = np.array([0.5, 1.5, 2.5, -0.5, -1.5, -2.5, 63.5, 64.0, 127.5, -127.5, -128.5, -129.5, 126.5,
+                     -0.0, 1e30, -1e30, np.inf, -np.inf, np.nan, 3.4e38, -3.4e38, 1e-40, 0.4999999], np.float32) / c1
+    flat = x.reshape(-1)
+    rng = np.random.default_rng(5)
+    idx = rng.choice(flat.size, size=4000, replace=False)
+    flat[idx] = np.resize(edge, idx.size)
+    y = ex.run_host(x)
+    want = port.run_weights(text, x, [w[p.name] for p in src.params if p.kind != "input"])
+    assert np.array_equal(bits(y), bits(want)), int(np.sum(bits(y) != bits(want)))
