@@ -243,15 +243,35 @@ __global__ void __launch_bounds__(128) k_input_s2d_ct(const float* __restrict__ 
   const int n_rows = N * GR;
   const int W4 = W >> 2, total4 = 2 * C * W4;
   const bool fast_q = q.lo > -2147483648.f && q.hi < 2147483648.f;
+  // the 2*C input row segments of one s2d row: segment cr = (channel, row parity);
+  // W4 <= 64: thread = (segment phase t / 64, 16-byte column t % 64), so the
+  // segment base is computed once per segment, not per 16-byte chunk
+  const bool seg_map = W4 <= 64 && blockDim.x == 128;
   auto prefetch = [&](float* buf, int row) {
     const int n = row / GR, si = row - n * GR - OFF;
-    for (int i = threadIdx.x; i < total4; i += blockDim.x) {
-      const int cr = static_cast<int>(fdiv(static_cast<uint32_t>(i), fd_w4)), x4 = i - cr * W4;
-      const int y = 2 * si - PAD + (cr & 1), c = cr >> 1;
-      const bool in = y >= 0 && y < H;
-      const float* src = x + ((static_cast<int64_t>(n) * C + c) * H + (in ? y : 0)) * W + 4 * x4;
-      const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(buf + 4 * i));
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(in ? 16 : 0) : "memory");
+    if (seg_map) {
+      const int x4 = threadIdx.x & 63;
+      if (x4 < W4) {
+        const uint32_t dst0 = static_cast<uint32_t>(__cvta_generic_to_shared(buf + 4 * x4));
+#pragma unroll
+        for (int cr = threadIdx.x >> 6; cr < 2 * C; cr += 2) {
+          const int y = 2 * si - PAD + (cr & 1), c = cr >> 1;
+          const bool in = y >= 0 && y < H;
+          const float* src = x + ((static_cast<int64_t>(n) * C + c) * H + (in ? y : 0)) * W + 4 * x4;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst0 + static_cast<uint32_t>(cr * W4 * 16)),
+                       "l"(src), "r"(in ? 16 : 0)
+                       : "memory");
+        }
+      }
+    } else {
+      for (int i = threadIdx.x; i < total4; i += blockDim.x) {
+        const int cr = static_cast<int>(fdiv(static_cast<uint32_t>(i), fd_w4)), x4 = i - cr * W4;
+        const int y = 2 * si - PAD + (cr & 1), c = cr >> 1;
+        const bool in = y >= 0 && y < H;
+        const float* src = x + ((static_cast<int64_t>(n) * C + c) * H + (in ? y : 0)) * W + 4 * x4;
+        const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(buf + 4 * i));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(in ? 16 : 0) : "memory");
+      }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
