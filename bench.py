@@ -261,18 +261,21 @@ def roofline(res, precision, pk):
     else:
         achieved, peak, unit = f["flops"] / secs / 1e12, tc, "TFLOP/s" if precision != "int8" else "TOP/s"
     total_ms = sum(per)
-    traffic = None
+    traffic = traffic_step = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
         t = json.load(open(tf)).get(precision, {}).get(name)
-        if t is not None:  # DRAM bytes of the family per step (ncu), same unit as `algorithmic.bytes`
-            traffic = t["bytes_per_step"]
+        if t is not None:  # ncu DRAM bytes of the family: per launch (like `achieved`) and per step
+            traffic_step = t["bytes_per_step"]
+            traffic = traffic_step / max(1, t.get("launches", f["n"]))
     # whole-step roofline: sum over launches of max(bytes/BW, flops/peak)
     t_roof = sum(max(L["bytes"] / (hbm * 1e9), L["flops"] / (tc * 1e12)) for L in desc["launches"])
     return {"kernel": name, "launches": f["n"], "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
             "frac": achieved / peak, "traffic": traffic, "share_of_step": f["ms"] / total_ms,
             "peak_source": pk["source"] + ("" if precision != "int8" else "; int8 tensor peak: " + pk["i8_source"]),
-            "algorithmic": {"bytes": f["bytes"], "ops": f["flops"], "avg_ms": f["ms"] / f["n"]},
+            "traffic_per_step": traffic_step,
+            "algorithmic": {"bytes": f["bytes"], "ops": f["flops"], "avg_ms": f["ms"] / f["n"],
+                            "bytes_per_launch": f["bytes"] / f["n"], "ops_per_launch": f["flops"] / f["n"]},
             "step_roofline_ms": t_roof * 1e3, "step_profiled_ms": total_ms,
             "step_frac": (t_roof * 1e3) / total_ms}
 
