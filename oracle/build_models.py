@@ -48,11 +48,16 @@ CONFIGS = {
     # model interchange: weights embedded in the metadata
     # pool (modelzoo.bind_weights), folded by the reference's own passes
     "resnet18_small_const": (modelzoo.resnet18, dict(image=32, num_classes=10, widths=(16, 16, 32, 32))),
+    # BASELINE config C4 at its benchmark batch (static-batch reshape heads): throughput
+    # modules only (tests/side_bench.py); the int8 DQN reuses dqn's calibrated k
+    "vgg16_b256": (modelzoo.vgg16, dict(batch=256)),
+    "dqn_b256": (modelzoo.dqn, dict(batch=256)),
 }
+K_FROM = {"dqn_b256": "dqn"}
 BIND = {"resnet18_small_const"}
 # float-only (BASELINE lists them as bf16 configs; an int8 calibration sweep of
 # the 224x224 VGG-16 in the reference interpreter takes about an hour)
-NO_INT8 = {"vgg16"}
+NO_INT8 = {"vgg16", "vgg16_b256"}
 
 
 def build(name: str, out_dir: str) -> dict:
@@ -65,7 +70,10 @@ def build(name: str, out_dir: str) -> dict:
     batch = kw.get("batch", 1)  # static-batch modules calibrate on their own batch
     x = modelzoo.make_inputs(src, batch, seed=0)
     t0 = time.time()
-    k = None if name in NO_INT8 else ref.calibrate(src.text, PRE, [x] + ref.weight_list(src, w))
+    if name in K_FROM:
+        k = json.load(open(os.path.join(out_dir, K_FROM[name] + ".json")))["calibration"]["k"]
+    else:
+        k = None if name in NO_INT8 else ref.calibrate(src.text, PRE, [x] + ref.weight_list(src, w))
     t_cal = time.time() - t0
     fused_fp32 = ref.compile(src.text, FP32, 0)
     fused_int8 = None if k is None else ref.compile(src.text, INT8, k)
@@ -79,8 +87,9 @@ def build(name: str, out_dir: str) -> dict:
         "bind_weights": name in BIND,
         "builder_kwargs": {k2: list(v) if isinstance(v, tuple) else v for k2, v in kw.items()},
         "weights_seed": 1,
-        "calibration": None if k is None else {"inputs_seed": 0, "images": batch, "k": k, "scale": 2.0 ** k,
-                                               "seconds": round(t_cal, 1), "pre_passes": PRE},
+        "calibration": None if k is None else (
+            {"k": k, "scale": 2.0 ** k, "k_from": K_FROM[name]} if name in K_FROM else
+            {"inputs_seed": 0, "images": batch, "k": k, "scale": 2.0 ** k, "seconds": round(t_cal, 1), "pre_passes": PRE}),
         "passes": {"fp32": FP32, "int8": None if k is None else INT8},
         "groups": {"fp32": fused_fp32.count("[Primitive=true]"),
                    "int8": None if fused_int8 is None else fused_int8.count("[Primitive=true]")},

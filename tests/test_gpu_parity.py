@@ -281,3 +281,19 @@ def test_int8_input_quantization_edge_values(gpu):
     y = ex.run_host(x)
     want = port.run_weights(text, x, [w[p.name] for p in src.params if p.kind != "input"])
     assert np.array_equal(bits(y), bits(want)), int(np.sum(bits(y) != bits(want)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,prec,fm", [("dqn_b256", "int8", 0), ("vgg16_b256", "fp32", 1)])
+def test_config_c4_at_batch256_matches_small_batch_golden(gpu, name, prec, fm):
+    """BASELINE config C4 modules compiled at the benchmark batch (static
+    reshape heads): images 0-1 of a batch-256 run equal the reference's batch-2
+    goldens bit for bit (per-sample independence; int8, and fp32-strict)."""
+    base = name.split("_b256")[0]
+    gold = np.load(os.path.join(GOLD, "%s_b2.npz" % base))[prec]
+    ex, src = setup(name, prec, 256, float_mode=fm)
+    x = modelzoo.make_inputs(src, 256, seed=0)
+    x2 = modelzoo.make_inputs(src, 2, seed=0)
+    assert np.array_equal(x[:2], x2)
+    y = ex.run_host(x)
+    assert np.array_equal(bits(y[:2]), bits(gold)), int(np.sum(bits(y[:2]) != bits(gold)))
