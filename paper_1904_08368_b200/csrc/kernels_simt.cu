@@ -1197,9 +1197,8 @@ __global__ void __launch_bounds__(256) k_dense(const float* __restrict__ x, int 
 // chunk's weight loads before the row staging so the L2 round trip overlaps
 // it.  Grid: ceil(M/32) x ceil(N/R) (the head: 32 x 16 = 512 blocks).
 constexpr int kDkWarps = 8;
-constexpr int kDkChunk = 1024;  // K elements per staged chunk (multiple of 8 * kDkWarps)
 
-template <int MODE, int R, bool CAL>
+template <int MODE, int R, int kDkChunk, bool CAL>  // kDkChunk: K elements per staged chunk (multiple of 8 * kDkWarps)
 __global__ void __launch_bounds__(256) k_dense_ks(const float* __restrict__ x, int N, int K, int Kp,
                                                   const void* __restrict__ w, int M, float pre_mul, int quant, QDev q,
                                                   float acc_scale, EpiDev epi, OutDev out) {
@@ -1208,7 +1207,13 @@ __global__ void __launch_bounds__(256) k_dense_ks(const float* __restrict__ x, i
   constexpr int kSlice = kDkChunk / kDkWarps;            // K per warp per chunk
   constexpr int kLoads = MODE == 0 ? kSlice / 4 : kSlice / 8;  // weight words (int32 / uint4) per thread
   __shared__ __align__(16) uint8_t stage[MODE == 0 ? R * kDkChunk : R * kDkChunk * 4];
-  __shared__ float red[kDkWarps][R][32];
+  // the cross-warp partial sums: their own array when both fit the 48 KB of static
+  // shared memory, else the staging buffer once the K loop is done
+  constexpr int kStageBytes = MODE == 0 ? R * kDkChunk : R * kDkChunk * 4;
+  constexpr bool kAliasRed = kStageBytes + static_cast<int>(sizeof(float)) * kDkWarps * R * 32 > 48 * 1024;
+  static_assert(!kAliasRed || static_cast<int>(sizeof(float)) * kDkWarps * R * 32 <= kStageBytes, "red fits stage");
+  __shared__ float red_own[kAliasRed ? 1 : kDkWarps][kAliasRed ? 1 : R][32];
+  auto red = kAliasRed ? reinterpret_cast<float (*)[R][32]>(stage) : reinterpret_cast<float (*)[R][32]>(&red_own[0][0][0]);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int j = blockIdx.x * 32 + lane;
   const bool jv = j < M;
@@ -1296,6 +1301,7 @@ __global__ void __launch_bounds__(256) k_dense_ks(const float* __restrict__ x, i
     }
   }
   // 4. cross-warp reduction (fixed order) + epilogue
+  if constexpr (kAliasRed) __syncthreads();  // every warp is done reading the staged rows
 #pragma unroll
   for (int r = 0; r < R; ++r) red[warp][r][lane] = MODE == 0 ? __int_as_float(acc[r]) : res[r];
   __syncthreads();
@@ -1538,14 +1544,18 @@ void launch_dense(const float* x, int N, int K, int Kp, const void* w, int M, in
   bool cal = quant && q.ovf;
   for (int k = 0; k < epi.n_ops; ++k) cal = cal || (epi.op[k] == E_REQ && epi.q[k].ovf);
   if (mode == 0 || mode == 2) {  // K split across warps (exact int32 sum / bf16 tolerance)
-    constexpr int R0 = 16, R2 = 4;
-    const int R = mode == 0 ? R0 : R2;
+    // bf16: 32 rows per block over 256-element K chunks, so large fc layers (VGG fc6:
+    // 205 MB of weights) re-read their weights once per 32 batch rows, not per 4
+    constexpr int R0 = 16, R2 = 4, R2L = 32;
+    const bool big = mode == 2 && K >= 4096;
+    const int R = mode == 0 ? R0 : big ? R2L : R2;
     dim3 g2(static_cast<unsigned>((M + 31) / 32), static_cast<unsigned>((N + R - 1) / R));
     if (mode == 0) {
-      auto k2 = cal ? k_dense_ks<0, R0, true> : k_dense_ks<0, R0, false>;
+      auto k2 = cal ? k_dense_ks<0, R0, 1024, true> : k_dense_ks<0, R0, 1024, false>;
       pdl_launch(k2, g2, 256, 0, s, x, N, K, Kp, w, M, pre_mul, quant, q, acc_scale, epi, out);
     } else {
-      auto k2 = cal ? k_dense_ks<2, R2, true> : k_dense_ks<2, R2, false>;
+      auto k2 = big ? (cal ? k_dense_ks<2, R2L, 256, true> : k_dense_ks<2, R2L, 256, false>)
+                    : (cal ? k_dense_ks<2, R2, 1024, true> : k_dense_ks<2, R2, 1024, false>);
       pdl_launch(k2, g2, 256, 0, s, x, N, K, Kp, w, M, pre_mul, quant, q, acc_scale, epi, out);
     }
     return;
