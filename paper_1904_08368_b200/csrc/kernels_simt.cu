@@ -1460,8 +1460,108 @@ void launch_conv_i8_simt(const int8_t* x, const int8_t* w, const ConvGeom& g, fl
   pdl_launch(k_conv_i8_simt, grid, 256, 0, s, x, w, g, acc_scale, epi, out);
 }
 
+// ---- 3x3 / stride 1 / pad 1 convolution over a tiny channel count (a network's
+// first layer, e.g. VGG-16's 3 -> 64), bf16 mode.  K = 9*C is too small for a
+// tensor-core formulation; one thread per output pixel keeps the 9*C input taps
+// in registers (the padded layout makes the border taps plain zero loads) and
+// runs them against the weights staged in shared memory ([k][OC] fp32, the
+// 16-OC rows read as broadcasts), 16 output channels per pass.
+template <int C>
+__global__ void __launch_bounds__(256) k_conv3x3_tinyc(const uint16_t* __restrict__ x, const uint16_t* __restrict__ w,
+                                                       ConvGeom g, EpiDev epi, OutDev out, FastDiv fd_ow, FastDiv fd_oh) {
+  pdl_trigger();
+  extern __shared__ __align__(16) float ws[];  // [9 * C][OC]
+  const int OC = g.OC;
+  for (int i = threadIdx.x; i < 9 * C * OC; i += blockDim.x) {
+    const int k = i / OC, oc = i - k * OC;
+    const int tap = k / C, ic = k - tap * C;
+    ws[i] = bf16_to_f32(w[static_cast<int64_t>(oc) * g.Kp + tap * g.Cs + ic]);
+  }
+  __syncthreads();
+  pdl_wait();
+  const int Hp = g.H + 2 * kPad, Wp = g.W + 2 * kPad;
+  const bool fast_store = !out.side && out.primary_fmt == FMT_BF16 && out.plan.kind == LAY_NORMAL &&
+                          out.plan.cpc % 16 == 0;
+  const uint32_t total = static_cast<uint32_t>(g.N) * g.OH * g.OW;
+  for (uint32_t m = blockIdx.x * blockDim.x + threadIdx.x; m < total; m += gridDim.x * blockDim.x) {
+    const uint32_t t = fdiv(m, fd_ow);
+    const int ow = static_cast<int>(m - t * static_cast<uint32_t>(g.OW));
+    const uint32_t n32 = fdiv(t, fd_oh);
+    const int oh = static_cast<int>(t - n32 * static_cast<uint32_t>(g.OH));
+    const int n = static_cast<int>(n32);
+    float xin[9 * C];
+#pragma unroll
+    for (int kh = 0; kh < 3; ++kh)
+#pragma unroll
+      for (int kw = 0; kw < 3; ++kw) {
+        // padded input (oh + kh, ow + kw): the zero border covers the pad-1 taps
+        const int64_t pix = (static_cast<int64_t>(n) * Hp + oh + kh) * Wp + ow + kw;
+        const uint2 u = __ldg(reinterpret_cast<const uint2*>(x + lay_off(g.in, pix, 0)));
+        const float v4[4] = {__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u),
+                             __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xffff0000u)};
+#pragma unroll
+        for (int c = 0; c < C; ++c) xin[(kh * 3 + kw) * C + c] = v4[c];
+      }
+    const int64_t opix = pad_pix(n, oh, ow, g.OH, g.OW);
+    for (int oc0 = 0; oc0 < OC; oc0 += 16) {
+      float acc[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+#pragma unroll
+      for (int k = 0; k < 9 * C; ++k) {
+        const float4* wp = reinterpret_cast<const float4*>(ws + k * OC + oc0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 wv = wp[q];
+          acc[4 * q] = __fmaf_rn(xin[k], wv.x, acc[4 * q]);
+          acc[4 * q + 1] = __fmaf_rn(xin[k], wv.y, acc[4 * q + 1]);
+          acc[4 * q + 2] = __fmaf_rn(xin[k], wv.z, acc[4 * q + 2]);
+          acc[4 * q + 3] = __fmaf_rn(xin[k], wv.w, acc[4 * q + 3]);
+        }
+      }
+      int32_t code = 0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc[j] = apply_epi(epi, acc[j], opix, oc0 + j, &code);
+      if (fast_store) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t w4[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            w4[q] = static_cast<uint32_t>(f32_to_bf16(acc[8 * h + 2 * q])) |
+                    (static_cast<uint32_t>(f32_to_bf16(acc[8 * h + 2 * q + 1])) << 16);
+          *reinterpret_cast<uint4*>(static_cast<char*>(out.primary) + lay_byte(out.plan, opix, oc0 + 8 * h)) =
+              make_uint4(w4[0], w4[1], w4[2], w4[3]);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) store_out(out, acc[j], code, opix, oc0 + j);
+      }
+    }
+  }
+}
+
 void launch_conv_bf16_simt(const uint16_t* x, const uint16_t* w, const ConvGeom& g, const EpiDev& epi,
                            const OutDev& out, cudaStream_t s) {
+  if (g.KH == 3 && g.KW == 3 && g.sh == 1 && g.sw == 1 && g.ph == 1 && g.pw == 1 && g.C <= 4 && g.OC % 16 == 0 &&
+      g.in.kind == LAY_NORMAL && g.in.cpc >= 4 && 9 * g.C * g.OC * 4 <= 48 * 1024 &&
+      static_cast<int64_t>(g.N) * g.OH * g.OW < (int64_t(1) << 31) && !std::getenv("MRB200_NO_TINYC")) {
+    static int sms = [] {
+      int d = 0, v = 0;
+      cudaGetDevice(&d);
+      cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+      return v > 0 ? v : 148;
+    }();
+    const size_t smem = static_cast<size_t>(9) * g.C * g.OC * 4;
+    const FastDiv a = make_fastdiv(static_cast<uint32_t>(g.OW)), b = make_fastdiv(static_cast<uint32_t>(g.OH));
+    const int grid = sms * 8;
+    switch (g.C) {
+      case 1: pdl_launch(k_conv3x3_tinyc<1>, grid, 256, smem, s, x, w, g, epi, out, a, b); return;
+      case 2: pdl_launch(k_conv3x3_tinyc<2>, grid, 256, smem, s, x, w, g, epi, out, a, b); return;
+      case 3: pdl_launch(k_conv3x3_tinyc<3>, grid, 256, smem, s, x, w, g, epi, out, a, b); return;
+      default: pdl_launch(k_conv3x3_tinyc<4>, grid, 256, smem, s, x, w, g, epi, out, a, b); return;
+    }
+  }
   int64_t M = static_cast<int64_t>(g.N) * g.OH * g.OW;
   dim3 grid(static_cast<unsigned>((M + 63) / 64), static_cast<unsigned>((g.OC + 63) / 64));
   pdl_launch(k_conv_bf16_simt, grid, 256, 0, s, x, w, g, epi, out);
