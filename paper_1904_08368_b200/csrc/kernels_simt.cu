@@ -1519,9 +1519,44 @@ __global__ void __launch_bounds__(256) k_conv3x3_tinyc(const uint16_t* __restric
           acc[4 * q + 3] = __fmaf_rn(xin[k], wv.w, acc[4 * q + 3]);
         }
       }
-      int32_t code = 0;
+      // the op list once over the 16 values (op-major: one switch per op, not per value)
+      int32_t codes[16];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) acc[j] = apply_epi(epi, acc[j], opix, oc0 + j, &code);
+      for (int j = 0; j < 16; ++j) codes[j] = 0;
+      for (int op = 0; op < epi.n_ops; ++op) {
+        const int kind = epi.op[op];
+        if (kind == E_MULC || kind == E_BIAS) {
+          const float4* vp = reinterpret_cast<const float4*>(epi.vec[op] + oc0);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float4 v4 = __ldg(vp + q);
+            const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+              acc[4 * q + r] = kind == E_MULC ? __fmul_rn(acc[4 * q + r], vv[r]) : __fadd_rn(acc[4 * q + r], vv[r]);
+          }
+        } else if (kind == E_MULS) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[j] = __fmul_rn(acc[j], epi.s[op]);
+        } else if (kind == E_RELU) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[j] = relu_ref(acc[j]);
+        } else if (kind == E_CLIP) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[j] = clip_ref(acc[j], epi.s[op], epi.s2[op]);
+        } else if (kind == E_REQ) {
+          const QDev qd = epi.q[op];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            codes[j] = quant_code(acc[j], qd);
+            acc[j] = __fmul_rn(static_cast<float>(codes[j]), qd.c2);
+          }
+        } else if (kind == E_RES) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            acc[j] = __fadd_rn(acc[j], load_fmt(epi.res[op], epi.res_fmt[op], lay_off(epi.res_lay[op], opix, oc0 + j)));
+        }
+      }
       if (fast_store) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -1535,7 +1570,7 @@ __global__ void __launch_bounds__(256) k_conv3x3_tinyc(const uint16_t* __restric
         }
       } else {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) store_out(out, acc[j], code, opix, oc0 + j);
+        for (int j = 0; j < 16; ++j) store_out(out, acc[j], codes[j], opix, oc0 + j);
       }
     }
   }
