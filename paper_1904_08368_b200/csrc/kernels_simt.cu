@@ -1415,6 +1415,17 @@ void launch_input_convert(const float* x, int N, int C, int H, int W, void* out,
         pdl_launch(k_input_s2d_ct<3, 3, 8, false, false>, std::min(rows, sms * 8), 128, smem, s, x, N, H, W, out, L, pre_mul, q, fd);
       return;
     }
+    // 3x3/s2/pad-1 stems over 3 channels (MobileNet-v1): the same kernel with PAD 1
+    if (C == 3 && s2d_pad == 1 && L.kb == 16 && (fmt == FMT_I8 || fmt == FMT_BF16) && smem <= 48 * 1024) {
+      const FastDiv fd = make_fastdiv(static_cast<uint32_t>(W / 4));
+      if (fmt == FMT_I8)
+        pdl_launch(q.ovf ? k_input_s2d_ct<3, 1, 16, false, true> : k_input_s2d_ct<3, 1, 16, false, false>,
+                   std::min(rows, sms * 8), 128, smem, s, x, N, H, W, out, L, pre_mul, q, fd);
+      else
+        pdl_launch(k_input_s2d_ct<3, 1, 8, false, false>, std::min(rows, sms * 8), 128, smem, s, x, N, H, W, out, L,
+                   pre_mul, q, fd);
+      return;
+    }
     pdl_launch(k_input_s2d, std::min(rows, sms * 8), 128, 2 * 2 * C * W * sizeof(float), s, x, N, C, H, W, out, fmt, L,
                                                                                   s2d_pad, pre_mul, q);
     return;
