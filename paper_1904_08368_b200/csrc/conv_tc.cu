@@ -263,6 +263,20 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+#ifndef MRB200_SIDE_SATPACK
+#define MRB200_SIDE_SATPACK 1  // A/B: +1-1.8 % (side codes: rint, then the saturating pack clips)
+#endif
+#ifndef MRB200_P2_SATPACK
+#define MRB200_P2_SATPACK 1  // A/B: +0.6 % (saturating I2IP pack does the clip at 127)
+#endif
+// 4 int32 -> 4 saturated int8 bytes (a in byte 0) with two I2IP
+__device__ __forceinline__ uint32_t pack4_sat_s8(int a, int b, int c, int d) {
+  uint32_t hi, r;
+  asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, 0;" : "=r"(hi) : "r"(d), "r"(c));
+  asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(b), "r"(a), "r"(hi));
+  return r;
+}
+
 __device__ __forceinline__ uint32_t pack4_i8(int a, int b, int c, int d) {
   return (static_cast<uint32_t>(a) & 0xff) | ((static_cast<uint32_t>(b) & 0xff) << 8) |
          ((static_cast<uint32_t>(c) & 0xff) << 16) | ((static_cast<uint32_t>(d) & 0xff) << 24);
@@ -423,6 +437,9 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
         // acc*s and *c1 are exact (powers of two, |acc| < 2^24 by the exactness bound),
         // so the fma rounds once exactly where fadd did; relu/rint/clip become integer clamps
         const float4* bp = reinterpret_cast<const float4*>(s_vec + kVecSlots * 256 + cl);
+#if MRB200_P2_SATPACK
+        int32_t code_raw[16];
+#endif
         float bb[16];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -432,7 +449,11 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int r = __float2int_rn(__fmaf_rn(static_cast<float>(static_cast<int32_t>(raw[i])), a.p2_scale, bb[i]));
+#if MRB200_P2_SATPACK
+          code_raw[i] = r;
+#else
           code[i] = min(max(r, 0), a.p2_hi);
+#endif
         }
         if (CAL && e.q[2].ovf) {  // calibration: the rounded site value max(r, 0) must not exceed 128
 #pragma unroll
@@ -440,6 +461,19 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
             if (__float2int_rn(__fmaf_rn(static_cast<float>(static_cast<int32_t>(raw[i])), a.p2_scale, bb[i])) > 128)
               atomicOr(e.q[2].ovf, 1);
         }
+#if MRB200_P2_SATPACK
+        if (a.p2_hi == 127) {
+          // codes are >= 0 after the relu clamp; the saturating pack does the clip at 127
+          uint32_t wds[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) wds[j] = pack4_sat_s8(max(code_raw[4 * j], 0), max(code_raw[4 * j + 1], 0),
+                                                            max(code_raw[4 * j + 2], 0), max(code_raw[4 * j + 3], 0));
+          st16(o.primary, gran_byte(o.plan, d.pix, o.plan.Pp, c0), make_uint4(wds[0], wds[1], wds[2], wds[3]));
+          return;
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) code[i] = min(max(code_raw[i], 0), a.p2_hi);
+#endif
         st16(o.primary, gran_byte(o.plan, d.pix, o.plan.Pp, c0),
              make_uint4(pack4_i8(code[0], code[1], code[2], code[3]), pack4_i8(code[4], code[5], code[6], code[7]),
                         pack4_i8(code[8], code[9], code[10], code[11]), pack4_i8(code[12], code[13], code[14], code[15])));
@@ -497,6 +531,21 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
   if (o.side) {
     if (o.side_fmt == FMT_I8) {
       int sc[16];
+#if MRB200_SIDE_SATPACK
+      if (o.side_q.is_signed && o.side_q.lo == -128.f && o.side_q.hi == 127.f) {  // uniform
+        // rint, then the saturating pack clips to [-128, 127] (F2I of a huge value
+        // saturates first; NaN -> 0 as the reference's wrapped cast)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          if constexpr (CAL) quant_observe(v[i], o.side_q);
+          sc[i] = __float2int_rz(rintf(__fmul_rn(v[i], o.side_q.c1)));
+        }
+        st16(o.side, gran_byte(o.slay, d.side_base, d.side_pstride, c0),
+             make_uint4(pack4_sat_s8(sc[0], sc[1], sc[2], sc[3]), pack4_sat_s8(sc[4], sc[5], sc[6], sc[7]),
+                        pack4_sat_s8(sc[8], sc[9], sc[10], sc[11]), pack4_sat_s8(sc[12], sc[13], sc[14], sc[15])));
+        return;
+      }
+#endif
 #pragma unroll
       for (int i = 0; i < 16; ++i) sc[i] = quant_code_fast_t<CAL>(v[i], o.side_q);
       st16(o.side, gran_byte(o.slay, d.side_base, d.side_pstride, c0),
