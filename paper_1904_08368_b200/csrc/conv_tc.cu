@@ -533,12 +533,13 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
       int sc[16];
 #if MRB200_SIDE_SATPACK
       if (o.side_q.is_signed && o.side_q.lo == -128.f && o.side_q.hi == 127.f) {  // uniform
-        // rint, then the saturating pack clips to [-128, 127] (F2I of a huge value
-        // saturates first; NaN -> 0 as the reference's wrapped cast)
+        // round-to-nearest-even conversion (== trunc(rint(y))), then the saturating
+        // pack clips to [-128, 127] (F2I of a huge value saturates first; NaN -> 0
+        // as the reference's wrapped cast)
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           if constexpr (CAL) quant_observe(v[i], o.side_q);
-          sc[i] = __float2int_rz(rintf(__fmul_rn(v[i], o.side_q.c1)));
+          sc[i] = __float2int_rn(__fmul_rn(v[i], o.side_q.c1));  // cvt.rni: == trunc(rint(y)), one F2I
         }
         st16(o.side, gran_byte(o.slay, d.side_base, d.side_pstride, c0),
              make_uint4(pack4_sat_s8(sc[0], sc[1], sc[2], sc[3]), pack4_sat_s8(sc[4], sc[5], sc[6], sc[7]),
