@@ -523,8 +523,7 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
       uint32_t w4[4];
 #pragma unroll
       for (int h = 0; h < 4; ++h)
-        w4[h] = static_cast<uint32_t>(f32_to_bf16(v[8 * j + 2 * h])) |
-                (static_cast<uint32_t>(f32_to_bf16(v[8 * j + 2 * h + 1])) << 16);
+        w4[h] = pack_bf16x2(v[8 * j + 2 * h], v[8 * j + 2 * h + 1]);
       st16(o.primary, gran_byte(o.plan, d.pix, o.plan.Pp, c0 + 8 * j), make_uint4(w4[0], w4[1], w4[2], w4[3]));
     }
   }
@@ -558,8 +557,7 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
         uint32_t w4[4];
 #pragma unroll
         for (int h = 0; h < 4; ++h)
-          w4[h] = static_cast<uint32_t>(f32_to_bf16(v[8 * j + 2 * h])) |
-                  (static_cast<uint32_t>(f32_to_bf16(v[8 * j + 2 * h + 1])) << 16);
+          w4[h] = pack_bf16x2(v[8 * j + 2 * h], v[8 * j + 2 * h + 1]);
         st16(o.side, gran_byte(o.slay, d.side_base, d.side_pstride, c0 + 8 * j), make_uint4(w4[0], w4[1], w4[2], w4[3]));
       }
     }
@@ -970,8 +968,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                  make_uint4(__float_as_uint(mx[0]), __float_as_uint(mx[1]), __float_as_uint(mx[2]), __float_as_uint(mx[3])));
           } else {  // bf16 pipeline: 4 channels = 8 bytes
             *reinterpret_cast<uint2*>(static_cast<char*>(o.primary) + gran_byte(o.plan, pix, o.plan.Pp, c)) =
-                make_uint2(static_cast<uint32_t>(f32_to_bf16(mx[0])) | (static_cast<uint32_t>(f32_to_bf16(mx[1])) << 16),
-                           static_cast<uint32_t>(f32_to_bf16(mx[2])) | (static_cast<uint32_t>(f32_to_bf16(mx[3])) << 16));
+                make_uint2(pack_bf16x2(mx[0], mx[1]),
+                           pack_bf16x2(mx[2], mx[3]));
           }
           if (o.side) {
             char* sbase = static_cast<char*>(o.side) + lay_byte(o.slay, pix, c);
@@ -982,8 +980,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
               *reinterpret_cast<uint32_t*>(sbase) = u;
             } else {
               *reinterpret_cast<uint2*>(sbase) =
-                  make_uint2(static_cast<uint32_t>(f32_to_bf16(mx[0])) | (static_cast<uint32_t>(f32_to_bf16(mx[1])) << 16),
-                             static_cast<uint32_t>(f32_to_bf16(mx[2])) | (static_cast<uint32_t>(f32_to_bf16(mx[3])) << 16));
+                  make_uint2(pack_bf16x2(mx[0], mx[1]),
+                             pack_bf16x2(mx[2], mx[3]));
             }
           }
         }

@@ -133,6 +133,18 @@ __device__ __forceinline__ uint16_t f32_to_bf16(float f) {
   return static_cast<uint16_t>(u >> 16);
 }
 
+// Two floats -> packed bf16x2 (lo in the low half), round to nearest even in one
+// cvt (the bf16 pipeline's stores; matches f32_to_bf16 except NaN payloads).
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+#ifdef MRB200_NO_BF16X2_CVT
+  return static_cast<uint32_t>(f32_to_bf16(lo)) | (static_cast<uint32_t>(f32_to_bf16(hi)) << 16);
+#else
+  uint32_t d;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
+#endif
+}
+
 __device__ __forceinline__ float relu_ref(float x) { return x > 0.f ? x : 0.0f; }
 
 __device__ __forceinline__ float clip_ref(float x, float lo, float hi) {

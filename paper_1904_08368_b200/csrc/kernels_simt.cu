@@ -99,7 +99,7 @@ __global__ void k_input_convert(const float* __restrict__ x, int N, int C, int H
       uint32_t w4[4];
 #pragma unroll
       for (int h = 0; h < 4; ++h)
-        w4[h] = static_cast<uint32_t>(f32_to_bf16(v[2 * h])) | (static_cast<uint32_t>(f32_to_bf16(v[2 * h + 1])) << 16);
+        w4[h] = pack_bf16x2(v[2 * h], v[2 * h + 1]);
       *reinterpret_cast<uint4*>(dst) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
     } else {
       uint32_t w4[4];
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(128) k_input_s2d(const float* __restrict__ x, 
           } else if (fmt == FMT_BF16) {
 #pragma unroll
             for (int h = 0; h < 4; ++h)
-              w4[h] = static_cast<uint32_t>(f32_to_bf16(v[2 * h])) | (static_cast<uint32_t>(f32_to_bf16(v[2 * h + 1])) << 16);
+              w4[h] = pack_bf16x2(v[2 * h], v[2 * h + 1]);
           } else {
 #pragma unroll
             for (int h = 0; h < 4; ++h) {
@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(128) k_input_s2d_ct(const float* __restrict__ 
         if constexpr (CPC == 8) {
 #pragma unroll
           for (int h = 0; h < 4; ++h)
-            w4[h] = static_cast<uint32_t>(f32_to_bf16(v[2 * h])) | (static_cast<uint32_t>(f32_to_bf16(v[2 * h + 1])) << 16);
+            w4[h] = pack_bf16x2(v[2 * h], v[2 * h + 1]);
         } else {
 #pragma unroll
           for (int h = 0; h < 4; ++h) {
@@ -761,8 +761,8 @@ __global__ void __launch_bounds__(256) k_dwconv_fast(const void* __restrict__ x,
         *reinterpret_cast<float4*>(d4) = make_float4(r[0], r[1], r[2], r[3]);
       } else if (out.primary_fmt == FMT_BF16) {
         *reinterpret_cast<uint2*>(d4) =
-            make_uint2(static_cast<uint32_t>(f32_to_bf16(r[0])) | (static_cast<uint32_t>(f32_to_bf16(r[1])) << 16),
-                       static_cast<uint32_t>(f32_to_bf16(r[2])) | (static_cast<uint32_t>(f32_to_bf16(r[3])) << 16));
+            make_uint2(pack_bf16x2(r[0], r[1]),
+                       pack_bf16x2(r[2], r[3]));
       } else {
         uint32_t u = 0;
 #pragma unroll
@@ -778,8 +778,8 @@ __global__ void __launch_bounds__(256) k_dwconv_fast(const void* __restrict__ x,
           *reinterpret_cast<uint32_t*>(s4p) = u;
         } else {
           *reinterpret_cast<uint2*>(s4p) =
-              make_uint2(static_cast<uint32_t>(f32_to_bf16(r[0])) | (static_cast<uint32_t>(f32_to_bf16(r[1])) << 16),
-                         static_cast<uint32_t>(f32_to_bf16(r[2])) | (static_cast<uint32_t>(f32_to_bf16(r[3])) << 16));
+              make_uint2(pack_bf16x2(r[0], r[1]),
+                         pack_bf16x2(r[2], r[3]));
         }
       }
     }
@@ -922,8 +922,8 @@ __global__ void __launch_bounds__(256, dw_minb(PL)) k_dw3x3_rb(const void* __res
         *reinterpret_cast<float4*>(d4) = make_float4(r[0], r[1], r[2], r[3]);
       } else if (out.primary_fmt == FMT_BF16) {
         *reinterpret_cast<uint2*>(d4) =
-            make_uint2(static_cast<uint32_t>(f32_to_bf16(r[0])) | (static_cast<uint32_t>(f32_to_bf16(r[1])) << 16),
-                       static_cast<uint32_t>(f32_to_bf16(r[2])) | (static_cast<uint32_t>(f32_to_bf16(r[3])) << 16));
+            make_uint2(pack_bf16x2(r[0], r[1]),
+                       pack_bf16x2(r[2], r[3]));
       } else {
         uint32_t u = 0;
 #pragma unroll
@@ -939,8 +939,8 @@ __global__ void __launch_bounds__(256, dw_minb(PL)) k_dw3x3_rb(const void* __res
           *reinterpret_cast<uint32_t*>(s4p) = u;
         } else {
           *reinterpret_cast<uint2*>(s4p) =
-              make_uint2(static_cast<uint32_t>(f32_to_bf16(r[0])) | (static_cast<uint32_t>(f32_to_bf16(r[1])) << 16),
-                         static_cast<uint32_t>(f32_to_bf16(r[2])) | (static_cast<uint32_t>(f32_to_bf16(r[3])) << 16));
+              make_uint2(pack_bf16x2(r[0], r[1]),
+                         pack_bf16x2(r[2], r[3]));
         }
       }
     }
@@ -1014,8 +1014,8 @@ __global__ void k_maxpool(const void* __restrict__ x, int xfmt, ConvGeom g, OutD
         *reinterpret_cast<float4*>(d4) = make_float4(a4[0], a4[1], a4[2], a4[3]);
       } else {
         *reinterpret_cast<uint2*>(d4) =
-            make_uint2(static_cast<uint32_t>(f32_to_bf16(a4[0])) | (static_cast<uint32_t>(f32_to_bf16(a4[1])) << 16),
-                       static_cast<uint32_t>(f32_to_bf16(a4[2])) | (static_cast<uint32_t>(f32_to_bf16(a4[3])) << 16));
+            make_uint2(pack_bf16x2(a4[0], a4[1]),
+                       pack_bf16x2(a4[2], a4[3]));
       }
     }
     if (out.side) {
@@ -1574,8 +1574,7 @@ __global__ void __launch_bounds__(256) k_conv3x3_tinyc(const uint16_t* __restric
           uint32_t w4[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            w4[q] = static_cast<uint32_t>(f32_to_bf16(acc[8 * h + 2 * q])) |
-                    (static_cast<uint32_t>(f32_to_bf16(acc[8 * h + 2 * q + 1])) << 16);
+            w4[q] = pack_bf16x2(acc[8 * h + 2 * q], acc[8 * h + 2 * q + 1]);
           *reinterpret_cast<uint4*>(static_cast<char*>(out.primary) + lay_byte(out.plan, opix, oc0 + 8 * h)) =
               make_uint4(w4[0], w4[1], w4[2], w4[3]);
         }
