@@ -297,3 +297,19 @@ def test_config_c4_at_batch256_matches_small_batch_golden(gpu, name, prec, fm):
     assert np.array_equal(x[:2], x2)
     y = ex.run_host(x)
     assert np.array_equal(bits(y[:2]), bits(gold)), int(np.sum(bits(y[:2]) != bits(gold)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,batch,gold_b,prec", [("resnet18", 1, 2, "int8"), ("resnet18", 3, 2, "int8"),
+                                                     ("resnet18_tiny", 1, 4, "int8"), ("resnet18_tiny", 5, 4, "int8"),
+                                                     ("resnet18_tiny", 9, 4, "int8"), ("resnet18_tiny", 7, 4, "fp32")])
+def test_ragged_batches_match_golden_rows(gpu, name, batch, gold_b, prec):
+    """Batch sizes that fill no tile (1, 3, 5, 7, 9): the rows the golden covers
+    match it bit for bit (int8; fp32-strict), the tail tiles are masked."""
+    gold = np.load(os.path.join(GOLD, "%s_b%d.npz" % (name, gold_b)))[prec]
+    ex, src = setup(name, prec, batch, float_mode=mrb.MR_FLOAT_FP32_STRICT if prec == "fp32" else 0)
+    x = modelzoo.make_inputs(src, max(batch, gold_b), seed=0)
+    assert np.array_equal(x[:gold_b], modelzoo.make_inputs(src, gold_b, seed=0))
+    y = ex.run_host(np.ascontiguousarray(x[:batch]))
+    k = min(batch, gold_b)
+    assert np.array_equal(bits(y[:k]), bits(gold[:k])), int(np.sum(bits(y[:k]) != bits(gold[:k])))
