@@ -225,6 +225,9 @@ __global__ void __launch_bounds__(128) k_input_s2d(const float* __restrict__ x, 
 // PHASED writes LAY_S2DP: the s2d grid is walked from (-2, -2) over the
 // 2*Hq x 2*Wq extent of the 4 phase sub-grids (every position written, zeros
 // outside the image), so no separate border pass is needed.
+#ifndef MRB200_S2D_BPS
+#define MRB200_S2D_BPS 16  // S2D row-conversion blocks per SM (A/B: 16 > 12 > 8; 24, 32 = 16)
+#endif
 #ifndef MRB200_S2D_STAGES
 #define MRB200_S2D_STAGES 2  // deeper rings measured slower inside the CUDA graph
 #endif
@@ -1388,11 +1391,11 @@ void launch_input_convert(const float* x, int N, int C, int H, int W, void* out,
     const FastDiv fd = make_fastdiv(static_cast<uint32_t>(W / 4));
     const int rows = N * 2 * L.Hq;
     if (fmt == FMT_BF16) {
-      pdl_launch(k_input_s2d_ct<3, 3, 8, true, false>, std::min(rows, sms2 * 8), 128, kS2dStages * 2 * C * W * sizeof(float), s, x,
+      pdl_launch(k_input_s2d_ct<3, 3, 8, true, false>, std::min(rows, sms2 * MRB200_S2D_BPS), 128, kS2dStages * 2 * C * W * sizeof(float), s, x,
                  N, H, W, out, L, pre_mul, q, fd);
       return;
     }
-    pdl_launch(q.ovf ? k_input_s2d_ct<3, 3, 16, true, true> : k_input_s2d_ct<3, 3, 16, true, false>, std::min(rows, sms2 * 8), 128, kS2dStages * 2 * C * W * sizeof(float), s,
+    pdl_launch(q.ovf ? k_input_s2d_ct<3, 3, 16, true, true> : k_input_s2d_ct<3, 3, 16, true, false>, std::min(rows, sms2 * MRB200_S2D_BPS), 128, kS2dStages * 2 * C * W * sizeof(float), s,
                x, N, H, W, out, L, pre_mul, q, fd);
     return;
   }
