@@ -1084,6 +1084,51 @@ __global__ void __launch_bounds__(256) k_sum_hw_warp(const float* __restrict__ x
   }
 }
 
+// Same sum, one warp per (image, 32-channel group = 8 granules): the warp stages
+// the 8 granule planes (HW <= 64 pixels of 16 B each) in shared memory with all
+// lanes loading (12-16 independent 16-byte loads per lane for 7x7), then every
+// lane runs one channel's sequential seeded sum in (h, w) order.  Granule plane
+// stride S = 1 (mod 8) float4 puts the 8 granules of one pixel on distinct banks.
+constexpr int kSumWarps = 4;
+__global__ void __launch_bounds__(kSumWarps * 32) k_sum_hw_warp32(const float* __restrict__ x, Lay L, int N, int H,
+                                                                  int W, int C, float* __restrict__ y) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ float4 st[kSumWarps][8 * 65];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int HW = H * W, S = ((HW + 7) / 8) * 8 + 1, groups = C / 32;
+  const int64_t items = static_cast<int64_t>(N) * groups;
+  for (int64_t it = static_cast<int64_t>(blockIdx.x) * kSumWarps + warp; it < items;
+       it += static_cast<int64_t>(gridDim.x) * kSumWarps) {
+    const int n = static_cast<int>(it / groups), c0 = 32 * static_cast<int>(it - static_cast<int64_t>(n) * groups);
+    // all of the lane's loads are issued before the first shared-memory store
+    // (a rolled load->store loop would serialise ~13 L2/HBM round trips)
+    float4 v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int idx = lane + 32 * u;
+      if (idx < 8 * HW) {
+        const int g = idx / HW, p = idx - g * HW, h = p / W, w = p - h * W;
+        v[u] = __ldg(reinterpret_cast<const float4*>(x + lay_off(L, pad_pix(n, h, w, H, W), c0 + 4 * g)));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int idx = lane + 32 * u;
+      if (idx < 8 * HW) {
+        const int g = idx / HW;
+        st[warp][g * S + idx - g * HW] = v[u];
+      }
+    }
+    __syncwarp();
+    const float* col = reinterpret_cast<const float*>(st[warp] + (lane >> 2) * S) + (lane & 3);
+    float acc = col[0];
+    for (int p = 1; p < HW; ++p) acc = __fadd_rn(acc, col[4 * p]);
+    y[static_cast<int64_t>(n) * C + c0 + lane] = acc;
+    __syncwarp();
+  }
+}
+
 // ---- dense ----------------------------------------------------------------------------
 // Block = kDenseRows data rows x 256 outputs.  The rows get their prologue
 // (pre_mul, realize chain) once into shared memory; each thread owns one
@@ -1668,6 +1713,12 @@ void launch_maxpool(const void* x, int xfmt, const ConvGeom& g, const OutDev& ou
 
 void launch_sum_hw(const float* x, const Lay& L, int N, int H, int W, int C, float* y, cudaStream_t s) {
   if (H * W <= 64 && C % 4 == 0 && L.cpc >= 4 && L.cpc % 4 == 0 && L.kind == LAY_NORMAL && L.kb >= 16) {
+    if (C % 32 == 0) {
+      const int64_t items32 = static_cast<int64_t>(N) * (C / 32);
+      pdl_launch(k_sum_hw_warp32, static_cast<int>(std::min<int64_t>((items32 + kSumWarps - 1) / kSumWarps, 148 * 16)),
+                 kSumWarps * 32, 0, s, x, L, N, H, W, C, y);
+      return;
+    }
     const int64_t items = static_cast<int64_t>(N) * (C / 4);
     pdl_launch(k_sum_hw_warp, static_cast<int>(std::min<int64_t>((items + 7) / 8, 148 * 8)), 256, 0, s, x, L, N, H, W,
                C, y);
