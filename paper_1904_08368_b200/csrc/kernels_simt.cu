@@ -1749,7 +1749,14 @@ void launch_dense(const float* x, int N, int K, int Kp, const void* w, int M, in
     const bool big = mode == 2 && K >= 4096;
     const int R = mode == 0 ? R0 : big ? R2L : R2;
     dim3 g2(static_cast<unsigned>((M + 31) / 32), static_cast<unsigned>((N + R - 1) / R));
-    if (mode == 0) {
+    if (mode == 0 && Kp <= 512) {
+      // short K (the ResNet-18 head, K = 512): 512-element chunks keep all 8 warps
+      // busy, 8 rows per block double the grid (1024 blocks for 256 x 1000)
+      constexpr int RS = 8;
+      dim3 g3(static_cast<unsigned>((M + 31) / 32), static_cast<unsigned>((N + RS - 1) / RS));
+      auto k3 = cal ? k_dense_ks<0, RS, 512, true> : k_dense_ks<0, RS, 512, false>;
+      pdl_launch(k3, g3, 256, 0, s, x, N, K, Kp, w, M, pre_mul, quant, q, acc_scale, epi, out);
+    } else if (mode == 0) {
       auto k2 = cal ? k_dense_ks<0, R0, 1024, true> : k_dense_ks<0, R0, 1024, false>;
       pdl_launch(k2, g2, 256, 0, s, x, N, K, Kp, w, M, pre_mul, quant, q, acc_scale, epi, out);
     } else {
