@@ -1294,6 +1294,42 @@ __global__ void __launch_bounds__(256) k_dense_ks(const float* __restrict__ x, i
     // the DRAM round trips)
     __syncthreads();  // the previous chunk is consumed
     constexpr int kU = 8;
+    if (MODE == 0 && (K & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+      // int8 codes, K % 4 == 0: one 16-byte row load -> 4 codes -> one 4-byte
+      // shared store (the per-element index math dominated the head's issue slots)
+      const int kc4 = kc >> 2;
+      for (int base = threadIdx.x; base < R * kc4; base += kU * blockDim.x) {
+        float4 v[kU];
+        bool live[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int idx = base + u * blockDim.x;
+          const int r = idx / kc4, k = k0 + 4 * (idx - r * kc4);
+          live[u] = idx < R * kc4 && n0 + r < N && k < K;
+          v[u] = live[u] ? __ldg(reinterpret_cast<const float4*>(x + static_cast<int64_t>(n0 + r) * K + k))
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int idx = base + u * blockDim.x;
+          if (idx >= R * kc4) break;
+          const int r = idx / kc4, k4 = idx - r * kc4;
+          uint32_t packed = 0;
+          if (live[u]) {
+            const float e[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              float t = e[b];
+              if (pre_mul != 0.f) t = __fmul_rn(t, pre_mul);
+              const uint8_t code =
+                  static_cast<uint8_t>(static_cast<int8_t>(quant ? quant_code_t<CAL>(t, q) : static_cast<int32_t>(t)));
+              packed |= static_cast<uint32_t>(code) << (8 * b);
+            }
+          }
+          *reinterpret_cast<uint32_t*>(stage + r * kDkChunk + 4 * k4) = packed;
+        }
+      }
+    } else
     for (int base = threadIdx.x; base < R * kc; base += kU * blockDim.x) {
       float v[kU];
       bool live[kU];
