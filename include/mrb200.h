@@ -56,7 +56,11 @@ typedef enum mr_status {
   MR_ERR_UNSUPPORTED_GROUP = 100, /* a Primitive body with no kernel pattern */
   MR_ERR_CUDA = 101,
   MR_ERR_INVALID_ARGUMENT = 102,
-  MR_ERR_OUT_OF_MEMORY = 103
+  MR_ERR_OUT_OF_MEMORY = 103,
+  MR_ERR_INEXACT_INT8 = 104       /* an int8 contraction whose partial sums are not
+                                     proven below 2^24 quanta: the int32 tensor-core
+                                     sum could differ from interp()'s fp32 sum, so
+                                     mr_exec_set_weights refuses the weights */
 } mr_status;
 
 /* Element type, matching microrelay::BaseType (dtype.hpp:18-43). */
@@ -113,8 +117,11 @@ mr_status mr_exec_set_weights(mr_exec_t ex, int32_t n, const mr_tensor* weights)
 
 /* The interp(m, "main", args) replacement, device-resident: `inputs` are the
  * n_data_inputs leading @main args as DEVICE float32 NCHW buffers, `output`
- * a DEVICE buffer for @main's result.  Stream-ordered on `stream`
- * (a cudaStream_t; NULL = legacy default stream); does not synchronize. */
+ * a DEVICE buffer for @main's result, written by the final launch itself (no
+ * extra copy; one captured graph per (input, output) address set).
+ * Stream-ordered on `stream` (a cudaStream_t; NULL = legacy default stream);
+ * does not synchronize.  Every mr_exec_* call makes the executor's device
+ * current for its duration and restores the caller's device on return. */
 mr_status mr_exec_run(mr_exec_t ex, const mr_tensor* inputs, mr_tensor* output, void* stream);
 
 /* Same, end to end from HOST buffers: copies inputs H2D (pinned staging),

@@ -28,6 +28,8 @@ HEADER = os.path.join(os.path.dirname(_HERE), "include", "mrb200.h")
 MR_FLOAT_BF16 = 0
 MR_FLOAT_FP32_STRICT = 1
 MR_FLOAT = 2
+MR_ERR_UNSUPPORTED_GROUP = 100
+MR_ERR_INEXACT_INT8 = 104
 
 # every symbol include/mrb200.h declares
 EXPORTS = [

@@ -63,6 +63,8 @@ inline int epi_signature(const EpiDev& e, const OutDev& o) {
     return q.lo >= -2147483520.f && q.hi <= 2147483520.f && q.lo == q.lo && q.hi == q.hi;
   };
   if (o.side && o.side_fmt == FMT_I8 && !q_ok(o.side_q)) return SIG_ANY;
+  // the side-code fast paths scale by c1 > 0 (a realize site's 2^(b-s)/rho)
+  if (o.side && o.side_fmt == FMT_I8 && !(o.side_q.c1 > 0.f && std::isfinite(o.side_q.c1))) return SIG_ANY;
   if (e.n_ops == 1 && e.op[0] == E_BIAS && o.primary_fmt != FMT_I8) return SIG_BIAS;
   if (e.n_ops == 2 && e.op[0] == E_BIAS && e.op[1] == E_RELU && o.primary_fmt != FMT_I8) return SIG_BIAS_RELU;
   if (e.n_ops == 3 && e.op[0] == E_BIAS && e.op[1] == E_RELU && e.op[2] == E_REQ && o.primary_fmt == FMT_I8 &&
@@ -269,6 +271,17 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 #ifndef MRB200_P2_SATPACK
 #define MRB200_P2_SATPACK 1  // A/B: +0.6 % (saturating I2IP pack does the clip at 127)
 #endif
+#ifndef MRB200_MAGIC_RNI
+#define MRB200_MAGIC_RNI 1  // rint-to-int by the 1.5*2^23 add instead of a quarter-rate F2I (below)
+#endif
+// Round-to-nearest-even float -> integer without F2I (a conversion-pipe op at a
+// quarter of the FMA rate, the epilogues' bottleneck: ncu source view of the
+// layer-1 convs).  For |x| < 2^22, x + 1.5*2^23 rounds once, at integer
+// granularity, ties to even -- exactly rint(x) -- and its bit pattern is
+// 0x4B400000 + rint(x).  Larger |x| leave that exponent, so the pattern is
+// monotone in x outside the window: callers clamp the pattern, not the value.
+constexpr float kRniMagic = 12582912.0f;  // 1.5 * 2^23
+constexpr int32_t kRniBase = 0x4B400000;
 // 4 int32 -> 4 saturated int8 bytes (a in byte 0) with two I2IP
 __device__ __forceinline__ uint32_t pack4_sat_s8(int a, int b, int c, int d) {
   uint32_t hi, r;
@@ -333,9 +346,51 @@ __device__ __forceinline__ void epilogue_values(const TcArgs& a, const uint32_t*
   }
 }
 
+// Operands of a specialised epilogue that do not depend on the accumulator --
+// the bias (or b*c1) and the fp32 residual -- loaded BEFORE the chunk's TMEM load,
+// so their latency overlaps it (ncu: these loads were the epilogue's top stall).
+template <int SIG>
+__device__ __forceinline__ void epilogue_prefetch(const TcArgs& a, const RowDst& d, int c0, const float* s_vec,
+                                                  bool p2ok, int cl, float (&pb)[16], float (&pr)[16]) {
+  if constexpr (SIG != SIG_ANY) {
+    const float4* p;
+    if (SIG == SIG_BIAS_RELU_REQ && p2ok) p = reinterpret_cast<const float4*>(s_vec + kVecSlots * 256 + cl);
+    else if (a.vec_slot[0] >= 0) p = reinterpret_cast<const float4*>(s_vec + a.vec_slot[0] * 256 + cl);
+    else p = reinterpret_cast<const float4*>(a.epi.vec[0] + c0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float4 f = p[j];
+      pb[4 * j] = f.x; pb[4 * j + 1] = f.y; pb[4 * j + 2] = f.z; pb[4 * j + 3] = f.w;
+    }
+    if constexpr (SIG == SIG_BIAS_RES_RELU) {
+      const EpiDev& e = a.epi;
+      const Lay& L = e.res_lay[1];
+      if (e.res_fmt[1] == FMT_F32) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float4 f = *reinterpret_cast<const float4*>(static_cast<const char*>(e.res[1]) + gran_byte(L, d.pix, L.Pp, c0 + 4 * j));
+          pr[4 * j] = f.x; pr[4 * j + 1] = f.y; pr[4 * j + 2] = f.z; pr[4 * j + 3] = f.w;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const uint4 u = *reinterpret_cast<const uint4*>(static_cast<const char*>(e.res[1]) + gran_byte(L, d.pix, L.Pp, c0 + 8 * j));
+          const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            pr[8 * j + 2 * h] = __uint_as_float(w4[h] << 16);
+            pr[8 * j + 2 * h + 1] = __uint_as_float(w4[h] & 0xffff0000u);
+          }
+        }
+      }
+    }
+  }
+}
+
 template <int EB, int SIG, bool CAL>
 __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* raw, const RowDst& d, int c0,
-                                               const float* s_vec, bool p2ok, int cl) {
+                                               const float* s_vec, bool p2ok, int cl, const float (&pb)[16],
+                                               const float (&pr)[16]) {
   const OutDev& o = a.out;
   const int pf = o.primary_fmt;
   const int peb = pf == FMT_F32 ? 4 : pf == FMT_BF16 ? 2 : 1;  // 16-byte granules per 16 channels
@@ -436,19 +491,21 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
         // code = clip(rint(relu(acc*s + b) * c1)) == clamp(rni(fma(acc, s*c1, b*c1)), 0, hi):
         // acc*s and *c1 are exact (powers of two, |acc| < 2^24 by the exactness bound),
         // so the fma rounds once exactly where fadd did; relu/rint/clip become integer clamps
-        const float4* bp = reinterpret_cast<const float4*>(s_vec + kVecSlots * 256 + cl);
 #if MRB200_P2_SATPACK
         int32_t code_raw[16];
 #endif
-        float bb[16];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float4 f = bp[j];
-          bb[4 * j] = f.x; bb[4 * j + 1] = f.y; bb[4 * j + 2] = f.z; bb[4 * j + 3] = f.w;
-        }
+        const float (&bb)[16] = pb;  // b*c1 (epilogue_prefetch)
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const int r = __float2int_rn(__fmaf_rn(static_cast<float>(static_cast<int32_t>(raw[i])), a.p2_scale, bb[i]));
+          const float y = __fmaf_rn(static_cast<float>(static_cast<int32_t>(raw[i])), a.p2_scale, bb[i]);
+#if MRB200_MAGIC_RNI
+          // pattern clamp at rint == 0 (the relu; y is finite: |acc| <= 2^24 and b*c1
+          // checked finite), then the pack's saturation clips at 127; a pattern
+          // above the window (y >= 2^22) saturates there too
+          const int r = max(__float_as_int(__fadd_rn(y, kRniMagic)), kRniBase) - kRniBase;
+#else
+          const int r = __float2int_rn(y);
+#endif
 #if MRB200_P2_SATPACK
           code_raw[i] = r;
 #else
@@ -480,15 +537,11 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
         return;
       }
     }
-    float t[16];
-    vec16k(0, t);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = __fadd_rn(v[i], t[i]);
+    for (int i = 0; i < 16; ++i) v[i] = __fadd_rn(v[i], pb[i]);  // bias (epilogue_prefetch)
     if constexpr (SIG == SIG_BIAS_RES_RELU) {
-      float r[16];
-      res16(1, r);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = __fadd_rn(v[i], r[i]);
+      for (int i = 0; i < 16; ++i) v[i] = __fadd_rn(v[i], pr[i]);  // residual (epilogue_prefetch)
     }
     if constexpr (SIG == SIG_BIAS_RELU || SIG == SIG_BIAS_RELU_REQ || SIG == SIG_BIAS_RES_RELU) {
 #pragma unroll
@@ -580,7 +633,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // carve: [B resident or B stages][A stages][barriers]
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // (pointer arithmetic on smem_raw, not an integer round trip, so the compiler
+  // keeps the shared address space: LDS for the staged vectors, not generic LD)
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* smB = base;
   uint8_t* smA = smB + (a.resident_b ? a.b_res_bytes : a.b_stage_bytes * a.n_stages);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smA + a.a_stage_bytes * a.n_stages);
@@ -876,7 +931,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
               d.side_base = d.pix;
               d.side_pstride = sl.Pp;
             }
-            epilogue_chunk<EB, SIG, CAL>(a, mx, d, n_tile * a.bn + c, s_vec, p2ok, c);
+            float pb[16], pr[16];
+            epilogue_prefetch<SIG>(a, d, n_tile * a.bn + c, s_vec, p2ok, c, pb, pr);
+            epilogue_chunk<EB, SIG, CAL>(a, mx, d, n_tile * a.bn + c, s_vec, p2ok, c, pb, pr);
           }
         }
         goto epilogue_done;
@@ -1043,9 +1100,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         }
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
                                static_cast<uint32_t>((acc * a.sub + sb) * a.bn + c);
+        float pb[16], pr[16];
+        if (valid && !d.border) epilogue_prefetch<SIG>(a, d, n_tile * a.bn + c, s_vec, p2ok, c, pb, pr);
         uint32_t raw[16];
         tmem_ld16(taddr, raw);  // warp-collective: every lane executes it
-        if (valid && !(a.dbg & 1)) epilogue_chunk<EB, SIG, CAL>(a, raw, d, n_tile * a.bn + c, s_vec, p2ok, c);
+        if (valid && !(a.dbg & 1)) epilogue_chunk<EB, SIG, CAL>(a, raw, d, n_tile * a.bn + c, s_vec, p2ok, c, pb, pr);
       }
       tc_fence_before();
       __syncwarp();

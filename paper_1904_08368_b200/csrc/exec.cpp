@@ -136,12 +136,15 @@ struct Exec {
   std::vector<const float*> cur_inputs;  // one per data input (@main params 0 .. n_data_inputs-1)
   float* out_internal = nullptr;  // result buffer (NCHW float32)
   int out_alias_buf = -1;         // >= 0: out_internal is this arena buffer (row-major fp32 result)
+  float* out_redirect = nullptr;  // mr_exec_run: the final launch writes the caller's buffer
+  bool enforce_exact = true;      // int8 groups must prove the 2^24 bound (off for calibration trials)
   int64_t out_elems = 0;
   std::vector<int64_t> out_shape;
   // captured launch lists, one per input buffer address (the input pointer is
   // baked into the graph): the caller's buffer and the two pipeline stages
   struct GraphEnt {
     std::vector<const float*> in;
+    float* out;
     cudaGraph_t g;
     cudaGraphExec_t e;
   };
@@ -193,7 +196,31 @@ struct Exec {
     if (host_stage_out) cudaFreeHost(host_stage_out);
   }
 
-  void* ptr(int buf) const { return arena + bufs[buf].offset; }
+  void* ptr(int buf) const {
+    if (buf == out_alias_buf && out_redirect) return out_redirect;
+    return arena + bufs[buf].offset;
+  }
+  float* out_dst() const { return out_redirect ? out_redirect : out_internal; }
+};
+
+// Makes `dev` current for one API call and restores the caller's device: an
+// executor can be driven from any host thread whatever its current device.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) {
+      cudaError_t e = cudaSetDevice(dev);
+      if (e != cudaSuccess) throw Status{MR_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e)};
+    } else {
+      prev = -1;
+    }
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
 };
 
 namespace {
@@ -1025,7 +1052,7 @@ void build(Exec& ex) {
     int is4d = rv.shape.size() == 4 ? 1 : 0;
     float c2 = rr.has_q ? rr.q.c2 : 1.f;
     L.fn = [e, rbuf, fmt, lay, c2, N, C, H, W, is4d](cudaStream_t s) {
-      launch_to_nchw(e->ptr(rbuf), fmt, lay, c2, e->out_internal, N, C, H, W, is4d, s);
+      launch_to_nchw(e->ptr(rbuf), fmt, lay, c2, e->out_dst(), N, C, H, W, is4d, s);
     };
     ex.launches.push_back(L);
     ++B.launch_idx;
@@ -1157,6 +1184,9 @@ void prepare_weights(Exec& ex, cudaStream_t s) {
       os << (bound <= 16777216.0 ? "proven" : "unproven") << " (max partial sum <= " << static_cast<int64_t>(bound)
          << " quanta)";
       ex.group_exact[gi] = os.str();
+      if (bound > 16777216.0 && ex.enforce_exact)
+        fail(MR_ERR_INEXACT_INT8, "%" + g.name + ": int8 partial sums are not proven below 2^24 quanta (" +
+                                      os.str() + "); the int32 accumulation could differ from interp()'s fp32 sum");
     }
   }
 }
@@ -1231,7 +1261,7 @@ void run_launches(Exec& ex, cudaStream_t s) {
 
 cudaGraphExec_t ensure_graph(Exec& ex) {
   for (auto& g : ex.graphs)
-    if (g.in == ex.cur_inputs) return g.e;
+    if (g.in == ex.cur_inputs && g.out == ex.out_redirect) return g.e;
   if (ex.graphs.size() >= 4) {  // bounded cache: drop the oldest capture
     cudaGraphExecDestroy(ex.graphs.front().e);
     cudaGraphDestroy(ex.graphs.front().g);
@@ -1241,7 +1271,7 @@ cudaGraphExec_t ensure_graph(Exec& ex) {
   CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
   CK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
   run_launches(ex, cap);
-  Exec::GraphEnt ent{ex.cur_inputs, nullptr, nullptr};
+  Exec::GraphEnt ent{ex.cur_inputs, ex.out_redirect, nullptr, nullptr};
   cudaError_t ce = cudaStreamEndCapture(cap, &ent.g);
   cudaStreamDestroy(cap);
   if (ce != cudaSuccess) fail(MR_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
@@ -1346,9 +1376,10 @@ void load_weights(Exec& ex, int32_t n, const mr_tensor* w, cudaMemcpyKind kind) 
   make_describe(ex);
 }
 
-std::unique_ptr<Exec> make_exec(Program P, const mr_exec_options& o) {
+std::unique_ptr<Exec> make_exec(Program P, const mr_exec_options& o, bool enforce_exact = true) {
   auto ex = std::make_unique<Exec>();
   ex->opt = o;
+  ex->enforce_exact = enforce_exact;
   ex->P = std::move(P);
   if (ex->opt.n_data_inputs < 1) fail(MR_ERR_INVALID_ARGUMENT, "at least one data input");
   build(*ex);
@@ -1391,7 +1422,7 @@ mr_status mr_exec_create(const char* text, const mr_exec_options* opts, mr_exec_
   mr_exec_default_options(&o);
   if (opts) o = *opts;
   if (o.batch < 1) fail(MR_ERR_INVALID_ARGUMENT, "batch must be >= 1");
-  CK(cudaSetDevice(o.device));
+  DeviceGuard dg(o.device);
   Module m = parse_fused_module(text);
   *out = reinterpret_cast<mr_exec_t>(make_exec(lower_module(m, o.batch, o.n_data_inputs), o).release());
   API_END
@@ -1399,29 +1430,51 @@ mr_status mr_exec_create(const char* text, const mr_exec_options* opts, mr_exec_
 
 mr_status mr_exec_set_weights(mr_exec_t h, int32_t n, const mr_tensor* w) {
   API_BEGIN
+  if (!h) fail(MR_ERR_INVALID_ARGUMENT, "null executor");
   Exec& ex = *reinterpret_cast<Exec*>(h);
-  CK(cudaSetDevice(ex.opt.device));
+  DeviceGuard dg(ex.opt.device);
   load_weights(ex, n, w, cudaMemcpyHostToDevice);
   API_END
 }
 
-mr_status mr_exec_run(mr_exec_t h, const mr_tensor* inputs, mr_tensor* output, void* stream) {
-  API_BEGIN
-  Exec& ex = *reinterpret_cast<Exec*>(h);
-  if (!ex.weights_ready) fail(MR_ERR_INVALID_ARGUMENT, "mr_exec_set_weights first");
-  check_input(ex, inputs);
+// The caller's device output becomes the final launch's destination for one run.
+struct OutRedirect {
+  Exec& ex;
+  OutRedirect(Exec& e, void* p) : ex(e) { ex.out_redirect = static_cast<float*>(p); }
+  ~OutRedirect() { ex.out_redirect = nullptr; }
+};
+
+void check_device_output(const Exec& ex, const mr_tensor* output) {
   if (!output || !output->data) fail(MR_ERR_INVALID_ARGUMENT, "null output");
   if (numel(*output) != ex.out_elems) fail(MR_ERR_TYPE_MISMATCH, "output size mismatch");
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, output->data) != cudaSuccess ||
+      (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged) || a.device != ex.opt.device) {
+    cudaGetLastError();
+    fail(MR_ERR_INVALID_ARGUMENT, "output must be device memory on the executor's device");
+  }
+}
+
+mr_status mr_exec_run(mr_exec_t h, const mr_tensor* inputs, mr_tensor* output, void* stream) {
+  API_BEGIN
+  if (!h) fail(MR_ERR_INVALID_ARGUMENT, "null executor");
+  Exec& ex = *reinterpret_cast<Exec*>(h);
+  DeviceGuard dg(ex.opt.device);
+  if (!ex.weights_ready) fail(MR_ERR_INVALID_ARGUMENT, "mr_exec_set_weights first");
+  check_input(ex, inputs);
+  check_device_output(ex, output);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   set_inputs(ex, inputs);
+  OutRedirect r(ex, output->data);
   run_body(ex, s);
-  CK(cudaMemcpyAsync(output->data, ex.out_internal, static_cast<size_t>(ex.out_elems) * 4, cudaMemcpyDeviceToDevice, s));
   API_END
 }
 
 mr_status mr_exec_run_host(mr_exec_t h, const mr_tensor* inputs, mr_tensor* output, void* stream) {
   API_BEGIN
+  if (!h) fail(MR_ERR_INVALID_ARGUMENT, "null executor");
   Exec& ex = *reinterpret_cast<Exec*>(h);
+  DeviceGuard dg(ex.opt.device);
   check_input(ex, inputs);
   if (!output || !output->data) fail(MR_ERR_INVALID_ARGUMENT, "null output");
   if (numel(*output) != ex.out_elems) fail(MR_ERR_TYPE_MISMATCH, "output size mismatch");
@@ -1449,7 +1502,9 @@ mr_status mr_exec_run_host(mr_exec_t h, const mr_tensor* inputs, mr_tensor* outp
 
 mr_status mr_exec_submit_host(mr_exec_t h, const mr_tensor* inputs, mr_tensor* output, void* stream) {
   API_BEGIN
+  if (!h) fail(MR_ERR_INVALID_ARGUMENT, "null executor");
   Exec& ex = *reinterpret_cast<Exec*>(h);
+  DeviceGuard dg(ex.opt.device);
   if (!ex.weights_ready) fail(MR_ERR_INVALID_ARGUMENT, "mr_exec_set_weights first");
   check_input(ex, inputs);
   if (!output || !output->data) fail(MR_ERR_INVALID_ARGUMENT, "null output");
@@ -1490,7 +1545,9 @@ mr_status mr_exec_submit_host(mr_exec_t h, const mr_tensor* inputs, mr_tensor* o
 
 mr_status mr_exec_sync(mr_exec_t h) {
   API_BEGIN
+  if (!h) fail(MR_ERR_INVALID_ARGUMENT, "null executor");
   Exec& ex = *reinterpret_cast<Exec*>(h);
+  DeviceGuard dg(ex.opt.device);
   if (!ex.pipe_fresh) {  // (the stream may be the legacy default stream, handle 0)
     if (ex.copy_stream) CK(cudaStreamSynchronize(ex.copy_stream));
     CK(cudaStreamSynchronize(ex.pipe_stream));
@@ -1519,35 +1576,63 @@ int32_t mr_exec_launch_count(mr_exec_t h) {
   return n;
 }
 
+namespace {
+struct EventList {  // RAII: the per-launch events are freed on every exit path
+  std::vector<cudaEvent_t> ev;
+  explicit EventList(size_t n) : ev(n, nullptr) {
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+  }
+  ~EventList() {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+};
+mr_status profile_impl(Exec& ex, const mr_tensor* inputs, mr_tensor* output, void* stream, float* ms, int32_t cap,
+                       int32_t* count) {
+  API_BEGIN
+  DeviceGuard dg(ex.opt.device);
+  if (!ex.weights_ready) fail(MR_ERR_INVALID_ARGUMENT, "mr_exec_set_weights first");
+  if (cap > 0 && !ms) fail(MR_ERR_INVALID_ARGUMENT, "null ms");
+  check_input(ex, inputs);
+  if (output && output->data) check_device_output(ex, output);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  set_inputs(ex, inputs);
+  OutRedirect r(ex, output ? output->data : nullptr);
+  EventList E(ex.launches.size() + 1);
+  CK(cudaEventRecord(E.ev[0], s));
+  for (size_t i = 0; i < ex.launches.size(); ++i) {
+    ex.launches[i].fn(s);
+    CK(cudaEventRecord(E.ev[i + 1], s));
+  }
+  CK(cudaEventSynchronize(E.ev.back()));
+  CK(cudaGetLastError());
+  int32_t n = 0;
+  for (size_t i = 0; i < ex.launches.size() && n < cap; ++i) CK(cudaEventElapsedTime(&ms[n++], E.ev[i], E.ev[i + 1]));
+  *count = n;
+  API_END
+}
+}  // namespace
+
 int32_t mr_exec_profile(mr_exec_t h, const mr_tensor* inputs, mr_tensor* output, void* stream, float* ms,
                         int32_t cap) {
-  try {
-    Exec& ex = *reinterpret_cast<Exec*>(h);
-    check_input(ex, inputs);
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    set_inputs(ex, inputs);
-    std::vector<cudaEvent_t> ev(ex.launches.size() + 1);
-    for (auto& e : ev) CK(cudaEventCreate(&e));
-    CK(cudaEventRecord(ev[0], s));
-    for (size_t i = 0; i < ex.launches.size(); ++i) {
-      ex.launches[i].fn(s);
-      CK(cudaEventRecord(ev[i + 1], s));
-    }
-    CK(cudaEventSynchronize(ev.back()));
-    CK(cudaGetLastError());
-    int32_t n = 0;
-    for (size_t i = 0; i < ex.launches.size() && n < cap; ++i) CK(cudaEventElapsedTime(&ms[n++], ev[i], ev[i + 1]));
-    for (auto& e : ev) cudaEventDestroy(e);
-    if (output && output->data)
-      CK(cudaMemcpyAsync(output->data, ex.out_internal, static_cast<size_t>(ex.out_elems) * 4, cudaMemcpyDeviceToDevice, s));
-    return n;
-  } catch (const Status& st) {
-    g_last_error = st.msg;
+  if (!h) {
+    g_last_error = "null executor";
     return -1;
   }
+  int32_t n = 0;
+  return profile_impl(*reinterpret_cast<Exec*>(h), inputs, output, stream, ms, cap, &n) == MR_OK ? n : -1;
 }
 
-void mr_exec_destroy(mr_exec_t h) { delete reinterpret_cast<Exec*>(h); }
+void mr_exec_destroy(mr_exec_t h) {
+  if (!h) return;
+  Exec* ex = reinterpret_cast<Exec*>(h);
+  try {
+    DeviceGuard dg(ex->opt.device);
+    delete ex;
+  } catch (...) {
+    delete ex;
+  }
+}
 
 const char* mr_last_error_message(void) { return g_last_error.c_str(); }
 
@@ -1579,7 +1664,7 @@ mr_status mr_calibrate(const char* text, const mr_exec_options* opts, int32_t n_
   mr_exec_default_options(&o);
   if (opts) o = *opts;
   o.use_cuda_graph = 0;
-  CK(cudaSetDevice(o.device));
+  DeviceGuard dg(o.device);
   const Program P0 = lower_module(parse_fused_module(text), o.batch, o.n_data_inputs);
   if (!P0.any_quant) fail(MR_ERR_INVALID_ARGUMENT, "module has no quantize sites");
   CK(cudaMalloc(&flag_mem.p, sizeof(int32_t)));
@@ -1593,7 +1678,7 @@ mr_status mr_calibrate(const char* text, const mr_exec_options* opts, int32_t n_
     g_calib_ovf = flag;  // every QDev of this trial reports overflow
     std::unique_ptr<Exec> ex;
     try {
-      ex = make_exec(std::move(P), o);
+      ex = make_exec(std::move(P), o, /*enforce_exact=*/false);  // overflow search only
       mr_exec_t h = reinterpret_cast<mr_exec_t>(ex.get());
       mr_status st = mr_exec_set_weights(h, n_weights, weights);  // weight sites
       if (st != MR_OK) throw Status{static_cast<int>(st), g_last_error};
@@ -1652,7 +1737,7 @@ mr_status mr_group_compile(const char* text, const char* group, const mr_exec_op
   g->n_operands = n_ops;
   Program gp = lower_module(gm.m, o.batch, g->n_data, &gm.coded);  // host-side errors before any device work
   gp.any_quant = gp.any_quant || gm.module_quant;  // same float format as inside the whole module
-  CK(cudaSetDevice(o.device));
+  DeviceGuard dg(o.device);
   mr_exec_options go = o;
   go.n_data_inputs = g->n_data;
   g->ex = make_exec(std::move(gp), go);
@@ -1682,7 +1767,7 @@ mr_status mr_group_launch(mr_group_t g, const mr_tensor* in, int32_t n_in, mr_te
     fail(MR_ERR_ARITY_MISMATCH, "function expects " + std::to_string(g->n_operands) + " arguments, got " +
                                     std::to_string(n_in));
   if (!in) fail(MR_ERR_INVALID_ARGUMENT, "null operands");
-  CK(cudaSetDevice(ex.opt.device));
+  DeviceGuard dg(ex.opt.device);
   std::vector<mr_tensor> ordered(g->perm.size());
   for (size_t k = 0; k < g->perm.size(); ++k) ordered[k] = in[g->perm[k]];
   std::vector<const void*> addrs;
@@ -1697,10 +1782,11 @@ mr_status mr_group_launch(mr_group_t g, const mr_tensor* in, int32_t n_in, mr_te
   check_input(ex, ordered.data());
   if (!out || !out->data) fail(MR_ERR_INVALID_ARGUMENT, "null output");
   if (numel(*out) != ex.out_elems) fail(MR_ERR_TYPE_MISMATCH, "output size mismatch");
+  check_device_output(ex, out);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   set_inputs(ex, ordered.data());
+  OutRedirect r(ex, out->data);
   run_body(ex, s);
-  CK(cudaMemcpyAsync(out->data, ex.out_internal, static_cast<size_t>(ex.out_elems) * 4, cudaMemcpyDeviceToDevice, s));
   API_END
 }
 
@@ -1708,7 +1794,15 @@ void mr_group_reload(mr_group_t g) {
   if (g) g->staged.clear();
 }
 
-void mr_group_destroy(mr_group_t g) { delete g; }
+void mr_group_destroy(mr_group_t g) {
+  if (!g) return;
+  try {
+    DeviceGuard dg(g->ex->opt.device);
+    delete g;
+  } catch (...) {
+    delete g;
+  }
+}
 
 const char* mr_build_info(void) { return MRB200_BUILD_INFO; }
 

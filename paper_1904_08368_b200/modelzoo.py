@@ -273,6 +273,59 @@ def make_inputs(src: ModelSource, batch: int, seed: int = 0) -> np.ndarray:
     return x
 
 
+def make_inputs_diverse(src: ModelSource, batch: int, seed: int = 0, start: int = 0, rows=None) -> np.ndarray:
+    """Synthetic images whose rows differ in kind, not just in noise, so that
+    batch-indexing or row-permutation bugs change the logits and the top-1
+    classes spread (U[0,1) images of a random-init net all share one arg-max).
+
+    Image i draws its own generator (seed, i), so row i is the same at every
+    batch size and any seeded subset of a large batch can be regenerated
+    alone.  Kind = i % 8: 0 U[0,1); 1 affine U[0,1)*s+o (signed); 2 N(0, sigma);
+    3 ramp along h or w plus noise; 4 checkerboard of random period/amplitude;
+    5 per-channel constant colour plus small noise; 6 per-channel sinusoid;
+    7 sparse bright blobs on zero (exercises the input clip).  DQN frames are
+    then mapped to integer pixels in [0, 255].  Rows start .. start+batch-1,
+    or the explicit global row indices `rows` (a seeded subset of a large batch)."""
+    rows = list(range(start, start + batch)) if rows is None else [int(r) for r in rows]
+    batch = len(rows)
+    c, h, w = src.input_shape
+    x = np.empty((batch, c, h, w), np.float32)
+    hh, ww = np.meshgrid(np.arange(h, dtype=np.float32), np.arange(w, dtype=np.float32), indexing="ij")
+    for j, i in enumerate(rows):
+        r = np.random.Generator(np.random.PCG64([seed, i]))
+        kind = i % 8
+        if kind == 0:
+            img = r.random((c, h, w), dtype=np.float32)
+        elif kind == 1:
+            img = r.random((c, h, w), dtype=np.float32) * r.uniform(0.2, 3.0) + r.uniform(-1.0, 1.0)
+        elif kind == 2:
+            img = r.standard_normal((c, h, w), dtype=np.float32) * r.uniform(0.3, 2.0)
+        elif kind == 3:
+            ramp = hh / h if r.random() < 0.5 else ww / w
+            img = ramp[None] * r.uniform(-2, 2, (c, 1, 1)) + 0.1 * r.standard_normal((c, h, w))
+        elif kind == 4:
+            p = int(r.integers(2, 17))
+            cb = ((hh // p + ww // p) % 2)[None]
+            img = cb * r.uniform(-2, 2, (c, 1, 1)) + r.uniform(-0.5, 0.5, (c, 1, 1))
+        elif kind == 5:
+            img = r.uniform(-1.5, 1.5, (c, 1, 1)) + 0.05 * r.standard_normal((c, h, w))
+        elif kind == 6:
+            f = r.uniform(0.02, 0.4, (c, 2))
+            ph = r.uniform(0, 6.3, (c, 1, 1))
+            img = np.sin(f[:, :1, None] * hh[None] + f[:, 1:, None] * ww[None] + ph) * r.uniform(0.5, 2.5)
+        else:
+            img = np.zeros((c, h, w), np.float32)
+            for _ in range(int(r.integers(3, 12))):
+                y0, x0 = int(r.integers(0, h)), int(r.integers(0, w))
+                rad = int(r.integers(2, max(3, h // 6)))
+                img[:, max(0, y0 - rad):y0 + rad, max(0, x0 - rad):x0 + rad] += r.uniform(-40, 40, (c, 1, 1))
+        x[j] = img
+    if src.name.startswith("dqn"):
+        lo, hi = x.min(axis=(1, 2, 3), keepdims=True), x.max(axis=(1, 2, 3), keepdims=True)
+        x = np.floor((x - lo) / np.maximum(hi - lo, 1e-6) * 255.999).astype(np.float32)
+    return x
+
+
 def bind_weights(src: ModelSource, weights: Dict[str, np.ndarray],
                  kinds=("conv_w", "dense_w", "bias", "dw_w")) -> ModelSource:
     """Model interchange: the same network with its

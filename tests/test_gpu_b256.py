@@ -1,0 +1,150 @@
+"""GPU parity at the benchmarked batch, against the
+REFERENCE on diverse inputs.
+
+The b2 goldens leave every tcgen05 conv with at most one tile per CTA; at
+batch 256 every CTA of the persistent conv kernel walks ~11 tiles, so the TMEM
+accumulator double buffer, the tfull/tempty phase flips and the A-ring wrap
+across tiles only run here.  Inputs are modelzoo.make_inputs_diverse (eight
+image kinds, signed, saturating), so rows differ and a row-permutation or
+batch-indexing bug changes bits.  References: tests/golden/*_div_*.npz,
+written by tests/golden/make_golden.py (`diverse`, `c5`) from oracle/_ref/mr_ref,
+the unmodified reference's interp(), one batch-1 call per image.
+
+Bars: int8 bit-exact on every row; fp32-strict bit-exact on every row; bf16
+(and tf32) normwise max|d|/max|ref| <= 1e-2 on the logits and top-1 agreement
+>= 99 % against the reference's fp32 rows, with the exact count printed.
+"""
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+import paper_1904_08368_b200 as mrb
+from paper_1904_08368_b200 import modelzoo
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+TOL = 1e-2
+TOP1 = 0.99
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+def gold(name):
+    return np.load(os.path.join(GOLD, name))
+
+
+def setup(name, prec, batch, **kw):
+    text, meta, src = mrb.load_model(name, prec)
+    w = modelzoo.make_weights(src, seed=meta["weights_seed"])
+    ex = mrb.Executor(text, batch=batch, **kw)
+    ex.set_weights([w[p.name] for p in src.params if p.kind != "input"])
+    return ex, src
+
+
+def inputs(src, g, batch, rows=None):
+    x = modelzoo.make_inputs_diverse(src, batch, seed=0, rows=rows)
+    assert hashlib.sha256(x.tobytes()).hexdigest() == str(g["x_sha256"]), "input generator drifted"
+    return x
+
+
+def diff_rows(y, r):
+    return [int(i) for i in np.nonzero(np.any(bits(y).reshape(len(y), -1) != bits(r).reshape(len(r), -1), 1))[0]]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,gname,batch", [("resnet18", "resnet18_div_b256.npz", 256),
+                                              ("mobilenet_v1", "mobilenet_v1_div_b256.npz", 256),
+                                              ("dqn_b256", "dqn_b256_div_b256.npz", 256),
+                                              ("resnet18_tiny", "resnet18_tiny_div_b64.npz", 64)])
+def test_int8_every_row_bitexact(gpu, name, gname, batch):
+    g = gold(gname)
+    ex, src = setup(name, "int8", batch)
+    x = inputs(src, g, batch)
+    y = ex.run_host(x)
+    bad = diff_rows(y, g["int8"])
+    print("%s int8 b%d: %d distinct reference top-1 classes, %d distinct rows; rows differing: %s"
+          % (name, batch, len(set(g["int8"].argmax(1).tolist())), len({r.tobytes() for r in g["int8"]}), bad[:8]))
+    assert not bad
+
+
+@pytest.mark.gpu
+def test_resnet18_int8_b256_every_group_proven_exact(gpu):
+    """The int32 tensor-core sum equals interp()'s fp32 sum only under the 2^24
+    bound; set_weights refuses an unproven group
+    (MR_ERR_INEXACT_INT8), and every quantized ResNet-18 group proves it."""
+    ex, _ = setup("resnet18", "int8", 256)
+    groups = [g for g in ex.describe()["groups"] if g["exact"]]
+    assert len(groups) >= 20
+    for g in groups:
+        assert g["exact"].startswith("proven"), (g["name"], g["exact"])
+
+
+@pytest.mark.gpu
+def test_tiny_int8_b64_simt_path_every_row(gpu):
+    g = gold("resnet18_tiny_div_b64.npz")
+    ex, src = setup("resnet18_tiny", "int8", 64, force_simt=True)
+    y = ex.run_host(inputs(src, g, 64))
+    assert not diff_rows(y, g["int8"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,gname,batch", [("resnet18", "resnet18_div_b256.npz", 256),
+                                              ("dqn_b256", "dqn_b256_div_b256.npz", 256),
+                                              ("resnet18_tiny", "resnet18_tiny_div_b64.npz", 64)])
+def test_fp32_strict_every_row_bitexact(gpu, name, gname, batch):
+    g = gold(gname)
+    ex, src = setup(name, "fp32", batch, float_mode=mrb.MR_FLOAT_FP32_STRICT)
+    y = ex.run_host(inputs(src, g, batch))
+    assert not diff_rows(y, g["fp32"])
+
+
+def float_check(name, gname, batch, mode):
+    g = gold(gname)
+    ex, src = setup(name, "fp32", batch, float_mode=mode)
+    y = ex.run_host(inputs(src, g, batch))
+    r = g["fp32"]
+    err = float(np.max(np.abs(y - r)) / np.max(np.abs(r)))
+    agree = int(np.sum(y.argmax(1) == r.argmax(1)))
+    return err, agree, len(set(r.argmax(1).tolist()))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,gname,batch", [("resnet18", "resnet18_div_b256.npz", 256),
+                                              ("mobilenet_v1", "mobilenet_v1_div_b256.npz", 256),
+                                              ("dqn_b256", "dqn_b256_div_b256.npz", 256)])
+def test_bf16_b256_against_reference_fp32(gpu, name, gname, batch):
+    err, agree, classes = float_check(name, gname, batch, mrb.MR_FLOAT_BF16)
+    print("%s bf16 b%d vs reference fp32: normwise %.5f, top-1 agreement %d/%d (%d distinct classes)"
+          % (name, batch, err, agree, batch, classes))
+    assert err <= TOL
+    assert agree >= TOP1 * batch
+
+
+@pytest.mark.gpu
+def test_c5_batch4096_seeded_subset_matches_reference(gpu):
+    """Config C5 on one GPU: ResNet-18 int8 at batch 4096 over diverse rows
+    0..4095; rows 0..255 and a seeded random subset of 256 rows (make_golden.py
+    c5_rows, seed 5) are bit-exact against the reference.  The per-GPU shard
+    sizes of the 2/4/8-GPU split (2048, 1024, 512 rows) reproduce their rows of
+    the batch-4096 result bit for bit (per-sample independence)."""
+    from paper_1904_08368_b200.shard import shard_range
+    _, _, src = mrb.load_model("resnet18", "int8")
+    x = modelzoo.make_inputs_diverse(src, 4096, seed=0)
+    big, _ = setup("resnet18", "int8", 4096)
+    y = big.run_host(x)
+    g0 = gold("resnet18_div_b256.npz")
+    assert not diff_rows(y[:256], g0["int8"])
+    sub = gold("resnet18_div_c5sub256.npz")
+    rows = sub["rows"]
+    assert hashlib.sha256(x[rows].tobytes()).hexdigest() == str(sub["x_sha256"])
+    assert not diff_rows(y[rows], sub["int8"])
+    del big
+    for world in (2, 4, 8):
+        a, b = shard_range(4096, world - 1, world)  # the last rank's shard
+        ex, _ = setup("resnet18", "int8", b - a)
+        ys = ex.run_host(np.ascontiguousarray(x[a:b]))
+        assert not diff_rows(ys, y[a:b]), world
+        del ex
