@@ -45,14 +45,15 @@
 
 #include "conv_tc.hpp"
 #include "launch.hpp"
+#include "tc_common.cuh"
 
 namespace mrb200 {
 
 namespace {
+using namespace tc;
 
 constexpr int kTileM = 128;
 constexpr int kEpiWarps = 16;
-constexpr int kThreadsTc = (2 + kEpiWarps) * 32;
 constexpr int kSmemBudget = 227 * 1024 - 1024;
 
 enum EpiSig : int { SIG_ANY = 0, SIG_BIAS = 1, SIG_BIAS_RELU = 2, SIG_BIAS_RELU_REQ = 3, SIG_BIAS_RES_RELU = 4 };
@@ -142,128 +143,7 @@ struct TcArgs {
   OutDev out;
 };
 
-// ---- PTX helpers -------------------------------------------------------------------
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(0x989680u)  // suspend-time hint: the warp sleeps until the phase flips
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::
-          "r"(smem_u32(dst)),
-      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
-                                            int c3) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
-      "[%2];" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-      : "memory");
-}
-
-// K-major UMMA shared-memory descriptor (sm_100 version 1): start>>4 [0,14),
-// LBO>>4 [16,30), SBO>>4 [32,46), version [46,48) = 1, base offset 0,
-// layout type [61,64) (0 none, 2 128B swizzle, 4 64B swizzle).  The high word
-// is per-kernel constant (TcArgs::desc_hi).
-__host__ __device__ __forceinline__ uint32_t umma_desc_hi(uint32_t sbo, uint32_t layout) {
-  return ((sbo >> 4) & 0x3FFF) | (1u << 14) | (layout << 29);
-}
-
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t hi) {
-  const uint32_t lo = ((saddr >> 4) & 0x3FFF) | (((lbo >> 4) & 0x3FFF) << 16);
-  return (static_cast<uint64_t>(hi) << 32) | lo;
-}
-
-template <int EB>
-__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
-  if constexpr (EB == 1) {
-    asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
-  } else {
-    asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
-  }
-}
-
-// Warp-collective forms: every lane executes them with warp-uniform operands
-// (kept in uniform registers), elect.sync picks the one issuing lane (always
-// the same lane, so the commit tracks the MMAs it issued).
-template <int EB>
-__device__ __forceinline__ void umma_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
-  if constexpr (EB == 1) {
-    asm volatile(
-        "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
-  } else {
-    asm volatile(
-        "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
-        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
-  }
-}
-
-__device__ __forceinline__ bool elect_one() {
-  uint32_t p;
-  asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\nselp.u32 %0, 1, 0, e;\n}\n" : "=r"(p));
-  return p != 0;
-}
-
-__device__ __forceinline__ void umma_commit_elect(uint64_t* bar) {
-  asm volatile(
-      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(smem_u32(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
+// ---- PTX helpers: tc_common.cuh ----------------------------------------------------
 
 #ifndef MRB200_SIDE_SATPACK
 #define MRB200_SIDE_SATPACK 1  // A/B: +1-1.8 % (side codes: rint, then the saturating pack clips)
@@ -628,8 +508,11 @@ __device__ __forceinline__ int tile_start(const TcArgs& a, int mt, int msub) {
 }
 __device__ __forceinline__ int tile_row0(const TcArgs& a, int mt, int msub) { return tile_start(a, mt, msub) + a.dmin; }
 
-template <int EB, int SIG, bool CAL>
-__global__ void __launch_bounds__(kThreadsTc, 1)
+// EPIW epilogue warps (a multiple of 4: one group per TMEM lane quarter).
+// (Measured: 12 warps with twice the registers, each keeping the next item's
+// residual loads in flight, made the residual convs 1.21-1.29x slower.)
+template <int EB, int SIG, bool CAL, int EPIW = kEpiWarps>
+__global__ void __launch_bounds__((2 + EPIW) * 32, 1)
     k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // carve: [B resident or B stages][A stages][barriers]
@@ -660,6 +543,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   const int n_tile = blockIdx.x % a.n_tiles;
   const int m_start = blockIdx.x / a.n_tiles;
   const int m_step = gridDim.x / a.n_tiles;
+  const int m_end = a.m_tiles;
   const int tcols = 2 * a.sub * a.bn;
   const uint32_t tmem_cols = tcols <= 32 ? 32 : tcols <= 64 ? 64 : tcols <= 128 ? 128 : tcols <= 256 ? 256 : 512;
 
@@ -670,7 +554,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], kEpiWarps);
+      mbar_init(&tempty[i], EPIW);
     }
     mbar_init(bfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -724,7 +608,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       const int row_bytes = a.kb == 16 ? 128 : a.kb;
       int stage = 0;
       uint32_t phase = 0;
-      for (int mt = m_start; mt < a.m_tiles; mt += m_step) {
+      for (int mt = m_start; mt < m_end; mt += m_step) {
         const int row0 = tile_row0(a, mt, msub);
         // no-swizzle (kb 16) maps move 8-pixel 128-byte rows; swizzled maps one pixel row
         const int r0 = a.kb == 16 ? floor_div8(row0) : row0;
@@ -972,7 +856,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);  // TMEM drained into shared memory
         if (stamp) a.stamps[si * 8 + 1] = clock64();
-        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(EPIW * 32) : "memory");
         if (stamp) a.stamps[si * 8 + 2] = clock64();
         // pooled row p: out (pw, 4 channels) = max over the valid window taps.
         // relu_last: every staged value is >= +0 and not NaN (relu is the
@@ -981,7 +865,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         // +0; otherwise the ordered, seeded form is evaluated.
         const OutDev& o = a.out;
         const int granules = a.bn / 4;
-        for (int it = threadIdx.x - 64; it < ((a.dbg & 1) ? 0 : a.pow * granules); it += kEpiWarps * 32) {
+        for (int it = threadIdx.x - 64; it < ((a.dbg & 1) ? 0 : a.pow * granules); it += EPIW * 32) {
           const int g4 = static_cast<int>(fdiv(static_cast<uint32_t>(it), a.fd_pow)), pw = it - g4 * a.pow;  // pixel-fastest: coalesced stores
           const int c0 = g4 * 4;
           const int x0 = pw * a.psw - a.ppw;
@@ -1043,7 +927,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           }
         }
         if (stamp) a.stamps[si * 8 + 3] = clock64();
-        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");  // staging free for the next band
+        asm volatile("bar.sync 1, %0;" ::"n"(EPIW * 32) : "memory");  // staging free for the next band
         if (stamp) a.stamps[si * 8 + 4] = clock64();
         if (++acc == 2) {
           acc = 0;
@@ -1051,60 +935,71 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         }
         continue;
       }
-      int cur_sb = -1;
-      RowDst d;
-      bool valid = false;
       // each warp of a lane quarter takes a contiguous run of items, so a
       // sub-tile's row decode is done once per warp
-      const int n_items = a.sub * chunks, per = (n_items + 3) >> 2;
-      const int it_end = min(n_items, (slice + 1) * per);
+      constexpr int kSlices = EPIW / 4;
+      const int n_items = a.sub * chunks, per = (n_items + kSlices - 1) / kSlices;
+      const int it_begin = slice * per, it_end = min(n_items, (slice + 1) * per);
       const int lgc = 31 - __clz(chunks);  // chunks = bn / 16 is a power of two
-      for (int item = slice * per; item < it_end; ++item) {
-        const int sb = item >> lgc;
-        const int c = (item & (chunks - 1)) * 16;
-        if (sb != cur_sb) {
-          cur_sb = sb;
-          const uint32_t q = static_cast<uint32_t>(mt * a.sub + sb) * kTileM + row;  // grids < 2^31 pixels
-          valid = q < static_cast<uint32_t>(a.Pg);
-          d.border = false;
-          d.pix = 0;
-          if (valid) {
-            const uint32_t t = fdiv(q, a.fd_wg);
-            const int x = static_cast<int>(q - t * static_cast<uint32_t>(a.Wg));
-            const uint32_t n32 = fdiv(t, a.fd_hg);
-            const int y = static_cast<int>(t - n32 * static_cast<uint32_t>(a.Hg));
-            const int n = static_cast<int>(n32);
-            if (a.out_mode == OUT_SAME) {
-              d.pix = q;
-              d.border = x == 0 || x == a.Wg - 1 || y == 0 || y == a.Hg - 1;
+      // where sub-tile sb's row of this lane lands (valid: a real output pixel)
+      auto decode = [&](int sb, RowDst& dd, bool& vv) {
+        const uint32_t q = static_cast<uint32_t>(mt * a.sub + sb) * kTileM + row;  // grids < 2^31 pixels
+        vv = q < static_cast<uint32_t>(a.Pg);
+        dd.border = false;
+        dd.pix = 0;
+        dd.side_base = 0;
+        dd.side_pstride = 0;
+        if (vv) {
+          const uint32_t t = fdiv(q, a.fd_wg);
+          const int x = static_cast<int>(q - t * static_cast<uint32_t>(a.Wg));
+          const uint32_t n32 = fdiv(t, a.fd_hg);
+          const int y = static_cast<int>(t - n32 * static_cast<uint32_t>(a.Hg));
+          const int n = static_cast<int>(n32);
+          if (a.out_mode == OUT_SAME) {
+            dd.pix = q;
+            dd.border = x == 0 || x == a.Wg - 1 || y == 0 || y == a.Hg - 1;
+          } else {
+            vv = y < a.OH && x < a.OW;
+            dd.pix = (static_cast<int64_t>(n) * (a.OH + 2 * kPad) + y + kPad) * (a.OW + 2 * kPad) + x + kPad;
+          }
+          if (a.out.side) {
+            if (sl.kind == LAY_PHASE) {
+              const uint32_t p32 = static_cast<uint32_t>(dd.pix);
+              const uint32_t tt = fdiv(p32, a.fd_swp);
+              const int wp = static_cast<int>(p32 - tt * static_cast<uint32_t>(sl.Wp));
+              const uint32_t nn = fdiv(tt, a.fd_shp);
+              const int hp = static_cast<int>(tt - nn * static_cast<uint32_t>(sl.Hp));
+              dd.side_base = static_cast<int64_t>((hp & 1) * 2 + (wp & 1)) * sl.Pp +
+                             (static_cast<int64_t>(nn) * sl.Hq + hp / 2) * sl.Wq + wp / 2;
+              dd.side_pstride = 4 * sl.Pp;
             } else {
-              valid = y < a.OH && x < a.OW;
-              d.pix = (static_cast<int64_t>(n) * (a.OH + 2 * kPad) + y + kPad) * (a.OW + 2 * kPad) + x + kPad;
-            }
-            if (a.out.side) {
-              if (sl.kind == LAY_PHASE) {
-                const uint32_t p32 = static_cast<uint32_t>(d.pix);
-                const uint32_t tt = fdiv(p32, a.fd_swp);
-                const int wp = static_cast<int>(p32 - tt * static_cast<uint32_t>(sl.Wp));
-                const uint32_t nn = fdiv(tt, a.fd_shp);
-                const int hp = static_cast<int>(tt - nn * static_cast<uint32_t>(sl.Hp));
-                d.side_base = static_cast<int64_t>((hp & 1) * 2 + (wp & 1)) * sl.Pp +
-                              (static_cast<int64_t>(nn) * sl.Hq + hp / 2) * sl.Wq + wp / 2;
-                d.side_pstride = 4 * sl.Pp;
-              } else {
-                d.side_base = d.pix;
-                d.side_pstride = sl.Pp;
-              }
+              dd.side_base = dd.pix;
+              dd.side_pstride = sl.Pp;
             }
           }
         }
-        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
-                               static_cast<uint32_t>((acc * a.sub + sb) * a.bn + c);
-        float pb[16], pr[16];
-        if (valid && !d.border) epilogue_prefetch<SIG>(a, d, n_tile * a.bn + c, s_vec, p2ok, c, pb, pr);
-        uint32_t raw[16];
-        tmem_ld16(taddr, raw);  // warp-collective: every lane executes it
-        if (valid && !(a.dbg & 1)) epilogue_chunk<EB, SIG, CAL>(a, raw, d, n_tile * a.bn + c, s_vec, p2ok, c, pb, pr);
+      };
+      auto taddr_of = [&](int sb, int c) {
+        return tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+               static_cast<uint32_t>((acc * a.sub + sb) * a.bn + c);
+      };
+      {
+        int cur_sb = -1;
+        RowDst d;
+        bool valid = false;
+        for (int item = it_begin; item < it_end; ++item) {
+          const int sb = item >> lgc;
+          const int c = (item & (chunks - 1)) * 16;
+          if (sb != cur_sb) {
+            cur_sb = sb;
+            decode(sb, d, valid);
+          }
+          float pb[16], pr[16];
+          if (valid && !d.border) epilogue_prefetch<SIG>(a, d, n_tile * a.bn + c, s_vec, p2ok, c, pb, pr);
+          uint32_t raw[16];
+          tmem_ld16(taddr_of(sb, c), raw);  // warp-collective: every lane executes it
+          if (valid && !(a.dbg & 1)) epilogue_chunk<EB, SIG, CAL>(a, raw, d, n_tile * a.bn + c, s_vec, p2ok, c, pb, pr);
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -1401,6 +1296,10 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
     return false;
   };
   if (a.win) {
+    // (Measured: computing only the 4 conv outputs (2p+a, 2q+b) per pooled pixel and
+    // taking the other 5 window taps from neighbours -- lane shuffles and a shared-
+    // memory ring of row maxima -- cut the MMAs to 4/9 but ran 0.170 vs 0.156 ms:
+    // the kernel is bound by its epilogue's issue rate, not by the tensor pipe.)
     found = sp.OC % 64 == 0 && try_cfg(64, 3, true);
   } else if (sp.pool) {
     // fused max_pool2d: one super-tile = the pkh conv rows of one pooled row,
@@ -1706,12 +1605,13 @@ bool tc_conv_launch(TcConvPlan* p, const void* x, const Lay& xl, const void* w, 
       a.p2_hi = static_cast<int32_t>(epi.q[2].hi);
     }
   }
-#define MRB_TC_LAUNCH(EB_, SIG_, CAL_)                                                                    \
+#define MRB_TC_LAUNCH_W(EB_, SIG_, CAL_, W_)                                                              \
   do {                                                                                                    \
-    cudaFuncSetAttribute(k_conv_tc<EB_, SIG_, CAL_>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
+    cudaFuncSetAttribute(k_conv_tc<EB_, SIG_, CAL_, W_>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
                          static_cast<int>(p->smem));                                                      \
-    pdl_launch(k_conv_tc<EB_, SIG_, CAL_>, p->grid, kThreadsTc, p->smem, s, p->tmA, p->tmB, a);           \
+    pdl_launch(k_conv_tc<EB_, SIG_, CAL_, W_>, p->grid, (2 + W_) * 32, p->smem, s, p->tmA, p->tmB, a);    \
   } while (0)
+#define MRB_TC_LAUNCH(EB_, SIG_, CAL_) MRB_TC_LAUNCH_W(EB_, SIG_, CAL_, kEpiWarps)
 #define MRB_TC_SIGS(EB_, CAL_)                                                  \
   switch (sig) {                                                                \
     case SIG_BIAS: MRB_TC_LAUNCH(EB_, SIG_BIAS, CAL_); break;                   \
@@ -1734,6 +1634,7 @@ bool tc_conv_launch(TcConvPlan* p, const void* x, const Lay& xl, const void* w, 
   }
 #undef MRB_TC_SIGS
 #undef MRB_TC_LAUNCH
+#undef MRB_TC_LAUNCH_W
   if ((dbg & 16) && a.pool) {
     cudaStreamCaptureStatus cs;
     cudaStreamIsCapturing(s, &cs);
@@ -1758,7 +1659,8 @@ const char* tc_conv_describe(const TcConvPlan* p, char* buf, int n) {
   static const char* kinds[] = {"s1", "s2-phase", "stem-s2d", "stem-pool"};
   std::snprintf(buf, n,
                 "tcgen05 %s %s %dx(M128)xN%d kb=%d taps=%d steps=%d grid=%dx%d rows=%dx%d pps=%d stages=%d B=%s ctas=%d smem=%zu",
-                p->spec.elem_bytes == 1 ? "i8" : "bf16", kinds[p->spec.kind], a.sub, a.bn, a.kb, p->spec.taps, a.n_steps,
+                p->spec.elem_bytes == 1 ? "i8" : "bf16",
+                kinds[p->spec.kind], a.sub, a.bn, a.kb, p->spec.taps, a.n_steps,
                 a.Hg, a.Wg, a.nbox, a.hbox, a.pps, a.n_stages,
                 a.resident_b ? "resident" : a.tap_groups > 1 ? "streamed-by-kernel-row" : "streamed", p->grid, p->smem);
   return buf;

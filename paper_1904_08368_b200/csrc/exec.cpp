@@ -21,6 +21,7 @@
 
 #include "../../include/mrb200.h"
 #include "conv_tc.hpp"
+#include "dense_tc.hpp"
 #include "kernels.cuh"
 #include "launch.hpp"
 #include "lower.hpp"
@@ -101,6 +102,7 @@ struct Buffer {
 struct LaunchRec {
   std::string name;   // group / conversion
   std::string kernel;
+  int kernels = 1;    // device kernels this record launches
   double bytes = 0;   // algorithmic HBM bytes
   double flops = 0;   // algorithmic ops (2 per MAC)
   std::function<void(cudaStream_t)> fn;
@@ -163,6 +165,7 @@ struct Exec {
   std::vector<int64_t> in_elems;
   std::string describe;
   std::vector<TcConvPlan*> tc_plans;
+  std::vector<DenseTcPlan*> group_dense;    // tcgen05 dense plan per group (nullptr: none)
 
   void drop_graphs() {
     for (auto& g : graphs) {
@@ -185,6 +188,7 @@ struct Exec {
     }
     if (fresh) cudaEventDestroy(fresh);
     for (auto* p : tc_plans) tc_conv_destroy(p);
+    for (auto* p : group_dense) if (p) dense_tc_destroy(p);
     if (arena) cudaFree(arena);
     for (void* p : param_dev) if (p) cudaFree(p);
     for (void* p : group_w) if (p) cudaFree(p);
@@ -226,13 +230,15 @@ struct DeviceGuard {
 namespace {
 
 enum Path { P_NONE = 0, P_CONV_I8_SIMT, P_CONV_I8_TC, P_CONV_BF16_SIMT, P_CONV_BF16_TC, P_CONV_F32, P_DENSE_I8,
-            P_DENSE_F32, P_DENSE_BF16, P_POOL, P_DW };
+            P_DENSE_F32, P_DENSE_BF16, P_POOL, P_DW, P_DENSE_I8_TC, P_DENSE_BF16_TC };
 
 const char* path_name(int p) {
   static const char* n[] = {"none", "conv_i8_simt", "conv_i8_tcgen05", "conv_bf16_simt", "conv_bf16_tcgen05",
-                            "conv_f32_strict", "dense_i8", "dense_f32_strict", "dense_bf16", "max_pool", "dwconv"};
+                            "conv_f32_strict", "dense_i8", "dense_f32_strict", "dense_bf16", "max_pool", "dwconv",
+                            "dense_i8_tcgen05", "dense_bf16_tcgen05"};
   return n[p];
 }
+
 
 int float_fmt(const Exec& ex) {
   // int8 pipelines keep the float residual stream exact in float32; the
@@ -447,7 +453,15 @@ void plan(Exec& ex, bool use_tc) {
         }
         break;
       case GroupKind::Dense:
-        ex.group_path[gi] = g.weight.quant ? P_DENSE_I8 : ffmt == FMT_F32 ? P_DENSE_F32 : P_DENSE_BF16;
+      {
+        static const bool no_dense_tc = [] {  // A/B switch: the CUDA-core dense
+          const char* e = std::getenv("MRB200_NO_DENSE_TC");
+          return e && std::atoi(e);
+        }();
+        const bool tc = use_tc && !no_dense_tc;
+        ex.group_path[gi] = g.weight.quant ? (tc ? P_DENSE_I8_TC : P_DENSE_I8)
+                            : ffmt == FMT_F32 ? P_DENSE_F32 : (tc ? P_DENSE_BF16_TC : P_DENSE_BF16);
+      }
         break;
       case GroupKind::MaxPool: ex.group_path[gi] = P_POOL; break;
       case GroupKind::DwConv: ex.group_path[gi] = P_DW; break;
@@ -679,7 +693,7 @@ void build(Exec& ex) {
   // int8 exactness precondition: operand scales must be powers of two.
   for (size_t gi = 0; gi < P.groups.size(); ++gi) {
     int path = ex.group_path[gi];
-    if (path == P_CONV_I8_SIMT || path == P_CONV_I8_TC || path == P_DENSE_I8) {
+    if (path == P_CONV_I8_SIMT || path == P_CONV_I8_TC || path == P_DENSE_I8 || path == P_DENSE_I8_TC) {
       float sw = P.groups[gi].weight.q.c2;
       if (!is_pow2(io[gi].data_scale) || !is_pow2(sw))
         fail(MR_ERR_UNSUPPORTED_GROUP, "group %" + P.groups[gi].name + ": quantize scales are not powers of two");
@@ -936,6 +950,33 @@ void build(Exec& ex) {
         };
         break;
       }
+      case P_DENSE_I8_TC:
+      case P_DENSE_BF16_TC: {
+        DenseTcSpec ds{path == P_DENSE_I8_TC ? 1 : 2, static_cast<int>(g.in_shape[0]), static_cast<int>(g.in_shape[1]),
+                       static_cast<int>(g.out_shape[1])};
+        DenseTcPlan* dp = dense_tc_create(ds);
+        if (!dp) fail(MR_ERR_UNSUPPORTED_GROUP, "group %" + g.name + ": tcgen05 dense plan failed");
+        ex.group_dense.resize(P.groups.size(), nullptr);
+        ex.group_dense[gi] = dp;
+        char buf[256];
+        ex.group_note.resize(P.groups.size());
+        ex.group_note[gi] = dense_tc_describe(dp, buf, sizeof(buf));
+        const int opbuf = B.scratch(dense_tc_operand_bytes(dp), "%" + g.name + ":operand");
+        const int64_t wsb = dense_tc_workspace_bytes(dp);
+        const int wsbuf = wsb ? B.scratch(wsb, "%" + g.name + ":splitk") : -1;
+        L.kernels = dense_tc_launches(dp);
+        float pre = g.data.pre_mul;
+        int quant = g.data.quant || gio.requant_data ? 1 : 0;
+        QDev q = to_qdev(g.data.quant ? g.data.q : gio.requant_q);
+        std::string gname = g.name;
+        L.fn = [e, gidx, dbuf, dp, opbuf, wsbuf, pre, quant, q, acc_scale, outdev, epidev, gname](cudaStream_t s) {
+          EpiDev d = epidev();
+          if (!dense_tc_launch(dp, static_cast<const float*>(e->ptr(dbuf)), pre, quant, q, e->ptr(opbuf),
+                               e->group_w[gidx], wsbuf >= 0 ? e->ptr(wsbuf) : nullptr, acc_scale, d, outdev(), s))
+            fail(MR_ERR_CUDA, "group %" + gname + ": TMA descriptor encoding failed");
+        };
+        break;
+      }
       case P_DENSE_I8:
       case P_DENSE_F32:
       case P_DENSE_BF16: {
@@ -1143,11 +1184,19 @@ void prepare_weights(Exec& ex, cudaStream_t s) {
     } else {
       n = static_cast<int64_t>(O) * KH * KW * cs;
     }
-    const bool dense_t = g.kind == GroupKind::Dense && fmt != FMT_F32;  // transposed k_dense layouts
+    const DenseTcPlan* dtc = gi < ex.group_dense.size() ? ex.group_dense[gi] : nullptr;
+    const bool dense_t = g.kind == GroupKind::Dense && fmt != FMT_F32 && !dtc;  // transposed k_dense layouts
     if (dense_t) n = static_cast<int64_t>(O) * cs;
+    if (dtc) {  // tcgen05 dense: K-major rows [Mpad][Kp]
+      cs = dense_tc_kp(I, static_cast<int>(elem_bytes(fmt)));
+      n = dense_tc_weight_rows(dtc) * cs;
+    }
     void* dst = nullptr;
     CK(cudaMalloc(&dst, static_cast<size_t>(n * elem_bytes(fmt))));
-    if (dense_t)
+    if (dtc)
+      dense_tc_prep_weight(dtc, raw, static_cast<const float*>(ex.group_vecs[gi][0]), w.scalar_scale,
+                           w.quant ? 1 : 0, to_qdev(w.q), dst, s);
+    else if (dense_t)
       launch_dense_weight_t(raw, O, I, cs, static_cast<const float*>(ex.group_vecs[gi][0]), w.scalar_scale, fmt,
                             w.quant ? 1 : 0, to_qdev(w.q), dst, s);
     else
@@ -1172,7 +1221,8 @@ void prepare_weights(Exec& ex, cudaStream_t s) {
       std::vector<int64_t> sums(O, 0);
       int64_t per = n / O, worst = 0;
       for (int64_t k = 0; k < n; ++k) {
-        int o = dense_t ? static_cast<int>((k / 4) % O)
+        if (dtc && k / cs >= O) break;  // zero padding rows
+        int o = dtc ? static_cast<int>(k / cs) : dense_t ? static_cast<int>((k / 4) % O)
                 : wl != WL_ROWS ? static_cast<int>((k / ex.group_tc[gi].kb) % O) : static_cast<int>(k / per);
         sums[o] += std::abs(static_cast<int>(codes[k]));
       }
@@ -1232,7 +1282,8 @@ void make_describe(Exec& ex) {
   for (size_t i = 0; i < ex.launches.size(); ++i) {
     const LaunchRec& L = ex.launches[i];
     os << (i ? ", " : "") << "{\"name\": \"" << L.name << "\", \"kernel\": \"" << L.kernel
-       << "\", \"bytes\": " << static_cast<int64_t>(L.bytes) << ", \"flops\": " << static_cast<int64_t>(L.flops) << "}";
+       << "\", \"kernels\": " << L.kernels << ", \"bytes\": " << static_cast<int64_t>(L.bytes)
+       << ", \"flops\": " << static_cast<int64_t>(L.flops) << "}";
   }
   os << "], \"buffers\": [";
   for (size_t i = 0; i < ex.bufs.size(); ++i) {
@@ -1572,7 +1623,7 @@ const char* mr_exec_describe(mr_exec_t h) { return reinterpret_cast<Exec*>(h)->d
 int32_t mr_exec_launch_count(mr_exec_t h) {
   Exec& ex = *reinterpret_cast<Exec*>(h);
   int32_t n = 0;
-  for (const auto& L : ex.launches) n += L.fn ? 1 : 0;
+  for (const auto& L : ex.launches) n += L.fn ? L.kernels : 0;
   return n;
 }
 
