@@ -52,9 +52,14 @@ CONFIGS = {
     # modules only (tests/side_bench.py); the int8 DQN reuses dqn's calibrated k
     "vgg16_b256": (modelzoo.vgg16, dict(batch=256)),
     "dqn_b256": (modelzoo.dqn, dict(batch=256)),
+    # the reference's combine-conv pass on a net with parallel
+    # same-geometry convs (concat-weight conv + the Opaque split group in the output)
+    "branchy": (modelzoo.branchy, {}),
 }
 K_FROM = {"dqn_b256": "dqn"}
-BIND = {"resnet18_small_const"}
+BIND = {"resnet18_small_const", "branchy"}
+# pass lists with combine-conv before fuse (and before quantize for int8)
+COMBINE = {"branchy"}
 # float-only (BASELINE lists them as bf16 configs; an int8 calibration sweep of
 # the 224x224 VGG-16 in the reference interpreter takes about an hour)
 NO_INT8 = {"vgg16", "vgg16_b256"}
@@ -75,8 +80,10 @@ def build(name: str, out_dir: str) -> dict:
     else:
         k = None if name in NO_INT8 else ref.calibrate(src.text, PRE, [x] + ref.weight_list(src, w))
     t_cal = time.time() - t0
-    fused_fp32 = ref.compile(src.text, FP32, 0)
-    fused_int8 = None if k is None else ref.compile(src.text, INT8, k)
+    fp32_passes = FP32.replace(",fuse", ",combine-conv,fuse") if name in COMBINE else FP32
+    int8_passes = INT8.replace(",quantize", ",combine-conv,quantize") if name in COMBINE else INT8
+    fused_fp32 = ref.compile(src.text, fp32_passes, 0)
+    fused_int8 = None if k is None else ref.compile(src.text, int8_passes, k)
     open(os.path.join(out_dir, name + ".src.rly"), "w").write(src.text)
     open(os.path.join(out_dir, name + "_fp32.fused.rly"), "w").write(fused_fp32)
     if fused_int8 is not None:
@@ -90,7 +97,7 @@ def build(name: str, out_dir: str) -> dict:
         "calibration": None if k is None else (
             {"k": k, "scale": 2.0 ** k, "k_from": K_FROM[name]} if name in K_FROM else
             {"inputs_seed": 0, "images": batch, "k": k, "scale": 2.0 ** k, "seconds": round(t_cal, 1), "pre_passes": PRE}),
-        "passes": {"fp32": FP32, "int8": None if k is None else INT8},
+        "passes": {"fp32": fp32_passes, "int8": None if k is None else int8_passes},
         "groups": {"fp32": fused_fp32.count("[Primitive=true]"),
                    "int8": None if fused_int8 is None else fused_int8.count("[Primitive=true]")},
     }

@@ -554,7 +554,8 @@ GroupIO resolve_inputs(Exec& ex, int gi) {
   }
   io.res_rep.assign(g.epi.size(), -1);
   for (size_t i = 0; i < g.epi.size(); ++i)
-    if (g.epi[i].kind == EpiKind::Residual) io.res_rep[i] = want_rep(ex, g.epi[i].value, ffmt, nullptr);
+    if (g.epi[i].kind == EpiKind::Residual)  // 2-D values (dense outputs) stay row-major float32
+      io.res_rep[i] = want_rep(ex, g.epi[i].value, P.values[g.epi[i].value].shape.size() == 2 ? FMT_F32 : ffmt, nullptr);
   return io;
 }
 
@@ -969,8 +970,10 @@ void build(Exec& ex) {
         int quant = g.data.quant || gio.requant_data ? 1 : 0;
         QDev q = to_qdev(g.data.quant ? g.data.q : gio.requant_q);
         std::string gname = g.name;
-        L.fn = [e, gidx, dbuf, dp, opbuf, wsbuf, pre, quant, q, acc_scale, outdev, epidev, gname](cudaStream_t s) {
+        L.fn = [e, gidx, dbuf, dp, opbuf, wsbuf, pre, quant, q, acc_scale, outdev, epidev, residual_fix,
+                gname](cudaStream_t s) {
           EpiDev d = epidev();
+          residual_fix(d);
           if (!dense_tc_launch(dp, static_cast<const float*>(e->ptr(dbuf)), pre, quant, q, e->ptr(opbuf),
                                e->group_w[gidx], wsbuf >= 0 ? e->ptr(wsbuf) : nullptr, acc_scale, d, outdev(), s))
             fail(MR_ERR_CUDA, "group %" + gname + ": TMA descriptor encoding failed");
@@ -986,8 +989,9 @@ void build(Exec& ex) {
         float pre = g.data.pre_mul;
         int quant = g.data.quant || gio.requant_data ? 1 : 0;
         QDev q = to_qdev(g.data.quant ? g.data.q : gio.requant_q);
-        L.fn = [e, gidx, dbuf, N, K, M, mode, pre, quant, q, acc_scale, outdev, epidev](cudaStream_t s) {
+        L.fn = [e, gidx, dbuf, N, K, M, mode, pre, quant, q, acc_scale, outdev, epidev, residual_fix](cudaStream_t s) {
           EpiDev d = epidev();
+          residual_fix(d);
           launch_dense(static_cast<const float*>(e->ptr(dbuf)), N, K, e->group_kp[gidx], e->group_w[gidx], M, mode,
                        pre, quant, q, acc_scale, d, outdev(), s);
         };

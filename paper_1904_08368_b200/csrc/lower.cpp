@@ -127,8 +127,20 @@ bool is_transpose(const ExprP& e, std::initializer_list<int64_t> perm) {
 
 }  // namespace
 
-Program lower_module(const Module& m, int64_t batch, int n_data_inputs,
+Program lower_module(const Module& m0, int64_t batch, int n_data_inputs,
                      const std::map<std::string, QParams>* coded_inputs) {
+  // combine-conv's weight tuples / split groups -> plain conv groups (combine.cpp)
+  Module m = m0;
+  m.body = std::make_shared<Block>(*m0.body);
+  for (const auto& [n, v] : m.body->lets)
+    if (v->kind == Expr::Tuple || v->kind == Expr::Proj) {
+      try {
+        normalize_combined(m);
+      } catch (const ParseError& e) {
+        bad(MR_ERR_UNSUPPORTED_GROUP, e.msg);
+      }
+      break;
+    }
   Program P;
   std::map<std::string, int> value_of;
   auto add_value = [&](const std::string& name) {

@@ -77,6 +77,22 @@ class Lexer {
         t.kind = c == '%' ? Tok::Local : Tok::Global;
         t.text = ident();
         if (t.text.empty()) fail("expected a name after sigil");
+        // a tuple projection %t.k (printer.cpp): the name, then '.' and the field
+        const size_t dot = t.text.find('.');
+        if (t.kind == Tok::Local && dot != std::string::npos && dot + 1 < t.text.size() &&
+            t.text.find_first_not_of("0123456789", dot + 1) == std::string::npos) {
+          Tok dt = t, ft = t;
+          t.text = t.text.substr(0, dot);
+          out.push_back(t);
+          dt.kind = Tok::Punct;
+          dt.text = ".";
+          out.push_back(dt);
+          ft.kind = Tok::Int;
+          ft.text = ft.text.substr(dot + 1);
+          ft.ival = std::strtoll(ft.text.c_str(), nullptr, 10);
+          out.push_back(ft);
+          continue;
+        }
       } else if (std::isalpha(static_cast<unsigned char>(c)) || c == '_') {
         t.kind = Tok::Ident;
         t.text = ident();
@@ -467,10 +483,30 @@ class Parser {
       e->lit = pool_[i.ival];
       return e;
     }
+    if (is("(")) {  // tuple literal (combine-conv's weight tuples)
+      next();
+      e->kind = Expr::Tuple;
+      while (!is(")")) {
+        e->args.push_back(expr());
+        if (is(",")) next();
+      }
+      expect(")");
+      return e;
+    }
     Tok head = next();
     if (head.kind == Tok::Local && !is("(")) {
       e->kind = Expr::Var;
       e->name = head.text;
+      if (is(".")) {  // tuple projection %t.k
+        next();
+        Tok k = next();
+        if (k.kind != Tok::Int) fail("tuple field index");
+        auto pr = std::make_shared<Expr>();
+        pr->kind = Expr::Proj;
+        pr->index = k.ival;
+        pr->args.push_back(e);
+        return pr;
+      }
       return e;
     }
     if (head.kind != Tok::Ident && head.kind != Tok::Local)

@@ -61,7 +61,10 @@ struct Block {
 };
 
 struct Expr {
-  enum Kind { Var, Const, Call, Fn } kind = Var;
+  // Tuple / Proj: the combine-conv pass's weight tuples and split projections
+  // (rewrites.cpp:365-385), resolved away by normalize_combined (combine.cpp)
+  enum Kind { Var, Const, Call, Fn, Tuple, Proj } kind = Var;
+  int64_t index = 0;           // Proj: tuple field
   std::string name;            // Var: variable; Call: operator name or callee var
   bool callee_is_var = false;  // Call of a let-bound function (%fusedN(...))
   std::vector<ExprP> args;
@@ -89,6 +92,15 @@ struct ParseError {
 };
 
 Module parse_fused_module(const std::string& text);
+
+// combine-conv (rewrites.cpp:276-401) output -> the module FuseOps would have
+// produced without the Opaque split: one conv group per concatenated weight,
+// with the consumers' leading elementwise ops (and a residual add) fused back
+// into the slice convs.  Bit-identical: every output channel of the combined
+// conv is computed independently, and the moved ops keep their order.
+// Returns the number of combined convs resolved; throws ParseError on a
+// combine pattern it cannot resolve.
+int normalize_combined(Module& m);
 
 // Attribute helpers.
 int64_t attr_int(const AttrMap& a, const std::string& k, int64_t dflt);

@@ -244,6 +244,47 @@ def dqn(num_actions: int = 18, seed: int = 1, batch: int = 1) -> ModelSource:
 MODELS = {"resnet18": resnet18, "mobilenet_v1": mobilenet_v1, "vgg16": vgg16, "dqn": dqn}
 
 
+def branchy(image: int = 32, num_classes: int = 10, seed: int = 1, width: int = 32) -> ModelSource:
+    """A small Inception-style net whose blocks hold PARALLEL convs over one
+    input with the same in-channels, kernel and attributes -- the pattern the
+    reference's combine-conv pass (rewrites.cpp:276-401) merges into one conv
+    over concatenated weights + a split:
+      stem 3x3 -> {1x1 a, 1x1 b, 1x1 c (half width)} -> 3x3 on a and b -> add
+      -> {3x3 p, 3x3 r} -> add -> relu -> global sums -> two dense heads -> add.
+    combine-conv only merges convs that bind back to back (none of them used
+    before the last one binds, rewrites.cpp:306-323) and whose weights have a
+    known shape (let-bound constants: use bind_weights), so the parallel convs
+    are emitted first and carry no folded batch-norm."""
+    b = _Builder(seed)
+    x = b.param("x", ("?n", 3, image, image), "input")
+    y = b.conv_bn(x, 3, width, 3, 1, 1, "stem")
+
+    def parallel(src, specs):
+        convs = []
+        for tag, cout, k, pad in specs:  # the convs bind back to back
+            w = b.param("w_" + tag, (cout, width, k, k), "conv_w")
+            convs.append(b.let("conv2d(%s, %s, strides=(1, 1), padding=(%d, %d))" % (src, w, pad, pad)))
+        outs = []
+        for (tag, cout, k, pad), cv in zip(specs, convs):
+            bb = b.param("b_" + tag, (cout,), "bias")
+            outs.append(b.let("bias_add(%s, %s)" % (cv, bb)))
+        return outs
+
+    a, c, d = parallel(y, [("b1a", width, 1, 0), ("b1b", width, 1, 0), ("b1c", width // 2, 1, 0)])
+    a, c, d = (b.let("relu(%s)" % v) for v in (a, c, d))
+    a = b.conv_bn(a, width, width, 3, 1, 1, "b1a2", relu=False)
+    c = b.conv_bn(c, width, width, 3, 1, 1, "b1b2", relu=False)
+    z = b.let("relu(%s)" % b.let("add(%s, %s)" % (a, c)))
+    p, r = parallel(z, [("b2p", width, 3, 1), ("b2r", width, 3, 1)])
+    z = b.let("relu(%s)" % b.let("add(%s, %s)" % (p, r)))
+    g = b.let("sum(%s, axis=(2, 3))" % z)
+    g = b.let("multiply(%s, const %s)" % (g, fmt_f32(1.0 / (image * image))))
+    gd = b.let("sum(%s, axis=(2, 3))" % d)
+    gd = b.let("multiply(%s, const %s)" % (gd, fmt_f32(1.0 / (image * image))))
+    h = b.let("add(%s, %s)" % (b.dense(g, width, num_classes, "fc"), b.dense(gd, width // 2, num_classes, "fcd")))
+    return b.finish("branchy", h, (3, image, image), num_classes)
+
+
 def make_weights(src: ModelSource, seed: int = 1) -> Dict[str, np.ndarray]:
     """Seeded random-init weights for every non-input parameter (host fp32)."""
     rng = np.random.Generator(np.random.PCG64(seed + 1000))

@@ -40,7 +40,7 @@ def make(name, batch):
         res[prec] = r.out
         res[prec + "_seconds"] = np.asarray(r.seconds)
     res["x_sha256"] = np.asarray(sha(x))
-    res["w_sha256"] = np.asarray(sha(np.concatenate([v.ravel() for v in w.values()])))
+    res["w_sha256"] = np.asarray(sha(np.concatenate([v.ravel() for v in w.values()] or [np.zeros(0, np.float32)])))
     np.savez(os.path.join(OUT, "%s_b%d.npz" % (name, batch)), **res)
     print(name, batch, {k: v.shape for k, v in res.items()})
 
@@ -84,7 +84,7 @@ def make_diverse(name, batch, jobs=None, precs=("int8", "fp32"), rows=None, tag=
             res[prec] = r.out
             res[prec + "_seconds"] = np.asarray(r.seconds)
     res["x_sha256"] = np.asarray(sha(x))
-    res["w_sha256"] = np.asarray(sha(np.concatenate([v.ravel() for v in w.values()])))
+    res["w_sha256"] = np.asarray(sha(np.concatenate([v.ravel() for v in w.values()] or [np.zeros(0, np.float32)])))
     if rows is not None:
         res["rows"] = np.asarray(rows, np.int64)
     np.savez(os.path.join(OUT, tag or "%s_div_b%d.npz" % (name, batch)), **res)
@@ -94,8 +94,9 @@ def make_diverse(name, batch, jobs=None, precs=("int8", "fp32"), rows=None, tag=
 
 
 if __name__ == "__main__":
-    todo = {"resnet18_tiny": 4, "resnet18": 2, "mobilenet_v1": 2, "dqn": 2, "vgg16": 2, "resnet18_small_const": 4}
-    diverse = {"resnet18": 256, "mobilenet_v1": 256, "dqn_b256": 256, "resnet18_tiny": 64}
+    todo = {"resnet18_tiny": 4, "resnet18": 2, "mobilenet_v1": 2, "dqn": 2, "vgg16": 2, "resnet18_small_const": 4,
+            "branchy": 4}
+    diverse = {"resnet18": 256, "mobilenet_v1": 256, "dqn_b256": 256, "resnet18_tiny": 64, "branchy": 64}
     args = sys.argv[1:]
     if args and args[0] == "c5":  # ResNet-18 int8, seeded 256-row subset of the batch-4096 config
         make_diverse("resnet18", 256, precs=("int8",), rows=c5_rows(), tag="resnet18_div_c5sub256.npz")

@@ -137,8 +137,8 @@ def test_lower_layout_pass_module(prec):
 def test_combine_conv_is_identity_on_baseline_models():
     """the reference's combine-conv pass finds no
     same-geometry parallel conv2d pairs in the BASELINE models, so its output
-    lowers to the same groups as the plain pipeline (concat / split groups would
-    be rejected at compile time with MR_ERR_UNSUPPORTED_GROUP)."""
+    lowers to the same groups as the plain pipeline (the concat / split form it
+    produces where it does fire: test_combine_conv_concat_split_lowers)."""
     from oracle import ref
     if not ref.available():
         pytest.skip("oracle/_ref/mr_ref not built (needs /root/reference)")
@@ -149,6 +149,26 @@ def test_combine_conv_is_identity_on_baseline_models():
         comb = ref.compile(src.text, "fold-scale,fold,dce,combine-conv,fuse", 0)
         a, b = mrb.lower(plain, 2), mrb.lower(comb, 2)
         assert [g["desc"] for g in a["groups"]] == [g["desc"] for g in b["groups"]]
+
+
+@pytest.mark.parametrize("prec", ["int8", "fp32"])
+def test_combine_conv_concat_split_lowers(prec):
+    """SURVEY.md 8(f) rank 4, combine-conv where it fires (modelzoo.branchy:
+    three 1x1 convs and two 3x3 convs sharing inputs).  The reference's output
+    holds weight tuples, concat-weight conv groups, Opaque split groups and
+    projections, with the member convs' bias/relu left in the consumers
+    (rewrites.cpp:365-385, registry.cpp:695-696); the lowering slices each
+    combined conv per output-channel block and re-fuses the consumers' leading
+    elementwise ops, so no split / concat / tuple survives and every group is
+    an ordinary conv or dense with its epilogue (combine.cpp)."""
+    text, _, _ = mrb.load_model("branchy", prec)
+    assert "split(" in text and "concat(" in text  # the reference did combine
+    d = mrb.lower(text, 4)
+    descs = [g["desc"] for g in d["groups"]]
+    assert len(d["groups"]) == 10 and d["result_shape"] == [4, 10]
+    assert not any("split" in x or "concat" in x for x in descs)
+    assert sum(g["anchor"] == "conv2d" for g in d["groups"]) == 8  # stem + 3 + 2 slices + the two 3x3 consumers
+    assert any(x.endswith("bias -> add -> relu -> sum") for x in descs)  # the anchorless add group, re-fused
 
 
 @pytest.mark.parametrize("prec", ["int8", "fp32"])

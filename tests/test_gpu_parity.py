@@ -279,3 +279,21 @@ def test_ragged_batches_match_golden_rows(gpu, name, batch, gold_b, prec):
     y = ex.run_host(np.ascontiguousarray(x[:batch]))
     k = min(batch, gold_b)
     assert np.array_equal(bits(y[:k]), bits(gold[:k])), int(np.sum(bits(y[:k]) != bits(gold[:k])))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prec,fm", [("int8", 0), ("fp32", 1), ("fp32", 0)])
+@pytest.mark.parametrize("gold_name,batch,diverse", [("branchy_b4.npz", 4, False), ("branchy_div_b64.npz", 64, True)])
+def test_combine_conv_module_matches_reference(gpu, prec, fm, gold_name, batch, diverse):
+    """the reference's combine-conv output (concat-weight
+    convs + Opaque split groups, models/branchy_*.fused.rly) runs through the
+    executor with the combined convs sliced per output-channel block: int8 and
+    fp32-strict bit-exact, bf16 in tolerance, against reference-generated goldens."""
+    gold = np.load(os.path.join(GOLD, gold_name))[prec]
+    ex, src = setup("branchy", prec, batch, float_mode=fm)
+    x = modelzoo.make_inputs_diverse(src, batch, seed=0) if diverse else modelzoo.make_inputs(src, batch, seed=0)
+    y = ex.run_host(x)
+    if prec == "int8" or fm == mrb.MR_FLOAT_FP32_STRICT:
+        assert np.array_equal(bits(y), bits(gold)), int(np.sum(bits(y) != bits(gold)))
+    else:
+        assert normwise(y, gold) <= BF16_TOL
