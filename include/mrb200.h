@@ -81,8 +81,12 @@ typedef struct mr_tensor {
  * groups) without quantize chains. */
 typedef enum mr_float_mode {
   MR_FLOAT_BF16 = 0,        /* bf16 operands, fp32 accumulate (tcgen05 kind::f16) */
-  MR_FLOAT_FP32_STRICT = 1  /* fp32, reference accumulation order, no FMA:
+  MR_FLOAT_FP32_STRICT = 1, /* fp32, reference accumulation order, no FMA:
                                bit-exact with kernels.cpp, slow (for checking) */
+  MR_FLOAT_TF32 = 2         /* float32 activations; convs and dense on tcgen05
+                               kind::tf32 (fp32 accumulate); groups with no tf32
+                               formulation (3-channel stems, pooling, depthwise)
+                               run the strict fp32 kernels */
 } mr_float_mode;
 
 typedef struct mr_exec_options {

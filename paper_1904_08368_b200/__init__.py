@@ -27,6 +27,7 @@ HEADER = os.path.join(os.path.dirname(_HERE), "include", "mrb200.h")
 
 MR_FLOAT_BF16 = 0
 MR_FLOAT_FP32_STRICT = 1
+MR_FLOAT_TF32 = 2
 MR_FLOAT = 2
 MR_ERR_UNSUPPORTED_GROUP = 100
 MR_ERR_INEXACT_INT8 = 104
@@ -153,9 +154,9 @@ class Executor:
     fused_text   print_module output of run_pipeline(..., "fuse") (optionally
                  with "quantize"), i.e. models/*.fused.rly
     batch        binds @main's symbolic batch dim ?n
-    float_mode   MR_FLOAT_BF16 (default) or MR_FLOAT_FP32_STRICT for the
-                 float parts of the module; int8 realized groups are always
-                 bit-exact int8 x int8 -> int32
+    float_mode   MR_FLOAT_BF16 (default), MR_FLOAT_TF32 or MR_FLOAT_FP32_STRICT
+                 for the float parts of the module; int8 realized groups are
+                 always bit-exact int8 x int8 -> int32
     """
 
     def __init__(self, fused_text: str, batch: int = 1, device: int = 0, float_mode: int = MR_FLOAT_BF16,

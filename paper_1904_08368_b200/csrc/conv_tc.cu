@@ -274,7 +274,7 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
   const OutDev& o = a.out;
   const int pf = o.primary_fmt;
   const int peb = pf == FMT_F32 ? 4 : pf == FMT_BF16 ? 2 : 1;  // 16-byte granules per 16 channels
-  const int seb = o.side_fmt == FMT_BF16 ? 2 : 1;
+  const int seb = o.side_fmt == FMT_F32 ? 4 : o.side_fmt == FMT_BF16 ? 2 : 1;
   if (d.border) {
     for (int g = 0; g < peb; ++g) st16(o.primary, gran_byte(o.plan, d.pix, o.plan.Pp, c0 + g * 16 / peb), make_uint4(0, 0, 0, 0));
     if (o.side)
@@ -445,6 +445,10 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
          make_uint4(pack4_i8(code[0], code[1], code[2], code[3]), pack4_i8(code[4], code[5], code[6], code[7]),
                     pack4_i8(code[8], code[9], code[10], code[11]), pack4_i8(code[12], code[13], code[14], code[15])));
   } else if (pf == FMT_F32) {
+    if constexpr (EB == 4) {  // tf32 pipeline: store what the next tf32 MMA reads, rounded (not truncated)
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = f32_out(o, v[i]);
+    }
 #pragma unroll
     for (int j = 0; j < 4; ++j)
       st16(o.primary, gran_byte(o.plan, d.pix, o.plan.Pp, c0 + 4 * j),
@@ -484,6 +488,12 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
       st16(o.side, gran_byte(o.slay, d.side_base, d.side_pstride, c0),
            make_uint4(pack4_i8(sc[0], sc[1], sc[2], sc[3]), pack4_i8(sc[4], sc[5], sc[6], sc[7]),
                       pack4_i8(sc[8], sc[9], sc[10], sc[11]), pack4_i8(sc[12], sc[13], sc[14], sc[15])));
+    } else if (o.side_fmt == FMT_F32) {  // tf32 mode: a second float32 layout (e.g. the phase split)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        st16(o.side, gran_byte(o.slay, d.side_base, d.side_pstride, c0 + 4 * j),
+             make_uint4(__float_as_uint(f32_out(o, v[4 * j])), __float_as_uint(f32_out(o, v[4 * j + 1])),
+                        __float_as_uint(f32_out(o, v[4 * j + 2])), __float_as_uint(f32_out(o, v[4 * j + 3]))));
     } else {
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
@@ -1426,6 +1436,7 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
   // N>>3 [17,23), M>>4 [24,29)
   uint32_t idesc = 0;
   if (eb == 1) idesc |= (2u << 4) | (1u << 7) | (1u << 10);  // S32 <- s8 x s8
+  else if (eb == 4) idesc |= (1u << 4) | (2u << 7) | (2u << 10);  // F32 <- tf32 x tf32
   else idesc |= (1u << 4) | (1u << 7) | (1u << 10);          // F32 <- bf16 x bf16
   idesc |= static_cast<uint32_t>(a.bn >> 3) << 17;
   idesc |= static_cast<uint32_t>(kTileM >> 4) << 24;
@@ -1629,6 +1640,8 @@ bool tc_conv_launch(TcConvPlan* p, const void* x, const Lay& xl, const void* w, 
     } else {
       MRB_TC_SIGS(1, false)
     }
+  } else if (p->spec.elem_bytes == 4) {
+    MRB_TC_SIGS(4, false)
   } else {
     MRB_TC_SIGS(2, false)
   }
@@ -1659,7 +1672,7 @@ const char* tc_conv_describe(const TcConvPlan* p, char* buf, int n) {
   static const char* kinds[] = {"s1", "s2-phase", "stem-s2d", "stem-pool"};
   std::snprintf(buf, n,
                 "tcgen05 %s %s %dx(M128)xN%d kb=%d taps=%d steps=%d grid=%dx%d rows=%dx%d pps=%d stages=%d B=%s ctas=%d smem=%zu",
-                p->spec.elem_bytes == 1 ? "i8" : "bf16",
+                p->spec.elem_bytes == 1 ? "i8" : p->spec.elem_bytes == 4 ? "tf32" : "bf16",
                 kinds[p->spec.kind], a.sub, a.bn, a.kb, p->spec.taps, a.n_steps,
                 a.Hg, a.Wg, a.nbox, a.hbox, a.pps, a.n_stages,
                 a.resident_b ? "resident" : a.tap_groups > 1 ? "streamed-by-kernel-row" : "streamed", p->grid, p->smem);

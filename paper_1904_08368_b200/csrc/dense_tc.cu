@@ -269,7 +269,9 @@ __global__ void __launch_bounds__(256) k_dense_operand(const float* __restrict__
       t[b] = live[b] ? x[static_cast<int64_t>(n) * K + k + b] : 0.f;
       if (live[b] && pre_mul != 0.f) t[b] = __fmul_rn(t[b], pre_mul);
     }
-    if constexpr (EB == 1) {
+    if constexpr (EB == 4) {  // tf32: rounded to tf32 (the MMA would truncate to its top 19 bits)
+      static_cast<float4*>(A)[i] = make_float4(tf32_rn(t[0]), tf32_rn(t[1]), tf32_rn(t[2]), tf32_rn(t[3]));
+    } else if constexpr (EB == 1) {
       uint32_t packed = 0;
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
@@ -303,6 +305,7 @@ __global__ void k_dense_weight_rows(const float* __restrict__ w, int M, int K, i
       if (scalar != 0.f) v = __fmul_rn(v, scalar);
     }
     if (eb == 1) static_cast<int8_t*>(out)[i] = static_cast<int8_t>(live ? (quant ? quant_code(v, q) : static_cast<int32_t>(v)) : 0);
+    else if (eb == 4) static_cast<float*>(out)[i] = live ? tf32_rn(v) : 0.f;
     else static_cast<uint16_t*>(out)[i] = live ? f32_to_bf16(v) : 0;
   }
 }
@@ -346,7 +349,7 @@ struct DenseTcPlan {
 };
 
 DenseTcPlan* dense_tc_create(const DenseTcSpec& sp) {
-  if (sp.eb != 1 && sp.eb != 2) return nullptr;
+  if (sp.eb != 1 && sp.eb != 2 && sp.eb != 4) return nullptr;
   if (!encode_tiled()) return nullptr;
   auto* p = new DenseTcPlan();
   p->spec = sp;
@@ -376,8 +379,9 @@ DenseTcPlan* dense_tc_create(const DenseTcSpec& sp) {
   p->smem = 1024 + static_cast<size_t>(a.stages) * per_stage + 256;
   // instruction descriptor: D format, A/B formats, K-major both, N >> 3, M >> 4
   uint32_t idesc = 0;
-  if (sp.eb == 1) idesc |= (2u << 4) | (1u << 7) | (1u << 10);  // S32 <- s8 x s8
-  else idesc |= (1u << 4) | (1u << 7) | (1u << 10);             // F32 <- bf16 x bf16
+  if (sp.eb == 1) idesc |= (2u << 4) | (1u << 7) | (1u << 10);       // S32 <- s8 x s8
+  else if (sp.eb == 4) idesc |= (1u << 4) | (2u << 7) | (2u << 10);  // F32 <- tf32 x tf32
+  else idesc |= (1u << 4) | (1u << 7) | (1u << 10);                  // F32 <- bf16 x bf16
   idesc |= static_cast<uint32_t>(a.bn >> 3) << 17;
   idesc |= static_cast<uint32_t>(128 >> 4) << 24;
   a.idesc = idesc;
@@ -408,7 +412,7 @@ int dense_tc_launches(const DenseTcPlan* p) { return p->args.splits > 1 ? 3 : 2;
 const char* dense_tc_describe(const DenseTcPlan* p, char* buf, int n) {
   const DenseTcArgs& a = p->args;
   std::snprintf(buf, n, "tcgen05 %s dense %dx(M128)xN%d kblocks=%d splits=%d stages=%d grid=%ux%ux%u smem=%zu",
-                p->spec.eb == 1 ? "i8" : "bf16", a.ms, a.bn, a.kblocks, a.splits, a.stages, p->grid.x, p->grid.y,
+                p->spec.eb == 1 ? "i8" : p->spec.eb == 4 ? "tf32" : "bf16", a.ms, a.bn, a.kblocks, a.splits, a.stages, p->grid.x, p->grid.y,
                 p->grid.z, p->smem);
   return buf;
 }
@@ -445,6 +449,9 @@ bool dense_tc_launch(DenseTcPlan* p, const float* x, float pre_mul, int quant, Q
     if (sp.eb == 1)
       pdl_launch(cal ? k_dense_operand<1, true> : k_dense_operand<1, false>, dim3(blocks), dim3(256), 0, s, x, sp.N,
                  sp.K, a.Npad, Kp, pre_mul, quant, q, operand);
+    else if (sp.eb == 4)
+      pdl_launch(k_dense_operand<4, false>, dim3(blocks), dim3(256), 0, s, x, sp.N, sp.K, a.Npad, Kp, pre_mul, 0, q,
+                 operand);
     else
       pdl_launch(k_dense_operand<2, false>, dim3(blocks), dim3(256), 0, s, x, sp.N, sp.K, a.Npad, Kp, pre_mul, 0, q,
                  operand);
@@ -462,20 +469,23 @@ bool dense_tc_launch(DenseTcPlan* p, const float* x, float pre_mul, int quant, Q
     if (epi.n_ops == 2 && epi.op[0] == E_BIAS && epi.op[1] == E_RELU) sig = DSIG_BIAS_RELU;
   }
   using KFn = void (*)(CUtensorMap, CUtensorMap, DenseTcArgs);
-  static const KFn kfns[2][3] = {{k_dense_tc<1, DSIG_ANY>, k_dense_tc<1, DSIG_BIAS>, k_dense_tc<1, DSIG_BIAS_RELU>},
-                                 {k_dense_tc<2, DSIG_ANY>, k_dense_tc<2, DSIG_BIAS>, k_dense_tc<2, DSIG_BIAS_RELU>}};
-  static bool attr_set[2][3] = {};
-  KFn kern = kfns[sp.eb - 1][sig];
-  if (!attr_set[sp.eb - 1][sig]) {
+  static const KFn kfns[3][3] = {{k_dense_tc<1, DSIG_ANY>, k_dense_tc<1, DSIG_BIAS>, k_dense_tc<1, DSIG_BIAS_RELU>},
+                                 {k_dense_tc<2, DSIG_ANY>, k_dense_tc<2, DSIG_BIAS>, k_dense_tc<2, DSIG_BIAS_RELU>},
+                                 {k_dense_tc<4, DSIG_ANY>, k_dense_tc<4, DSIG_BIAS>, k_dense_tc<4, DSIG_BIAS_RELU>}};
+  static bool attr_set[3][3] = {};
+  const int ei = sp.eb == 1 ? 0 : sp.eb == 2 ? 1 : 2;
+  KFn kern = kfns[ei][sig];
+  if (!attr_set[ei][sig]) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr_set[sp.eb - 1][sig] = true;
+    attr_set[ei][sig] = true;
   }
   pdl_launch(kern, p->grid, dim3(kDenseThreads), p->smem, s, p->tmA, p->tmB, a);
   // 3. split-K reduction + epilogue
   if (a.splits > 1) {
     const int64_t total = static_cast<int64_t>(sp.N) * sp.M;
     const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 8));
-    pdl_launch(sp.eb == 1 ? k_dense_reduce<1> : k_dense_reduce<2>, dim3(blocks), dim3(256), 0, s, a);
+    pdl_launch(sp.eb == 1 ? k_dense_reduce<1> : sp.eb == 4 ? k_dense_reduce<4> : k_dense_reduce<2>, dim3(blocks),
+               dim3(256), 0, s, a);
   }
   return true;
 }

@@ -230,12 +230,13 @@ struct DeviceGuard {
 namespace {
 
 enum Path { P_NONE = 0, P_CONV_I8_SIMT, P_CONV_I8_TC, P_CONV_BF16_SIMT, P_CONV_BF16_TC, P_CONV_F32, P_DENSE_I8,
-            P_DENSE_F32, P_DENSE_BF16, P_POOL, P_DW, P_DENSE_I8_TC, P_DENSE_BF16_TC };
+            P_DENSE_F32, P_DENSE_BF16, P_POOL, P_DW, P_DENSE_I8_TC, P_DENSE_BF16_TC, P_CONV_TF32_TC,
+            P_DENSE_TF32_TC };
 
 const char* path_name(int p) {
   static const char* n[] = {"none", "conv_i8_simt", "conv_i8_tcgen05", "conv_bf16_simt", "conv_bf16_tcgen05",
                             "conv_f32_strict", "dense_i8", "dense_f32_strict", "dense_bf16", "max_pool", "dwconv",
-                            "dense_i8_tcgen05", "dense_bf16_tcgen05"};
+                            "dense_i8_tcgen05", "dense_bf16_tcgen05", "conv_tf32_tcgen05", "dense_tf32_tcgen05"};
   return n[p];
 }
 
@@ -243,7 +244,7 @@ const char* path_name(int p) {
 int float_fmt(const Exec& ex) {
   // int8 pipelines keep the float residual stream exact in float32; the
   // strict mode computes everything in float32; bf16 mode stores bf16.
-  if (ex.P.any_quant || ex.opt.float_mode == MR_FLOAT_FP32_STRICT) return FMT_F32;
+  if (ex.P.any_quant || ex.opt.float_mode == MR_FLOAT_FP32_STRICT || ex.opt.float_mode == MR_FLOAT_TF32) return FMT_F32;
   return FMT_BF16;
 }
 
@@ -300,7 +301,11 @@ int64_t lay_elems(const Lay& L) {
 int want_rep(Exec& ex, int v, int fmt, const QParams* q, int kind = LAY_NORMAL, int s2d_pad = 0, int kb = 0) {
   auto& rs = ex.reps[v];
   if (ex.P.values[v].shape.size() != 4) kind = LAY_NORMAL;
-  if (fmt == FMT_F32 || kind == LAY_S2D || kind == LAY_S2DP) kb = 16;
+  // float32 values are P16 (16-byte chunks: warp-coalesced residual loads),
+  // except in the tf32 mode, where tcgen05 convs read them in 128-byte chunks
+  // and every consumer shares that one representation
+  const bool tf32 = ex.opt.float_mode == MR_FLOAT_TF32 && !ex.P.any_quant;
+  if ((fmt == FMT_F32 && !tf32) || kind == LAY_S2D || kind == LAY_S2DP) kb = 16;
   for (size_t i = 0; i < rs.size(); ++i) {
     const Rep& r = rs[i];
     if (r.nchw_user) continue;
@@ -348,11 +353,11 @@ void decide_tc(Exec& ex) {
   for (size_t gi = 0; gi < P.groups.size(); ++gi) {
     int& path = ex.group_path[gi];
     const GroupDesc& g = P.groups[gi];
-    if (path != P_CONV_I8_TC && path != P_CONV_BF16_TC) continue;
+    if (path != P_CONV_I8_TC && path != P_CONV_BF16_TC && path != P_CONV_TF32_TC) continue;
     bool has_sum = g_has_sum(g);
     const auto& os = has_sum ? g.pre_sum_shape : g.out_shape;
     TcConvSpec sp{};
-    sp.elem_bytes = path == P_CONV_I8_TC ? 1 : 2;
+    sp.elem_bytes = path == P_CONV_I8_TC ? 1 : path == P_CONV_TF32_TC ? 4 : 2;
     sp.N = static_cast<int>(g.in_shape[0]);
     sp.C = static_cast<int>(g.in_shape[1]);
     sp.H = static_cast<int>(g.in_shape[2]);
@@ -427,7 +432,7 @@ void decide_tc(Exec& ex) {
       if (sp.kind == TC_S1) ex.want_kb[g.data.value] = sp.kb;
       if (sp.kind == TC_S2_PHASE) phase_kb[g.data.value] = sp.kb;
     } else {
-      path = path == P_CONV_I8_TC ? P_CONV_I8_SIMT : P_CONV_BF16_SIMT;
+      path = path == P_CONV_I8_TC ? P_CONV_I8_SIMT : path == P_CONV_TF32_TC ? P_CONV_F32 : P_CONV_BF16_SIMT;
     }
   }
 }
@@ -446,6 +451,8 @@ void plan(Exec& ex, bool use_tc) {
       case GroupKind::Conv:
         if (g.weight.quant) {
           ex.group_path[gi] = use_tc ? P_CONV_I8_TC : P_CONV_I8_SIMT;
+        } else if (ex.opt.float_mode == MR_FLOAT_TF32 && !P.any_quant) {
+          ex.group_path[gi] = use_tc ? P_CONV_TF32_TC : P_CONV_F32;
         } else if (ffmt == FMT_F32) {
           ex.group_path[gi] = P_CONV_F32;
         } else {
@@ -459,7 +466,9 @@ void plan(Exec& ex, bool use_tc) {
           return e && std::atoi(e);
         }();
         const bool tc = use_tc && !no_dense_tc;
+        const bool tf32 = ex.opt.float_mode == MR_FLOAT_TF32 && !P.any_quant;
         ex.group_path[gi] = g.weight.quant ? (tc ? P_DENSE_I8_TC : P_DENSE_I8)
+                            : tf32 ? (tc ? P_DENSE_TF32_TC : P_DENSE_F32)
                             : ffmt == FMT_F32 ? P_DENSE_F32 : (tc ? P_DENSE_BF16_TC : P_DENSE_BF16);
       }
         break;
@@ -521,7 +530,7 @@ GroupIO resolve_inputs(Exec& ex, int gi) {
   int path = ex.group_path[gi];
   // data layout kind the tcgen05 formulation needs (CUDA-core kernels read NORMAL)
   int kind = LAY_NORMAL, s2d_pad = 0, kb = 0;
-  if (path == P_CONV_I8_TC || path == P_CONV_BF16_TC) {
+  if (path == P_CONV_I8_TC || path == P_CONV_BF16_TC || path == P_CONV_TF32_TC) {
     const TcConvSpec& sp = ex.group_tc[gi];
     kind = sp.kind == TC_S2_PHASE ? LAY_PHASE : sp.kind == TC_STEM_S2D ? LAY_S2D : sp.kind == TC_STEM_POOL ? LAY_S2DP : LAY_NORMAL;
     s2d_pad = static_cast<int>(g.ph);
@@ -546,7 +555,7 @@ GroupIO resolve_inputs(Exec& ex, int gi) {
       io.requant_q = dv.q;
       io.data_scale = dv.q.c2;
     }
-  } else if (path == P_CONV_F32 || path == P_CONV_BF16_SIMT || path == P_CONV_BF16_TC) {
+  } else if (path == P_CONV_F32 || path == P_CONV_BF16_SIMT || path == P_CONV_BF16_TC || path == P_CONV_TF32_TC) {
     if (g.data.pre_mul != 0.f) fail(MR_ERR_UNSUPPORTED_GROUP, "group %" + g.name + ": scaled conv input");
     io.data_rep = want_rep(ex, g.data.value, ffmt, nullptr, kind, s2d_pad, kb);
   } else {  // pool / depthwise: float input
@@ -711,7 +720,8 @@ void build(Exec& ex) {
     for (size_t r = 0; r < ex.reps[v].size(); ++r) {
       const Rep& rep = ex.reps[v][r];
       if (rep.nchw_user || r == 0 || vi.producer < 0) continue;  // rep 0 is the primary
-      if ((rep.fmt == FMT_I8 || rep.fmt == FMT_BF16) && P.groups[vi.producer].kind != GroupKind::Dense &&
+      const bool tf32_side = rep.fmt == FMT_F32 && ex.opt.float_mode == MR_FLOAT_TF32 && !P.any_quant;
+      if ((rep.fmt == FMT_I8 || rep.fmt == FMT_BF16 || tf32_side) && P.groups[vi.producer].kind != GroupKind::Dense &&
           !g_has_sum(P.groups[vi.producer])) {
         if (side_rep[vi.producer] >= 0)
           fail(MR_ERR_UNSUPPORTED_GROUP, "value %" + vi.name + " needs more than two representations");
@@ -815,6 +825,8 @@ void build(Exec& ex) {
       out.primary_fmt = orep.fmt;
       out.plan = orep.lay;
     }
+    // tf32 mode: 4-D float32 activations are stored tf32-rounded (consumers' MMAs read tf32)
+    out.tf32 = ex.opt.float_mode == MR_FLOAT_TF32 && !P.any_quant && P.values[ov].shape.size() == 4 ? 1 : 0;
     if (sbuf >= 0) {
       const Rep& sr = ex.reps[ov][side_rep[sgi]];
       out.slay = sr.lay;
@@ -934,7 +946,8 @@ void build(Exec& ex) {
         break;
       }
       case P_CONV_I8_TC:
-      case P_CONV_BF16_TC: {
+      case P_CONV_BF16_TC:
+      case P_CONV_TF32_TC: {
         TcConvPlan* tp = tc_conv_create(ex.group_tc[gi]);
         if (!tp) fail(MR_ERR_UNSUPPORTED_GROUP, "group %" + g.name + ": tcgen05 plan failed");
         ex.tc_plans.push_back(tp);
@@ -952,8 +965,9 @@ void build(Exec& ex) {
         break;
       }
       case P_DENSE_I8_TC:
-      case P_DENSE_BF16_TC: {
-        DenseTcSpec ds{path == P_DENSE_I8_TC ? 1 : 2, static_cast<int>(g.in_shape[0]), static_cast<int>(g.in_shape[1]),
+      case P_DENSE_BF16_TC:
+      case P_DENSE_TF32_TC: {
+        DenseTcSpec ds{path == P_DENSE_I8_TC ? 1 : path == P_DENSE_TF32_TC ? 4 : 2, static_cast<int>(g.in_shape[0]), static_cast<int>(g.in_shape[1]),
                        static_cast<int>(g.out_shape[1])};
         DenseTcPlan* dp = dense_tc_create(ds);
         if (!dp) fail(MR_ERR_UNSUPPORTED_GROUP, "group %" + g.name + ": tcgen05 dense plan failed");
@@ -1019,7 +1033,8 @@ void build(Exec& ex) {
     ++B.launch_idx;
     // CUDA-core producers write interior pixels only: clear the P16 borders
     // (the tcgen05 conv writes its own, it computes over the padded grid).
-    bool tc_same = (path == P_CONV_I8_TC || path == P_CONV_BF16_TC) && ex.group_tc[gi].kind == TC_S1;
+    bool tc_same = (path == P_CONV_I8_TC || path == P_CONV_BF16_TC || path == P_CONV_TF32_TC) &&
+                   ex.group_tc[gi].kind == TC_S1;
     const auto& zshape = fp >= 0 ? P.groups[fp].out_shape : g.out_shape;
     if (!tc_same && !has_sum && zshape.size() == 4) {
       // interior-only producer: keep the padding ring zero without a per-run pass
@@ -1166,7 +1181,8 @@ void prepare_weights(Exec& ex, cudaStream_t s) {
     }
     int fmt, cs;
     int wl = WL_ROWS;
-    if (path == P_CONV_I8_TC || path == P_CONV_BF16_TC) wl = ex.group_tc[gi].kind == TC_STEM_S2D || ex.group_tc[gi].kind == TC_STEM_POOL ? WL_S2D : WL_TC;
+    if (path == P_CONV_I8_TC || path == P_CONV_BF16_TC || path == P_CONV_TF32_TC)
+      wl = ex.group_tc[gi].kind == TC_STEM_S2D || ex.group_tc[gi].kind == TC_STEM_POOL ? WL_S2D : WL_TC;
     if (w.quant) {
       fmt = FMT_I8;
       cs = static_cast<int>(round_up(I, 4));
@@ -1178,7 +1194,7 @@ void prepare_weights(Exec& ex, cudaStream_t s) {
       cs = g.kind == GroupKind::Dense ? static_cast<int>(round_up(I, 8)) : I;  // dense: [K/8][M][8] (k_dense)
     }
     int64_t n;
-    if (fmt == FMT_F32) {
+    if (fmt == FMT_F32 && wl == WL_ROWS) {
       n = static_cast<int64_t>(O) * I * KH * KW;
     } else if (wl == WL_TC || wl == WL_S2D) {
       const TcConvSpec& sp = ex.group_tc[gi];

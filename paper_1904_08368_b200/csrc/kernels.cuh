@@ -88,9 +88,11 @@ struct OutDev {
   int32_t primary_fmt;  // FMT_I8 => the epilogue's last op is a Requant; the code is stored
   Lay plan;             // primary layout
   void* side;           // optional second copy of the final float value for other consumers:
-  int32_t side_fmt;     //   FMT_I8 (realize codes with side_q) or FMT_BF16, any P16 kind
+  int32_t side_fmt;     //   FMT_I8 (realize codes with side_q), FMT_BF16 or (tf32 mode) FMT_F32, any kind
   Lay slay;
   QDev side_q;
+  int32_t tf32;         // tf32 mode: float32 activations are stored rounded to tf32 (the tensor
+                        //   cores read only the top 19 bits; truncation would bias every product)
 };
 
 // Division by a launch-constant divisor d for dividends n < 2^31 as a
@@ -146,6 +148,15 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 }
 
 __device__ __forceinline__ float relu_ref(float x) { return x > 0.f ? x : 0.0f; }
+
+// float32 -> the nearest tf32 value (10 explicit mantissa bits, ties away), as a float32.
+__device__ __forceinline__ float tf32_rn(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+// A float32 activation as stored by `o` (rounded to tf32 in the tf32 mode).
+__device__ __forceinline__ float f32_out(const OutDev& o, float v) { return o.tf32 ? tf32_rn(v) : v; }
 
 __device__ __forceinline__ float clip_ref(float x, float lo, float hi) {
   float a = x < lo ? lo : x;   // std::max(x, lo)
@@ -294,7 +305,7 @@ __device__ __forceinline__ float apply_epi(const EpiDev& e, float v, int64_t pix
 __device__ __forceinline__ void store_out(const OutDev& o, float v, int32_t code, int64_t pix, int32_t c) {
   int64_t i = lay_off(o.plan, pix, c);
   if (o.primary_fmt == FMT_F32) {
-    static_cast<float*>(o.primary)[i] = v;
+    static_cast<float*>(o.primary)[i] = f32_out(o, v);
   } else if (o.primary_fmt == FMT_BF16) {
     static_cast<uint16_t*>(o.primary)[i] = f32_to_bf16(v);
   } else {
@@ -302,6 +313,7 @@ __device__ __forceinline__ void store_out(const OutDev& o, float v, int32_t code
   }
   if (o.side) {
     if (o.side_fmt == FMT_I8) static_cast<int8_t*>(o.side)[lay_off(o.slay, pix, c)] = static_cast<int8_t>(quant_code(v, o.side_q));
+    else if (o.side_fmt == FMT_F32) static_cast<float*>(o.side)[lay_off(o.slay, pix, c)] = f32_out(o, v);
     else static_cast<uint16_t*>(o.side)[lay_off(o.slay, pix, c)] = f32_to_bf16(v);
   }
 }

@@ -408,7 +408,7 @@ __global__ void k_zero_border(void* buf, Lay L, int N) {
 // ---- hoisted weight prologue ----------------------------------------------------
 // OIHW float32 -> kernel layout.  v = w [* oc_scale[o]] [* scalar]; then
 //   WL_ROWS (I8 / BF16): [O][KH][KW][Cs]               CUDA-core kernels
-//   WL_TC   (I8 / BF16): [KH*KW][I/cpc][O][cpc]        tcgen05 B operand (16-byte K chunks)
+//   WL_TC   (I8 / BF16 / F32 for tf32): [KH*KW][I/cpc][O][cpc]  tcgen05 B operand (16-byte K chunks)
 //   F32 strict:          [O][I][KH][KW]                reference loop order
 //   WL_S2D  (I8 / BF16): [TA*TA][4I/cpc][O][cpc]      stride-2 stem over the space-to-depth
 //                        input: tap (a, b), s2d channel (py*2+px)*I + c  <-  w[o][c][2a+py][2b+px]
@@ -416,17 +416,19 @@ __global__ void k_weight_prep(const float* __restrict__ w, int O, int I, int KH,
                               const float* __restrict__ oc_scale, float scalar, int fmt, int quant, QDev q,
                               void* out) {
   // WL_TC / WL_S2D: Cs carries the chunk width in bytes (16, 64 or 128)
-  const int cpc = (wl == WL_ROWS ? 16 : Cs) / (fmt == FMT_I8 ? 1 : 2);
+  // (F32 with WL_TC: the tf32 tcgen05 B operand, 4-byte elements)
+  const bool strict = fmt == FMT_F32 && wl == WL_ROWS;
+  const int cpc = (wl == WL_ROWS ? 16 : Cs) / (fmt == FMT_I8 ? 1 : fmt == FMT_BF16 ? 2 : 4);
   const int TA = (KH + 1) / 2;
   const int planes = wl == WL_S2D ? (4 * I + cpc - 1) / cpc : (I + cpc - 1) / cpc;
   int64_t total;
-  if (fmt == FMT_F32) total = static_cast<int64_t>(O) * I * KH * KW;
+  if (strict) total = static_cast<int64_t>(O) * I * KH * KW;
   else if (wl == WL_TC) total = static_cast<int64_t>(KH) * KW * planes * O * cpc;
   else if (wl == WL_S2D) total = static_cast<int64_t>(TA) * TA * planes * O * cpc;
   else total = static_cast<int64_t>(O) * KH * KW * Cs;
   GRID_STRIDE(i, total) {
     int o, ic, kh, kw;
-    if (fmt == FMT_F32) {
+    if (strict) {
       kw = static_cast<int>(i % KW);
       int64_t t = i / KW;
       kh = static_cast<int>(t % KH);
@@ -471,8 +473,8 @@ __global__ void k_weight_prep(const float* __restrict__ w, int O, int I, int KH,
       if (oc_scale) v = __fmul_rn(v, oc_scale[o]);
       if (scalar != 0.f) v = __fmul_rn(v, scalar);
     }
-    if (fmt == FMT_F32) {
-      static_cast<float*>(out)[i] = v;
+    if (fmt == FMT_F32) {  // WL_TC: the tf32 B operand, rounded to tf32 (the MMA would truncate)
+      static_cast<float*>(out)[i] = live ? (strict ? v : tf32_rn(v)) : 0.f;
     } else if (fmt == FMT_BF16) {
       static_cast<uint16_t*>(out)[i] = live ? f32_to_bf16(v) : 0;
     } else {
@@ -761,7 +763,7 @@ __global__ void __launch_bounds__(256) k_dwconv_fast(const void* __restrict__ x,
       }
       char* d4 = static_cast<char*>(out.primary) + lay_byte(out.plan, pix, c0 + 4 * s4);
       if (out.primary_fmt == FMT_F32) {
-        *reinterpret_cast<float4*>(d4) = make_float4(r[0], r[1], r[2], r[3]);
+        *reinterpret_cast<float4*>(d4) = make_float4(f32_out(out, r[0]), f32_out(out, r[1]), f32_out(out, r[2]), f32_out(out, r[3]));
       } else if (out.primary_fmt == FMT_BF16) {
         *reinterpret_cast<uint2*>(d4) =
             make_uint2(pack_bf16x2(r[0], r[1]),
@@ -922,7 +924,7 @@ __global__ void __launch_bounds__(256, dw_minb(PL)) k_dw3x3_rb(const void* __res
       char* d4 = static_cast<char*>(out.primary) + lay_byte(out.plan, pix, c0);
       const float* r = acc[o];
       if (out.primary_fmt == FMT_F32) {
-        *reinterpret_cast<float4*>(d4) = make_float4(r[0], r[1], r[2], r[3]);
+        *reinterpret_cast<float4*>(d4) = make_float4(f32_out(out, r[0]), f32_out(out, r[1]), f32_out(out, r[2]), f32_out(out, r[3]));
       } else if (out.primary_fmt == FMT_BF16) {
         *reinterpret_cast<uint2*>(d4) =
             make_uint2(pack_bf16x2(r[0], r[1]),
@@ -1014,7 +1016,7 @@ __global__ void k_maxpool(const void* __restrict__ x, int xfmt, ConvGeom g, OutD
       char* d4 = static_cast<char*>(out.primary) + lay_byte(out.plan, pix, c0 + 4 * s4);
       const float* a4 = acc + 4 * s4;
       if (out.primary_fmt == FMT_F32) {
-        *reinterpret_cast<float4*>(d4) = make_float4(a4[0], a4[1], a4[2], a4[3]);
+        *reinterpret_cast<float4*>(d4) = make_float4(f32_out(out, a4[0]), f32_out(out, a4[1]), f32_out(out, a4[2]), f32_out(out, a4[3]));
       } else {
         *reinterpret_cast<uint2*>(d4) =
             make_uint2(pack_bf16x2(a4[0], a4[1]),

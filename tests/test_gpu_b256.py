@@ -148,3 +148,25 @@ def test_c5_batch4096_seeded_subset_matches_reference(gpu):
         ys = ex.run_host(np.ascontiguousarray(x[a:b]))
         assert not diff_rows(ys, y[a:b]), world
         del ex
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,gname,batch", [("resnet18", "resnet18_div_b256.npz", 256),
+                                              ("mobilenet_v1", "mobilenet_v1_div_b256.npz", 256),
+                                              ("dqn_b256", "dqn_b256_div_b256.npz", 256),
+                                              ("resnet18_tiny", "resnet18_tiny_div_b64.npz", 64)])
+def test_tf32_b256_against_reference_fp32(gpu, name, gname, batch):
+    """MR_FLOAT_TF32 (north_star: 'bf16/tf32 for float'): float32 activations,
+    convs and dense on tcgen05 kind::tf32; same bar as bf16, exact count printed."""
+    err, agree, classes = float_check(name, gname, batch, mrb.MR_FLOAT_TF32)
+    print("%s tf32 b%d vs reference fp32: normwise %.6f, top-1 agreement %d/%d (%d distinct classes)"
+          % (name, batch, err, agree, batch, classes))
+    assert err <= TOL
+    assert agree >= TOP1 * batch
+
+
+@pytest.mark.gpu
+def test_tf32_runs_tcgen05_kernels(gpu):
+    ex, _ = setup("resnet18", "fp32", 2, float_mode=mrb.MR_FLOAT_TF32)
+    kernels = [g["kernel"] for g in ex.describe()["groups"]]
+    assert kernels.count("conv_tf32_tcgen05") >= 18 and "dense_tf32_tcgen05" in kernels
