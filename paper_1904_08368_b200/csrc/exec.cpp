@@ -477,6 +477,21 @@ void plan(Exec& ex, bool use_tc) {
     }
   }
   decide_tc(ex);
+  // bf16 depthwise inputs in 128-byte chunks (64 channels per plane): a pixel's
+  // channels are one contiguous 128-byte row, so 16 lanes of k_dw3x3_rb read
+  // (and the producing conv writes) whole lines instead of 16-byte pieces
+  static const bool dw_wide = [] {
+    const char* e = std::getenv("MRB200_DW_PL16");
+    return !e || std::atoi(e) != 0;
+  }();
+  for (size_t gi = 0; gi < P.groups.size() && dw_wide; ++gi) {
+    const GroupDesc& g = P.groups[gi];
+    if (g.kind != GroupKind::DwConv || ffmt != FMT_BF16 || g.in_shape[1] % 64 != 0 || g.kh != 3 || g.kw != 3) continue;
+    const ValueInfo& dv = P.values[g.data.value];
+    bool only_dw = !dv.is_data;
+    for (int c : dv.consumers) only_dw = only_dw && P.groups[c].kind == GroupKind::DwConv;
+    if (only_dw && !ex.want_kb.count(g.data.value)) ex.want_kb[g.data.value] = 128;
+  }
   // primary representations of group outputs (chunk width from want_kb)
   for (size_t gi = 0; gi < P.groups.size(); ++gi) {
     const GroupDesc& g = P.groups[gi];
