@@ -442,8 +442,8 @@ bool dense_tc_launch(DenseTcPlan* p, const float* x, float pre_mul, int quant, Q
   a.ws = ws;
   bool cal = quant && q.ovf;
   for (int k = 0; k < epi.n_ops; ++k) cal = cal || (epi.op[k] == E_REQ && epi.q[k].ovf);
-  // 1. operand
-  {
+  // 1. operand (x == nullptr: the producer already wrote it -- the fused sum)
+  if (x) {
     const int64_t total = static_cast<int64_t>(a.Npad) * (Kp / 4);
     const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 8));
     if (sp.eb == 1)
@@ -482,7 +482,7 @@ bool dense_tc_launch(DenseTcPlan* p, const float* x, float pre_mul, int quant, Q
   pdl_launch(kern, p->grid, dim3(kDenseThreads), p->smem, s, p->tmA, p->tmB, a);
   // 3. split-K reduction + epilogue
   if (a.splits > 1) {
-    const int64_t total = static_cast<int64_t>(sp.N) * sp.M;
+    const int64_t total = static_cast<int64_t>(sp.N) * sp.M;  // (split-K reduction)
     const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 8));
     pdl_launch(sp.eb == 1 ? k_dense_reduce<1> : sp.eb == 4 ? k_dense_reduce<4> : k_dense_reduce<2>, dim3(blocks),
                dim3(256), 0, s, a);

@@ -27,7 +27,8 @@ const char* dense_tc_describe(const DenseTcPlan* p, char* buf, int n);
 // [M, K] float32 weight (+ folded per-row scale, scalar, realize chain) -> B [Mpad, Kp]
 void dense_tc_prep_weight(const DenseTcPlan* p, const float* w, const float* oc_scale, float scalar, int quant,
                           QDev q, void* out, cudaStream_t s);
-// operand prologue + tcgen05 contraction (+ split-K reduction); false: TMA encoding failed
+// operand prologue + tcgen05 contraction (+ split-K reduction); false: TMA encoding failed.
+// x == nullptr: `operand` was written by the producer (the fused sum_hw).
 bool dense_tc_launch(DenseTcPlan* p, const float* x, float pre_mul, int quant, QDev q, void* operand, const void* w,
                      void* ws, float acc_scale, const EpiDev& epi, const OutDev& out, cudaStream_t s);
 

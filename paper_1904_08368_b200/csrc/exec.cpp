@@ -166,6 +166,7 @@ struct Exec {
   std::string describe;
   std::vector<TcConvPlan*> tc_plans;
   std::vector<DenseTcPlan*> group_dense;    // tcgen05 dense plan per group (nullptr: none)
+  std::map<int, int> sum_operand;            // dense group -> operand buffer its producer's sum_hw writes
 
   void drop_graphs() {
     for (auto& g : graphs) {
@@ -991,19 +992,22 @@ void build(Exec& ex) {
         char buf[256];
         ex.group_note.resize(P.groups.size());
         ex.group_note[gi] = dense_tc_describe(dp, buf, sizeof(buf));
-        const int opbuf = B.scratch(dense_tc_operand_bytes(dp), "%" + g.name + ":operand");
+        auto fused_op = ex.sum_operand.find(static_cast<int>(gi));
+        const bool op_ready = fused_op != ex.sum_operand.end();  // written by the producer's sum_hw
+        const int opbuf = op_ready ? fused_op->second : B.scratch(dense_tc_operand_bytes(dp), "%" + g.name + ":operand");
+        if (op_ready) B.use(opbuf);
         const int64_t wsb = dense_tc_workspace_bytes(dp);
         const int wsbuf = wsb ? B.scratch(wsb, "%" + g.name + ":splitk") : -1;
-        L.kernels = dense_tc_launches(dp);
+        L.kernels = dense_tc_launches(dp) - (op_ready ? 1 : 0);
         float pre = g.data.pre_mul;
         int quant = g.data.quant || gio.requant_data ? 1 : 0;
         QDev q = to_qdev(g.data.quant ? g.data.q : gio.requant_q);
         std::string gname = g.name;
-        L.fn = [e, gidx, dbuf, dp, opbuf, wsbuf, pre, quant, q, acc_scale, outdev, epidev, residual_fix,
-                gname](cudaStream_t s) {
+        L.fn = [e, gidx, dbuf, dp, opbuf, wsbuf, pre, quant, q, acc_scale, outdev, epidev, residual_fix, gname,
+                op_ready](cudaStream_t s) {
           EpiDev d = epidev();
           residual_fix(d);
-          if (!dense_tc_launch(dp, static_cast<const float*>(e->ptr(dbuf)), pre, quant, q, e->ptr(opbuf),
+          if (!dense_tc_launch(dp, op_ready ? nullptr : static_cast<const float*>(e->ptr(dbuf)), pre, quant, q, e->ptr(opbuf),
                                e->group_w[gidx], wsbuf >= 0 ? e->ptr(wsbuf) : nullptr, acc_scale, d, outdev(), s))
             fail(MR_ERR_CUDA, "group %" + gname + ": TMA descriptor encoding failed");
         };
@@ -1084,9 +1088,43 @@ void build(Exec& ex) {
       int N = static_cast<int>(ps[0]), H = static_cast<int>(ps[2]), W = static_cast<int>(ps[3]);
       int C = static_cast<int>(ps[1]);
       B.use(pre_sum_buf);
-      S.fn = [e, pre_sum_buf, pre_lay, obuf, N, H, W, C](cudaStream_t s) {
+      // cross-group fusion: when a tcgen05 dense is the
+      // sum's only consumer (the classifier head), the sum kernel applies the
+      // dense's data prologue (multiply by 1/HW, realize chain) and writes its A
+      // operand directly -- no float32 round trip, no operand launch
+      const ValueInfo& sv = P.values[g.out_value];
+      int dgi = -1;
+      static const bool no_fuse = [] {  // A/B switch
+        const char* e2 = std::getenv("MRB200_NO_SUM_FUSE");
+        return e2 && std::atoi(e2);
+      }();
+      if (!no_fuse && sv.consumers.size() == 1 && !sv.is_result && C % 32 == 0 && H * W <= 64) {
+        const int c = sv.consumers[0];
+        const int dp = ex.group_path[c];
+        const int eb = dp == P_DENSE_I8_TC ? 1 : dp == P_DENSE_BF16_TC ? 2 : dp == P_DENSE_TF32_TC ? 4 : 0;
+        if (eb && P.groups[c].data.value == g.out_value && (C * eb) % 128 == 0) dgi = c;
+      }
+      SumOperand sop{};
+      int opbuf = -1;
+      if (dgi >= 0) {
+        const GroupDesc& dg = P.groups[dgi];
+        const GroupIO& dio = io[dgi];
+        const int dp = ex.group_path[dgi];
+        sop.eb = dp == P_DENSE_I8_TC ? 1 : dp == P_DENSE_BF16_TC ? 2 : 4;
+        sop.Kp = C;
+        sop.pre_mul = dg.data.pre_mul;
+        sop.quant = dg.data.quant || dio.requant_data ? 1 : 0;
+        sop.q = to_qdev(dg.data.quant ? dg.data.q : dio.requant_q);
+        opbuf = B.scratch(round_up(N, 128) * static_cast<int64_t>(C) * sop.eb, "%" + dg.name + ":operand");
+        ex.sum_operand[dgi] = opbuf;
+        S.kernel = "sum_hw+dense_operand";
+        S.bytes = 4.0 * ps[0] * ps[1] * ps[2] * ps[3] + static_cast<double>(sop.eb) * ps[0] * ps[1];
+      }
+      S.fn = [e, pre_sum_buf, pre_lay, obuf, N, H, W, C, sop, opbuf](cudaStream_t s) {
+        SumOperand o = sop;
+        if (opbuf >= 0) o.ptr = e->ptr(opbuf);
         launch_sum_hw(static_cast<const float*>(e->ptr(pre_sum_buf)), pre_lay, N, H, W, C,
-                      static_cast<float*>(e->ptr(obuf)), s);
+                      opbuf >= 0 ? nullptr : static_cast<float*>(e->ptr(obuf)), s, opbuf >= 0 ? &o : nullptr);
       };
       ex.launches.push_back(S);
       ++B.launch_idx;

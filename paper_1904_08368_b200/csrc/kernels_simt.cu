@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <stdexcept>
 #include <cstdlib>
 
 #include "kernels.cuh"
@@ -1094,8 +1095,9 @@ __global__ void __launch_bounds__(256) k_sum_hw_warp(const float* __restrict__ x
 // lane runs one channel's sequential seeded sum in (h, w) order.  Granule plane
 // stride S = 1 (mod 8) float4 puts the 8 granules of one pixel on distinct banks.
 constexpr int kSumWarps = 4;
+template <bool CAL>
 __global__ void __launch_bounds__(kSumWarps * 32) k_sum_hw_warp32(const float* __restrict__ x, Lay L, int N, int H,
-                                                                  int W, int C, float* __restrict__ y) {
+                                                                  int W, int C, float* __restrict__ y, SumOperand op) {
   pdl_trigger();
   pdl_wait();
   __shared__ float4 st[kSumWarps][8 * 65];
@@ -1126,9 +1128,28 @@ __global__ void __launch_bounds__(kSumWarps * 32) k_sum_hw_warp32(const float* _
     }
     __syncwarp();
     const float* col = reinterpret_cast<const float*>(st[warp] + (lane >> 2) * S) + (lane & 3);
-    float acc = col[0];
-    for (int p = 1; p < HW; ++p) acc = __fadd_rn(acc, col[4 * p]);
-    y[static_cast<int64_t>(n) * C + c0 + lane] = acc;
+    // all the lane's shared-memory reads first, then the seeded sequential sum
+    // (a load in the dependency chain of every add would cost ~30 cycles each)
+    float vals[64];
+#pragma unroll
+    for (int p = 0; p < 64; ++p) vals[p] = p < HW ? col[4 * p] : 0.f;
+    float acc = vals[0];
+#pragma unroll
+    for (int p = 1; p < 64; ++p)
+      if (p < HW) acc = __fadd_rn(acc, vals[p]);
+    const int c = c0 + lane;
+    if (y) y[static_cast<int64_t>(n) * C + c] = acc;
+    if (op.ptr) {  // the consumer dense's operand: its data prologue applied once here
+      float t = acc;
+      if (op.pre_mul != 0.f) t = __fmul_rn(t, op.pre_mul);
+      const int64_t o = static_cast<int64_t>(n) * op.Kp + c;
+      if (op.eb == 1)
+        static_cast<int8_t*>(op.ptr)[o] = static_cast<int8_t>(op.quant ? quant_code_t<CAL>(t, op.q) : static_cast<int32_t>(t));
+      else if (op.eb == 2)
+        static_cast<uint16_t*>(op.ptr)[o] = f32_to_bf16(t);
+      else
+        static_cast<float*>(op.ptr)[o] = tf32_rn(t);
+    }
     __syncwarp();
   }
 }
@@ -1752,14 +1773,19 @@ void launch_maxpool(const void* x, int xfmt, const ConvGeom& g, const OutDev& ou
   pdl_launch(k_maxpool, grid_stride_blocks(total), kThreads, 0, s, x, xfmt, g, out);
 }
 
-void launch_sum_hw(const float* x, const Lay& L, int N, int H, int W, int C, float* y, cudaStream_t s) {
+void launch_sum_hw(const float* x, const Lay& L, int N, int H, int W, int C, float* y, cudaStream_t s,
+                   const SumOperand* op) {
   if (H * W <= 64 && C % 4 == 0 && L.cpc >= 4 && L.cpc % 4 == 0 && L.kind == LAY_NORMAL && L.kb >= 16) {
     if (C % 32 == 0) {
       const int64_t items32 = static_cast<int64_t>(N) * (C / 32);
-      pdl_launch(k_sum_hw_warp32, static_cast<int>(std::min<int64_t>((items32 + kSumWarps - 1) / kSumWarps, 148 * 16)),
-                 kSumWarps * 32, 0, s, x, L, N, H, W, C, y);
+      const SumOperand o = op ? *op : SumOperand{};
+      const bool cal = op && op->quant && op->q.ovf;
+      pdl_launch(cal ? k_sum_hw_warp32<true> : k_sum_hw_warp32<false>,
+                 static_cast<int>(std::min<int64_t>((items32 + kSumWarps - 1) / kSumWarps, 148 * 16)), kSumWarps * 32,
+                 0, s, x, L, N, H, W, C, y, o);
       return;
     }
+    if (op) throw std::runtime_error("sum -> dense operand fusion needs C % 32 == 0");
     const int64_t items = static_cast<int64_t>(N) * (C / 4);
     pdl_launch(k_sum_hw_warp, static_cast<int>(std::min<int64_t>((items + 7) / 8, 148 * 8)), 256, 0, s, x, L, N, H, W,
                C, y);

@@ -46,7 +46,17 @@ void launch_conv_f32_strict(const float* x, const float* w, const ConvGeom& g, c
 void launch_dwconv(const void* x, int xfmt, const float* w, const ConvGeom& g, int strict, const EpiDev& epi,
                    const OutDev& out, cudaStream_t s);
 void launch_maxpool(const void* x, int xfmt, const ConvGeom& g, const OutDev& out, cudaStream_t s);
-void launch_sum_hw(const float* x, const Lay& L, int N, int H, int W, int C, float* y, cudaStream_t s);
+// The consumer dense's A operand written by the sum itself (cross-group fusion of
+// sum -> multiply(1/HW) -> realize -> dense): [Npad][Kp] int8 codes / bf16 / tf32.
+struct SumOperand {
+  void* ptr = nullptr;
+  int eb = 1, Kp = 0;
+  float pre_mul = 0.f;
+  int quant = 0;
+  QDev q{};
+};
+void launch_sum_hw(const float* x, const Lay& L, int N, int H, int W, int C, float* y, cudaStream_t s,
+                   const SumOperand* op = nullptr);
 void launch_dense_weight_t(const float* w, int M, int K, int Kp, const float* oc_scale, float scalar, int fmt,
                            int quant, QDev q, void* out, cudaStream_t s);
 void launch_dense(const float* x, int N, int K, int Kp, const void* w, int M, int mode, float pre_mul,
