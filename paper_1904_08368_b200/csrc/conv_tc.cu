@@ -151,6 +151,9 @@ struct TcArgs {
 #ifndef MRB200_P2_SATPACK
 #define MRB200_P2_SATPACK 1  // A/B: +0.6 % (saturating I2IP pack does the clip at 127)
 #endif
+#ifndef MRB200_TC_TIMELINE
+#define MRB200_TC_TIMELINE 0
+#endif
 #ifndef MRB200_MAGIC_RNI
 #define MRB200_MAGIC_RNI 1  // rint-to-int by the 1.5*2^23 add instead of a quarter-rate F2I (below)
 #endif
@@ -549,6 +552,18 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
     return t;
   };
   if ((a.dbg & 1024) && threadIdx.x == 0) atomicMin(&a.stamps[0], gtime());
+  // dbg 2048: CTA 0's per-tile timeline, tile index k = (mt - m_start) / m_step < 64
+  auto tstamp = [&](int mt, int f) {
+#if MRB200_TC_TIMELINE  // experiment builds only (make EXTRA=-DMRB200_TC_TIMELINE=1)
+    if ((a.dbg & 2048) && blockIdx.x == 0) {
+      const int k = (mt - (static_cast<int>(blockIdx.x) / a.n_tiles)) / (static_cast<int>(gridDim.x) / a.n_tiles);
+      if (k < 64) a.stamps[k * 8 + f] = gtime();
+    }
+#else
+    (void)mt;
+    (void)f;
+#endif
+  };
   pdl_trigger();  // the next launch may start its own prologue as SMs free up
   const int n_tile = blockIdx.x % a.n_tiles;
   const int m_start = blockIdx.x / a.n_tiles;
@@ -624,6 +639,7 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
         const int r0 = a.kb == 16 ? floor_div8(row0) : row0;
         for (int ks = 0; ks < a.k_stages; ++ks) {
           mbar_wait(&empty[stage], phase ^ 1);
+          if (ks == 0) tstamp(mt, 6);
           const bool load_b = !a.resident_b;
           mbar_expect_tx(&full[stage], a.a_stage_bytes + (load_b ? a.b_stage_bytes : 0));
           // A stage layout [pps][subs][hg rows][row]: one box per (plane, sub-grid, row block)
@@ -643,6 +659,7 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
             phase ^= 1;
           }
         }
+        tstamp(mt, 7);
       }
     }
   } else if (warp == 1) {
@@ -701,10 +718,12 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
         const int row0 = tile_row0(a, mt, msub);
         const uint32_t shift16 = a.kb == 16 ? static_cast<uint32_t>(row0 - 8 * floor_div8(row0)) * 16 : 0u;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tstamp(mt, 0);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc) * sub * bn;
         for (int ks = 0; ks < a.k_stages; ++ks) {
           mbar_wait(&full[stage], phase);
+          if (ks == 0) tstamp(mt, 1);
           tc_fence_after();
           const uint32_t sA = smA_u + stage * a.a_stage_bytes + shift16;
           const uint32_t sB = a.resident_b ? smB_u + ks * a.b_ks_stride : smB_u + stage * a.b_stage_bytes;
@@ -737,6 +756,7 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
           }
         }
         umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        tstamp(mt, 2);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -837,6 +857,7 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
       if ((a.dbg & 16) && a.pool && blockIdx.x == 0 && threadIdx.x == 64 && (mt - m_start) / m_step < 16)
         a.stamps[((mt - m_start) / m_step) * 8 + 5] = clock64();
       mbar_wait(&tfull[acc], acc_phase);
+      if (warp == 2 && lane == 0) tstamp(mt, 3);
       tc_fence_after();
       if (a.pool) {
         // ---- fused max_pool2d: stage the band's conv outputs, then pool ----
@@ -1014,6 +1035,8 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0 && warp == 2) tstamp(mt, 4);
+      if (lane == 0 && warp == 1 + EPIW) tstamp(mt, 5);
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -1269,6 +1292,9 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
         const int bst = 3 * pps * cand * kb;
         const int ast = pps * a.subs * nbox3 * hbox3 * row_bytes;
         int ns = (kSmemBudget - barrier_bytes) / (ast + bst);
+        // (Measured: accepting 2 stages for a 2-tile super-tile -- half the per-tile
+        // weight re-streaming of layers 3-4 -- made those convs 1.02-1.12x slower:
+        // the streamed-weight pipeline is latency-bound, depth beats width.)
         if (ns >= 3) {
           a.resident_b = 0;
           a.tap_groups = 3;
@@ -1575,7 +1601,7 @@ bool tc_conv_launch(TcConvPlan* p, const void* x, const Lay& xl, const void* w, 
   }();
   a.dbg = dbg;
   static unsigned long long* stamps = nullptr;
-  if ((dbg & (16 | 1024)) && !stamps) cudaMalloc(&stamps, 8 * 16 * 8);
+  if ((dbg & (16 | 1024 | 2048)) && !stamps) cudaMalloc(&stamps, 8 * 64 * 8 + 64);
   a.stamps = stamps;
   if (dbg & 1024) {
     unsigned long long init[4] = {~0ull, 0ull, ~0ull, 0ull};
@@ -1602,6 +1628,28 @@ bool tc_conv_launch(TcConvPlan* p, const void* x, const Lay& xl, const void* w, 
                    tc_conv_describe(p, buf, sizeof(buf)));
     }
   } stamp_print{s, stamps, p, (dbg & 1024) != 0};
+  struct TilePrint {  // dbg 2048: CTA 0's per-tile pipeline timeline (globaltimer ns, first 64 tiles)
+    cudaStream_t s;
+    unsigned long long* st;
+    bool on;
+    ~TilePrint() {
+      if (!on) return;
+      cudaStreamCaptureStatus cs;
+      cudaStreamIsCapturing(s, &cs);
+      if (cs != cudaStreamCaptureStatusNone) return;
+      unsigned long long h[64 * 8];
+      cudaStreamSynchronize(s);
+      cudaMemcpy(h, st, sizeof(h), cudaMemcpyDeviceToHost);
+      const unsigned long long t0 = h[6];
+      std::fprintf(stderr, "TILE  tma_first tma_last | mma_tempty mma_full0 mma_tfull | epi2_tfull epi2_done epi17_done (us from tile 0 TMA)\n");
+      for (int t = 0; t < 64 && h[t * 8 + 6]; ++t) {
+        auto us = [&](int f) { return h[t * 8 + f] ? (static_cast<double>(h[t * 8 + f]) - t0) / 1e3 : -1.0; };
+        std::fprintf(stderr, "TILE %2d %8.2f %8.2f | %8.2f %8.2f %8.2f | %8.2f %8.2f %8.2f\n", t, us(6), us(7), us(0),
+                     us(1), us(2), us(3), us(4), us(5));
+      }
+    }
+  } tile_print{s, stamps, (dbg & 2048) != 0};
+  if (dbg & 2048) cudaMemsetAsync(stamps, 0, 8 * 64 * 8, s);
   const int sig = epi_signature(epi, out);
   auto pow2 = [](float f) {
     int e = 0;

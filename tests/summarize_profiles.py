@@ -47,7 +47,7 @@ def main():
         fam[k] = (c + 1, t + float(r[I["Metric Value"]]))
     conv_i8 = sum(t for k, (c, t) in fam.items() if k.startswith("k_conv_tc<1"))
     other_i8 = sum(t for k, (c, t) in fam.items()
-                   if k.startswith(("k_input_s2d_ct<3, 3, 16", "k_dense_ks<0", "k_to_nchw")))
+                   if k.startswith(("k_input_s2d_ct<3, 3, 16", "k_dense_tc<1", "k_to_nchw")))
     other_i8 += sum(t for k, (c, t) in fam.items() if k.startswith("k_sum_hw")) / 2
     lines = ["# ncu launch list, round %s (final build)" % tag[1:], "",
              "Command (after the same command exited 0 without ncu, tests/final_profiles.sh):",
@@ -65,34 +65,59 @@ def main():
                  bench["roofline"]["share_of_step"])]
     open(os.path.join(PROF, tag + "_launches.md"), "w").write("\n".join(lines) + "\n")
 
-    # --set full summary
-    raw = subprocess.run(["ncu", "-i", os.path.join(OUT, "conv_full.ncu-rep"), "--page", "raw", "--csv"],
-                         capture_output=True, text=True).stdout
-    rr = list(csv.reader(raw.splitlines()))
-    if len(rr) > 2:
+    # --set full summaries: every captured launch, one row each
+    def full_table(rep, title, cmd, md):
+        if rep.endswith(".csv"):
+            if not os.path.exists(rep):
+                return
+            raw = open(rep).read()
+        else:
+            raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rr = list(csv.reader(raw.splitlines()))
+        if len(rr) <= 2:
+            return
         h, units, ks = rr[0], rr[1], rr[2:]
         J = {k: i for i, k in enumerate(h)}
-        want = [("gpu__time_duration.sum", "duration"), ("dram__bytes_read.sum", "DRAM read"),
-                ("dram__bytes_write.sum", "DRAM write"),
-                ("sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor pipe active % (elapsed)"),
-                ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots busy %"),
-                ("lts__t_sector_hit_rate.pct", "L2 hit rate %"), ("launch__registers_per_thread", "registers/thread"),
-                ("launch__grid_size", "grid"), ("launch__block_size", "block"),
-                ("smsp__sass_inst_executed_op_utcmma.sum", "tcgen05.mma instructions"),
-                ("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio", "stall long_scoreboard / issue"),
-                ("smsp__average_warps_issue_stalled_wait_per_issue_active.ratio", "stall wait / issue")]
-        names = ["stem+maxpool (fused21+20, TC_STEM_POOL)", "layer1 Ga (fused19: conv+bias+relu+requant)",
-                 "layer1 Gb (fused18: conv+bias+residual+relu, fp32 + int8 codes)"]
-        out = ["# ncu --set full, round %s (final build): first three tcgen05 conv launches of one int8 ResNet-18 b256 step"
-               % tag[1:], "",
-               "Command: `ncu --set full --clock-control none --import-source on -k regex:k_conv_tc -c 3 python "
-               "tests/profile_run.py int8 256 1`",
-               "(tests/final_profiles.sh; per-launch, cold-cache, serialised replay: absolute times differ from the "
-               "in-graph bench, shares agree).", "", "| metric | " + " | ".join(names) + " |", "|---|---|---|---|"]
-        for key, label in want:
-            if key in J:
-                out.append("| %s (%s) | %s |" % (label, units[J[key]], " | ".join(k[J[key]] for k in ks[:3])))
-        open(os.path.join(PROF, tag + "_conv_tc_full.md"), "w").write("\n".join(out) + "\n")
+        want = [("gpu__time_duration.sum", "us"), ("dram__bytes_read.sum", "DRAM rd MB"),
+                ("dram__bytes_write.sum", "DRAM wr MB"),
+                ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor pipe %"),
+                ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM %"),
+                ("sm__issue_active.avg.pct_of_peak_sustained_elapsed", "issue %"),
+                ("lts__t_sector_hit_rate.pct", "L2 hit %"), ("launch__registers_per_thread", "regs")]
+        out = ["# " + title, "", "Command: `%s`" % cmd,
+               "(per-launch, cold-cache, serialised replay under ncu: absolute times differ from the in-graph "
+               "bench, shares agree; DRAM MB in the units ncu reports).", "",
+               "| # | kernel | " + " | ".join(l for _, l in want) + " |", "|---|---|" + "---|" * len(want)]
+        kn = J.get("Kernel Name")
+        for i, k in enumerate(ks):
+            name = k[kn].split("(")[0].replace("void ", "").split("::")[-1][:48] if kn is not None else "?"
+            vals = []
+            for key, _ in want:
+                v = k[J[key]] if key in J else ""
+                try:
+                    v = "%.1f" % float(v.replace(",", ""))
+                except ValueError:
+                    pass
+                vals.append(v)
+            out.append("| %d | %s | %s |" % (i, name, " | ".join(vals)))
+        open(os.path.join(PROF, md), "w").write("\n".join(out) + "\n")
+
+    full_table(os.path.join(OUT, "conv_full_raw.csv"),
+               "ncu --set full, round %s: every tcgen05 conv launch of one int8 ResNet-18 b256 step "
+               "(input conversion, stem+pool, 19 convs, the fused sum + tcgen05 dense head)" % tag[1:],
+               "ncu --set full --clock-control none -k regex:\"k_conv_tc|k_dense_tc|k_sum_hw|k_input\" "
+               "-c 25 python tests/profile_run.py int8 256 1", tag + "_conv_tc_full.md")
+    full_table(os.path.join(OUT, "dw_full_raw.csv"),
+               "ncu --set full, round %s: the 13 depthwise launches of one MobileNet-v1 bf16 b256 step" % tag[1:],
+               "ncu --set full --clock-control none -k regex:k_dw3x3 -c 13 python tests/profile_model.py mobilenet_v1 fp32 256 1",
+               tag + "_dw_full.md")
+    for side in ("bench_c5", "bench_mbv1", "bench_vgg", "bench_dqn"):
+        f = os.path.join(OUT, side + ".json")
+        if os.path.exists(f):
+            try:
+                json.dump(last_json(f), open(os.path.join(PROF, "%s_%s.json" % (tag, side)), "w"))
+            except Exception:
+                pass
     print("profiles/ updated:", bench["value"], bench["ms_per_step"])
 
 
