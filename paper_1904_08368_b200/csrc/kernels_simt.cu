@@ -816,26 +816,27 @@ __global__ void __launch_bounds__(256, dw_minb(PL)) k_dw3x3_rb(const void* __res
   pdl_wait();
   constexpr int OUTS = dw_outs(PL), NCOL = (OUTS - 1) * SW + 3;
   const int owq = (g.OW + OUTS - 1) / OUTS;
-  const uint32_t pieces = static_cast<uint32_t>(g.C / 4);
-  const uint32_t total = pieces * g.N * g.OH * owq;
+  // blockIdx.y = a group of PL 4-channel pieces; the block's threads walk the
+  // output pixels of that channel group, so the 36 weights (and the epilogue's
+  // per-channel vectors) are loaded once per thread, not once per item
+  const uint32_t lo = threadIdx.x % PL, slot = threadIdx.x / PL, slots = blockDim.x / PL;
+  const uint32_t total = static_cast<uint32_t>(g.N) * g.OH * owq;
   const int Wp = g.W + 2 * kPad, Hp = g.H + 2 * kPad;
   const int OWp = g.OW + 2 * kPad, OHp = g.OH + 2 * kPad;
   const bool f32 = xfmt == FMT_F32;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const uint32_t lo = i & (PL - 1), ii = i / PL;
+  const int c0 = static_cast<int>(blockIdx.y * PL + lo) * 4;
+  float wr[4][9];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int tp = 0; tp < 9; ++tp) wr[k][tp] = __ldg(w + static_cast<int64_t>(c0 + k) * 9 + tp);
+  for (uint32_t ii = blockIdx.x * slots + slot; ii < total; ii += gridDim.x * slots) {
     const uint32_t t = fdiv(ii, fd_owq);
     const int oq = static_cast<int>(ii - t * static_cast<uint32_t>(owq));
-    const uint32_t t2 = fdiv(t, fd_oh);
-    const int oh = static_cast<int>(t - t2 * static_cast<uint32_t>(g.OH));
-    const uint32_t phi = fdiv(t2, fd_n);
-    const int n = static_cast<int>(t2 - phi * static_cast<uint32_t>(g.N));
-    const uint32_t pc = phi * PL + lo;
-    const int c0 = static_cast<int>(pc) * 4, ow0 = oq * OUTS;
-    float wr[4][9];
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-#pragma unroll
-      for (int tp = 0; tp < 9; ++tp) wr[k][tp] = __ldg(w + static_cast<int64_t>(c0 + k) * 9 + tp);
+    const uint32_t n32 = fdiv(t, fd_oh);
+    const int oh = static_cast<int>(t - n32 * static_cast<uint32_t>(g.OH));
+    const int n = static_cast<int>(n32);
+    const int ow0 = oq * OUTS;
     float acc[OUTS][4];
 #pragma unroll
     for (int o = 0; o < OUTS; ++o)
@@ -1750,7 +1751,13 @@ void launch_dwconv(const void* x, int xfmt, const float* w, const ConvGeom& g, i
                     c = make_fastdiv(static_cast<uint32_t>(g.N));
       auto kern = g.sw == 1 ? (pl16 ? k_dw3x3_rb<1, 16> : pl8 ? k_dw3x3_rb<1, 8> : k_dw3x3_rb<1, 1>)
                             : (pl16 ? k_dw3x3_rb<2, 16> : pl8 ? k_dw3x3_rb<2, 8> : k_dw3x3_rb<2, 1>);
-      pdl_launch(kern, grid_stride_blocks(tot), 256, 0, s, x, xfmt, w, g, strict, epi, out, a, b, c);
+      const int pl = pl16 ? 16 : pl8 ? 8 : 1;
+      const int64_t pix_items = static_cast<int64_t>(g.N) * g.OH * owq;
+      const unsigned gy = static_cast<unsigned>(g.C / (4 * pl));
+      // about 8 resident blocks' worth per SM over the whole grid
+      const unsigned gx = static_cast<unsigned>(std::max<int64_t>(
+          1, std::min<int64_t>((pix_items + 256 / pl - 1) / (256 / pl), (148 * 8 + gy - 1) / gy)));
+      pdl_launch(kern, dim3(gx, gy), 256, 0, s, x, xfmt, w, g, strict, epi, out, a, b, c);
       return;
     }
   }
