@@ -808,7 +808,11 @@ __global__ void __launch_bounds__(256) k_dwconv_fast(const void* __restrict__ x,
 // row, so every warp load / store is two whole 128-byte lines.
 constexpr int dw_outs(int pl) { return pl >= 8 ? 4 : 2; }
 constexpr int dw_minb(int pl) { return pl >= 8 ? 2 : 3; }
-template <int SW, int PL>
+// DSIG: compile-time epilogue for MobileNet's (bf16 out, no side output)
+// multiply(gamma') -> bias_add -> clip(0, 6) / relu with the per-channel vectors
+// held in registers; DSIG 0 interprets the op list.
+enum DwSig : int { DW_ANY = 0, DW_MULC_BIAS_CLIP = 1, DW_MULC_BIAS_RELU = 2 };
+template <int SW, int PL, int DSIG = DW_ANY>
 __global__ void __launch_bounds__(256, dw_minb(PL)) k_dw3x3_rb(const void* __restrict__ x, int xfmt, const float* __restrict__ w,
                                                   ConvGeom g, int strict, EpiDev epi, OutDev out, FastDiv fd_owq,
                                                   FastDiv fd_oh, FastDiv fd_n) {
@@ -830,6 +834,14 @@ __global__ void __launch_bounds__(256, dw_minb(PL)) k_dw3x3_rb(const void* __res
   for (int k = 0; k < 4; ++k)
 #pragma unroll
     for (int tp = 0; tp < 9; ++tp) wr[k][tp] = __ldg(w + static_cast<int64_t>(c0 + k) * 9 + tp);
+  float sv[2][4];  // DSIG != DW_ANY: gamma' and bias of this thread's 4 channels
+  if constexpr (DSIG != DW_ANY) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const float4 f = *reinterpret_cast<const float4*>(epi.vec[j] + c0);
+      sv[j][0] = f.x; sv[j][1] = f.y; sv[j][2] = f.z; sv[j][3] = f.w;
+    }
+  }
   for (uint32_t ii = blockIdx.x * slots + slot; ii < total; ii += gridDim.x * slots) {
     const uint32_t t = fdiv(ii, fd_owq);
     const int oq = static_cast<int>(ii - t * static_cast<uint32_t>(owq));
@@ -871,6 +883,22 @@ __global__ void __launch_bounds__(256, dw_minb(PL)) k_dw3x3_rb(const void* __res
             const float xv = col[o * SW + kw][k], wv = wr[k][kh * 3 + kw];
             acc[o][k] = strict ? __fadd_rn(acc[o][k], __fmul_rn(xv, wv)) : __fmaf_rn(xv, wv, acc[o][k]);
           }
+    }
+    if constexpr (DSIG != DW_ANY) {
+#pragma unroll
+      for (int o = 0; o < OUTS; ++o) {
+        if (ow0 + o >= g.OW) break;
+        float r[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          r[k] = __fadd_rn(__fmul_rn(acc[o][k], sv[0][k]), sv[1][k]);
+          r[k] = DSIG == DW_MULC_BIAS_CLIP ? clip_ref(r[k], epi.s[2], epi.s2[2]) : relu_ref(r[k]);
+        }
+        const int64_t pix = (static_cast<int64_t>(n) * OHp + oh + kPad) * OWp + ow0 + o + kPad;
+        *reinterpret_cast<uint2*>(static_cast<char*>(out.primary) + lay_byte(out.plan, pix, c0)) =
+            make_uint2(pack_bf16x2(r[0], r[1]), pack_bf16x2(r[2], r[3]));
+      }
+      continue;
     }
     // epilogue: the op list once per thread over OUTS x 4 values
     int32_t code[OUTS][4];
@@ -1751,6 +1779,18 @@ void launch_dwconv(const void* x, int xfmt, const float* w, const ConvGeom& g, i
                     c = make_fastdiv(static_cast<uint32_t>(g.N));
       auto kern = g.sw == 1 ? (pl16 ? k_dw3x3_rb<1, 16> : pl8 ? k_dw3x3_rb<1, 8> : k_dw3x3_rb<1, 1>)
                             : (pl16 ? k_dw3x3_rb<2, 16> : pl8 ? k_dw3x3_rb<2, 8> : k_dw3x3_rb<2, 1>);
+      // MobileNet's bf16 depthwise epilogues at compile time
+      const bool simple = (pl16 || pl8) && out.primary_fmt == FMT_BF16 && !out.side && epi.n_ops == 3 &&
+                          epi.op[0] == E_MULC && epi.op[1] == E_BIAS && (epi.op[2] == E_CLIP || epi.op[2] == E_RELU);
+      if (simple) {
+        const bool clip = epi.op[2] == E_CLIP;
+        if (g.sw == 1)
+          kern = pl16 ? (clip ? k_dw3x3_rb<1, 16, DW_MULC_BIAS_CLIP> : k_dw3x3_rb<1, 16, DW_MULC_BIAS_RELU>)
+                      : (clip ? k_dw3x3_rb<1, 8, DW_MULC_BIAS_CLIP> : k_dw3x3_rb<1, 8, DW_MULC_BIAS_RELU>);
+        else
+          kern = pl16 ? (clip ? k_dw3x3_rb<2, 16, DW_MULC_BIAS_CLIP> : k_dw3x3_rb<2, 16, DW_MULC_BIAS_RELU>)
+                      : (clip ? k_dw3x3_rb<2, 8, DW_MULC_BIAS_CLIP> : k_dw3x3_rb<2, 8, DW_MULC_BIAS_RELU>);
+      }
       const int pl = pl16 ? 16 : pl8 ? 8 : 1;
       const int64_t pix_items = static_cast<int64_t>(g.N) * g.OH * owq;
       const unsigned gy = static_cast<unsigned>(g.C / (4 * pl));
