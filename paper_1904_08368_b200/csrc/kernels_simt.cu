@@ -811,7 +811,8 @@ constexpr int dw_minb(int pl) { return pl >= 8 ? 2 : 3; }
 // DSIG: compile-time epilogue for MobileNet's (bf16 out, no side output)
 // multiply(gamma') -> bias_add -> clip(0, 6) / relu with the per-channel vectors
 // held in registers; DSIG 0 interprets the op list.
-enum DwSig : int { DW_ANY = 0, DW_MULC_BIAS_CLIP = 1, DW_MULC_BIAS_RELU = 2 };
+// DW_MULC_BIAS_CLIP_REQ: the int8 modules' form, realize codes as the primary output.
+enum DwSig : int { DW_ANY = 0, DW_MULC_BIAS_CLIP = 1, DW_MULC_BIAS_RELU = 2, DW_MULC_BIAS_CLIP_REQ = 3 };
 template <int SW, int PL, int DSIG = DW_ANY>
 __global__ void __launch_bounds__(256, dw_minb(PL)) k_dw3x3_rb(const void* __restrict__ x, int xfmt, const float* __restrict__ w,
                                                   ConvGeom g, int strict, EpiDev epi, OutDev out, FastDiv fd_owq,
@@ -892,11 +893,18 @@ __global__ void __launch_bounds__(256, dw_minb(PL)) k_dw3x3_rb(const void* __res
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           r[k] = __fadd_rn(__fmul_rn(acc[o][k], sv[0][k]), sv[1][k]);
-          r[k] = DSIG == DW_MULC_BIAS_CLIP ? clip_ref(r[k], epi.s[2], epi.s2[2]) : relu_ref(r[k]);
+          r[k] = DSIG == DW_MULC_BIAS_RELU ? relu_ref(r[k]) : clip_ref(r[k], epi.s[2], epi.s2[2]);
         }
         const int64_t pix = (static_cast<int64_t>(n) * OHp + oh + kPad) * OWp + ow0 + o + kPad;
-        *reinterpret_cast<uint2*>(static_cast<char*>(out.primary) + lay_byte(out.plan, pix, c0)) =
-            make_uint2(pack_bf16x2(r[0], r[1]), pack_bf16x2(r[2], r[3]));
+        char* dst = static_cast<char*>(out.primary) + lay_byte(out.plan, pix, c0);
+        if constexpr (DSIG == DW_MULC_BIAS_CLIP_REQ) {
+          uint32_t u = 0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) u |= (static_cast<uint32_t>(quant_code(r[k], epi.q[3])) & 0xff) << (8 * k);
+          *reinterpret_cast<uint32_t*>(dst) = u;
+        } else {
+          *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16x2(r[0], r[1]), pack_bf16x2(r[2], r[3]));
+        }
       }
       continue;
     }
@@ -1782,6 +1790,10 @@ void launch_dwconv(const void* x, int xfmt, const float* w, const ConvGeom& g, i
       // MobileNet's bf16 depthwise epilogues at compile time
       const bool simple = (pl16 || pl8) && out.primary_fmt == FMT_BF16 && !out.side && epi.n_ops == 3 &&
                           epi.op[0] == E_MULC && epi.op[1] == E_BIAS && (epi.op[2] == E_CLIP || epi.op[2] == E_RELU);
+      const bool simple_q = !pl16 && !pl8 && out.primary_fmt == FMT_I8 && !out.side && epi.n_ops == 4 &&
+                            epi.op[0] == E_MULC && epi.op[1] == E_BIAS && epi.op[2] == E_CLIP && epi.op[3] == E_REQ &&
+                            !epi.q[3].ovf;
+      if (simple_q) kern = g.sw == 1 ? k_dw3x3_rb<1, 1, DW_MULC_BIAS_CLIP_REQ> : k_dw3x3_rb<2, 1, DW_MULC_BIAS_CLIP_REQ>;
       if (simple) {
         const bool clip = epi.op[2] == E_CLIP;
         if (g.sw == 1)
