@@ -997,6 +997,60 @@ __global__ void __launch_bounds__(256, dw_minb(PL)) k_dw3x3_rb(const void* __res
 // index math; the window's taps are 16-byte loads from the padded P16 input
 // (padded taps skipped, like the reference's bounds test).  Also emits the
 // consumers' second copy (int8 codes or bf16) when requested.
+// 2x2 / stride-2 / pad-0 pooling (VGG): every window tap is inside the image, so
+// the reference's seeded ordered max is max(max(a, b), max(c, d)) in tap order
+// with its std::max comparison; one thread = one output pixel x one 16-byte input
+// granule (8 bf16 / 4 fp32 channels), 4 loads issued together, one 16-byte store
+// when the output layout keeps the granule's channels contiguous.
+template <int EB>
+__global__ void __launch_bounds__(256) k_maxpool2x2(const void* __restrict__ x, ConvGeom g, OutDev out,
+                                                    FastDiv fd_ow, FastDiv fd_oh, FastDiv fd_n, int vec_store) {
+  pdl_trigger();
+  pdl_wait();
+  constexpr int CPG = 16 / EB;
+  const uint32_t grans = static_cast<uint32_t>(g.C / CPG);
+  const uint32_t total = grans * g.N * g.OH * g.OW;
+  const int Hp = g.H + 2 * kPad, Wp = g.W + 2 * kPad, OHp = g.OH + 2 * kPad, OWp = g.OW + 2 * kPad;
+  const int64_t row = static_cast<int64_t>(Wp) * g.in.kb;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const uint32_t t = fdiv(i, fd_ow);
+    const int ow = static_cast<int>(i - t * static_cast<uint32_t>(g.OW));
+    const uint32_t t2 = fdiv(t, fd_oh);
+    const int oh = static_cast<int>(t - t2 * static_cast<uint32_t>(g.OH));
+    const uint32_t gran = fdiv(t2, fd_n);
+    const int n = static_cast<int>(t2 - gran * static_cast<uint32_t>(g.N));
+    const int c0 = static_cast<int>(gran) * CPG;
+    const char* src = static_cast<const char*>(x) +
+                      lay_byte(g.in, (static_cast<int64_t>(n) * Hp + 2 * oh + kPad) * Wp + 2 * ow + kPad, c0);
+    const uint4 q[4] = {__ldg(reinterpret_cast<const uint4*>(src)), __ldg(reinterpret_cast<const uint4*>(src + g.in.kb)),
+                        __ldg(reinterpret_cast<const uint4*>(src + row)),
+                        __ldg(reinterpret_cast<const uint4*>(src + row + g.in.kb))};
+    float acc[8];
+#pragma unroll
+    for (int tp = 0; tp < 4; ++tp) {
+      const uint32_t w4[4] = {q[tp].x, q[tp].y, q[tp].z, q[tp].w};
+#pragma unroll
+      for (int k = 0; k < CPG; ++k) {
+        const float v = EB == 4 ? __uint_as_float(w4[k]) : __uint_as_float(k & 1 ? (w4[k >> 1] & 0xffff0000u) : (w4[k >> 1] << 16));
+        acc[k] = tp == 0 ? v : (acc[k] < v ? v : acc[k]);  // std::max(acc, v), taps in (kh, kw) order
+      }
+    }
+    const int64_t pix = (static_cast<int64_t>(n) * OHp + oh + kPad) * OWp + ow + kPad;
+    if (vec_store) {
+      char* d = static_cast<char*>(out.primary) + lay_byte(out.plan, pix, c0);
+      if constexpr (EB == 4)
+        *reinterpret_cast<float4*>(d) = make_float4(f32_out(out, acc[0]), f32_out(out, acc[1]), f32_out(out, acc[2]),
+                                                    f32_out(out, acc[3]));
+      else
+        *reinterpret_cast<uint4*>(d) = make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]),
+                                                  pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7]));
+    } else {
+#pragma unroll
+      for (int k = 0; k < CPG; ++k) store_out(out, acc[k], 0, pix, c0 + k);
+    }
+  }
+}
+
 __global__ void k_maxpool(const void* __restrict__ x, int xfmt, ConvGeom g, OutDev out) {
   pdl_trigger();
   pdl_wait();
@@ -1828,6 +1882,19 @@ void launch_dwconv(const void* x, int xfmt, const float* w, const ConvGeom& g, i
 
 void launch_maxpool(const void* x, int xfmt, const ConvGeom& g, const OutDev& out, cudaStream_t s) {
   int cpg = xfmt == FMT_F32 ? 4 : 8;
+  if (g.KH == 2 && g.KW == 2 && g.sh == 2 && g.sw == 2 && g.ph == 0 && g.pw == 0 && g.H % 2 == 0 && g.W % 2 == 0 &&
+      g.C % cpg == 0 && g.in.kind == LAY_NORMAL && g.in.cpc % cpg == 0 && !out.side && out.primary_fmt == xfmt &&
+      out.plan.kind == LAY_NORMAL && (xfmt == FMT_F32 || xfmt == FMT_BF16)) {
+    const int vec = out.plan.cpc >= cpg && out.plan.cpc % cpg == 0 && out.primary_fmt != FMT_I8 ? 1 : 0;
+    const int64_t total = static_cast<int64_t>(g.C / cpg) * g.N * g.OH * g.OW;
+    if (total < (int64_t(1) << 31)) {
+      const FastDiv a = make_fastdiv(static_cast<uint32_t>(g.OW)), b = make_fastdiv(static_cast<uint32_t>(g.OH)),
+                    c = make_fastdiv(static_cast<uint32_t>(g.N));
+      pdl_launch(xfmt == FMT_F32 ? k_maxpool2x2<4> : k_maxpool2x2<2>, grid_stride_blocks(total), 256, 0, s, x, g, out,
+                 a, b, c, vec);
+      return;
+    }
+  }
   int64_t total = static_cast<int64_t>(g.N) * g.OH * g.OW * ((g.C + cpg - 1) / cpg);
   pdl_launch(k_maxpool, grid_stride_blocks(total), kThreads, 0, s, x, xfmt, g, out);
 }
