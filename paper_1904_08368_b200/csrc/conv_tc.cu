@@ -1107,14 +1107,25 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
       bool k3 = sp.KH == 3 && sp.KW == 3, k1 = sp.KH == 1 && sp.KW == 1;
       if (!k3 && !k1) return false;
       kb = swz_kb(sp.C);
+      // a few channels (a 3-channel first conv, VGG-16): one 16-byte chunk per pixel
+      // (no swizzle, 8-pixel core-matrix rows) and two taps per 32-byte MMA K step
+      // (the second K half = the next tap's row shift, LBO = the shift difference);
+      // the 9th tap pairs with a zero-weight dummy tap
+      // (whatever chunk width was asked for: a single 16-byte plane has no other form)
+      const bool tiny = k3 && sp.C * eb <= 16 && (eb == 1 || eb == 2);
+      if (tiny) {
+        kb = 16;
+        pair_taps = true;
+      }
       if (!kb) return false;
       a.Hg = sp.H + 2 * kPad;
       a.Wg = sp.W + 2 * kPad;
       a.out_mode = OUT_SAME;
-      cc = sp.C * eb / kb;
+      cc = tiny ? 1 : sp.C * eb / kb;
       a.subs = 1;
       for (int kh = 0; kh < sp.KH; ++kh)
         for (int kw = 0; kw < sp.KW; ++kw) taps.push_back({0, k3 ? (kh - 1) * a.Wg + (kw - 1) : 0});
+      if (tiny) taps.push_back({0, taps.back().delta + 1});  // zero-weight partner of the 9th tap
       break;
     }
     case TC_S2_PHASE: {
@@ -1388,7 +1399,7 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
       for (int t = 0; t < ntaps; t += 2) {
         MmaStep m;
         m.a_off = static_cast<uint32_t>(taps[t].delta - dmin) * 16;
-        m.a_lbo = 16;
+        m.a_lbo = static_cast<uint32_t>(taps[t + 1].delta - taps[t].delta) * 16;  // the pair's second tap
         m.b_off = static_cast<uint32_t>(t * bplanes) * b_plane;
         m.b_lbo = static_cast<uint32_t>(bplanes) * b_plane;
         a.steps[a.n_steps++] = m;

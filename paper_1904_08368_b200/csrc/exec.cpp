@@ -1266,6 +1266,8 @@ void prepare_weights(Exec& ex, cudaStream_t s) {
     }
     void* dst = nullptr;
     CK(cudaMalloc(&dst, static_cast<size_t>(n * elem_bytes(fmt))));
+    if ((wl == WL_TC || wl == WL_S2D) && ex.group_tc[gi].taps > KH * KW)  // zero-weight dummy taps (paired-tap convs)
+      CK(cudaMemsetAsync(dst, 0, static_cast<size_t>(n * elem_bytes(fmt)), s));
     if (dtc)
       dense_tc_prep_weight(dtc, raw, static_cast<const float*>(ex.group_vecs[gi][0]), w.scalar_scale,
                            w.quant ? 1 : 0, to_qdev(w.q), dst, s);
