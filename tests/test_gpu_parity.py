@@ -297,3 +297,40 @@ def test_combine_conv_module_matches_reference(gpu, prec, fm, gold_name, batch, 
         assert np.array_equal(bits(y), bits(gold)), int(np.sum(bits(y) != bits(gold)))
     else:
         assert normwise(y, gold) <= BF16_TOL
+
+
+@pytest.mark.gpu
+def test_unproven_int8_group_is_refused(gpu):
+    """SURVEY F4 / ADVICE: int8 exactness needs every partial sum below 2^24 quanta.
+    Weights scaled so every code saturates at +-127 on K = 4608 break the bound
+    (127 * 4608 * 128 > 2^24): set_weights must refuse with MR_ERR_INEXACT_INT8 (104)
+    instead of running a group whose result could differ from interp()."""
+    text, meta, src = mrb.load_model("resnet18", "int8")
+    w = modelzoo.make_weights(src, seed=meta["weights_seed"])
+    big = {k: (v * 1e4 if v.ndim == 4 and v.shape[1] == 512 else v) for k, v in w.items()}
+    ex = mrb.Executor(text, batch=2)
+    with pytest.raises(mrb.BackendError) as e:
+        ex.set_weights([big[p.name] for p in src.params if p.kind != "input"])
+    assert e.value.code == mrb.MR_ERR_INEXACT_INT8
+    assert "2^24" in str(e.value)
+
+
+@pytest.mark.gpu
+def test_run_device_writes_caller_output_and_rejects_host_pointer(gpu):
+    """mr_exec_run: the final launch writes the caller's device buffer (one graph
+    per input/output address set; two outputs hold the same bits), and a host
+    pointer as output fails cleanly with MR_ERR_INVALID_ARGUMENT."""
+    import torch
+    ex, src = setup("resnet18_tiny", "int8", 4)
+    gold = np.load(os.path.join(GOLD, "resnet18_tiny_b4.npz"))["int8"]
+    xd = torch.from_numpy(modelzoo.make_inputs(src, 4, seed=0)).cuda()
+    outs = [torch.full(ex.output_shape, float("nan"), device="cuda") for _ in range(2)]
+    for o in outs + outs:
+        ex.run_device(xd.data_ptr(), xd.shape, o.data_ptr())
+    torch.cuda.synchronize()
+    for o in outs:
+        assert np.array_equal(bits(o.cpu().numpy()), bits(gold))
+    host = np.empty(ex.output_shape, np.float32)
+    with pytest.raises(mrb.BackendError) as e:
+        ex.run_device(xd.data_ptr(), xd.shape, host.ctypes.data)
+    assert e.value.code == 102
