@@ -125,6 +125,11 @@ struct TcArgs {
   MmaStep steps[kMaxSteps];
   uint32_t b_ks_stride;  // resident B: bytes between consecutive K stages
   int32_t resident_b;
+  // CTA pair (cluster of 2, tcgen05 cta_group::2): one M=256 MMA covers both
+  // CTAs' 128-row tiles; each CTA stages its own A rows and HALF of the N tile's
+  // weight rows (bn_local = bn / 2), so per-SM weight traffic and smem halve.
+  // m_tiles then counts pair units (CTA r takes super-tile 2 * unit + r).
+  int32_t pair, bn_local;
   int32_t a_stage_bytes, b_stage_bytes, b_res_bytes, n_stages;
   uint32_t idesc;
   int32_t out_mode, OH, OW;  // OUT_REMAP: valid outputs are grid (y < OH, x < OW)
@@ -524,7 +529,9 @@ __device__ __forceinline__ int tile_row0(const TcArgs& a, int mt, int msub) { re
 // EPIW epilogue warps (a multiple of 4: one group per TMEM lane quarter).
 // (Measured: 12 warps with twice the registers, each keeping the next item's
 // residual loads in flight, made the residual convs 1.21-1.29x slower.)
-template <int EB, int SIG, bool CAL, int EPIW = kEpiWarps>
+// PAIR: cluster-of-2 instantiation (tcgen05 cta_group::2 only -- a kernel using
+// cta_group::2 must be launched in clusters, so the two modes are separate kernels).
+template <int EB, int SIG, bool CAL, bool PAIR, int EPIW = kEpiWarps>
 __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
     k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -565,9 +572,15 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
 #endif
   };
   pdl_trigger();  // the next launch may start its own prologue as SMs free up
-  const int n_tile = blockIdx.x % a.n_tiles;
-  const int m_start = blockIdx.x / a.n_tiles;
-  const int m_step = gridDim.x / a.n_tiles;
+  // pair mode: the cluster's two CTAs share one work unit; rank 0 (leader)
+  // issues the MMAs and owns the full / tempty / bfull barriers the pair uses
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  const int cta = PAIR ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+  const int ncta = PAIR ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
+  auto own = [&](int mt) { return PAIR ? 2 * mt + static_cast<int>(rank) : mt; };  // this CTA's super-tile
+  const int n_tile = cta % a.n_tiles;
+  const int m_start = cta / a.n_tiles;
+  const int m_step = ncta / a.n_tiles;
   const int m_end = a.m_tiles;
   const int tcols = 2 * a.sub * a.bn;
   const uint32_t tmem_cols = tcols <= 32 ? 32 : tcols <= 64 ? 64 : tcols <= 128 ? 128 : tcols <= 256 ? 256 : 512;
@@ -579,29 +592,36 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], EPIW);
+      mbar_init(&tempty[i], EPIW * (PAIR ? 2 : 1));
     }
     mbar_init(bfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
     // resident weights are static (prepared at set_weights): load them before
-    // waiting for the previous kernel
-    if (a.resident_b) {
+    // waiting for the previous kernel (pair: after the cluster barrier below,
+    // which publishes the leader's bfull initialisation to the peer)
+    if (a.resident_b && !PAIR) {
       mbar_expect_tx(bfull, a.b_res_bytes);
       tma_load_4d(smB, &tmB, bfull, 0, n_tile * a.bn / (a.kb == 16 ? 8 : 1), 0, 0);
     }
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(tmem_cols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (PAIR) {  // one warp of each CTA of the pair, jointly
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(tmem_cols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(tmem_cols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   // stage this CTA's per-channel epilogue vectors (and b*c1) in shared memory
   float* s_vec = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + a.vec_off);
   int* s_p2ok = reinterpret_cast<int*>(s_vec + (kVecSlots + 1) * 256);
   {
-    const int c0 = (blockIdx.x % a.n_tiles) * a.bn;
+    const int c0 = n_tile * a.bn;
     if (!(a.dbg & 128))
     for (int k = 0; k < a.epi.n_ops; ++k)
       if (a.vec_slot[k] >= 0)
@@ -620,9 +640,14 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
     if (threadIdx.x == 0) *s_p2ok = ok;
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (PAIR && a.resident_b && threadIdx.x == 0) {  // each CTA its half of the N tile's rows
+    if (rank == 0) mbar_expect_tx(bfull, 2 * a.b_res_bytes);
+    tma_load_4d_pair(smB, &tmB, mapa_u32(bfull, 0), 0, n_tile * a.bn + static_cast<int>(rank) * a.bn_local, 0, 0);
+  }
   pdl_wait();  // activations (A, residuals, outputs) belong to the previous kernels from here on
   if ((a.dbg & 1024) && threadIdx.x == 0) atomicMax(&a.stamps[1], gtime());
 
@@ -634,26 +659,39 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int mt = m_start; mt < m_end; mt += m_step) {
-        const int row0 = tile_row0(a, mt, msub);
+        const int row0 = tile_row0(a, own(mt), msub);
         // no-swizzle (kb 16) maps move 8-pixel 128-byte rows; swizzled maps one pixel row
         const int r0 = a.kb == 16 ? floor_div8(row0) : row0;
         for (int ks = 0; ks < a.k_stages; ++ks) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (ks == 0) tstamp(mt, 6);
           const bool load_b = !a.resident_b;
-          mbar_expect_tx(&full[stage], a.a_stage_bytes + (load_b ? a.b_stage_bytes : 0));
+          const uint32_t stage_tx = a.a_stage_bytes + (load_b ? a.b_stage_bytes : 0);
+          if (!PAIR) mbar_expect_tx(&full[stage], stage_tx);
+          else if (rank == 0) mbar_expect_tx(&full[stage], 2 * stage_tx);  // both CTAs' bytes land on the leader's barrier
+          const uint32_t full_c = PAIR ? mapa_u32(&full[stage], 0) : 0u;
           // A stage layout [pps][subs][hg rows][row]: one box per (plane, sub-grid, row block)
           uint8_t* dA = smA + stage * a.a_stage_bytes;
           const int kc = ks / a.tap_groups, tg = ks - kc * a.tap_groups;  // chunk stage, kernel row
           const int rg = r0 + tg * a.Wg;
           for (int pl = 0; pl < a.pps; ++pl)
             for (int sg = 0; sg < a.subs; ++sg)
-              for (int bx = 0; bx < a.nbox; ++bx)
-                tma_load_4d(dA + ((pl * a.subs + sg) * a.hg + bx * a.hbox) * row_bytes, &tmA, &full[stage], 0,
-                            rg + bx * a.hbox, a.region_sg[sg], kc * a.pps + pl);
-          if (load_b)
-            tma_load_4d(smB + stage * a.b_stage_bytes, &tmB, &full[stage], 0, n_tile * a.bn / (a.kb == 16 ? 8 : 1),
-                        kc * a.pps, tg * (a.tap_groups > 1 ? 3 : 0));
+              for (int bx = 0; bx < a.nbox; ++bx) {
+                uint8_t* dst = dA + ((pl * a.subs + sg) * a.hg + bx * a.hbox) * row_bytes;
+                if constexpr (PAIR)
+                  tma_load_4d_pair(dst, &tmA, full_c, 0, rg + bx * a.hbox, a.region_sg[sg], kc * a.pps + pl);
+                else
+                  tma_load_4d(dst, &tmA, &full[stage], 0, rg + bx * a.hbox, a.region_sg[sg], kc * a.pps + pl);
+              }
+          if (load_b) {
+            const int brow = n_tile * a.bn / (a.kb == 16 ? 8 : 1) + static_cast<int>(rank) * a.bn_local;
+            if constexpr (PAIR)
+              tma_load_4d_pair(smB + stage * a.b_stage_bytes, &tmB, full_c, 0, brow, kc * a.pps,
+                               tg * (a.tap_groups > 1 ? 3 : 0));
+            else
+              tma_load_4d(smB + stage * a.b_stage_bytes, &tmB, &full[stage], 0, brow, kc * a.pps,
+                          tg * (a.tap_groups > 1 ? 3 : 0));
+          }
           if (++stage == a.n_stages) {
             stage = 0;
             phase ^= 1;
@@ -669,7 +707,7 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
     // (a handful of uniform adds per tcgen05.mma, no per-MMA loads).  A
     // super-tile is `sub` 128-row M tiles sharing every B descriptor: one
     // stage wait, one accumulator wait and two commits per super-tile.
-    if (elect_one()) {
+    if (rank == 0 && elect_one()) {  // pair: the leader issues for both CTAs
       if (a.resident_b) mbar_wait(bfull, 0);
       int stage = 0;
       uint32_t phase = 0;
@@ -682,7 +720,7 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
       const uint32_t n_steps = static_cast<uint32_t>(a.n_steps);
       const uint32_t sub_step16 = static_cast<uint32_t>(kTileM * a.kb) >> 4;  // 128 rows, in descriptor units
       const bool no_mma = (a.dbg & 4) != 0;
-      if (a.win) {
+      if (!PAIR && a.win) {
         // TC_STEM_POOL: one A stage per M tile, 3 window rows x 3 window columns
         for (int mt = m_start; mt < a.m_tiles; mt += m_step) {
           const int row0 = tile_row0(a, mt, msub);
@@ -715,7 +753,7 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
         }
       } else
       for (int mt = m_start; mt < a.m_tiles; mt += m_step) {
-        const int row0 = tile_row0(a, mt, msub);
+        const int row0 = tile_row0(a, own(mt), msub);
         const uint32_t shift16 = a.kb == 16 ? static_cast<uint32_t>(row0 - 8 * floor_div8(row0)) * 16 : 0u;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tstamp(mt, 0);
@@ -730,32 +768,48 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
           const uint32_t a16 = sA >> 4, b16 = sB >> 4;
           // the sub-tile count is a compile-time constant inside the step loop
           // (the issue loop is on the critical path of the N=64 convs)
-          auto issue = [&](auto sub_c) {
+          auto issue = [&](auto sub_c, auto pair_c) {
             constexpr uint32_t S = decltype(sub_c)::value;
+            constexpr bool P = decltype(pair_c)::value;
             for (uint32_t st = 0; st < n_steps; ++st) {
               const uint64_t bd = hi | (a.steps[st].b_lo + b16);
               const uint32_t alo = a.steps[st].a_lo + a16;
               const uint32_t accum = (ks | st) != 0 ? 1u : 0u;
 #pragma unroll
-              for (uint32_t sb = 0; sb < S; ++sb)
-                umma<EB>(tmem_d + sb * bn, hi | (alo + sb * sub_step16), bd, idesc, accum);
+              for (uint32_t sb = 0; sb < S; ++sb) {
+                if constexpr (P) umma_pair<EB>(tmem_d + sb * bn, hi | (alo + sb * sub_step16), bd, idesc, accum);
+                else umma<EB>(tmem_d + sb * bn, hi | (alo + sb * sub_step16), bd, idesc, accum);
+              }
             }
           };
+          using T_ = std::true_type;
+          using F_ = std::false_type;
           if (!no_mma) {
-            switch (sub) {
-              case 1: issue(std::integral_constant<uint32_t, 1>{}); break;
-              case 2: issue(std::integral_constant<uint32_t, 2>{}); break;
-              case 3: issue(std::integral_constant<uint32_t, 3>{}); break;
-              default: issue(std::integral_constant<uint32_t, 4>{}); break;
+            if constexpr (PAIR) {
+              switch (sub) {
+                case 1: issue(std::integral_constant<uint32_t, 1>{}, T_{}); break;
+                default: issue(std::integral_constant<uint32_t, 2>{}, T_{}); break;
+              }
+            } else {
+              switch (sub) {
+                case 1: issue(std::integral_constant<uint32_t, 1>{}, F_{}); break;
+                case 2: issue(std::integral_constant<uint32_t, 2>{}, F_{}); break;
+                case 3: issue(std::integral_constant<uint32_t, 3>{}, F_{}); break;
+                default: issue(std::integral_constant<uint32_t, 4>{}, F_{}); break;
+              }
             }
           }
-          umma_commit(&empty[stage]);  // frees the smem stage when these MMAs retire
+          // frees the smem stage (both CTAs' halves in pair mode) when these MMAs retire
+          if constexpr (PAIR) umma_commit_pair(&empty[stage], 3);
+          else umma_commit(&empty[stage]);
           if (++stage == a.n_stages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        // accumulator ready for the epilogue (pair: both CTAs' epilogues)
+        if constexpr (PAIR) umma_commit_pair(&tfull[acc], 3);
+        else umma_commit(&tfull[acc]);
         tstamp(mt, 2);
         if (++acc == 2) {
           acc = 0;
@@ -779,7 +833,7 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
     float* stg = reinterpret_cast<float*>(smem_pool);
     const bool p2ok = a.p2 && *s_p2ok && !(a.dbg & 64);
     {
-      if (a.win) {
+      if (!PAIR && a.win) {
         // TC_STEM_POOL epilogue: lane = pooled pixel, warp slice = 16-channel
         // chunk.  The reference pools relu(bias + acc * s) with its ordered
         // max over the valid window taps; bias_add / relu / (* s > 0) are
@@ -974,7 +1028,7 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
       const int lgc = 31 - __clz(chunks);  // chunks = bn / 16 is a power of two
       // where sub-tile sb's row of this lane lands (valid: a real output pixel)
       auto decode = [&](int sb, RowDst& dd, bool& vv) {
-        const uint32_t q = static_cast<uint32_t>(mt * a.sub + sb) * kTileM + row;  // grids < 2^31 pixels
+        const uint32_t q = static_cast<uint32_t>(own(mt) * a.sub + sb) * kTileM + row;  // grids < 2^31 pixels
         vv = q < static_cast<uint32_t>(a.Pg);
         dd.border = false;
         dd.pix = 0;
@@ -1038,7 +1092,10 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if constexpr (PAIR) mbar_arrive_cluster(mapa_u32(&tempty[acc], 0));  // the leader's MMA waits on both CTAs
+        else mbar_arrive(&tempty[acc]);
+      }
       if (lane == 0 && warp == 2) tstamp(mt, 4);
       if (lane == 0 && warp == 1 + EPIW) tstamp(mt, 5);
       if (++acc == 2) {
@@ -1050,10 +1107,19 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
 epilogue_done:
   if ((a.dbg & 1024) && threadIdx.x == 64) atomicMax(&a.stamps[3], gtime());
   tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols));
+  if constexpr (PAIR) {
+    // the peer's last tempty arrivals target the leader: neither CTA leaves first
+    cluster_sync_all();
+    if (warp == 1) {
+      tc_fence_after();
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols));
+    }
+  } else {
+    __syncthreads();
+    if (warp == 1) {
+      tc_fence_after();
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols));
+    }
   }
 }
 
@@ -1270,8 +1336,12 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
   a.tap_groups = 1;
   const bool trs_ok = sp.kind == TC_S1 && ntaps == 9 && kb >= 64 && !pair_taps && !a.win && !sp.pool &&
                       !std::getenv("MRB200_NO_TAP_ROWS");
-  auto try_cfg = [&](int cand, int sub, bool resident) {
-    if (sp.OC % cand || 2 * sub * cand > 512) return false;
+  // pair mode (cta_group::2) for this attempt: each CTA stages bn / 2 weight rows
+  int pm = 0;
+  auto try_cfg = [&](int cand_full, int sub, bool resident) {
+    if (sp.OC % cand_full || 2 * sub * cand_full > 512) return false;
+    if (pm && ((cand_full >> 1) % 16 || sub > 2)) return false;
+    const int cand = cand_full >> pm;  // weight rows staged per CTA
     int hg, nbox, hbox;
     if (!geom(sub, &hg, &nbox, &hbox)) return false;
     const int rows_bytes = hg * row_bytes;
@@ -1283,10 +1353,11 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
         int ns = (kSmemBudget - barrier_bytes - b_res) / a_stage(pps);
         if (ns >= 3) {
           a.resident_b = 1;
+          a.tap_groups = 1;  // (a later search may follow a streamed-by-kernel-row success)
           a.b_res_bytes = b_res;
           a.pps = pps;
           a.n_stages = ns > 8 ? 8 : ns;
-          a.bn = cand;
+          a.bn = cand_full;
           a.sub = sub;
           a.hg = hg;
           a.nbox = nbox;
@@ -1316,7 +1387,7 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
           a.pps = pps;
           a.b_stage_bytes = bst;
           a.n_stages = ns > 8 ? 8 : ns;
-          a.bn = cand;
+          a.bn = cand_full;
           a.sub = sub;
           a.hg = nbox3 * hbox3;
           a.nbox = nbox3;
@@ -1332,10 +1403,11 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
       int ns = (kSmemBudget - barrier_bytes) / (a_stage(pps) + bst);
       if (ns >= 2) {
         a.resident_b = 0;
+        a.tap_groups = 1;
         a.pps = pps;
         a.b_stage_bytes = bst;
         a.n_stages = ns > 6 ? 6 : ns;
-        a.bn = cand;
+        a.bn = cand_full;
         a.sub = sub;
         a.hg = hg;
         a.nbox = nbox;
@@ -1376,16 +1448,52 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
     found = try_cfg(sp.OC, sub, true);
     if (!found || a.n_stages < 2) return false;
   } else {
-    for (int cand = bn > 256 ? 256 : bn; cand >= 16 && !found; cand /= 2) {
-      for (int sub : {4, 2, 1}) {
-        if (!force_stream && try_cfg(cand, sub, true)) { found = true; break; }
-        if (try_cfg(cand, sub, false)) { found = true; break; }
+    static const int pair_maxbn = [] {
+      const char* e = std::getenv("MRB200_TC_PAIR_MAXBN");
+      return e ? std::atoi(e) : 128;  // more units: better balance (measured: 256 slower on layers 3-4)
+    }();
+    auto search = [&] {
+      const int top = std::min(bn, pm ? pair_maxbn : 256);
+      for (int cand = top; cand >= 16; cand /= 2)
+        for (int sub : {4, 2, 1}) {
+          if (!force_stream && try_cfg(cand, sub, true)) return true;
+          if (try_cfg(cand, sub, false)) return true;
+        }
+      return false;
+    };
+    // CTA pairs for the 3x3 convs bound by delivering weight rows into shared
+    // memory (the pair stages half of them per SM), from per-launch A/B on
+    // ResNet-18 b256: int8 -- the convs whose single-CTA plan streams its
+    // weights, minus residual-add epilogues over K < 4608 bytes (epilogue-bound:
+    // layer 3's are 1.09x slower as pairs, layer 4's K = 4608 ones 1.13x faster);
+    // bf16/tf32 (twice the operand bytes) -- every 3x3 conv except those
+    // whose single-CTA plan takes 4-sub-tile super-tiles (layer 1: 1.16-1.4x
+    // slower as pairs, which allow 2).  1x1 convs stay single (1.2x slower).
+    // MRB200_TC_PAIR: 0 never, 2 wherever legal (A/B switch);
+    // MRB200_TC_PAIR_MAXBN caps the pair N tile.
+    static const int pair_env = [] {
+      const char* e = std::getenv("MRB200_TC_PAIR");
+      return e ? std::atoi(e) : 1;
+    }();
+    const bool pair_ok = kb >= 64 && sp.kind != TC_STEM_S2D;
+    found = search();
+    const bool pair_auto =
+        found && ntaps == 9 && (eb == 1 ? (!a.resident_b && (!sp.residual || 9 * cc * kb >= 4608)) : a.sub < 4);
+    if (pair_ok && pair_env && (pair_env == 2 || pair_auto)) {
+      const TcArgs single = a;
+      pm = 1;
+      if (!search()) {
+        a = single;
+        pm = 0;
       }
     }
   }
   if (!found) return false;
+  a.pair = pm;
+  a.bn_local = a.bn >> pm;
   a.m_tiles = a.pool ? sp.N * sp.poh
                      : static_cast<int>((a.Pg + kTileM * (a.win ? 1 : a.sub) - 1) / (kTileM * (a.win ? 1 : a.sub)));
+  if (a.pair) a.m_tiles = (a.m_tiles + 1) / 2;  // pair units (an odd last CTA tile reads zeros, writes nothing)
   const int rows_bytes = a.hg * row_bytes;
   a.Cc = cc;
   a.k_stages = cc / a.pps * a.tap_groups;
@@ -1393,7 +1501,7 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
   // MMA step table (byte offsets; A relative to stage base [+ row shift for kb 16])
   const uint32_t a_sub = static_cast<uint32_t>(rows_bytes);
   const uint32_t a_plane = a_sub * static_cast<uint32_t>(a.subs);
-  const uint32_t b_plane = static_cast<uint32_t>(a.bn) * static_cast<uint32_t>(kb);
+  const uint32_t b_plane = static_cast<uint32_t>(a.bn_local) * static_cast<uint32_t>(kb);
   const int bplanes = a.resident_b ? cc : a.pps;  // chunk planes per tap in the smem B buffer
   a.b_ks_stride = a.resident_b ? static_cast<uint32_t>(a.pps) * b_plane : 0;
   a.n_steps = 0;
@@ -1480,15 +1588,16 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
   else if (eb == 4) idesc |= (1u << 4) | (2u << 7) | (2u << 10);  // F32 <- tf32 x tf32
   else idesc |= (1u << 4) | (1u << 7) | (1u << 10);          // F32 <- bf16 x bf16
   idesc |= static_cast<uint32_t>(a.bn >> 3) << 17;
-  idesc |= static_cast<uint32_t>(kTileM >> 4) << 24;
+  idesc |= static_cast<uint32_t>((a.pair ? 2 * kTileM : kTileM) >> 4) << 24;
   a.idesc = idesc;
   int sms = 148;
   int dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int per_n = sms / a.n_tiles;
+  const int units = a.pair ? sms / 2 : sms;  // CTA pairs or CTAs
+  int per_n = units / a.n_tiles;
   if (per_n < 1) per_n = 1;
   if (per_n > a.m_tiles) per_n = a.m_tiles;
-  p.grid = per_n * a.n_tiles;
+  p.grid = per_n * a.n_tiles * (a.pair ? 2 : 1);
   int body = a.resident_b ? a.b_res_bytes : a.b_stage_bytes * a.n_stages;
   p.smem = 1024 + body + a.a_stage_bytes * a.n_stages + barrier_bytes;
   return true;
@@ -1569,7 +1678,7 @@ static bool encode_maps(TcConvPlan& p, const void* x, const Lay& xl, const void*
     const cuuint64_t brows = kb == 16 ? OC / 8 : OC;
     cuuint64_t dims[4] = {brow, brows, static_cast<cuuint64_t>(a.Cc), static_cast<cuuint64_t>(p.spec.taps)};
     cuuint64_t strides[3] = {brow, static_cast<cuuint64_t>(OC) * kb, static_cast<cuuint64_t>(OC) * kb * a.Cc};
-    cuuint32_t box[4] = {static_cast<cuuint32_t>(brow), static_cast<cuuint32_t>(kb == 16 ? a.bn / 8 : a.bn),
+    cuuint32_t box[4] = {static_cast<cuuint32_t>(brow), static_cast<cuuint32_t>(kb == 16 ? a.bn_local / 8 : a.bn_local),
                          static_cast<cuuint32_t>(a.resident_b ? a.Cc : a.pps),
                          static_cast<cuuint32_t>(a.tap_groups > 1 ? p.spec.taps / a.tap_groups : p.spec.taps)};
     cuuint32_t es[4] = {1, 1, 1, 1};
@@ -1681,9 +1790,16 @@ bool tc_conv_launch(TcConvPlan* p, const void* x, const Lay& xl, const void* w, 
   }
 #define MRB_TC_LAUNCH_W(EB_, SIG_, CAL_, W_)                                                              \
   do {                                                                                                    \
-    cudaFuncSetAttribute(k_conv_tc<EB_, SIG_, CAL_, W_>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+    cudaFuncSetAttribute(k_conv_tc<EB_, SIG_, CAL_, false, W_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                          static_cast<int>(p->smem));                                                      \
-    pdl_launch(k_conv_tc<EB_, SIG_, CAL_, W_>, p->grid, (2 + W_) * 32, p->smem, s, p->tmA, p->tmB, a);    \
+    if (a.pair) {                                                                                         \
+      cudaFuncSetAttribute(k_conv_tc<EB_, SIG_, CAL_, true, W_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           static_cast<int>(p->smem));                                                    \
+      pdl_launch_cluster(k_conv_tc<EB_, SIG_, CAL_, true, W_>, p->grid, (2 + W_) * 32, p->smem, s, 2, p->tmA, \
+                         p->tmB, a);                                                                      \
+    } else {                                                                                              \
+      pdl_launch(k_conv_tc<EB_, SIG_, CAL_, false, W_>, p->grid, (2 + W_) * 32, p->smem, s, p->tmA, p->tmB, a); \
+    }                                                                                                     \
   } while (0)
 #define MRB_TC_LAUNCH(EB_, SIG_, CAL_) MRB_TC_LAUNCH_W(EB_, SIG_, CAL_, kEpiWarps)
 #define MRB_TC_SIGS(EB_, CAL_)                                                  \
@@ -1734,9 +1850,9 @@ const char* tc_conv_describe(const TcConvPlan* p, char* buf, int n) {
   const TcArgs& a = p->args;
   static const char* kinds[] = {"s1", "s2-phase", "stem-s2d", "stem-pool"};
   std::snprintf(buf, n,
-                "tcgen05 %s %s %dx(M128)xN%d kb=%d taps=%d steps=%d grid=%dx%d rows=%dx%d pps=%d stages=%d B=%s ctas=%d smem=%zu",
+                "tcgen05 %s %s %dx(M%d)xN%d kb=%d taps=%d steps=%d grid=%dx%d rows=%dx%d pps=%d stages=%d B=%s ctas=%d smem=%zu",
                 p->spec.elem_bytes == 1 ? "i8" : p->spec.elem_bytes == 4 ? "tf32" : "bf16",
-                kinds[p->spec.kind], a.sub, a.bn, a.kb, p->spec.taps, a.n_steps,
+                kinds[p->spec.kind], a.sub, a.pair ? 256 : 128, a.bn, a.kb, p->spec.taps, a.n_steps,
                 a.Hg, a.Wg, a.nbox, a.hbox, a.pps, a.n_stages,
                 a.resident_b ? "resident" : a.tap_groups > 1 ? "streamed-by-kernel-row" : "streamed", p->grid, p->smem);
   return buf;

@@ -24,6 +24,9 @@ struct TcConvSpec {
   // Fused max_pool2d consumer (cross-group fusion of conv -> max_pool2d, the
   // conv output never leaves the SM): window, stride, padding, pooled dims.
   int pool = 0, pkh = 0, pkw = 0, psh = 1, psw = 1, pph = 0, ppw = 0, poh = 0, pow = 0;
+  // the epilogue adds a residual (an epilogue-bound conv: the CTA-pair plan,
+  // which helps weight-streaming convs, does not pay there -- measured)
+  int residual = 0;
   // filled by planning
   int taps = 0, wplanes = 0;  // weight layout [taps][wplanes][OC][kb bytes]
   int kb = 0;                 // operand chunk bytes (the data representation's chunk width)

@@ -964,6 +964,7 @@ void build(Exec& ex) {
       case P_CONV_I8_TC:
       case P_CONV_BF16_TC:
       case P_CONV_TF32_TC: {
+        for (const EpiOp& op : g.epi) ex.group_tc[gi].residual |= op.kind == EpiKind::Residual ? 1 : 0;
         TcConvPlan* tp = tc_conv_create(ex.group_tc[gi]);
         if (!tp) fail(MR_ERR_UNSUPPORTED_GROUP, "group %" + g.name + ": tcgen05 plan failed");
         ex.tc_plans.push_back(tp);
@@ -1376,6 +1377,7 @@ void run_launches(Exec& ex, cudaStream_t s) {
     return e && std::atoi(e);
   }();
   for (auto& L : ex.launches) {
+    if (sync_debug) std::fprintf(stderr, "MRB200_SYNC_DEBUG launch %s (%s)\n", L.name.c_str(), L.kernel.c_str());
     L.fn(s);
     if (sync_debug) {  // debugging only: name the launch that faults
       cudaError_t err = cudaStreamSynchronize(s);

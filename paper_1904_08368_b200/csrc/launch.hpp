@@ -28,6 +28,33 @@ inline void pdl_launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, 
   cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
+// pdl_launch with thread-block clusters of `cluster` CTAs along x (CTA pairs
+// for the tcgen05 cta_group::2 conv plans); cluster 1 is pdl_launch.
+template <typename... KArgs, typename... Args>
+inline void pdl_launch_cluster(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, int cluster,
+                               Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  int n = 0;
+  if (pdl_enabled()) {
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n++].val.programmaticStreamSerializationAllowed = 1;
+  }
+  if (cluster > 1) {
+    at[n].id = cudaLaunchAttributeClusterDimension;
+    at[n].val.clusterDim.x = static_cast<unsigned>(cluster);
+    at[n].val.clusterDim.y = 1;
+    at[n++].val.clusterDim.z = 1;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = n;
+  cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 enum WeightLayout : int { WL_ROWS = 0, WL_TC = 1, WL_S2D = 2 };
 
 void launch_input_convert(const float* x, int N, int C, int H, int W, void* out, int fmt, const Lay& L,

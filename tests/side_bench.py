@@ -15,9 +15,10 @@ from paper_1904_08368_b200 import modelzoo  # noqa: E402
 
 name, batch, prec = sys.argv[1], int(sys.argv[2]), sys.argv[3]
 steps = int(sys.argv[4]) if len(sys.argv) > 4 else 50
+fmode = sys.argv[5] if len(sys.argv) > 5 else "bf16"  # float modules: bf16 | tf32
 text, meta, src = mrb.load_model(name, prec)
 w = modelzoo.make_weights(src, seed=meta["weights_seed"])
-ex = mrb.Executor(text, batch=batch)
+ex = mrb.Executor(text, batch=batch, **({"float_mode": mrb.MR_FLOAT_TF32} if fmode == "tf32" else {}))
 ex.set_weights([w[p.name] for p in src.params if p.kind != "input"])
 x = torch.from_numpy(modelzoo.make_inputs(src, batch, seed=0)).cuda()
 out = torch.empty(ex.output_shape, dtype=torch.float32, device="cuda")
@@ -32,7 +33,7 @@ for _ in range(steps):
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / steps
-line = {"model": name, "precision": "int8" if prec == "int8" else "bf16", "batch": batch,
+line = {"model": name, "precision": "int8" if prec == "int8" else fmode, "batch": batch,
         "ms_per_step": ms, "images_per_s": batch / ms * 1e3, "launches": ex.launch_count()}
 if os.environ.get("SIDE_PER_LAUNCH"):
     per = ex.profile_device(x.data_ptr(), x.shape, out.data_ptr(), sh)
