@@ -989,9 +989,11 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
           }
           const int64_t pix = (static_cast<int64_t>(n) * (a.poh + 2 * kPad) + p + kPad) * (a.pow + 2 * kPad) + pw + kPad;
           const int c = n_tile * a.bn + c0;
-          if (o.primary_fmt == FMT_F32) {
+          if (o.primary_fmt == FMT_F32) {  // (tf32 mode: the next conv's operand, rounded like store_out)
+            const float r0 = o.tf32 ? tf32_rn(mx[0]) : mx[0], r1 = o.tf32 ? tf32_rn(mx[1]) : mx[1];
+            const float r2 = o.tf32 ? tf32_rn(mx[2]) : mx[2], r3 = o.tf32 ? tf32_rn(mx[3]) : mx[3];
             st16(o.primary, gran_byte(o.plan, pix, o.plan.Pp, c),
-                 make_uint4(__float_as_uint(mx[0]), __float_as_uint(mx[1]), __float_as_uint(mx[2]), __float_as_uint(mx[3])));
+                 make_uint4(__float_as_uint(r0), __float_as_uint(r1), __float_as_uint(r2), __float_as_uint(r3)));
           } else {  // bf16 pipeline: 4 channels = 8 bytes
             *reinterpret_cast<uint2*>(static_cast<char*>(o.primary) + gran_byte(o.plan, pix, o.plan.Pp, c)) =
                 make_uint2(pack_bf16x2(mx[0], mx[1]),
@@ -1236,6 +1238,7 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
       a.OH = sp.OH;
       a.OW = sp.OW;
       cc = (4 * sp.C * eb + 15) / 16;  // 1 (int8) or 2 (bf16)
+      if (eb == 4) cc = (cc + 1) & ~1;  // tf32: 4 planes, the 4th zero (K step = two planes)
       a.subs = 1;
       for (int ta = 0; ta < TA; ++ta)
         for (int tb = 0; tb < TA; ++tb) taps.push_back({0, ta * a.Wg + tb});
@@ -1351,7 +1354,9 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
       for (int pps : {8, 4, 2, 1}) {
         if (cc % pps || (kb == 16 && (pps & 1) && !pair_taps) || steps_for(pps) > kMaxSteps) continue;
         int ns = (kSmemBudget - barrier_bytes - b_res) / a_stage(pps);
-        if (ns >= 3) {
+        // (the staged-pool stem holds its pooling band in shared memory too: 2 stages
+        // there -- the tf32 stem's 64 KB of weights leave no room for 3)
+        if (ns >= (sp.pool ? 2 : 3)) {
           a.resident_b = 1;
           a.tap_groups = 1;  // (a later search may follow a streamed-by-kernel-row success)
           a.b_res_bytes = b_res;

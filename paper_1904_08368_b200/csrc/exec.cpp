@@ -272,6 +272,9 @@ Lay make_lay(const std::vector<int64_t>& s, int fmt, int kind, int s2d_pad = 0, 
       L.Pp = round_up(s[0] * L.Hq * L.Wq, 8);
     } else if (kind == LAY_S2D) {  // 4*C s2d channels on a ceil((H+2p)/2) grid
       L.C = static_cast<int32_t>(4 * s[1]);
+      // float32 (the tf32 stem): an even number of 16-byte planes -- one
+      // kind::tf32 K step spans two; the extra channels are zeros
+      if (fmt == FMT_F32) L.C = static_cast<int32_t>(round_up(L.C, 2 * L.cpc));
       L.Hq = static_cast<int32_t>((s[2] + 2 * s2d_pad + 1) / 2);
       L.Wq = static_cast<int32_t>((s[3] + 2 * s2d_pad + 1) / 2);
       L.Pp = round_up(s[0] * L.Hq * L.Wq, 8);

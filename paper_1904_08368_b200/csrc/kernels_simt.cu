@@ -53,7 +53,7 @@ __global__ void k_input_convert(const float* __restrict__ x, int N, int C, int H
   const int eb = L.kb / L.cpc;
   const int gpc = L.kb / 16;       // 16-byte granules per chunk
   const int cpg = 16 / eb;         // channels per granule
-  const int planes = L.kind == LAY_S2D ? (4 * C + L.cpc - 1) / L.cpc : (C + L.cpc - 1) / L.cpc;
+  const int planes = L.kind == LAY_S2D ? (L.C + L.cpc - 1) / L.cpc : (C + L.cpc - 1) / L.cpc;
   const int64_t grid_pix = L.kind == LAY_S2D ? static_cast<int64_t>(N) * L.Hq * L.Wq
                                              : static_cast<int64_t>(N) * (H + 2 * kPad) * (W + 2 * kPad);
   const int64_t total = static_cast<int64_t>(planes) * gpc * grid_pix;
@@ -95,7 +95,10 @@ __global__ void k_input_convert(const float* __restrict__ x, int N, int C, int H
       if (pre_mul != 0.f && live[k]) v[k] = __fmul_rn(v[k], pre_mul);
     char* dst = static_cast<char*>(out) + dst_byte;
     if (fmt == FMT_F32) {
-      *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+      if (L.kind == LAY_S2D)  // float32 s2d feeds only the tf32 stem: round (the MMA would truncate)
+        *reinterpret_cast<float4*>(dst) = make_float4(tf32_rn(v[0]), tf32_rn(v[1]), tf32_rn(v[2]), tf32_rn(v[3]));
+      else
+        *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
     } else if (fmt == FMT_BF16) {
       uint32_t w4[4];
 #pragma unroll
@@ -150,7 +153,7 @@ __global__ void __launch_bounds__(128) k_input_s2d(const float* __restrict__ x, 
   const int n_rows = N * L.Hq;
   const int eb = L.kb >> lay_lg(L);
   const int gpc = L.kb / 16, cpg = 16 / eb;
-  const int planes = (4 * C + L.cpc - 1) / L.cpc;
+  const int planes = (L.C + L.cpc - 1) / L.cpc;
   const bool fast_q = q.lo > -2147483648.f && q.hi < 2147483648.f;  // realize clips: [-128, 127] / [0, 255]
   // per granule channel (pl, gr, k): staged row offset, column shift, row parity, liveness
   __shared__ int2 ktab[64];
@@ -192,8 +195,8 @@ __global__ void __launch_bounds__(128) k_input_s2d(const float* __restrict__ x, 
           }
           char* dst = static_cast<char*>(out) + (pl * L.Pp + pix) * L.kb + gr * 16;
           uint32_t w4[4];
-          if (fmt == FMT_F32) {
-            *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+          if (fmt == FMT_F32) {  // the tf32 stem's operand: rounded (the MMA would truncate)
+            *reinterpret_cast<float4*>(dst) = make_float4(tf32_rn(v[0]), tf32_rn(v[1]), tf32_rn(v[2]), tf32_rn(v[3]));
             continue;
           } else if (fmt == FMT_BF16) {
 #pragma unroll
@@ -421,7 +424,8 @@ __global__ void k_weight_prep(const float* __restrict__ w, int O, int I, int KH,
   const bool strict = fmt == FMT_F32 && wl == WL_ROWS;
   const int cpc = (wl == WL_ROWS ? 16 : Cs) / (fmt == FMT_I8 ? 1 : fmt == FMT_BF16 ? 2 : 4);
   const int TA = (KH + 1) / 2;
-  const int planes = wl == WL_S2D ? (4 * I + cpc - 1) / cpc : (I + cpc - 1) / cpc;
+  int planes = wl == WL_S2D ? (4 * I + cpc - 1) / cpc : (I + cpc - 1) / cpc;
+  if (wl == WL_S2D && fmt == FMT_F32) planes = (planes + 1) & ~1;  // tf32 stem: even planes (exec make_lay)
   int64_t total;
   if (strict) total = static_cast<int64_t>(O) * I * KH * KW;
   else if (wl == WL_TC) total = static_cast<int64_t>(KH) * KW * planes * O * cpc;
@@ -1596,7 +1600,7 @@ void launch_input_convert(const float* x, int N, int C, int H, int W, void* out,
                x, N, H, W, out, L, pre_mul, q, fd);
     return;
   }
-  const int s2d_planes = (4 * C + L.cpc - 1) / L.cpc;
+  const int s2d_planes = (L.C + L.cpc - 1) / L.cpc;
   if (L.kind == LAY_S2D && 2 * 2 * C * W * 4 <= 40 * 1024 && W % 4 == 0 && s2d_planes * (L.kb / 16) <= 4 &&
       reinterpret_cast<uintptr_t>(x) % 16 == 0) {
     static int sms = [] {
@@ -1630,7 +1634,7 @@ void launch_input_convert(const float* x, int N, int C, int H, int W, void* out,
                                                                                   s2d_pad, pre_mul, q);
     return;
   }
-  int planes = L.kind == LAY_S2D ? (4 * C + L.cpc - 1) / L.cpc : (C + L.cpc - 1) / L.cpc;
+  int planes = L.kind == LAY_S2D ? (L.C + L.cpc - 1) / L.cpc : (C + L.cpc - 1) / L.cpc;
   int64_t grid_pix = L.kind == LAY_S2D ? static_cast<int64_t>(N) * L.Hq * L.Wq
                                        : static_cast<int64_t>(N) * (H + 2 * kPad) * (W + 2 * kPad);
   pdl_launch(k_input_convert, grid_stride_blocks(planes * (L.kb / 16) * grid_pix), kThreads, 0, s, x, N, C, H, W, out, fmt, L, s2d_pad,
@@ -1655,6 +1659,7 @@ void launch_weight_prep(const float* w, int O, int I, int KH, int KW, int Cs, in
   int cpc = (wl == WL_ROWS ? 16 : Cs) / (fmt == FMT_I8 ? 1 : 2);
   int TA = (KH + 1) / 2;
   int planes = wl == WL_S2D ? (4 * I + cpc - 1) / cpc : (I + cpc - 1) / cpc;
+  if (wl == WL_S2D && fmt == FMT_F32) planes = (planes + 1) & ~1;
   int64_t total;
   if (fmt == FMT_F32) total = static_cast<int64_t>(O) * I * KH * KW;
   else if (wl == WL_TC) total = static_cast<int64_t>(KH) * KW * planes * O * cpc;
