@@ -788,7 +788,9 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
             if constexpr (PAIR) {
               switch (sub) {
                 case 1: issue(std::integral_constant<uint32_t, 1>{}, T_{}); break;
-                default: issue(std::integral_constant<uint32_t, 2>{}, T_{}); break;
+                case 2: issue(std::integral_constant<uint32_t, 2>{}, T_{}); break;
+                case 3: issue(std::integral_constant<uint32_t, 3>{}, T_{}); break;
+                default: issue(std::integral_constant<uint32_t, 4>{}, T_{}); break;
               }
             } else {
               switch (sub) {
@@ -1343,7 +1345,7 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
   int pm = 0;
   auto try_cfg = [&](int cand_full, int sub, bool resident) {
     if (sp.OC % cand_full || 2 * sub * cand_full > 512) return false;
-    if (pm && ((cand_full >> 1) % 16 || sub > 2)) return false;
+    if (pm && (cand_full >> 1) % 16) return false;
     const int cand = cand_full >> pm;  // weight rows staged per CTA
     int hg, nbox, hbox;
     if (!geom(sub, &hg, &nbox, &hbox)) return false;
@@ -1471,9 +1473,10 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
     // ResNet-18 b256: int8 -- the convs whose single-CTA plan streams its
     // weights, minus residual-add epilogues over K < 4608 bytes (epilogue-bound:
     // layer 3's are 1.09x slower as pairs, layer 4's K = 4608 ones 1.13x faster);
-    // bf16/tf32 (twice the operand bytes) -- every 3x3 conv except those
-    // whose single-CTA plan takes 4-sub-tile super-tiles (layer 1: 1.16-1.4x
-    // slower as pairs, which allow 2).  1x1 convs stay single (1.2x slower).
+    // bf16/tf32 (twice the operand bytes) -- every 3x3 conv.  Never for N=64
+    // tiles (layer 1, 1.2x slower as pairs: the MMAs there are bound by reading
+    // the 128-row A operand from shared memory, which the pair does not
+    // reduce) nor 1x1 convs (1.2x slower).
     // MRB200_TC_PAIR: 0 never, 2 wherever legal (A/B switch);
     // MRB200_TC_PAIR_MAXBN caps the pair N tile.
     static const int pair_env = [] {
@@ -1483,7 +1486,7 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
     const bool pair_ok = kb >= 64 && sp.kind != TC_STEM_S2D;
     found = search();
     const bool pair_auto =
-        found && ntaps == 9 && (eb == 1 ? (!a.resident_b && (!sp.residual || 9 * cc * kb >= 4608)) : a.sub < 4);
+        found && ntaps == 9 && a.bn >= 128 && (eb > 1 || (!a.resident_b && (!sp.residual || 9 * cc * kb >= 4608)));
     if (pair_ok && pair_env && (pair_env == 2 || pair_auto)) {
       const TcArgs single = a;
       pm = 1;
