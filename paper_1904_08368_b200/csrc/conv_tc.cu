@@ -283,8 +283,10 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
   const int pf = o.primary_fmt;
   const int peb = pf == FMT_F32 ? 4 : pf == FMT_BF16 ? 2 : 1;  // 16-byte granules per 16 channels
   const int seb = o.side_fmt == FMT_F32 ? 4 : o.side_fmt == FMT_BF16 ? 2 : 1;
+  // o.primary null: no launch reads the primary output (exec.cpp Buffer::dead), only the side codes
   if (d.border) {
-    for (int g = 0; g < peb; ++g) st16(o.primary, gran_byte(o.plan, d.pix, o.plan.Pp, c0 + g * 16 / peb), make_uint4(0, 0, 0, 0));
+    if (o.primary)
+      for (int g = 0; g < peb; ++g) st16(o.primary, gran_byte(o.plan, d.pix, o.plan.Pp, c0 + g * 16 / peb), make_uint4(0, 0, 0, 0));
     if (o.side)
       for (int g = 0; g < seb; ++g)
         st16(o.side, gran_byte(o.slay, d.side_base, d.side_pstride, c0 + g * 16 / seb), make_uint4(0, 0, 0, 0));
@@ -448,7 +450,8 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
       // v (= code * c2) is only needed for a side output, never emitted here
     }
   }
-  if (pf == FMT_I8) {
+  if (!o.primary) {
+  } else if (pf == FMT_I8) {
     st16(o.primary, gran_byte(o.plan, d.pix, o.plan.Pp, c0),
          make_uint4(pack4_i8(code[0], code[1], code[2], code[3]), pack4_i8(code[4], code[5], code[6], code[7]),
                     pack4_i8(code[8], code[9], code[10], code[11]), pack4_i8(code[12], code[13], code[14], code[15])));

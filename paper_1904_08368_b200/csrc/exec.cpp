@@ -97,6 +97,10 @@ struct Buffer {
   // zero border forever: its producer writes only interior pixels, so the
   // buffer gets arena space of its own (never aliased) zeroed once at build
   bool zero_border = false;
+  // no launch reads it (e.g. the float32 output of a stage's last residual
+  // block, whose consumers all take the producer's int8 side codes): the
+  // producer skips the stores and the arena gives it no space
+  bool dead = false;
 };
 
 struct LaunchRec {
@@ -105,6 +109,7 @@ struct LaunchRec {
   int kernels = 1;    // device kernels this record launches
   double bytes = 0;   // algorithmic HBM bytes
   double flops = 0;   // algorithmic ops (2 per MAC)
+  int opt_primary = -1;  // a primary output buffer the kernel can skip (tcgen05 conv with a side output)
   std::function<void(cudaStream_t)> fn;
 };
 
@@ -911,7 +916,7 @@ void build(Exec& ex) {
     auto outdev = [e, pb, out]() {
       OutDev o = out;
       if (pb.presum >= 0) o.primary = e->ptr(pb.presum);
-      else o.primary = e->ptr(pb.out);
+      else o.primary = e->bufs[pb.out].dead ? nullptr : e->ptr(pb.out);
       o.side = pb.side >= 0 ? e->ptr(pb.side) : nullptr;
       return o;
     };
@@ -974,6 +979,7 @@ void build(Exec& ex) {
         char buf[256];
         ex.group_note.resize(P.groups.size());
         ex.group_note[gi] = tc_conv_describe(tp, buf, sizeof(buf));
+        if (pre_sum_buf < 0 && sbuf >= 0) L.opt_primary = obuf;
         std::string gname = g.name;
         Lay dlay = drep.lay;
         L.fn = [e, gidx, dbuf, dlay, acc_scale, tp, outdev, epidev, residual_fix, gname](cudaStream_t s) {
@@ -1175,6 +1181,17 @@ void build(Exec& ex) {
     ++B.launch_idx;
   }
 
+  for (size_t i = 0; i < ex.launches.size(); ++i) {
+    LaunchRec& L = ex.launches[i];
+    if (L.opt_primary < 0 || L.opt_primary == ex.out_alias_buf) continue;
+    Buffer& b = ex.bufs[L.opt_primary];
+    if (b.first == static_cast<int>(i) && b.last == static_cast<int>(i) && !b.zero_border) {
+      b.dead = true;
+      L.bytes -= static_cast<double>(b.bytes);
+      b.bytes = 0;
+      b.what += " (unread: not written)";
+    }
+  }
   assign_offsets(ex);
   CK(cudaMalloc(&ex.arena, static_cast<size_t>(std::max<int64_t>(ex.arena_bytes, 256))));
   if (ex.zero_bytes) CK(cudaMemset(ex.arena, 0, static_cast<size_t>(ex.zero_bytes)));
