@@ -130,6 +130,16 @@ struct TcArgs {
   // weight rows (bn_local = bn / 2), so per-SM weight traffic and smem halve.
   // m_tiles then counts pair units (CTA r takes super-tile 2 * unit + r).
   int32_t pair, bn_local;
+  // fused 1x1/s2 shortcut (TcConvSpec::sc_C): sc_k_stages extra pipeline stages
+  // per tile, each one sc_kb-byte chunk of the decimated block input (A2: the
+  // tile's own rows, no halo) and of the shortcut weights (B2: in the stage's B
+  // area, or after A2 when the main weights are resident), accumulated into a
+  // second TMEM accumulator pair at column 2*sub*bn; the epilogue adds
+  // acc2 * sc_scale + sc_bias where the residual was read
+  int32_t sc, sc_kb, sc_k_stages, sc_ksteps, sc_a_bytes, sc_b_bytes, sc_b_in_a;
+  uint32_t sc_desc_hi;
+  float sc_scale;
+  const float* sc_bias;
   int32_t a_stage_bytes, b_stage_bytes, b_res_bytes, n_stages;
   uint32_t idesc;
   int32_t out_mode, OH, OW;  // OUT_REMAP: valid outputs are grid (y < OH, x < OW)
@@ -188,6 +198,7 @@ struct RowDst {
   int64_t pix;        // NORMAL padded-grid index of the output pixel (primary, residual)
   int64_t side_base;  // side chunk index of plane 0
   int64_t side_pstride;
+  int64_t dec_pix;    // side2: decimated-grid index of an even (2i, 2j) pixel, else -1
   bool border;        // OUT_SAME: padded-grid border -> zeros
 };
 
@@ -253,7 +264,8 @@ __device__ __forceinline__ void epilogue_prefetch(const TcArgs& a, const RowDst&
     if constexpr (SIG == SIG_BIAS_RES_RELU) {
       const EpiDev& e = a.epi;
       const Lay& L = e.res_lay[1];
-      if (e.res_fmt[1] == FMT_F32) {
+      if (a.sc) {  // fused shortcut: computed from the second accumulator (k_conv_tc)
+      } else if (e.res_fmt[1] == FMT_F32) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const float4 f = *reinterpret_cast<const float4*>(static_cast<const char*>(e.res[1]) + gran_byte(L, d.pix, L.Pp, c0 + 4 * j));
@@ -488,17 +500,19 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
           if constexpr (CAL) quant_observe(v[i], o.side_q);
           sc[i] = __float2int_rn(__fmul_rn(v[i], o.side_q.c1));  // cvt.rni: == trunc(rint(y)), one F2I
         }
-        st16(o.side, gran_byte(o.slay, d.side_base, d.side_pstride, c0),
-             make_uint4(pack4_sat_s8(sc[0], sc[1], sc[2], sc[3]), pack4_sat_s8(sc[4], sc[5], sc[6], sc[7]),
-                        pack4_sat_s8(sc[8], sc[9], sc[10], sc[11]), pack4_sat_s8(sc[12], sc[13], sc[14], sc[15])));
+        const uint4 u = make_uint4(pack4_sat_s8(sc[0], sc[1], sc[2], sc[3]), pack4_sat_s8(sc[4], sc[5], sc[6], sc[7]),
+                                   pack4_sat_s8(sc[8], sc[9], sc[10], sc[11]), pack4_sat_s8(sc[12], sc[13], sc[14], sc[15]));
+        st16(o.side, gran_byte(o.slay, d.side_base, d.side_pstride, c0), u);
+        if (d.dec_pix >= 0) st16(o.side2, gran_byte(o.s2lay, d.dec_pix, o.s2lay.Pp, c0), u);
         return;
       }
 #endif
 #pragma unroll
       for (int i = 0; i < 16; ++i) sc[i] = quant_code_fast_t<CAL>(v[i], o.side_q);
-      st16(o.side, gran_byte(o.slay, d.side_base, d.side_pstride, c0),
-           make_uint4(pack4_i8(sc[0], sc[1], sc[2], sc[3]), pack4_i8(sc[4], sc[5], sc[6], sc[7]),
-                      pack4_i8(sc[8], sc[9], sc[10], sc[11]), pack4_i8(sc[12], sc[13], sc[14], sc[15])));
+      const uint4 u = make_uint4(pack4_i8(sc[0], sc[1], sc[2], sc[3]), pack4_i8(sc[4], sc[5], sc[6], sc[7]),
+                                 pack4_i8(sc[8], sc[9], sc[10], sc[11]), pack4_i8(sc[12], sc[13], sc[14], sc[15]));
+      st16(o.side, gran_byte(o.slay, d.side_base, d.side_pstride, c0), u);
+      if (d.dec_pix >= 0) st16(o.side2, gran_byte(o.s2lay, d.dec_pix, o.s2lay.Pp, c0), u);
     } else if (o.side_fmt == FMT_F32) {  // tf32 mode: a second float32 layout (e.g. the phase split)
 #pragma unroll
       for (int j = 0; j < 4; ++j)
@@ -536,7 +550,8 @@ __device__ __forceinline__ int tile_row0(const TcArgs& a, int mt, int msub) { re
 // cta_group::2 must be launched in clusters, so the two modes are separate kernels).
 template <int EB, int SIG, bool CAL, bool PAIR, int EPIW = kEpiWarps>
 __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
-    k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcArgs a) {
+    k_conv_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2, const TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // carve: [B resident or B stages][A stages][barriers]
   // (pointer arithmetic on smem_raw, not an integer round trip, so the compiler
@@ -585,7 +600,7 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
   const int m_start = cta / a.n_tiles;
   const int m_step = ncta / a.n_tiles;
   const int m_end = a.m_tiles;
-  const int tcols = 2 * a.sub * a.bn;
+  const int tcols = 2 * a.sub * a.bn * (a.sc ? 2 : 1);
   const uint32_t tmem_cols = tcols <= 32 ? 32 : tcols <= 64 ? 64 : tcols <= 128 ? 128 : tcols <= 256 ? 256 : 512;
 
   if (threadIdx.x == 0) {
@@ -601,6 +616,10 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+    if (a.sc) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA2) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB2) : "memory");
+    }
     // resident weights are static (prepared at set_weights): load them before
     // waiting for the previous kernel (pair: after the cluster barrier below,
     // which publishes the leader's bfull initialisation to the peer)
@@ -695,6 +714,18 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
               tma_load_4d(smB + stage * a.b_stage_bytes, &tmB, &full[stage], 0, brow, kc * a.pps,
                           tg * (a.tap_groups > 1 ? 3 : 0));
           }
+          if (++stage == a.n_stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        for (int j = 0; j < a.sc_k_stages; ++j) {  // fused shortcut: A2 = the tile's own rows, 1x1 tap
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], a.sc_a_bytes + a.sc_b_bytes);
+          uint8_t* dA = smA + stage * a.a_stage_bytes;
+          tma_load_4d(dA, &tmA2, &full[stage], 0, own(mt) * msub, 0, j);
+          tma_load_4d(a.sc_b_in_a ? dA + a.sc_a_bytes : smB + stage * a.b_stage_bytes, &tmB2, &full[stage], 0,
+                      n_tile * a.bn, j, 0);
           if (++stage == a.n_stages) {
             stage = 0;
             phase ^= 1;
@@ -812,6 +843,29 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
             phase ^= 1;
           }
         }
+        if (!PAIR && a.sc) {  // fused shortcut: second accumulator at column 2*sub*bn
+          const uint64_t hi2 = static_cast<uint64_t>(a.sc_desc_hi) << 32;
+          const uint32_t tmem_d2 = tmem_base + 2u * sub * bn + static_cast<uint32_t>(acc) * sub * bn;
+          const uint32_t sub2 = static_cast<uint32_t>(kTileM * a.sc_kb) >> 4;  // 128 rows x sc_kb, in 16 B
+          for (int j = 0; j < a.sc_k_stages; ++j) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t sA = smA_u + stage * a.a_stage_bytes;
+            const uint32_t sB = a.sc_b_in_a ? sA + a.sc_a_bytes : smB_u + stage * a.b_stage_bytes;
+            if (!no_mma)
+              for (int kk = 0; kk < a.sc_ksteps; ++kk) {
+                const uint64_t bd = hi2 | (((sB + kk * 32) >> 4) | (1u << 16));
+                for (uint32_t sb = 0; sb < sub; ++sb)
+                  umma<EB>(tmem_d2 + sb * bn, hi2 | ((((sA + kk * 32) >> 4) + sb * sub2) | (1u << 16)), bd, idesc,
+                           (j | kk) != 0 ? 1u : 0u);
+              }
+            umma_commit(&empty[stage]);
+            if (++stage == a.n_stages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
         // accumulator ready for the epilogue (pair: both CTAs' epilogues)
         if constexpr (PAIR) umma_commit_pair(&tfull[acc], 3);
         else umma_commit(&tfull[acc]);
@@ -890,6 +944,7 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
           if (vpool && !(a.dbg & 1)) {
             RowDst d;
             d.border = false;
+            d.dec_pix = -1;  // (the pooled stem never carries the decimated side copy)
             d.pix = (static_cast<int64_t>(n) * (a.poh + 2 * kPad) + pp + kPad) * (a.pow + 2 * kPad) + pq + kPad;
             if (a.out.side && sl.kind == LAY_PHASE) {
               const uint32_t p32 = static_cast<uint32_t>(d.pix);
@@ -1041,6 +1096,7 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
         dd.pix = 0;
         dd.side_base = 0;
         dd.side_pstride = 0;
+        dd.dec_pix = -1;
         if (vv) {
           const uint32_t t = fdiv(q, a.fd_wg);
           const int x = static_cast<int>(q - t * static_cast<uint32_t>(a.Wg));
@@ -1053,6 +1109,11 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
           } else {
             vv = y < a.OH && x < a.OW;
             dd.pix = (static_cast<int64_t>(n) * (a.OH + 2 * kPad) + y + kPad) * (a.OW + 2 * kPad) + x + kPad;
+          }
+          if (a.out.side2 && a.out_mode == OUT_SAME) {  // unpadded (y-1, x-1) both even -> decimated (i, j)
+            const int yy = y - 1, xx = x - 1;
+            if (yy >= 0 && xx >= 0 && !(yy & 1) && !(xx & 1) && y < a.Hg - 1 && x < a.Wg - 1)
+              dd.dec_pix = (static_cast<int64_t>(n) * a.out.s2lay.Hp + yy / 2 + 1) * a.out.s2lay.Wp + xx / 2 + 1;
           }
           if (a.out.side) {
             if (sl.kind == LAY_PHASE) {
@@ -1094,6 +1155,25 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
           uint32_t raw[16];
           tmem_ld16(taddr_of(sb, c), raw);  // warp-collective: every lane executes it
           if (!early && valid && !d.border) epilogue_prefetch<SIG>(a, d, n_tile * a.bn + c, s_vec, p2ok, c, pb, pr);
+          if constexpr (SIG == SIG_BIAS_RES_RELU && !PAIR) {
+            if (a.sc) {  // fused shortcut: residual = acc2 * sc_scale + sc_bias (the shortcut group's ops)
+              uint32_t raw2[16];
+              tmem_ld16(taddr_of(sb, c) + 2u * static_cast<uint32_t>(a.sub * a.bn), raw2);
+              const float4* bp = reinterpret_cast<const float4*>(a.sc_bias + n_tile * a.bn + c);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const float4 f = __ldg(bp + j);
+                const float bb[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                  const int i = 4 * j + h;
+                  const float v2 = EB == 1 ? __fmul_rn(static_cast<float>(static_cast<int32_t>(raw2[i])), a.sc_scale)
+                                           : __uint_as_float(raw2[i]);
+                  pr[i] = __fadd_rn(v2, bb[h]);
+                }
+              }
+            }
+          }
           if (valid && !(a.dbg & 1)) epilogue_chunk<EB, SIG, CAL>(a, raw, d, n_tile * a.bn + c, s_vec, p2ok, c, pb, pr);
         }
       }
@@ -1153,7 +1233,9 @@ struct TcConvPlan {
   size_t smem = 0;
   const void* map_x = nullptr;
   const void* map_w = nullptr;
-  CUtensorMap tmA, tmB;
+  const void* map_x2 = nullptr;
+  const void* map_w2 = nullptr;
+  CUtensorMap tmA, tmB, tmA2, tmB2;  // A2 / B2: the fused shortcut's operands (zeros when unused)
 };
 
 // Taps of a conv kind: (sub-grid, row offset in the sub-grid's pixel space).
@@ -1346,8 +1428,15 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
                       !std::getenv("MRB200_NO_TAP_ROWS");
   // pair mode (cta_group::2) for this attempt: each CTA stages bn / 2 weight rows
   int pm = 0;
+  // fused shortcut: its stage holds A2 (the tile's rows) and B2 (one sc_kb chunk of bn rows)
+  const bool scm = sp.sc_C > 0;
+  if (scm && (sp.kind != TC_S1 || ntaps != 9 || sp.pool || a.win || (sp.sc_kb != 64 && sp.sc_kb != 128) ||
+              sp.sc_C * eb % sp.sc_kb))
+    return false;
   auto try_cfg = [&](int cand_full, int sub, bool resident) {
-    if (sp.OC % cand_full || 2 * sub * cand_full > 512) return false;
+    if (sp.OC % cand_full || 2 * sub * cand_full * (scm ? 2 : 1) > 512) return false;
+    if (scm && (pm || sub > 2)) return false;
+    const int sc_a = scm ? kTileM * sub * sp.sc_kb : 0, sc_b = scm ? cand_full * sp.sc_kb : 0;
     if (pm && (cand_full >> 1) % 16) return false;
     const int cand = cand_full >> pm;  // weight rows staged per CTA
     int hg, nbox, hbox;
@@ -1359,6 +1448,7 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
       for (int pps : {8, 4, 2, 1}) {
         if (cc % pps || (kb == 16 && (pps & 1) && !pair_taps) || steps_for(pps) > kMaxSteps) continue;
         int ns = (kSmemBudget - barrier_bytes - b_res) / a_stage(pps);
+        if (scm && a_stage(pps) < sc_a + sc_b) continue;
         // (the staged-pool stem holds its pooling band in shared memory too: 2 stages
         // there -- the tf32 stem's 64 KB of weights leave no room for 3)
         if (ns >= (sp.pool ? 2 : 3)) {
@@ -1387,6 +1477,7 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
         if (cc % pps || 3 * pps * ksteps > kMaxSteps) continue;
         const int bst = 3 * pps * cand * kb;
         const int ast = pps * a.subs * nbox3 * hbox3 * row_bytes;
+        if (scm && (ast < sc_a || bst < sc_b)) continue;
         int ns = (kSmemBudget - barrier_bytes) / (ast + bst);
         // (Measured: accepting 2 stages for a 2-tile super-tile -- half the per-tile
         // weight re-streaming of layers 3-4 -- made those convs 1.02-1.12x slower:
@@ -1410,6 +1501,7 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
     for (int pps : {4, 2, 1}) {
       if (cc % pps || pair_taps || (kb == 16 && (pps & 1)) || steps_for(pps) > kMaxSteps) continue;
       const int bst = ntaps * pps * cand * kb;
+      if (scm && (a_stage(pps) < sc_a || bst < sc_b)) continue;
       int ns = (kSmemBudget - barrier_bytes) / (a_stage(pps) + bst);
       if (ns >= 2) {
         a.resident_b = 0;
@@ -1486,7 +1578,7 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
       const char* e = std::getenv("MRB200_TC_PAIR");
       return e ? std::atoi(e) : 1;
     }();
-    const bool pair_ok = kb >= 64 && sp.kind != TC_STEM_S2D;
+    const bool pair_ok = kb >= 64 && sp.kind != TC_STEM_S2D && !scm;
     found = search();
     const bool pair_auto =
         found && ntaps == 9 && a.bn >= 128 && (eb > 1 || (!a.resident_b && (!sp.residual || 9 * cc * kb >= 4608)));
@@ -1502,6 +1594,16 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
   if (!found) return false;
   a.pair = pm;
   a.bn_local = a.bn >> pm;
+  if (scm) {
+    a.sc = 1;
+    a.sc_kb = sp.sc_kb;
+    a.sc_k_stages = sp.sc_C * eb / sp.sc_kb;
+    a.sc_ksteps = sp.sc_kb / 32;
+    a.sc_a_bytes = kTileM * a.sub * sp.sc_kb;
+    a.sc_b_bytes = a.bn * sp.sc_kb;
+    a.sc_b_in_a = a.resident_b;
+    a.sc_desc_hi = umma_desc_hi(8 * sp.sc_kb, sp.sc_kb == 128 ? 2 : 4);
+  }
   a.m_tiles = a.pool ? sp.N * sp.poh
                      : static_cast<int>((a.Pg + kTileM * (a.win ? 1 : a.sub) - 1) / (kTileM * (a.win ? 1 : a.sub)));
   if (a.pair) a.m_tiles = (a.m_tiles + 1) / 2;  // pair units (an odd last CTA tile reads zeros, writes nothing)
@@ -1711,13 +1813,58 @@ static int dbg_env() {
   return d;
 }
 
+// The fused shortcut's maps: A2 = decimated codes (LAY_NORMAL, dims {kb, Pp, 1,
+// planes}, box = the tile's 128*sub rows), B2 = [1][planes][OC][kb] weights
+// (box = one chunk plane of bn rows).
+static bool encode_sc_maps(TcConvPlan& p, const TcShortcut& sc) {
+  const TcArgs& a = p.args;
+  auto enc = encode_fn();
+  const int kb = a.sc_kb;
+  const CUtensorMapSwizzle swz = kb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  const cuuint64_t planes = static_cast<cuuint64_t>(a.sc_k_stages);
+  {
+    cuuint64_t dims[4] = {static_cast<cuuint64_t>(kb), static_cast<cuuint64_t>(sc.lay.Pp), 1, planes};
+    cuuint64_t strides[3] = {static_cast<cuuint64_t>(kb), static_cast<cuuint64_t>(sc.lay.Pp) * kb,
+                             static_cast<cuuint64_t>(sc.lay.Pp) * kb};
+    cuuint32_t box[4] = {static_cast<cuuint32_t>(kb), static_cast<cuuint32_t>(kTileM * a.sub), 1, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    if (enc(&p.tmA2, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(sc.x), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  {
+    const int OC = p.spec.OC;
+    cuuint64_t dims[4] = {static_cast<cuuint64_t>(kb), static_cast<cuuint64_t>(OC), planes, 1};
+    cuuint64_t strides[3] = {static_cast<cuuint64_t>(kb), static_cast<cuuint64_t>(OC) * kb,
+                             static_cast<cuuint64_t>(OC) * kb * planes};
+    cuuint32_t box[4] = {static_cast<cuuint32_t>(kb), static_cast<cuuint32_t>(a.bn), 1, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    if (enc(&p.tmB2, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(sc.w), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  p.map_x2 = sc.x;
+  p.map_w2 = sc.w;
+  return true;
+}
+
 bool tc_conv_launch(TcConvPlan* p, const void* x, const Lay& xl, const void* w, float acc_scale, const EpiDev& epi,
-                    const OutDev& out, cudaStream_t s) {
+                    const OutDev& out, cudaStream_t s, const TcShortcut* sc) {
   if (p->map_x != x || p->map_w != w) {
     if (!encode_maps(*p, x, xl, w)) return false;
   }
+  if (p->args.sc) {
+    if (!sc || !sc->x || !sc->w || !sc->bias) return false;
+    if ((p->map_x2 != sc->x || p->map_w2 != sc->w) && !encode_sc_maps(*p, *sc)) return false;
+  }
   TcArgs a = p->args;
   a.acc_scale = acc_scale;
+  if (a.sc) {
+    a.sc_scale = sc->acc_scale;
+    a.sc_bias = sc->bias;
+  }
   // TC_STEM_POOL takes the window max on the accumulators: exact only when the
   // accumulator -> float map is non-decreasing
   if (a.win && !(acc_scale > 0.f)) return false;
@@ -1807,9 +1954,10 @@ bool tc_conv_launch(TcConvPlan* p, const void* x, const Lay& xl, const void* w, 
       cudaFuncSetAttribute(k_conv_tc<EB_, SIG_, CAL_, true, W_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                            static_cast<int>(p->smem));                                                    \
       pdl_launch_cluster(k_conv_tc<EB_, SIG_, CAL_, true, W_>, p->grid, (2 + W_) * 32, p->smem, s, 2, p->tmA, \
-                         p->tmB, a);                                                                      \
+                         p->tmB, p->tmA2, p->tmB2, a);                                                    \
     } else {                                                                                              \
-      pdl_launch(k_conv_tc<EB_, SIG_, CAL_, false, W_>, p->grid, (2 + W_) * 32, p->smem, s, p->tmA, p->tmB, a); \
+      pdl_launch(k_conv_tc<EB_, SIG_, CAL_, false, W_>, p->grid, (2 + W_) * 32, p->smem, s, p->tmA, p->tmB,   \
+                 p->tmA2, p->tmB2, a);                                                                    \
     }                                                                                                     \
   } while (0)
 #define MRB_TC_LAUNCH(EB_, SIG_, CAL_) MRB_TC_LAUNCH_W(EB_, SIG_, CAL_, kEpiWarps)
@@ -1866,6 +2014,11 @@ const char* tc_conv_describe(const TcConvPlan* p, char* buf, int n) {
                 kinds[p->spec.kind], a.sub, a.pair ? 256 : 128, a.bn, a.kb, p->spec.taps, a.n_steps,
                 a.Hg, a.Wg, a.nbox, a.hbox, a.pps, a.n_stages,
                 a.resident_b ? "resident" : a.tap_groups > 1 ? "streamed-by-kernel-row" : "streamed", p->grid, p->smem);
+  if (a.sc) {
+    const size_t l = std::strlen(buf);
+    std::snprintf(buf + l, n > static_cast<int>(l) ? n - l : 0, " +shortcut(1x1 K=%d kb=%d)", a.sc_k_stages * a.sc_kb,
+                  a.sc_kb);
+  }
   return buf;
 }
 

@@ -27,6 +27,13 @@ struct TcConvSpec {
   // the epilogue adds a residual (an epilogue-bound conv: the CTA-pair plan,
   // which helps weight-streaming convs, does not pay there -- measured)
   int residual = 0;
+  // Fused 1x1/stride-2 shortcut (cross-group fusion of a ResNet downsampling
+  // block): the residual operand of this 3x3 stride-1 conv is computed in the
+  // same kernel -- a second accumulator over sc_C input channels read from a
+  // stride-2 decimated int8 copy of the block input on this conv's own padded
+  // grid (chunk width sc_kb, the shortcut weights' layout) -- instead of being
+  // read back from the shortcut conv's float32 output.  0: none.
+  int sc_C = 0, sc_kb = 0;
   // filled by planning
   int taps = 0, wplanes = 0;  // weight layout [taps][wplanes][OC][kb bytes]
   int kb = 0;                 // operand chunk bytes (the data representation's chunk width)
@@ -34,11 +41,22 @@ struct TcConvSpec {
 
 struct TcConvPlan;
 
+// Device operands of the fused shortcut (TcConvSpec::sc_C): decimated codes
+// (LAY_NORMAL on this conv's output grid), the shortcut's tcgen05 weights
+// [1][sc_C/cpc][OC][cpc], its accumulator scale and bias vector.
+struct TcShortcut {
+  const void* x = nullptr;
+  Lay lay{};
+  const void* w = nullptr;
+  float acc_scale = 1.f;
+  const float* bias = nullptr;
+};
+
 // Compile-time eligibility (fills taps / wplanes).
 bool tc_conv_plan_ok(TcConvSpec& spec);
 TcConvPlan* tc_conv_create(const TcConvSpec& spec);
 bool tc_conv_launch(TcConvPlan* p, const void* x, const Lay& xl, const void* w, float acc_scale, const EpiDev& epi,
-                    const OutDev& out, cudaStream_t s);
+                    const OutDev& out, cudaStream_t s, const TcShortcut* sc = nullptr);
 void tc_conv_destroy(TcConvPlan* p);
 const char* tc_conv_describe(const TcConvPlan* p, char* buf, int n);
 

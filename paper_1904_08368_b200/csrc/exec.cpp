@@ -87,6 +87,9 @@ struct Rep {
   int64_t elems = 0;       // including the zero border and chunk padding
   Lay lay{};               // P16 (4-D) or row-major (2-D)
   int buf = -1;            // arena buffer id
+  // stride-2 decimated int8 codes (pixel (2i, 2j) at (i, j)): written by the
+  // producer next to its side codes, read as A2 by a conv with a fused shortcut
+  bool dec = false;
 };
 
 struct Buffer {
@@ -137,6 +140,7 @@ struct Exec {
   std::map<int, int> want_kb;               // value -> chunk width its tcgen05 consumers read
   std::vector<int> fused_pool;              // conv group -> its max_pool2d consumer executed in-kernel, or -1
   std::vector<char> fused_away;             // group executed inside another group's launch
+  std::vector<int> sc_of;                   // 3x3 conv -> the 1x1/stride-2 shortcut group fused into it (-1)
   bool weights_ready = false;
   int64_t zero_bytes = 0;  // arena prefix of the zero-border buffers
   // io
@@ -541,6 +545,7 @@ struct GroupIO {
   // the prologue re-quantizes with the same chain (c1 * c2 == 1: the codes come back exactly)
   bool requant_data = false;
   QParams requant_q;
+  int sc_rep = -1;  // fused shortcut: the decimated codes rep of the block input (Exec::sc_of)
 };
 
 namespace {
@@ -690,9 +695,9 @@ EpiDev make_epi(Exec& ex, int gi, const GroupIO& io, int upto) {
       case EpiKind::Bias: e.op[n] = E_BIAS; e.vec[n] = nullptr; break;        // patched in set_weights
       case EpiKind::Residual: {
         e.op[n] = E_RES;
-        const Rep& r = ex.reps[op.value][io.res_rep[i]];
         e.res[n] = nullptr;  // arena address patched at launch (residual_fix)
-        e.res_fmt[n] = r.fmt;
+        // (res_rep -1: a fused shortcut computes it in-kernel from its own accumulator)
+        e.res_fmt[n] = io.res_rep[i] >= 0 ? ex.reps[op.value][io.res_rep[i]].fmt : FMT_F32;
         break;
       }
       case EpiKind::Relu: e.op[n] = E_RELU; break;
@@ -717,6 +722,71 @@ std::string dims_str(const std::vector<int64_t>& s) {
 
 }  // namespace
 
+// Cross-group fusion of a ResNet downsampling block's shortcut: a 1x1/stride-2
+// conv group whose only consumer is the residual add of a 3x3 stride-1 conv
+// group (bias -> add -> relu) runs inside that conv's launch (TcConvSpec::sc_C).
+// Its input -- the block input's int8 codes -- comes from a decimated copy the
+// block input's producer writes next to its side codes; the float32 shortcut
+// output (written and read back in full otherwise) disappears.  The arithmetic
+// is the shortcut group's own: acc2 * (data c2 * weight c2) + bias, then the
+// reference's add.  MRB200_NO_SHORTCUT_FUSE=1 keeps the groups apart (A/B).
+void fuse_shortcuts(Exec& ex, std::vector<GroupIO>& io) {
+  Program& P = ex.P;
+  ex.sc_of.assign(P.groups.size(), -1);
+  static const bool off = [] {
+    const char* e = std::getenv("MRB200_NO_SHORTCUT_FUSE");
+    return e && std::atoi(e);
+  }();
+  if (off) return;
+  for (size_t gm = 0; gm < P.groups.size(); ++gm) {
+    const GroupDesc& m = P.groups[gm];
+    if (ex.group_path[gm] != P_CONV_I8_TC || ex.fused_away[gm] || ex.group_tc[gm].kind != TC_S1 || m.kh != 3 ||
+        m.kw != 3 || ex.fused_pool[gm] >= 0 || g_has_sum(m))
+      continue;
+    if (m.epi.size() != 3 || m.epi[0].kind != EpiKind::Bias || m.epi[1].kind != EpiKind::Residual ||
+        m.epi[2].kind != EpiKind::Relu)
+      continue;
+    const int vs = m.epi[1].value;
+    const ValueInfo& sv = P.values[vs];
+    const int gs = sv.producer;
+    if (gs < 0 || sv.is_result || sv.consumers.size() != 1 || sv.consumers[0] != static_cast<int>(gm)) continue;
+    const GroupDesc& sg = P.groups[gs];
+    if (sg.kind != GroupKind::Conv || ex.group_path[gs] != P_CONV_I8_TC || ex.fused_away[gs] || ex.fused_pool[gs] >= 0 ||
+        ex.group_tc[gs].kind != TC_S2_PHASE || sg.kh != 1 || sg.kw != 1 || sg.sh != 2 || sg.sw != 2 || sg.ph != 0 ||
+        sg.pw != 0 || sg.epi.size() != 1 || sg.epi[0].kind != EpiKind::Bias || sg.out_shape != m.out_shape)
+      continue;
+    // the block input's codes are its producer's side output (a tcgen05 conv over the padded grid)
+    const int vu = sg.data.value;
+    const ValueInfo& uv = P.values[vu];
+    const int gp = uv.producer;
+    const int dr = io[gs].data_rep;
+    if (gp < 0 || uv.is_data || dr <= 0 || ex.reps[vu][dr].fmt != FMT_I8 || ex.group_path[gp] != P_CONV_I8_TC ||
+        ex.group_tc[gp].kind != TC_S1 || ex.fused_pool[gp] >= 0 || g_has_sum(P.groups[gp]))
+      continue;
+    bool has_dec = false;  // one decimated copy per value
+    for (const Rep& r : ex.reps[vu]) has_dec = has_dec || r.dec;
+    if (has_dec) continue;
+    TcConvSpec spec = ex.group_tc[gm];
+    spec.sc_C = static_cast<int>(sg.in_shape[1]);
+    spec.sc_kb = ex.group_tc[gs].kb;
+    if (!tc_conv_plan_ok(spec)) continue;
+    ex.group_tc[gm] = spec;
+    ex.sc_of[gm] = gs;
+    ex.fused_away[gs] = 1;
+    Rep r;
+    r.fmt = FMT_I8;
+    r.has_q = true;
+    r.q = ex.reps[vu][dr].q;
+    r.dec = true;
+    r.lay = make_lay({sg.out_shape[0], sg.in_shape[1], sg.out_shape[2], sg.out_shape[3]}, FMT_I8, LAY_NORMAL, 0,
+                     spec.sc_kb);
+    r.elems = lay_elems(r.lay);
+    ex.reps[vu].push_back(r);
+    io[gm].sc_rep = static_cast<int>(ex.reps[vu].size()) - 1;
+    io[gm].res_rep[1] = -1;
+  }
+}
+
 void build(Exec& ex) {
   Program& P = ex.P;
   const bool use_tc = !ex.opt.force_simt;
@@ -734,16 +804,22 @@ void build(Exec& ex) {
     }
   }
 
+  fuse_shortcuts(ex, io);
+
   Builder B{ex, io};
   // Producer side outputs: every I8 rep of a float value not produced by a
   // Requant must come from the producer kernel's side output (or an input
   // conversion for @main data).
-  std::vector<int> side_rep(P.groups.size(), -1);
+  std::vector<int> side_rep(P.groups.size(), -1), side2_rep(P.groups.size(), -1);
   for (size_t v = 0; v < P.values.size(); ++v) {
     const ValueInfo& vi = P.values[v];
     for (size_t r = 0; r < ex.reps[v].size(); ++r) {
       const Rep& rep = ex.reps[v][r];
       if (rep.nchw_user || r == 0 || vi.producer < 0) continue;  // rep 0 is the primary
+      if (rep.dec) {
+        side2_rep[vi.producer] = static_cast<int>(r);
+        continue;
+      }
       const bool tf32_side = rep.fmt == FMT_F32 && ex.opt.float_mode == MR_FLOAT_TF32 && !P.any_quant;
       if ((rep.fmt == FMT_I8 || rep.fmt == FMT_BF16 || tf32_side) && P.groups[vi.producer].kind != GroupKind::Dense &&
           !g_has_sum(P.groups[vi.producer])) {
@@ -824,6 +900,10 @@ void build(Exec& ex) {
     const std::string oname = fp >= 0 ? P.groups[fp].out_name : g.out_name;
     int obuf = B.buffer_for(ov, 0, "%" + oname);
     int sbuf = side_rep[sgi] >= 0 ? B.buffer_for(ov, side_rep[sgi], "%" + oname + ":codes") : -1;
+    int sbuf2 = side2_rep[sgi] >= 0 ? B.buffer_for(ov, side2_rep[sgi], "%" + oname + ":codes_s2") : -1;
+    if (sbuf2 >= 0) ex.bufs[sbuf2].zero_border = true;  // interior pixels only: the border stays zero
+    const int sc_g = ex.sc_of[gi];
+    if (sc_g >= 0) B.use(ex.reps[P.groups[sc_g].data.value][gio.sc_rep].buf);
     const Rep& orep = ex.reps[ov][0];
 
     bool has_sum = g_has_sum(g);
@@ -857,16 +937,18 @@ void build(Exec& ex) {
       out.side_fmt = sr.fmt;
       out.side_q = to_qdev(sr.q);
     }
+    if (sbuf2 >= 0) out.s2lay = ex.reps[ov][side2_rep[sgi]].lay;
 
     LaunchRec L;
-    L.name = "%" + g.name + (fp >= 0 ? "+%" + P.groups[fp].name : "");
-    L.kernel = std::string(path_name(path)) + (fp >= 0 ? "+max_pool" : "");
+    L.name = "%" + g.name + (fp >= 0 ? "+%" + P.groups[fp].name : "") + (sc_g >= 0 ? "+%" + P.groups[sc_g].name : "");
+    L.kernel = std::string(path_name(path)) + (fp >= 0 ? "+max_pool" : "") + (sc_g >= 0 ? "+shortcut" : "");
     // algorithmic traffic: data once + output(s) once + residuals + weights
     double out_bytes = static_cast<double>(orep.elems) * elem_bytes(orep.fmt);
     if (sbuf >= 0) {
       const Rep& sr = ex.reps[ov][side_rep[sgi]];
       out_bytes += static_cast<double>(sr.elems) * elem_bytes(sr.fmt);
     }
+    if (sbuf2 >= 0) out_bytes += static_cast<double>(ex.reps[ov][side2_rep[sgi]].elems);
     double in_bytes = static_cast<double>(drep.elems) * elem_bytes(drep.fmt);
     for (size_t i = 0; i < g.epi.size(); ++i)
       if (gio.res_rep[i] >= 0) {
@@ -883,6 +965,14 @@ void build(Exec& ex) {
       flops = 2.0 * static_cast<double>(M) * static_cast<double>(wn);
     } else if (g.kind == GroupKind::DwConv) {
       flops = 2.0 * g.out_shape[0] * g.out_shape[1] * g.out_shape[2] * g.out_shape[3] * g.kh * g.kw;
+    }
+    if (sc_g >= 0) {  // the fused shortcut: decimated codes + its weights, its MACs
+      const GroupDesc& sg = P.groups[sc_g];
+      in_bytes += static_cast<double>(ex.reps[sg.data.value][gio.sc_rep].elems);
+      int64_t wn = 1;
+      for (auto d : sg.weight.shape) wn *= d;
+      wbytes += static_cast<double>(wn);
+      flops += 2.0 * static_cast<double>(sg.out_shape[0] * sg.out_shape[2] * sg.out_shape[3]) * static_cast<double>(wn);
     }
     L.bytes = in_bytes + out_bytes + wbytes;
     L.flops = flops;
@@ -911,13 +1001,14 @@ void build(Exec& ex) {
     }
     float acc_scale = g.weight.quant ? gio.data_scale * g.weight.q.c2 : 1.f;
     // buffers' final addresses are only known after assign_offsets: capture ids.
-    struct Ptrs { int out, side, presum; };
-    Ptrs pb{obuf, sbuf, pre_sum_buf};
+    struct Ptrs { int out, side, presum, side2; };
+    Ptrs pb{obuf, sbuf, pre_sum_buf, sbuf2};
     auto outdev = [e, pb, out]() {
       OutDev o = out;
       if (pb.presum >= 0) o.primary = e->ptr(pb.presum);
       else o.primary = e->bufs[pb.out].dead ? nullptr : e->ptr(pb.out);
       o.side = pb.side >= 0 ? e->ptr(pb.side) : nullptr;
+      o.side2 = pb.side2 >= 0 ? e->ptr(pb.side2) : nullptr;
       return o;
     };
     auto epidev = [e, gidx, epi]() {
@@ -939,7 +1030,7 @@ void build(Exec& ex) {
       int n = 0;
       for (size_t i = 0; i < gg.epi.size() && n < d.n_ops; ++i) {
         if (gg.epi[i].kind == EpiKind::SumHW || gg.epi[i].kind == EpiKind::Flatten) continue;
-        if (gg.epi[i].kind == EpiKind::Residual) {
+        if (gg.epi[i].kind == EpiKind::Residual && gio.res_rep[i] >= 0) {
           const Rep& r = e->reps[gg.epi[i].value][gio.res_rep[i]];
           d.res[n] = e->ptr(r.buf);
           d.res_lay[n] = r.lay;
@@ -982,10 +1073,31 @@ void build(Exec& ex) {
         if (pre_sum_buf < 0 && sbuf >= 0) L.opt_primary = obuf;
         std::string gname = g.name;
         Lay dlay = drep.lay;
-        L.fn = [e, gidx, dbuf, dlay, acc_scale, tp, outdev, epidev, residual_fix, gname](cudaStream_t s) {
+        // fused shortcut operands (buffer ids: addresses are final only after assign_offsets)
+        int sc_buf = -1, sc_bias_param = -1;
+        Lay sc_lay{};
+        float sc_scale = 1.f;
+        if (sc_g >= 0) {
+          const GroupDesc& sg = P.groups[sc_g];
+          const Rep& sr = ex.reps[sg.data.value][gio.sc_rep];
+          sc_buf = sr.buf;
+          sc_lay = sr.lay;
+          sc_scale = io[sc_g].data_scale * sg.weight.q.c2;
+          sc_bias_param = P.values[sg.epi[0].value].param_index;
+        }
+        L.fn = [e, gidx, dbuf, dlay, acc_scale, tp, outdev, epidev, residual_fix, gname, sc_g, sc_buf, sc_lay, sc_scale,
+                sc_bias_param](cudaStream_t s) {
           EpiDev d = epidev();
           residual_fix(d);
-          if (!tc_conv_launch(tp, e->ptr(dbuf), dlay, e->group_w[gidx], acc_scale, d, outdev(), s))
+          TcShortcut sc;
+          if (sc_g >= 0) {
+            sc.x = e->ptr(sc_buf);
+            sc.lay = sc_lay;
+            sc.w = e->group_w[sc_g];
+            sc.acc_scale = sc_scale;
+            sc.bias = static_cast<const float*>(e->param_dev[sc_bias_param]);
+          }
+          if (!tc_conv_launch(tp, e->ptr(dbuf), dlay, e->group_w[gidx], acc_scale, d, outdev(), s, sc_g >= 0 ? &sc : nullptr))
             fail(MR_ERR_CUDA, "group %" + gname + ": TMA descriptor encoding failed");
         };
         break;

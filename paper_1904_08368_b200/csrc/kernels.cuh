@@ -93,6 +93,11 @@ struct OutDev {
   QDev side_q;
   int32_t tf32;         // tf32 mode: float32 activations are stored rounded to tf32 (the tensor
                         //   cores read only the top 19 bits; truncation would bias every product)
+  // optional stride-2 decimated copy of the int8 side codes (tcgen05 conv only):
+  // pixel (2i, 2j) of the image -> (i, j) of the LAY_NORMAL layout s2lay, the
+  // A2 operand of a consumer conv with a fused 1x1/stride-2 shortcut
+  void* side2;
+  Lay s2lay;
 };
 
 // Division by a launch-constant divisor d for dividends n < 2^31 as a

@@ -83,6 +83,20 @@ def test_resnet18_int8_b256_every_group_proven_exact(gpu):
 
 
 @pytest.mark.gpu
+def test_resnet18_int8_shortcut_convs_fused_into_their_residual_consumer(gpu):
+    """Cross-group fusion: each downsampling block's 1x1/stride-2 shortcut group
+    runs inside the 3x3 conv that adds it (a second TMEM accumulator over the
+    block input's decimated codes); the every-row bit-exact test above runs
+    this plan.  Three blocks: layers 2-4."""
+    ex, _ = setup("resnet18", "int8", 256)
+    launches = ex.describe()["launches"]
+    fused = [L["name"] for L in launches if L["kernel"] == "conv_i8_tcgen05+shortcut"]
+    assert len(fused) == 3, fused
+    # input conversion, stem+pool, 19 - 3 convs, the head's sum_hw and dense
+    assert len(launches) == 1 + 1 + 16 + 1 + 1
+
+
+@pytest.mark.gpu
 def test_tiny_int8_b64_simt_path_every_row(gpu):
     g = gold("resnet18_tiny_div_b64.npz")
     ex, src = setup("resnet18_tiny", "int8", 64, force_simt=True)
