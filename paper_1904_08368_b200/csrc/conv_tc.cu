@@ -721,11 +721,19 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
         }
         for (int j = 0; j < a.sc_k_stages; ++j) {  // fused shortcut: A2 = the tile's own rows, 1x1 tap
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], a.sc_a_bytes + a.sc_b_bytes);
           uint8_t* dA = smA + stage * a.a_stage_bytes;
-          tma_load_4d(dA, &tmA2, &full[stage], 0, own(mt) * msub, 0, j);
-          tma_load_4d(a.sc_b_in_a ? dA + a.sc_a_bytes : smB + stage * a.b_stage_bytes, &tmB2, &full[stage], 0,
-                      n_tile * a.bn, j, 0);
+          uint8_t* dB = a.sc_b_in_a ? dA + a.sc_a_bytes : smB + stage * a.b_stage_bytes;
+          const int brow = n_tile * a.bn + static_cast<int>(rank) * a.bn_local;
+          if constexpr (PAIR) {  // each CTA its own rows and half the weight rows, on the leader's barrier
+            if (rank == 0) mbar_expect_tx(&full[stage], 2 * (a.sc_a_bytes + a.sc_b_bytes));
+            const uint32_t full_c = mapa_u32(&full[stage], 0);
+            tma_load_4d_pair(dA, &tmA2, full_c, 0, own(mt) * msub, 0, j);
+            tma_load_4d_pair(dB, &tmB2, full_c, 0, brow, j, 0);
+          } else {
+            mbar_expect_tx(&full[stage], a.sc_a_bytes + a.sc_b_bytes);
+            tma_load_4d(dA, &tmA2, &full[stage], 0, own(mt) * msub, 0, j);
+            tma_load_4d(dB, &tmB2, &full[stage], 0, brow, j, 0);
+          }
           if (++stage == a.n_stages) {
             stage = 0;
             phase ^= 1;
@@ -843,7 +851,7 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
             phase ^= 1;
           }
         }
-        if (!PAIR && a.sc) {  // fused shortcut: second accumulator at column 2*sub*bn
+        if (a.sc) {  // fused shortcut: second accumulator at column 2*sub*bn
           const uint64_t hi2 = static_cast<uint64_t>(a.sc_desc_hi) << 32;
           const uint32_t tmem_d2 = tmem_base + 2u * sub * bn + static_cast<uint32_t>(acc) * sub * bn;
           const uint32_t sub2 = static_cast<uint32_t>(kTileM * a.sc_kb) >> 4;  // 128 rows x sc_kb, in 16 B
@@ -855,11 +863,14 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
             if (!no_mma)
               for (int kk = 0; kk < a.sc_ksteps; ++kk) {
                 const uint64_t bd = hi2 | (((sB + kk * 32) >> 4) | (1u << 16));
-                for (uint32_t sb = 0; sb < sub; ++sb)
-                  umma<EB>(tmem_d2 + sb * bn, hi2 | ((((sA + kk * 32) >> 4) + sb * sub2) | (1u << 16)), bd, idesc,
-                           (j | kk) != 0 ? 1u : 0u);
+                for (uint32_t sb = 0; sb < sub; ++sb) {
+                  const uint64_t ad = hi2 | ((((sA + kk * 32) >> 4) + sb * sub2) | (1u << 16));
+                  if constexpr (PAIR) umma_pair<EB>(tmem_d2 + sb * bn, ad, bd, idesc, (j | kk) != 0 ? 1u : 0u);
+                  else umma<EB>(tmem_d2 + sb * bn, ad, bd, idesc, (j | kk) != 0 ? 1u : 0u);
+                }
               }
-            umma_commit(&empty[stage]);
+            if constexpr (PAIR) umma_commit_pair(&empty[stage], 3);
+            else umma_commit(&empty[stage]);
             if (++stage == a.n_stages) {
               stage = 0;
               phase ^= 1;
@@ -1155,7 +1166,7 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
           uint32_t raw[16];
           tmem_ld16(taddr_of(sb, c), raw);  // warp-collective: every lane executes it
           if (!early && valid && !d.border) epilogue_prefetch<SIG>(a, d, n_tile * a.bn + c, s_vec, p2ok, c, pb, pr);
-          if constexpr (SIG == SIG_BIAS_RES_RELU && !PAIR) {
+          if constexpr (SIG == SIG_BIAS_RES_RELU) {
             if (a.sc) {  // fused shortcut: residual = acc2 * sc_scale + sc_bias (the shortcut group's ops)
               uint32_t raw2[16];
               tmem_ld16(taddr_of(sb, c) + 2u * static_cast<uint32_t>(a.sub * a.bn), raw2);
@@ -1435,8 +1446,8 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
     return false;
   auto try_cfg = [&](int cand_full, int sub, bool resident) {
     if (sp.OC % cand_full || 2 * sub * cand_full * (scm ? 2 : 1) > 512) return false;
-    if (scm && (pm || sub > 2)) return false;
-    const int sc_a = scm ? kTileM * sub * sp.sc_kb : 0, sc_b = scm ? cand_full * sp.sc_kb : 0;
+    if (scm && sub > 2) return false;
+    const int sc_a = scm ? kTileM * sub * sp.sc_kb : 0, sc_b = scm ? (cand_full >> pm) * sp.sc_kb : 0;
     if (pm && (cand_full >> 1) % 16) return false;
     const int cand = cand_full >> pm;  // weight rows staged per CTA
     int hg, nbox, hbox;
@@ -1578,7 +1589,7 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
       const char* e = std::getenv("MRB200_TC_PAIR");
       return e ? std::atoi(e) : 1;
     }();
-    const bool pair_ok = kb >= 64 && sp.kind != TC_STEM_S2D && !scm;
+    const bool pair_ok = kb >= 64 && sp.kind != TC_STEM_S2D;
     found = search();
     const bool pair_auto =
         found && ntaps == 9 && a.bn >= 128 && (eb > 1 || (!a.resident_b && (!sp.residual || 9 * cc * kb >= 4608)));
@@ -1600,7 +1611,7 @@ static bool choose_kb(TcConvPlan& p, int kb_pick) {
     a.sc_k_stages = sp.sc_C * eb / sp.sc_kb;
     a.sc_ksteps = sp.sc_kb / 32;
     a.sc_a_bytes = kTileM * a.sub * sp.sc_kb;
-    a.sc_b_bytes = a.bn * sp.sc_kb;
+    a.sc_b_bytes = a.bn_local * sp.sc_kb;
     a.sc_b_in_a = a.resident_b;
     a.sc_desc_hi = umma_desc_hi(8 * sp.sc_kb, sp.sc_kb == 128 ? 2 : 4);
   }
@@ -1838,7 +1849,7 @@ static bool encode_sc_maps(TcConvPlan& p, const TcShortcut& sc) {
     cuuint64_t dims[4] = {static_cast<cuuint64_t>(kb), static_cast<cuuint64_t>(OC), planes, 1};
     cuuint64_t strides[3] = {static_cast<cuuint64_t>(kb), static_cast<cuuint64_t>(OC) * kb,
                              static_cast<cuuint64_t>(OC) * kb * planes};
-    cuuint32_t box[4] = {static_cast<cuuint32_t>(kb), static_cast<cuuint32_t>(a.bn), 1, 1};
+    cuuint32_t box[4] = {static_cast<cuuint32_t>(kb), static_cast<cuuint32_t>(a.bn_local), 1, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     if (enc(&p.tmB2, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(sc.w), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
