@@ -527,6 +527,8 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
         for (int h = 0; h < 4; ++h)
           w4[h] = pack_bf16x2(v[8 * j + 2 * h], v[8 * j + 2 * h + 1]);
         st16(o.side, gran_byte(o.slay, d.side_base, d.side_pstride, c0 + 8 * j), make_uint4(w4[0], w4[1], w4[2], w4[3]));
+        if (d.dec_pix >= 0)
+          st16(o.side2, gran_byte(o.s2lay, d.dec_pix, o.s2lay.Pp, c0 + 8 * j), make_uint4(w4[0], w4[1], w4[2], w4[3]));
       }
     }
   }
@@ -1181,6 +1183,14 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
                   const float v2 = EB == 1 ? __fmul_rn(static_cast<float>(static_cast<int32_t>(raw2[i])), a.sc_scale)
                                            : __uint_as_float(raw2[i]);
                   pr[i] = __fadd_rn(v2, bb[h]);
+                }
+              }
+              if constexpr (EB == 2) {  // the unfused bf16 pipeline stores the shortcut as bf16: same rounding
+#pragma unroll
+                for (int i = 0; i < 16; i += 2) {
+                  const uint32_t w = pack_bf16x2(pr[i], pr[i + 1]);
+                  pr[i] = __uint_as_float(w << 16);
+                  pr[i + 1] = __uint_as_float(w & 0xffff0000u);
                 }
               }
             }

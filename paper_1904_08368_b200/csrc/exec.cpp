@@ -740,7 +740,8 @@ void fuse_shortcuts(Exec& ex, std::vector<GroupIO>& io) {
   if (off) return;
   for (size_t gm = 0; gm < P.groups.size(); ++gm) {
     const GroupDesc& m = P.groups[gm];
-    if (ex.group_path[gm] != P_CONV_I8_TC || ex.fused_away[gm] || ex.group_tc[gm].kind != TC_S1 || m.kh != 3 ||
+    const int path = ex.group_path[gm];
+    if ((path != P_CONV_I8_TC && path != P_CONV_BF16_TC) || ex.fused_away[gm] || ex.group_tc[gm].kind != TC_S1 || m.kh != 3 ||
         m.kw != 3 || ex.fused_pool[gm] >= 0 || g_has_sum(m))
       continue;
     if (m.epi.size() != 3 || m.epi[0].kind != EpiKind::Bias || m.epi[1].kind != EpiKind::Residual ||
@@ -751,7 +752,7 @@ void fuse_shortcuts(Exec& ex, std::vector<GroupIO>& io) {
     const int gs = sv.producer;
     if (gs < 0 || sv.is_result || sv.consumers.size() != 1 || sv.consumers[0] != static_cast<int>(gm)) continue;
     const GroupDesc& sg = P.groups[gs];
-    if (sg.kind != GroupKind::Conv || ex.group_path[gs] != P_CONV_I8_TC || ex.fused_away[gs] || ex.fused_pool[gs] >= 0 ||
+    if (sg.kind != GroupKind::Conv || ex.group_path[gs] != path || ex.fused_away[gs] || ex.fused_pool[gs] >= 0 ||
         ex.group_tc[gs].kind != TC_S2_PHASE || sg.kh != 1 || sg.kw != 1 || sg.sh != 2 || sg.sw != 2 || sg.ph != 0 ||
         sg.pw != 0 || sg.epi.size() != 1 || sg.epi[0].kind != EpiKind::Bias || sg.out_shape != m.out_shape)
       continue;
@@ -760,7 +761,8 @@ void fuse_shortcuts(Exec& ex, std::vector<GroupIO>& io) {
     const ValueInfo& uv = P.values[vu];
     const int gp = uv.producer;
     const int dr = io[gs].data_rep;
-    if (gp < 0 || uv.is_data || dr <= 0 || ex.reps[vu][dr].fmt != FMT_I8 || ex.group_path[gp] != P_CONV_I8_TC ||
+    const int dfmt = path == P_CONV_I8_TC ? FMT_I8 : FMT_BF16;
+    if (gp < 0 || uv.is_data || dr <= 0 || ex.reps[vu][dr].fmt != dfmt || ex.group_path[gp] != path ||
         ex.group_tc[gp].kind != TC_S1 || ex.fused_pool[gp] >= 0 || g_has_sum(P.groups[gp]))
       continue;
     bool has_dec = false;  // one decimated copy per value
@@ -774,11 +776,11 @@ void fuse_shortcuts(Exec& ex, std::vector<GroupIO>& io) {
     ex.sc_of[gm] = gs;
     ex.fused_away[gs] = 1;
     Rep r;
-    r.fmt = FMT_I8;
-    r.has_q = true;
+    r.fmt = dfmt;
+    r.has_q = ex.reps[vu][dr].has_q;
     r.q = ex.reps[vu][dr].q;
     r.dec = true;
-    r.lay = make_lay({sg.out_shape[0], sg.in_shape[1], sg.out_shape[2], sg.out_shape[3]}, FMT_I8, LAY_NORMAL, 0,
+    r.lay = make_lay({sg.out_shape[0], sg.in_shape[1], sg.out_shape[2], sg.out_shape[3]}, dfmt, LAY_NORMAL, 0,
                      spec.sc_kb);
     r.elems = lay_elems(r.lay);
     ex.reps[vu].push_back(r);
@@ -948,7 +950,10 @@ void build(Exec& ex) {
       const Rep& sr = ex.reps[ov][side_rep[sgi]];
       out_bytes += static_cast<double>(sr.elems) * elem_bytes(sr.fmt);
     }
-    if (sbuf2 >= 0) out_bytes += static_cast<double>(ex.reps[ov][side2_rep[sgi]].elems);
+    if (sbuf2 >= 0) {
+      const Rep& r2 = ex.reps[ov][side2_rep[sgi]];
+      out_bytes += static_cast<double>(r2.elems) * elem_bytes(r2.fmt);
+    }
     double in_bytes = static_cast<double>(drep.elems) * elem_bytes(drep.fmt);
     for (size_t i = 0; i < g.epi.size(); ++i)
       if (gio.res_rep[i] >= 0) {
@@ -968,10 +973,11 @@ void build(Exec& ex) {
     }
     if (sc_g >= 0) {  // the fused shortcut: decimated codes + its weights, its MACs
       const GroupDesc& sg = P.groups[sc_g];
-      in_bytes += static_cast<double>(ex.reps[sg.data.value][gio.sc_rep].elems);
+      const Rep& r2 = ex.reps[sg.data.value][gio.sc_rep];
+      in_bytes += static_cast<double>(r2.elems) * elem_bytes(r2.fmt);
       int64_t wn = 1;
       for (auto d : sg.weight.shape) wn *= d;
-      wbytes += static_cast<double>(wn);
+      wbytes += static_cast<double>(wn) * (sg.weight.quant ? 1 : 2);
       flops += 2.0 * static_cast<double>(sg.out_shape[0] * sg.out_shape[2] * sg.out_shape[3]) * static_cast<double>(wn);
     }
     L.bytes = in_bytes + out_bytes + wbytes;
@@ -1082,7 +1088,7 @@ void build(Exec& ex) {
           const Rep& sr = ex.reps[sg.data.value][gio.sc_rep];
           sc_buf = sr.buf;
           sc_lay = sr.lay;
-          sc_scale = io[sc_g].data_scale * sg.weight.q.c2;
+          sc_scale = sg.weight.quant ? io[sc_g].data_scale * sg.weight.q.c2 : 1.f;
           sc_bias_param = P.values[sg.epi[0].value].param_index;
         }
         L.fn = [e, gidx, dbuf, dlay, acc_scale, tp, outdev, epidev, residual_fix, gname, sc_g, sc_buf, sc_lay, sc_scale,
