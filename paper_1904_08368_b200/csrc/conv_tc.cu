@@ -296,7 +296,12 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
   const int peb = pf == FMT_F32 ? 4 : pf == FMT_BF16 ? 2 : 1;  // 16-byte granules per 16 channels
   const int seb = o.side_fmt == FMT_F32 ? 4 : o.side_fmt == FMT_BF16 ? 2 : 1;
   // o.primary null: no launch reads the primary output (exec.cpp Buffer::dead), only the side codes
-  if (d.border) {
+  // Border rows of the padded grid store zeros through the same stores as every
+  // other row (a predicated select, not a branch: almost every warp's 32 rows
+  // hold a border pixel, and a separate zero path ran diverged for 60 % of the
+  // layer-1 warps -- 14 % of the kernel's instructions, ncu source view).
+  // Calibration runs keep the branch (their observers must not see these rows).
+  if (CAL && d.border) {
     if (o.primary)
       for (int g = 0; g < peb; ++g) st16(o.primary, gran_byte(o.plan, d.pix, o.plan.Pp, c0 + g * 16 / peb), make_uint4(0, 0, 0, 0));
     if (o.side)
@@ -304,6 +309,7 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
         st16(o.side, gran_byte(o.slay, d.side_base, d.side_pstride, c0 + g * 16 / seb), make_uint4(0, 0, 0, 0));
     return;
   }
+  const bool bz = !CAL && d.border;
   float v[16];
   int32_t code[16];
 #pragma unroll
@@ -409,9 +415,9 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
           const int r = __float2int_rn(y);
 #endif
 #if MRB200_P2_SATPACK
-          code_raw[i] = r;
+          code_raw[i] = bz ? 0 : r;
 #else
-          code[i] = min(max(r, 0), a.p2_hi);
+          code[i] = bz ? 0 : min(max(r, 0), a.p2_hi);
 #endif
         }
         if (CAL && e.q[2].ovf) {  // calibration: the rounded site value max(r, 0) must not exceed 128
@@ -462,6 +468,13 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
       // v (= code * c2) is only needed for a side output, never emitted here
     }
   }
+  if (bz) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      v[i] = 0.f;
+      code[i] = 0;
+    }
+  }
   if (!o.primary) {
   } else if (pf == FMT_I8) {
     st16(o.primary, gran_byte(o.plan, d.pix, o.plan.Pp, c0),
@@ -498,7 +511,7 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           if constexpr (CAL) quant_observe(v[i], o.side_q);
-          sc[i] = __float2int_rn(__fmul_rn(v[i], o.side_q.c1));  // cvt.rni: == trunc(rint(y)), one F2I
+          sc[i] = bz ? 0 : __float2int_rn(__fmul_rn(v[i], o.side_q.c1));  // cvt.rni: == trunc(rint(y)), one F2I
         }
         const uint4 u = make_uint4(pack4_sat_s8(sc[0], sc[1], sc[2], sc[3]), pack4_sat_s8(sc[4], sc[5], sc[6], sc[7]),
                                    pack4_sat_s8(sc[8], sc[9], sc[10], sc[11]), pack4_sat_s8(sc[12], sc[13], sc[14], sc[15]));
@@ -508,7 +521,7 @@ __device__ __forceinline__ void epilogue_chunk(const TcArgs& a, const uint32_t* 
       }
 #endif
 #pragma unroll
-      for (int i = 0; i < 16; ++i) sc[i] = quant_code_fast_t<CAL>(v[i], o.side_q);
+      for (int i = 0; i < 16; ++i) sc[i] = bz ? 0 : quant_code_fast_t<CAL>(v[i], o.side_q);
       const uint4 u = make_uint4(pack4_i8(sc[0], sc[1], sc[2], sc[3]), pack4_i8(sc[4], sc[5], sc[6], sc[7]),
                                  pack4_i8(sc[8], sc[9], sc[10], sc[11]), pack4_i8(sc[12], sc[13], sc[14], sc[15]));
       st16(o.side, gran_byte(o.slay, d.side_base, d.side_pstride, c0), u);
