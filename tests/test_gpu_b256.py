@@ -184,3 +184,61 @@ def test_tf32_runs_tcgen05_kernels(gpu):
     ex, _ = setup("resnet18", "fp32", 2, float_mode=mrb.MR_FLOAT_TF32)
     kernels = [g["kernel"] for g in ex.describe()["groups"]]
     assert kernels.count("conv_tf32_tcgen05") >= 18 and "dense_tf32_tcgen05" in kernels
+
+
+_PLAN_CHECK = r"""
+import hashlib, json, sys
+import numpy as np
+sys.path.insert(0, {root!r})
+import paper_1904_08368_b200 as mrb
+from paper_1904_08368_b200 import modelzoo
+text, meta, src = mrb.load_model("resnet18", {prec!r})
+w = modelzoo.make_weights(src, seed=meta["weights_seed"])
+ex = mrb.Executor(text, batch=256, **({{"float_mode": mrb.MR_FLOAT_BF16}} if {prec!r} == "fp32" else {{}}))
+ex.set_weights([w[p.name] for p in src.params if p.kind != "input"])
+y = ex.run_host(modelzoo.make_inputs_diverse(src, 256, seed=0))
+kinds = [L["kernel"] for L in ex.describe()["launches"]]
+plans = [g["plan"] for g in ex.describe()["groups"]]
+print(json.dumps({{"sha": hashlib.sha256(np.ascontiguousarray(y).tobytes()).hexdigest(),
+                   "pairs": sum("(M256)" in p for p in plans), "fused": sum(k.endswith("+shortcut") for k in kinds)}}))
+"""
+
+
+def _plan_run(prec, env):
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = dict(os.environ)
+    e.update(env)
+    p = subprocess.run([sys.executable, "-c", _PLAN_CHECK.format(root=root, prec=prec)], env=e, capture_output=True,
+                       text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    return json.loads(p.stdout.strip().splitlines()[-1])
+
+
+@pytest.mark.gpu
+def test_int8_plan_variants_are_bitwise_identical(gpu):
+    """The plan switches change how the convs run, never what they compute: CTA
+    pairs nowhere / wherever legal, and the shortcut fusion off, give the same
+    bits as the default plan (and the default plan matches the reference: the
+    every-row test above)."""
+    base = _plan_run("int8", {})
+    assert base["pairs"] > 0 and base["fused"] == 3
+    for env, pairs, fused in [({"MRB200_TC_PAIR": "0"}, 0, 3), ({"MRB200_TC_PAIR": "2"}, None, 3),
+                              ({"MRB200_NO_SHORTCUT_FUSE": "1"}, None, 0)]:
+        r = _plan_run("int8", env)
+        assert r["sha"] == base["sha"], env
+        if pairs is not None:
+            assert r["pairs"] == pairs, (env, r)
+        assert r["fused"] == fused, (env, r)
+
+
+@pytest.mark.gpu
+def test_bf16_shortcut_fusion_matches_unfused_bits(gpu):
+    """bf16: the fused shortcut rounds its value to bf16 exactly where the
+    unfused pipeline stores it, so the logits are bitwise those of the unfused plan."""
+    a = _plan_run("fp32", {})
+    b = _plan_run("fp32", {"MRB200_NO_SHORTCUT_FUSE": "1"})
+    assert a["fused"] == 3 and b["fused"] == 0
+    assert a["sha"] == b["sha"]
