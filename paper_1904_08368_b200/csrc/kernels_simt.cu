@@ -811,7 +811,7 @@ __global__ void __launch_bounds__(256) k_dwconv_fast(const void* __restrict__ x,
 // PL 16 (bf16 inputs in 128-byte chunks): 16 lanes cover one pixel's 64-channel
 // row, so every warp load / store is two whole 128-byte lines.
 constexpr int dw_outs(int pl) { return pl >= 8 ? 4 : 2; }
-constexpr int dw_minb(int pl) { return pl >= 8 ? 2 : 3; }
+constexpr int dw_minb(int pl) { return pl >= 16 ? 3 : pl >= 8 ? 2 : 3; }
 // DSIG: compile-time epilogue for MobileNet's (bf16 out, no side output)
 // multiply(gamma') -> bias_add -> clip(0, 6) / relu with the per-channel vectors
 // held in registers; DSIG 0 interprets the op list.
@@ -834,11 +834,21 @@ __global__ void __launch_bounds__(256, dw_minb(PL)) k_dw3x3_rb(const void* __res
   const int OWp = g.OW + 2 * kPad, OHp = g.OH + 2 * kPad;
   const bool f32 = xfmt == FMT_F32;
   const int c0 = static_cast<int>(blockIdx.y * PL + lo) * 4;
+  // PL 16: the block's 64 channels' weights in shared memory, [tap][channel] (one
+  // conflict-free 16-byte load per tap), freeing 36 registers for a third block per SM
+  constexpr bool SMW = PL == 16;
+  __shared__ __align__(16) float sw[SMW ? 9 * 64 : 4];
   float wr[4][9];
+  if constexpr (SMW) {
+    for (int i = threadIdx.x; i < 9 * 64; i += blockDim.x)
+      sw[i] = __ldg(w + static_cast<int64_t>(blockIdx.y * 64 + (i & 63)) * 9 + (i >> 6));
+    __syncthreads();
+  } else {
 #pragma unroll
-  for (int k = 0; k < 4; ++k)
+    for (int k = 0; k < 4; ++k)
 #pragma unroll
-    for (int tp = 0; tp < 9; ++tp) wr[k][tp] = __ldg(w + static_cast<int64_t>(c0 + k) * 9 + tp);
+      for (int tp = 0; tp < 9; ++tp) wr[k][tp] = __ldg(w + static_cast<int64_t>(c0 + k) * 9 + tp);
+  }
   float sv[2][4];  // DSIG != DW_ANY: gamma' and bias of this thread's 4 channels
   if constexpr (DSIG != DW_ANY) {
 #pragma unroll
@@ -880,14 +890,23 @@ __global__ void __launch_bounds__(256, dw_minb(PL)) k_dw3x3_rb(const void* __res
         }
       }
 #pragma unroll
-      for (int kw = 0; kw < 3; ++kw)
+      for (int kw = 0; kw < 3; ++kw) {
+        float w4[4];
+        if constexpr (SMW) {
+          const float4 f = *reinterpret_cast<const float4*>(sw + (kh * 3 + kw) * 64 + lo * 4);
+          w4[0] = f.x; w4[1] = f.y; w4[2] = f.z; w4[3] = f.w;
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) w4[k] = wr[k][kh * 3 + kw];
+        }
 #pragma unroll
         for (int o = 0; o < OUTS; ++o)
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            const float xv = col[o * SW + kw][k], wv = wr[k][kh * 3 + kw];
+            const float xv = col[o * SW + kw][k], wv = w4[k];
             acc[o][k] = strict ? __fadd_rn(acc[o][k], __fmul_rn(xv, wv)) : __fmaf_rn(xv, wv, acc[o][k]);
           }
+      }
     }
     if constexpr (DSIG != DW_ANY) {
 #pragma unroll
