@@ -4,6 +4,8 @@
 //           4 sub-tiles per step (k_conv_tc's MMA issuer)
 //   unroll  the same table, compile-time step count (fully unrolled)
 //   const   one descriptor pair (tc_align.cu's loop)
+//   +tmem   param loop while 3 warps stream tcgen05.ld from other TMEM columns
+//   +smem   param loop while 3 warps stream 16-byte shared-memory stores
 // with the 64-byte-swizzled K-major layout of the layer-1 A halo tile.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I paper_1904_08368_b200/csrc -o tc_issue tests/tc_issue.cu && ./tc_issue
 #include <cuda_runtime.h>
@@ -44,6 +46,27 @@ __global__ void __launch_bounds__(128, 1) k_issue(const __grid_constant__ Params
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = slot;
+  __shared__ volatile int stop;
+  if (threadIdx.x == 0) stop = 0;
+  __syncthreads();
+  if (MODE >= 3 && threadIdx.x >= 32) {
+    // interference: warps 1-3 read TMEM (mode 3: tcgen05.ld of columns 256-511, the
+    // epilogue's traffic) or stream stores into shared memory (mode 4: TMA-like writes)
+    const int w = threadIdx.x / 32;
+    uint32_t sink = 0;
+    while (!stop) {
+      if (MODE == 3) {
+        uint32_t r[16];
+        tmem_ld16(tmem + (static_cast<uint32_t>(w * 32) << 16) + 256 + (sink & 3) * 16, r);
+        sink += r[0] + r[15];
+      } else {
+        float4* dst = reinterpret_cast<float4*>(base + 72 * 1024) + (threadIdx.x - 32) + (sink & 7) * 96;
+        *dst = make_float4(1.f, 2.f, 3.f, static_cast<float>(sink));
+        sink += 1;
+      }
+    }
+    if (sink == 0xdeadbeef) out[1] = sink;
+  }
   if (threadIdx.x == 0) {
     const uint64_t hi = static_cast<uint64_t>(p.desc_hi) << 32;
     const uint32_t a16 = smem_u32(base) >> 4, b16 = smem_u32(base + 64 * 1024) >> 4;
@@ -51,7 +74,7 @@ __global__ void __launch_bounds__(128, 1) k_issue(const __grid_constant__ Params
     const unsigned long long t0 = clock64();
     for (int r = 0; r < p.reps; ++r) {
       const uint32_t dacc = (r & 1) * 256;
-      if (MODE == 0) {
+      if (MODE == 0 || MODE >= 3) {
         for (int st = 0; st < p.n_steps; ++st) {
           const uint64_t bd = hi | (p.steps[st].b_lo + b16);
           const uint32_t alo = p.steps[st].a_lo + a16;
@@ -77,6 +100,7 @@ __global__ void __launch_bounds__(128, 1) k_issue(const __grid_constant__ Params
     umma_commit(&bar);
     mbar_wait(&bar, 0);
     out[blockIdx.x] = clock64() - t0;
+    stop = 1;
   }
   tc_fence_before();
   __syncthreads();
@@ -104,10 +128,11 @@ int main() {
     }
   unsigned long long* d;
   cudaMalloc(&d, 148 * 8);
-  const char* names[] = {"param_runtime_steps", "unrolled_steps", "const_descriptors"};
+  const char* names[] = {"param_runtime_steps", "unrolled_steps", "const_descriptors", "with_tmem_reads",
+                         "with_smem_writes"};
   std::printf("{");
-  for (int mode = 0; mode < 3; ++mode) {
-    auto k = mode == 0 ? k_issue<0> : mode == 1 ? k_issue<1> : k_issue<2>;
+  for (int mode = 0; mode < 5; ++mode) {
+    auto k = mode == 0 ? k_issue<0> : mode == 1 ? k_issue<1> : mode == 2 ? k_issue<2> : mode == 3 ? k_issue<3> : k_issue<4>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
     k<<<1, 128, 112 * 1024>>>(p, d);
     cudaError_t e = cudaDeviceSynchronize();
