@@ -1967,6 +1967,9 @@ bool tc_conv_launch(TcConvPlan* p, const void* x, const Lay& xl, const void* w, 
   } tile_print{s, stamps, (dbg & 2048) != 0};
   if (dbg & 2048) cudaMemsetAsync(stamps, 0, 8 * 64 * 8, s);
   const int sig = epi_signature(epi, out);
+  // the fused shortcut replaces the residual read of the specialised bias -> add -> relu
+  // epilogue; any other epilogue form would read the (never written) shortcut tensor
+  if (a.sc && sig != SIG_BIAS_RES_RELU) return false;
   auto pow2 = [](float f) {
     int e = 0;
     return f > 0.f && std::isfinite(f) && std::frexp(f, &e) == 0.5f;

@@ -1104,7 +1104,7 @@ void build(Exec& ex) {
             sc.bias = static_cast<const float*>(e->param_dev[sc_bias_param]);
           }
           if (!tc_conv_launch(tp, e->ptr(dbuf), dlay, e->group_w[gidx], acc_scale, d, outdev(), s, sc_g >= 0 ? &sc : nullptr))
-            fail(MR_ERR_CUDA, "group %" + gname + ": TMA descriptor encoding failed");
+            fail(MR_ERR_CUDA, "group %" + gname + ": tcgen05 conv launch refused (TMA descriptor encoding or epilogue form)");
         };
         break;
       }
