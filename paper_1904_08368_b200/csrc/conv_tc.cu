@@ -1183,19 +1183,23 @@ __global__ void __launch_bounds__((2 + EPIW) * 32, 1)
           if (!early && valid && !d.border) epilogue_prefetch<SIG>(a, d, n_tile * a.bn + c, s_vec, p2ok, c, pb, pr);
           if constexpr (SIG == SIG_BIAS_RES_RELU) {
             if (a.sc) {  // fused shortcut: residual = acc2 * sc_scale + sc_bias (the shortcut group's ops)
-              uint32_t raw2[16];
-              tmem_ld16(taddr_of(sb, c) + 2u * static_cast<uint32_t>(a.sub * a.bn), raw2);
-              const float4* bp = reinterpret_cast<const float4*>(a.sc_bias + n_tile * a.bn + c);
+              // (two 8-column TMEM loads: fewer live registers in the 96-register epilogue)
 #pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const float4 f = __ldg(bp + j);
-                const float bb[4] = {f.x, f.y, f.z, f.w};
+              for (int hh = 0; hh < 2; ++hh) {
+                uint32_t raw2[8];
+                tmem_ld8(taddr_of(sb, c) + 2u * static_cast<uint32_t>(a.sub * a.bn) + 8u * hh, raw2);
+                const float4* bp = reinterpret_cast<const float4*>(a.sc_bias + n_tile * a.bn + c + 8 * hh);
 #pragma unroll
-                for (int h = 0; h < 4; ++h) {
-                  const int i = 4 * j + h;
-                  const float v2 = EB == 1 ? __fmul_rn(static_cast<float>(static_cast<int32_t>(raw2[i])), a.sc_scale)
-                                           : __uint_as_float(raw2[i]);
-                  pr[i] = __fadd_rn(v2, bb[h]);
+                for (int j = 0; j < 2; ++j) {
+                  const float4 f = __ldg(bp + j);
+                  const float bb[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+                  for (int h = 0; h < 4; ++h) {
+                    const int i = 4 * j + h;
+                    const float v2 = EB == 1 ? __fmul_rn(static_cast<float>(static_cast<int32_t>(raw2[i])), a.sc_scale)
+                                             : __uint_as_float(raw2[i]);
+                    pr[8 * hh + i] = __fadd_rn(v2, bb[h]);
+                  }
                 }
               }
               if constexpr (EB == 2) {  // the unfused bf16 pipeline stores the shortcut as bf16: same rounding
