@@ -836,12 +836,13 @@ __global__ void __launch_bounds__(256, dw_minb(PL)) k_dw3x3_rb(const void* __res
   const int c0 = static_cast<int>(blockIdx.y * PL + lo) * 4;
   // PL 16: the block's 64 channels' weights in shared memory, [tap][channel] (one
   // conflict-free 16-byte load per tap), freeing 36 registers for a third block per SM
-  constexpr bool SMW = PL == 16;
-  __shared__ __align__(16) float sw[SMW ? 9 * 64 : 4];
+  constexpr bool SMW = PL == 16 || PL == 1;
+  constexpr int CH = 4 * PL;  // channels of the block's group
+  __shared__ __align__(16) float sw[SMW ? 9 * CH : 4];
   float wr[4][9];
   if constexpr (SMW) {
-    for (int i = threadIdx.x; i < 9 * 64; i += blockDim.x)
-      sw[i] = __ldg(w + static_cast<int64_t>(blockIdx.y * 64 + (i & 63)) * 9 + (i >> 6));
+    for (int i = threadIdx.x; i < 9 * CH; i += blockDim.x)
+      sw[i] = __ldg(w + static_cast<int64_t>(blockIdx.y * CH + (i % CH)) * 9 + (i / CH));
     __syncthreads();
   } else {
 #pragma unroll
@@ -893,7 +894,7 @@ __global__ void __launch_bounds__(256, dw_minb(PL)) k_dw3x3_rb(const void* __res
       for (int kw = 0; kw < 3; ++kw) {
         float w4[4];
         if constexpr (SMW) {
-          const float4 f = *reinterpret_cast<const float4*>(sw + (kh * 3 + kw) * 64 + lo * 4);
+          const float4 f = *reinterpret_cast<const float4*>(sw + (kh * 3 + kw) * CH + lo * 4);
           w4[0] = f.x; w4[1] = f.y; w4[2] = f.z; w4[3] = f.w;
         } else {
 #pragma unroll
