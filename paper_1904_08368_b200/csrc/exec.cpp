@@ -15,6 +15,7 @@
 #include <functional>
 #include <map>
 #include <memory>
+#include <set>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -138,6 +139,7 @@ struct Exec {
   std::vector<std::string> group_note;      // kernel plan description
   std::vector<TcConvSpec> group_tc;         // tcgen05 formulation per conv group
   std::map<int, int> want_kb;               // value -> chunk width its tcgen05 consumers read
+  std::set<int> f32_wide;                   // float32 values read only by depthwise convs: 128-byte chunks
   std::vector<int> fused_pool;              // conv group -> its max_pool2d consumer executed in-kernel, or -1
   std::vector<char> fused_away;             // group executed inside another group's launch
   std::vector<int> sc_of;                   // 3x3 conv -> the 1x1/stride-2 shortcut group fused into it (-1)
@@ -318,7 +320,7 @@ int want_rep(Exec& ex, int v, int fmt, const QParams* q, int kind = LAY_NORMAL, 
   // except in the tf32 mode, where tcgen05 convs read them in 128-byte chunks
   // and every consumer shares that one representation
   const bool tf32 = ex.opt.float_mode == MR_FLOAT_TF32 && !ex.P.any_quant;
-  if ((fmt == FMT_F32 && !tf32) || kind == LAY_S2D || kind == LAY_S2DP) kb = 16;
+  if ((fmt == FMT_F32 && !tf32 && !ex.f32_wide.count(v)) || kind == LAY_S2D || kind == LAY_S2DP) kb = 16;
   for (size_t i = 0; i < rs.size(); ++i) {
     const Rep& r = rs[i];
     if (r.nchw_user) continue;
@@ -499,11 +501,19 @@ void plan(Exec& ex, bool use_tc) {
   }();
   for (size_t gi = 0; gi < P.groups.size() && dw_wide; ++gi) {
     const GroupDesc& g = P.groups[gi];
-    if (g.kind != GroupKind::DwConv || ffmt != FMT_BF16 || g.in_shape[1] % 64 != 0 || g.kh != 3 || g.kw != 3) continue;
+    // (float32 inputs -- the int8 modules' float path -- likewise: 32 channels per
+    // 128-byte row, 8 lanes per pixel, and the int8 codes written as whole sectors)
+    const bool f32_in = ffmt == FMT_F32 && g.in_shape[1] % 32 == 0 && P.any_quant;
+    if (g.kind != GroupKind::DwConv || (!f32_in && (ffmt != FMT_BF16 || g.in_shape[1] % 64 != 0)) || g.kh != 3 ||
+        g.kw != 3)
+      continue;
     const ValueInfo& dv = P.values[g.data.value];
     bool only_dw = !dv.is_data;
     for (int c : dv.consumers) only_dw = only_dw && P.groups[c].kind == GroupKind::DwConv;
-    if (only_dw && !ex.want_kb.count(g.data.value)) ex.want_kb[g.data.value] = 128;
+    if (only_dw && !ex.want_kb.count(g.data.value)) {
+      ex.want_kb[g.data.value] = 128;
+      if (f32_in) ex.f32_wide.insert(g.data.value);
+    }
   }
   // primary representations of group outputs (chunk width from want_kb)
   for (size_t gi = 0; gi < P.groups.size(); ++gi) {

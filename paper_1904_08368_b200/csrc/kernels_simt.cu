@@ -1857,7 +1857,7 @@ void launch_dwconv(const void* x, int xfmt, const float* w, const ConvGeom& g, i
     // bf16 inputs: sector-complete stores; fp32 inputs (4-channel planes): pixel-consecutive lanes
     // keep the larger input reads coalesced
     const bool pl16 = g.C % 64 == 0 && xfmt == FMT_BF16 && g.in.kb == 128 && g.in.cpc == 64;
-    const bool pl8 = g.C % 32 == 0 && xfmt == FMT_BF16;
+    const bool pl8 = g.C % 32 == 0 && (xfmt == FMT_BF16 || (xfmt == FMT_F32 && g.in.kb == 128 && g.in.cpc == 32));
     const int outs = pl16 ? dw_outs(16) : pl8 ? dw_outs(8) : dw_outs(1);
     const int owq = (g.OW + outs - 1) / outs;
     const int64_t tot = static_cast<int64_t>(g.C / 4) * g.N * g.OH * owq;
@@ -1869,10 +1869,12 @@ void launch_dwconv(const void* x, int xfmt, const float* w, const ConvGeom& g, i
       // MobileNet's bf16 depthwise epilogues at compile time
       const bool simple = (pl16 || pl8) && out.primary_fmt == FMT_BF16 && !out.side && epi.n_ops == 3 &&
                           epi.op[0] == E_MULC && epi.op[1] == E_BIAS && (epi.op[2] == E_CLIP || epi.op[2] == E_RELU);
-      const bool simple_q = !pl16 && !pl8 && out.primary_fmt == FMT_I8 && !out.side && epi.n_ops == 4 &&
+      const bool simple_q = !pl16 && out.primary_fmt == FMT_I8 && !out.side && epi.n_ops == 4 &&
                             epi.op[0] == E_MULC && epi.op[1] == E_BIAS && epi.op[2] == E_CLIP && epi.op[3] == E_REQ &&
                             !epi.q[3].ovf;
-      if (simple_q) kern = g.sw == 1 ? k_dw3x3_rb<1, 1, DW_MULC_BIAS_CLIP_REQ> : k_dw3x3_rb<2, 1, DW_MULC_BIAS_CLIP_REQ>;
+      if (simple_q)
+        kern = pl8 ? (g.sw == 1 ? k_dw3x3_rb<1, 8, DW_MULC_BIAS_CLIP_REQ> : k_dw3x3_rb<2, 8, DW_MULC_BIAS_CLIP_REQ>)
+                   : (g.sw == 1 ? k_dw3x3_rb<1, 1, DW_MULC_BIAS_CLIP_REQ> : k_dw3x3_rb<2, 1, DW_MULC_BIAS_CLIP_REQ>);
       if (simple) {
         const bool clip = epi.op[2] == E_CLIP;
         if (g.sw == 1)
