@@ -900,13 +900,24 @@ __global__ void __launch_bounds__(256, dw_minb(PL)) k_dw3x3_rb(const void* __res
 #pragma unroll
           for (int k = 0; k < 4; ++k) w4[k] = wr[k][kh * 3 + kw];
         }
+        // paired fp32 FMA (sm_100 FFMA2): per lane the same fused op as __fmaf_rn,
+        // half the issue slots (the strict path stays scalar: paired multiply + add
+        // measured not bit-exact against the reference on MobileNet-v1 int8)
+        const float2 w01 = make_float2(w4[0], w4[1]), w23 = make_float2(w4[2], w4[3]);
 #pragma unroll
-        for (int o = 0; o < OUTS; ++o)
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const float xv = col[o * SW + kw][k], wv = w4[k];
-            acc[o][k] = strict ? __fadd_rn(acc[o][k], __fmul_rn(xv, wv)) : __fmaf_rn(xv, wv, acc[o][k]);
+        for (int o = 0; o < OUTS; ++o) {
+          const float* xv = col[o * SW + kw];
+          float2 a01 = make_float2(acc[o][0], acc[o][1]), a23 = make_float2(acc[o][2], acc[o][3]);
+          const float2 x01 = make_float2(xv[0], xv[1]), x23 = make_float2(xv[2], xv[3]);
+          if (strict) {  // (scalar: the reference's separate multiply and add, never contracted)
+            a01 = make_float2(__fadd_rn(a01.x, __fmul_rn(x01.x, w01.x)), __fadd_rn(a01.y, __fmul_rn(x01.y, w01.y)));
+            a23 = make_float2(__fadd_rn(a23.x, __fmul_rn(x23.x, w23.x)), __fadd_rn(a23.y, __fmul_rn(x23.y, w23.y)));
+          } else {
+            a01 = __ffma2_rn(x01, w01, a01);
+            a23 = __ffma2_rn(x23, w23, a23);
           }
+          acc[o][0] = a01.x; acc[o][1] = a01.y; acc[o][2] = a23.x; acc[o][3] = a23.y;
+        }
       }
     }
     if constexpr (DSIG != DW_ANY) {
