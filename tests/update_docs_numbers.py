@@ -30,7 +30,7 @@ for L in d["per_launch"]:
 rows += ["", "Step: %.3f ms in the CUDA graph (%.1f k img/s int8; bf16 %.1f k img/s) against a %.3f ms"
          " per-group roofline sum: %d %% of roofline. Batch 4096 (C5, one GPU, `--global-batch 4096`):"
          " %.2f ms per step, %.1f k img/s. End to end through `mr_exec_submit_host` (pinned host"
-         " buffers, H2D + run + D2H every step): %.1f k img/s (PCIe-bound: 154 MB of fp32 input per step)."
+         " buffers, H2D + run + D2H every step): %.1f k img/s (PCIe-bound: 154 MB of fp32 input per step at the 55.3 GB/s host-to-device rate `tests/h2d_rate.py` measures with 1, 2 or 4 copy streams)."
          " Clocks: median %s MHz of %s, reasons %s." % (
              d["ms_per_step"], d["value"] / 1e3, d["bf16"]["value"] / 1e3, roof, round(100 * roof / d["ms_per_step"]),
              c5["ms_per_step"], c5["value"] / 1e3, d["e2e"]["value"] / 1e3, d["clocks"]["sm_mhz"],
